@@ -1,0 +1,177 @@
+/*
+ * int4linear.h -- C ABI of the B200-native INT4 quantized linear operator of
+ * arXiv 2306.11987 ("Training Transformers with 4-bit Integers": HQ + LSS).
+ *
+ * Problem (Eq. 1): Y = X W^T with X in R^{N x D} (N = S T
+ * tokens), W in R^{C x D}.  Forward = Procedure HQ-MM;
+ * backward = the STE gradients of Eq. 4 with the "type 3"
+ * MMs computed by Procedure LSS-MM.
+ *
+ * Conventions common to every entry point
+ *   - All tensors are row-major and contiguous.  Every pointer is a DEVICE
+ *     pointer unless stated otherwise; every pointer must be 16-byte aligned.
+ *   - X, W and grad_Y are bf16 (PAPER.md:56 uses 16-bit floats; bf16 matches the
+ *     cuBLAS BF16 baseline).  Step sizes are fp32 host scalars.
+ *   - Ownership: the caller allocates EVERY buffer (outputs, caches, plans,
+ *     workspace); the library never allocates device memory and keeps no
+ *     per-call state.  Buffer sizes are stated per field below.
+ *   - Execution: stream-ordered and asynchronous on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  No entry point
+ *     synchronises the device or reads device memory from the host, so the
+ *     sequence is CUDA-graph capturable.  Sampled counts stay on the device.
+ *   - Errors: return codes, never abort.  On a non-OK status nothing has been
+ *     launched, except I4_ERR_CUDA (a launch failed; see int4_last_error()).
+ *   - Integer codes are int8 holding INT4 values: X_hat, W_hat in [-7, 7]
+ *     (Q_N = Q_P = 7); grad_up in [-7, 7]; grad_down in [-8, 7].
+ *   - Clamp masks are bit-packed uint32 words [rows, cols / 32]; bit j of word
+ *     w is column 32 w + j (1 = inside [-Q_N, Q_P]).
+ *   - Shape limits: cols % 64 == 0 for D and C; D % 2^k == 0;
+ *     0 <= k <= 7; backward N <= 65536 (INT32 accumulator bound of the grad_W
+ *     GEMM, reading Z-21).
+ *   - Determinism: identical inputs and identical (seed, call_id, token_offset)
+ *     give byte-identical outputs.  Philox4x32-10 streams use GLOBAL token
+ *     indices (token_offset + t), so a token-sharded run draws the same numbers
+ *     as an unsharded one (reading Z-20).
+ */
+#ifndef INT4LINEAR_H
+#define INT4LINEAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define I4_API __attribute__((visibility("default")))
+#else
+#define I4_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    I4_OK = 0,
+    I4_ERR_SHAPE = 1,        /* shape / k out of the supported set            */
+    I4_ERR_ALIGN = 2,        /* pointer not 16-byte aligned                   */
+    I4_ERR_ARG = 3,          /* step size <= 0 or non-finite, bad enum, NULL  */
+    I4_ERR_UNSUPPORTED = 4,  /* device is not sm_100 (tcgen05 kind::i8)       */
+    I4_ERR_WORKSPACE = 5,    /* ws_bytes smaller than the *_workspace_size    */
+    I4_ERR_CUDA = 6          /* a CUDA API call or kernel launch failed       */
+} i4_status;
+
+typedef enum { I4_OUT_F32 = 0, I4_OUT_BF16 = 1 } i4_out_dtype;
+
+typedef enum {
+    I4_LSS_BERNOULLI = 0,      /* §4.2 + A.2 probabilities, dyadic weights (Z-17) */
+    I4_LSS_KEEP_POSITIVE = 1,  /* A.6: keep every item with score > 0 */
+    I4_LSS_NONE = 2            /* no sampling: all 2N items, the exact BS product  */
+} i4_lss_mode;
+
+/* Forward cache ("X_hat and W_hat have been already calculated
+ * in forward propagation").  Written by int4_linear_fwd, read by
+ * int4_linear_bwd.  Device buffers, caller-allocated:
+ *   xq       int8  [N, D]      X_hat = <XH>_{s_X}
+ *   wq       int8  [C, D]      W_hat = <WH>_{s_W}
+ *   wqT      int8  [D, C]      W_hat transposed (K-major B operand of grad_X)
+ *   x_mask   uint32 [N, D/32]  I_X (on XH / s_X, reading Z-8)
+ *   w_mask   uint32 [C, D/32]  I_W
+ *   x_sqnorm int32 [N]         sum_d X_hat[t, d]^2 (leverage scores)
+ * Host scalars: N, D, C, k, s_x, s_w are filled by int4_linear_fwd.  Set
+ * w_valid = 1 to reuse wq / wqT / w_mask from a previous call with the same W
+ * and s_w (one weight quantization per weight version); the library never
+ * changes w_valid. */
+typedef struct {
+    int8_t* xq;
+    int8_t* wq;
+    int8_t* wqT;
+    uint32_t* x_mask;
+    uint32_t* w_mask;
+    int32_t* x_sqnorm;
+    int64_t N, D, C;
+    int32_t k;
+    float s_x, s_w;
+    int32_t w_valid;
+} i4_fwd_cache;
+
+/* Bit-split + sampling plan (Procedure LSS-MM steps 1-4).  Device buffers,
+ * caller-allocated, written by bitsplit_lss:
+ *   hilo     int8  [2N, C]     rows 0..N-1 = grad_up (high 4 bits), N..2N-1 = grad_down
+ *   a_sq     int32 [2N]        sum_c code^2 per row of hilo
+ *   amax_bits uint32 [1]       bf16 bit pattern of max |grad_Y| (scratch)
+ *   s_down   float [1]         s_down = amax / 119 (s_up = 16 s_down), reading Z-9
+ *   items_w  int32 [2N + 128]  kept items of the grad_W mask, ascending ids h*N + t,
+ *                              padded with the sentinel 2N up to a multiple of 128
+ *   wexp_w   int8  [2N + 128]  log2 of each kept item's weight (~ m_i / p_i)
+ *   count_w  int32 [1]         number of kept items (device)
+ *   items_x, wexp_x, count_x   the same for the grad_X mask */
+typedef struct {
+    int8_t* hilo;
+    int32_t* a_sq;
+    uint32_t* amax_bits;
+    float* s_down;
+    int32_t* items_w;
+    int8_t* wexp_w;
+    int32_t* count_w;
+    int32_t* items_x;
+    int8_t* wexp_x;
+    int32_t* count_x;
+} i4_lss_plan;
+
+/* F1+F2 / F3: block-Hadamard transform + LSQ quantize of a bf16 matrix
+ * (Procedure HQ-MM steps 1-2; Eq. 2).
+ *   x_bf16      [rows, cols] input
+ *   k           Hadamard block exponent, block 2^k
+ *   step        LSQ step size s > 0
+ *   codes       int8 [rows, cols] out: clamp(round_half_even(v), -7, 7) with
+ *               v = fl32(fl32(x H_pm1) * fl32(2^{-k/2} / s))   (readings Z-1, Z-4, Z-7)
+ *   clamp_bits  uint32 [rows, cols/32] out, nullable: 1(-7 <= v <= 7)
+ *   row_sqnorm  int32 [rows] out, nullable: sum of code^2 per row */
+I4_API i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t k, float step,
+                         int8_t* codes, uint32_t* clamp_bits, int32_t* row_sqnorm, void* stream);
+
+/* Forward HQ-MM: quantizes X (and W unless cache->w_valid)
+ * into `cache`, then Y = s_X s_W (X_hat W_hat^T) with an INT32 tcgen05 GEMM
+ * and a dequantizing epilogue fl32(acc) * fl32(s_x s_w) (reading Z-22).
+ *   X [N, D] bf16, W [C, D] bf16, Y [N, C] fp32 or bf16 (y_dtype). */
+I4_API i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, int64_t C, int32_t k,
+                          float s_x, float s_w, void* Y, i4_out_dtype y_dtype, i4_fwd_cache* cache,
+                          void* stream);
+
+/* LSS-MM steps 1-4: per-tensor amax, stochastic
+ * 8-bit code, bit split (Eq. 5), integer leverage scores of both masks
+ * (PAPER.md:296 with b = x_sqnorm, :365), A.2 probabilities (PAPER.md:606-610,
+ * budget N per mask), Philox Bernoulli masks with dyadic weights, compaction.
+ *   dY [N, C] bf16; x_sqnorm int32 [N] (from the forward cache; may be NULL
+ *   only for mode I4_LSS_NONE).  seed/call_id/token_offset select the Philox
+ *   streams (Z-20).  Outputs in *plan (see i4_lss_plan). */
+I4_API i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed,
+                       uint32_t call_id, int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan,
+                       void* stream);
+
+/* Full LSS-MM backward (Eq. 4):
+ *   grad_X = [I_X o (s_W sum_kept w_i s_h code_i W_hat)] H^T   -> dX [N, D] fp32
+ *   grad_W = s_X [(sum_kept w_i s_h code_i (x) X_hat_t) o I_W] H^T -> dW [C, D] fp32
+ * Runs bitsplit_lss into *plan, then the compaction and the two INT32 GEMMs
+ * whose epilogues apply scale, mask and the inverse transform (reading Z-23).
+ * ws: device scratch of int4_bwd_workspace_size(N, D, C) bytes. */
+I4_API i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
+                          int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, float* dX,
+                          float* dW, void* ws, size_t ws_bytes, void* stream);
+
+/* Bytes of device scratch int4_linear_bwd needs for these shapes. */
+I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
+
+/* Exact INT8 x INT8 -> INT32 product acc = A B^T on the tcgen05 path used by
+ * every GEMM of the operator ("Multiply the two INT4 matrices").
+ * A [M, K] int8, B [Nn, K] int8, acc [M, Nn] int32; K % 16 == 0, Nn % 64 == 0.
+ * Exposed for the bit-exact accumulator parity check. */
+I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, const int8_t* B, int64_t M, int64_t Nn, int64_t K,
+                            int32_t* acc, void* stream);
+
+/* Thread-local message describing the last non-OK status of this thread. */
+I4_API const char* int4_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INT4LINEAR_H */

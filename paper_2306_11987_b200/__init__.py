@@ -1,0 +1,186 @@
+"""B200-native INT4 quantized linear operator of arXiv 2306.11987 (HQ + LSS).
+
+Thin Python binding over the C ABI in include/int4linear.h: argument
+marshalling only (torch tensors -> device pointers + sizes + the current
+stream).  Every step of the operator runs in the sm_100a kernels of
+libint4linear.so; there is no CPU or PyTorch fallback -- importing this
+package without the built library raises.
+
+Functions carry the ABI names: hadamard_quant, int4_linear_fwd,
+bitsplit_lss, int4_linear_bwd, int4_gemm_s8s8s32.  `Int4Linear` owns the
+caller-side buffers (forward cache, sampling plan, workspace) for one layer
+shape.
+"""
+import ctypes
+import os
+
+__all__ = [
+    "LIB_PATH", "lib", "I4Error", "I4FwdCache", "I4LssPlan",
+    "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
+    "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
+    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "Int4Linear",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
+
+LSS_BERNOULLI, LSS_KEEP_POSITIVE, LSS_NONE = 0, 1, 2
+OUT_F32, OUT_BF16 = 0, 1
+_STATUS = {0: "I4_OK", 1: "I4_ERR_SHAPE", 2: "I4_ERR_ALIGN", 3: "I4_ERR_ARG",
+           4: "I4_ERR_UNSUPPORTED", 5: "I4_ERR_WORKSPACE", 6: "I4_ERR_CUDA"}
+
+
+class I4Error(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class I4FwdCache(ctypes.Structure):
+    _fields_ = [("xq", ctypes.c_void_p), ("wq", ctypes.c_void_p), ("wqT", ctypes.c_void_p),
+                ("x_mask", ctypes.c_void_p), ("w_mask", ctypes.c_void_p), ("x_sqnorm", ctypes.c_void_p),
+                ("N", ctypes.c_int64), ("D", ctypes.c_int64), ("C", ctypes.c_int64),
+                ("k", ctypes.c_int32), ("s_x", ctypes.c_float), ("s_w", ctypes.c_float),
+                ("w_valid", ctypes.c_int32)]
+
+
+class I4LssPlan(ctypes.Structure):
+    _fields_ = [("hilo", ctypes.c_void_p), ("a_sq", ctypes.c_void_p), ("amax_bits", ctypes.c_void_p),
+                ("s_down", ctypes.c_void_p), ("items_w", ctypes.c_void_p), ("wexp_w", ctypes.c_void_p),
+                ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
+                ("count_x", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, u32, u64, f32 = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32,
+                                   ctypes.c_uint64, ctypes.c_float)
+    sigs = {
+        "hadamard_quant": [vp, i64, i64, i32, f32, vp, vp, vp, vp],
+        "int4_linear_fwd": [vp, vp, i64, i64, i64, i32, f32, f32, vp, i32, ctypes.POINTER(I4FwdCache), vp],
+        "bitsplit_lss": [vp, i64, i64, vp, u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp],
+        "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, vp,
+                            vp, ctypes.c_size_t, vp],
+        "int4_gemm_s8s8s32": [vp, vp, i64, i64, i64, vp, vp],
+    }
+    for name, args in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
+    L.int4_bwd_workspace_size.restype = ctypes.c_size_t
+    L.int4_last_error.argtypes = []
+    L.int4_last_error.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def _check(status):
+    if status != 0:
+        raise I4Error(status, lib.int4_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def hadamard_quant(x, k, step, codes, clamp_bits=None, row_sqnorm=None, stream=None):
+    """F1+F2: block-Hadamard + LSQ of a bf16 [rows, cols] tensor."""
+    rows, cols = x.shape
+    _check(lib.hadamard_quant(_ptr(x), rows, cols, k, float(step), _ptr(codes), _ptr(clamp_bits),
+                              _ptr(row_sqnorm), _stream(stream)))
+
+
+def int4_linear_fwd(X, W, k, s_x, s_w, Y, cache, stream=None):
+    """HQ-MM forward; cache is an I4FwdCache with device buffers."""
+    import torch
+    N, D = X.shape
+    C = W.shape[0]
+    y_dtype = OUT_BF16 if Y.dtype == torch.bfloat16 else OUT_F32
+    _check(lib.int4_linear_fwd(_ptr(X), _ptr(W), N, D, C, k, float(s_x), float(s_w), _ptr(Y), y_dtype,
+                               ctypes.byref(cache), _stream(stream)))
+
+
+def bitsplit_lss(dY, x_sqnorm, seed, call_id, token_offset, mode, plan, stream=None):
+    """LSS-MM steps 1-4 into an I4LssPlan."""
+    N, C = dY.shape
+    _check(lib.bitsplit_lss(_ptr(dY), N, C, _ptr(x_sqnorm), int(seed), int(call_id), int(token_offset), int(mode),
+                            ctypes.byref(plan), _stream(stream)))
+
+
+def int4_linear_bwd(dY, cache, seed, call_id, token_offset, mode, plan, dX, dW, ws, stream=None):
+    """LSS-MM backward."""
+    _check(lib.int4_linear_bwd(_ptr(dY), ctypes.byref(cache), int(seed), int(call_id), int(token_offset), int(mode),
+                               ctypes.byref(plan), _ptr(dX), _ptr(dW), _ptr(ws), ws.numel() * ws.element_size(),
+                               _stream(stream)))
+
+
+def int4_bwd_workspace_size(N, D, C):
+    return int(lib.int4_bwd_workspace_size(N, D, C))
+
+
+def int4_gemm_s8s8s32(A, B, acc, stream=None):
+    """acc = A B^T, int8 x int8 -> int32 on tcgen05."""
+    M, K = A.shape
+    Nn = B.shape[0]
+    _check(lib.int4_gemm_s8s8s32(_ptr(A), _ptr(B), M, Nn, K, _ptr(acc), _stream(stream)))
+
+
+class Int4Linear:
+    """Caller-side buffers of one INT4 linear layer shape [N, D] x [C, D].
+
+    Allocates (torch, on `device`) the forward cache, the sampling plan and the
+    backward workspace once; forward / backward then only launch kernels.
+    """
+
+    def __init__(self, N, D, C, k, device="cuda"):
+        import torch
+        self.N, self.D, self.C, self.k = N, D, C, k
+        dev = torch.device(device)
+        i8, i32, f32 = torch.int8, torch.int32, torch.float32
+        self.xq = torch.empty(N, D, dtype=i8, device=dev)
+        self.wq = torch.empty(C, D, dtype=i8, device=dev)
+        self.wqT = torch.empty(D, C, dtype=i8, device=dev)
+        self.x_mask = torch.empty(N, D // 32, dtype=i32, device=dev)
+        self.w_mask = torch.empty(C, D // 32, dtype=i32, device=dev)
+        self.x_sqnorm = torch.empty(N, dtype=i32, device=dev)
+        self.cache = I4FwdCache(xq=self.xq.data_ptr(), wq=self.wq.data_ptr(), wqT=self.wqT.data_ptr(),
+                                x_mask=self.x_mask.data_ptr(), w_mask=self.w_mask.data_ptr(),
+                                x_sqnorm=self.x_sqnorm.data_ptr(), w_valid=0)
+        n2 = 2 * N + 128
+        self.hilo = torch.empty(2 * N, C, dtype=i8, device=dev)
+        self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
+        self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
+        self.items_w = torch.empty(n2, dtype=i32, device=dev)
+        self.wexp_w = torch.empty(n2, dtype=i8, device=dev)
+        self.items_x = torch.empty(n2, dtype=i32, device=dev)
+        self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
+        sp = self.scalars.data_ptr()
+        self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
+                              items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
+                              items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12)
+        self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
+
+    def forward(self, X, W, s_x, s_w, Y, reuse_weight=False, stream=None):
+        self.cache.w_valid = 1 if reuse_weight else 0
+        int4_linear_fwd(X, W, self.k, s_x, s_w, Y, self.cache, stream)
+
+    def backward(self, dY, dX, dW, seed, call_id=0, token_offset=0, mode=LSS_BERNOULLI, stream=None):
+        int4_linear_bwd(dY, self.cache, seed, call_id, token_offset, mode, self.plan, dX, dW, self.ws, stream)
+
+    # views of the device-side sampling state (for tests and reports)
+    def s_down(self):
+        return self.scalars[1:2].view(__import__("torch").float32)
+
+    def counts(self):
+        return self.scalars[2:4]

@@ -1,0 +1,305 @@
+// C ABI of libint4linear (declared in include/int4linear.h): argument
+// validation, TMA tensor-map construction and the stream-ordered launch
+// sequence of HQ-MM and LSS-MM.
+// No host<->device synchronisation and no device allocation happen here.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/int4linear.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+i4_status fail(i4_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+i4_status fail(i4_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+i4_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(I4_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define I4_CHECK_CUDA(expr, where)                      \
+    do {                                                \
+        cudaError_t e_ = (expr);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+struct DeviceInfo {
+    bool ok = false;
+    int sms = 0;
+    std::string why;
+};
+
+DeviceInfo query_device() {
+    DeviceInfo d;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { d.why = "no CUDA device"; return d; }
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) { d.why = "cudaGetDeviceProperties failed"; return d; }
+    if (!(p.major == 10 && p.minor == 0)) {
+        char b[128];
+        snprintf(b, sizeof b, "device is sm_%d%d; this library is built for sm_100a (tcgen05 kind::i8)", p.major, p.minor);
+        d.why = b;
+        return d;
+    }
+    d.ok = true;
+    d.sms = p.multiProcessorCount;
+    return d;
+}
+
+const DeviceInfo& device_info() {
+    static DeviceInfo info;
+    static std::once_flag once;
+    std::call_once(once, [] { info = query_device(); });
+    return info;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D int8 tensor [rows, inner] with row pitch `pitch` bytes; box = 128 B x box_rows,
+// 128-byte swizzle (matches the UMMA K-major SWIZZLE_128B descriptor).
+bool make_tmap_i8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t pitch, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {pitch};
+    cuuint32_t box[2] = {128, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+i4_status check_device() {
+    const DeviceInfo& d = device_info();
+    if (!d.ok) return fail(I4_ERR_UNSUPPORTED, "%s", d.why.c_str());
+    return I4_OK;
+}
+
+i4_status check_step(float s, const char* name) {
+    if (!(s > 0.0f) || !std::isfinite(s)) return fail(I4_ERR_ARG, "%s must be positive and finite (got %g)", name, double(s));
+    return I4_OK;
+}
+
+i4_status check_k(int32_t k, int64_t cols) {
+    if (k < 0 || k > 7) return fail(I4_ERR_SHAPE, "k = %d outside [0, 7]", k);
+    if (cols % (int64_t(1) << k) != 0) return fail(I4_ERR_SHAPE, "cols = %lld not a multiple of 2^k (PAPER.md:132)", (long long)cols);
+    return I4_OK;
+}
+
+float step_recip(int32_t k, float s) { return float(std::pow(2.0, -double(k) / 2.0) / double(s)); }
+float inv_sqrt_block(int32_t k) { return float(std::pow(2.0, -double(k) / 2.0)); }
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+constexpr int64_t kMaxBwdTokens = 65536;
+
+#define I4_RETURN_IF(st) do { i4_status s_ = (st); if (s_ != I4_OK) return s_; } while (0)
+
+i4_status gemm(const int8_t* A, int64_t a_rows, int64_t a_pitch, const int8_t* B, int64_t b_rows, int64_t b_pitch,
+               int64_t K, const i4::GemmArgs& args, cudaStream_t s) {
+    CUtensorMap ta, tb;
+    const int bn = i4::gemm_block_n(args.Nn);
+    if (!make_tmap_i8(&ta, A, uint64_t(K), uint64_t(a_rows), uint64_t(a_pitch), 128) ||
+        !make_tmap_i8(&tb, B, uint64_t(K), uint64_t(b_rows), uint64_t(b_pitch), uint32_t(bn)))
+        return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    I4_CHECK_CUDA(i4::launch_gemm(&ta, &tb, args, device_info().sms, s), "gemm launch");
+    return I4_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* int4_last_error(void) { return g_last_error.c_str(); }
+
+i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t k, float step, int8_t* codes,
+                         uint32_t* clamp_bits, int32_t* row_sqnorm, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!x_bf16 || !codes) return fail(I4_ERR_ARG, "hadamard_quant: NULL input/output");
+    if (rows < 0 || cols <= 0 || cols % 32 != 0) return fail(I4_ERR_SHAPE, "hadamard_quant: cols = %lld must be a positive multiple of 32", (long long)cols);
+    I4_RETURN_IF(check_k(k, cols));
+    I4_RETURN_IF(check_step(step, "step"));
+    if (!aligned16(x_bf16) || !aligned16(codes)) return fail(I4_ERR_ALIGN, "hadamard_quant: pointers must be 16-byte aligned");
+    I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(x_bf16), rows, cols, k, step_recip(k, step),
+                                            codes, clamp_bits, row_sqnorm, static_cast<cudaStream_t>(stream)),
+                  "hadamard_quant");
+    return I4_OK;
+}
+
+i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, int64_t C, int32_t k, float s_x,
+                          float s_w, void* Y, i4_out_dtype y_dtype, i4_fwd_cache* cache, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!X || !W || !Y || !cache || !cache->xq || !cache->wq || !cache->wqT || !cache->x_mask || !cache->w_mask ||
+        !cache->x_sqnorm)
+        return fail(I4_ERR_ARG, "int4_linear_fwd: NULL pointer");
+    if (N <= 0 || D <= 0 || C <= 0 || D % 64 || C % 64)
+        return fail(I4_ERR_SHAPE, "int4_linear_fwd: need N > 0 and D, C positive multiples of 64 (N=%lld D=%lld C=%lld)",
+                    (long long)N, (long long)D, (long long)C);
+    if (N > (int64_t(1) << 31) / 2) return fail(I4_ERR_SHAPE, "int4_linear_fwd: N too large");
+    I4_RETURN_IF(check_k(k, D));
+    I4_RETURN_IF(check_step(s_x, "s_x"));
+    I4_RETURN_IF(check_step(s_w, "s_w"));
+    if (y_dtype != I4_OUT_F32 && y_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "bad y_dtype");
+    if (!aligned16(X) || !aligned16(W) || !aligned16(Y)) return fail(I4_ERR_ALIGN, "int4_linear_fwd: unaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(X), N, D, k, step_recip(k, s_x), cache->xq,
+                                            cache->x_mask, cache->x_sqnorm, s), "hadamard_quant(X)");
+    if (!cache->w_valid) {
+        I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(W), C, D, k, step_recip(k, s_w), cache->wq,
+                                                cache->w_mask, nullptr, s), "hadamard_quant(W)");
+        I4_CHECK_CUDA(i4::launch_transpose_i8(cache->wq, C, D, cache->wqT, s), "transpose(W_hat)");
+    }
+    i4::GemmArgs g{};
+    g.M = int32_t(N); g.Nn = int32_t(C); g.K = int32_t(D);
+    g.epi = i4::EPI_FWD;
+    g.out = Y;
+    g.out_bf16 = y_dtype == I4_OUT_BF16;
+    g.scale = s_x * s_w;                      // fl32(s_x s_w), reading Z-22
+    I4_RETURN_IF(gemm(cache->xq, N, D, cache->wq, C, D, D, g, s));
+    cache->N = N; cache->D = D; cache->C = C; cache->k = k; cache->s_x = s_x; cache->s_w = s_w;
+    return I4_OK;
+}
+
+i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed, uint32_t call_id,
+                       int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->items_w ||
+        !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x)
+        return fail(I4_ERR_ARG, "bitsplit_lss: NULL pointer");
+    if (mode != I4_LSS_BERNOULLI && mode != I4_LSS_KEEP_POSITIVE && mode != I4_LSS_NONE)
+        return fail(I4_ERR_ARG, "bitsplit_lss: bad mode");
+    if (mode != I4_LSS_NONE && !x_sqnorm) return fail(I4_ERR_ARG, "bitsplit_lss: x_sqnorm required");
+    if (N <= 0 || C <= 0 || C % 64) return fail(I4_ERR_SHAPE, "bitsplit_lss: need N > 0, C a multiple of 64");
+    if (N > kMaxBwdTokens || N > i4::sampler_max_tokens())
+        return fail(I4_ERR_SHAPE, "bitsplit_lss: N = %lld exceeds %lld tokens per call (reading Z-21)", (long long)N,
+                    (long long)kMaxBwdTokens);
+    if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
+    if (!aligned16(dY) || !aligned16(plan->hilo)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    I4_CHECK_CUDA(i4::launch_amax_bf16(static_cast<const uint16_t*>(dY), N * C, plan->amax_bits, s), "amax");
+    I4_CHECK_CUDA(i4::launch_bitsplit(static_cast<const uint16_t*>(dY), N, C, plan->amax_bits, seed, call_id,
+                                      token_offset, plan->hilo, plan->a_sq, plan->s_down, s), "bitsplit");
+    i4::SamplerArgs a{};
+    a.a_sq = plan->a_sq;
+    a.x_sqnorm = x_sqnorm;
+    a.N = int32_t(N);
+    a.mode = int32_t(mode);
+    a.seed_lo = uint32_t(seed);
+    a.seed_hi = uint32_t(seed >> 32);
+    a.call_id = call_id;
+    a.token_offset = token_offset;
+    a.items[0] = plan->items_w; a.wexp[0] = plan->wexp_w; a.count[0] = plan->count_w;
+    a.items[1] = plan->items_x; a.wexp[1] = plan->wexp_x; a.count[1] = plan->count_x;
+    I4_CHECK_CUDA(i4::launch_lss_sampler(a, s), "lss_sampler");
+    return I4_OK;
+}
+
+size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) {
+    const int64_t kcap = round_up(2 * N, 128);
+    const int64_t ax = round_up((2 * N + 128) * C, 256);
+    const int64_t aw = round_up(C * kcap, 256);
+    const int64_t bw = round_up(D * kcap, 256);
+    return size_t(ax + aw + bw);
+}
+
+i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
+                          int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, float* dX, float* dW,
+                          void* ws, size_t ws_bytes, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!cache || !dX || !dW || !ws) return fail(I4_ERR_ARG, "int4_linear_bwd: NULL pointer");
+    const int64_t N = cache->N, D = cache->D, C = cache->C;
+    const int32_t k = cache->k;
+    if (N <= 0 || D <= 0 || C <= 0) return fail(I4_ERR_ARG, "int4_linear_bwd: cache not filled by int4_linear_fwd");
+    if (ws_bytes < int4_bwd_workspace_size(N, D, C))
+        return fail(I4_ERR_WORKSPACE, "int4_linear_bwd: ws_bytes %zu < %zu", ws_bytes, int4_bwd_workspace_size(N, D, C));
+    if (!aligned16(dX) || !aligned16(dW) || !aligned16(ws)) return fail(I4_ERR_ALIGN, "int4_linear_bwd: unaligned pointer");
+    I4_RETURN_IF(bitsplit_lss(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    const int64_t kcap = round_up(2 * N, 128);
+    int8_t* a_x = static_cast<int8_t*>(ws);
+    int8_t* a_wt = a_x + round_up((2 * N + 128) * C, 256);
+    int8_t* b_wt = a_wt + round_up(C * kcap, 256);
+
+    I4_CHECK_CUDA(i4::launch_compact_rows(plan->hilo, C, plan->items_x, plan->count_x, 2 * N, a_x, s), "compact_rows");
+    I4_CHECK_CUDA(i4::launch_compact_wgrad(plan->hilo, cache->xq, N, C, D, plan->items_w, plan->wexp_w, plan->count_w,
+                                           kcap, a_wt, b_wt, s), "compact_wgrad");
+    // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
+    I4_CHECK_CUDA(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset dX");
+    {
+        i4::GemmArgs g{};
+        g.M = int32_t(2 * N + 128); g.m_dev = plan->count_x;
+        g.Nn = int32_t(D); g.K = int32_t(C);
+        g.epi = i4::EPI_DGRAD;
+        g.out = dX;
+        g.scale = cache->s_w * inv_sqrt_block(k);
+        g.s_down = plan->s_down;
+        g.k_had = k;
+        g.mask = cache->x_mask;
+        g.items = plan->items_x;
+        g.wexp = plan->wexp_x;
+        g.n_tokens = int32_t(N);
+        I4_RETURN_IF(gemm(a_x, 2 * N + 128, C, cache->wqT, D, C, C, g, s));
+    }
+    // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
+    {
+        i4::GemmArgs g{};
+        g.M = int32_t(C); g.Nn = int32_t(D); g.K = int32_t(kcap); g.k_dev = plan->count_w;
+        g.epi = i4::EPI_WGRAD;
+        g.out = dW;
+        g.scale = cache->s_x * inv_sqrt_block(k);
+        g.s_down = plan->s_down;
+        g.k_had = k;
+        g.mask = cache->w_mask;
+        I4_RETURN_IF(gemm(a_wt, C, kcap, b_wt, D, kcap, kcap, g, s));
+    }
+    return I4_OK;
+}
+
+i4_status int4_gemm_s8s8s32(const int8_t* A, const int8_t* B, int64_t M, int64_t Nn, int64_t K, int32_t* acc,
+                            void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!A || !B || !acc) return fail(I4_ERR_ARG, "int4_gemm_s8s8s32: NULL pointer");
+    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16)
+        return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: need Nn %% 64 == 0 and K %% 16 == 0");
+    if (!aligned16(A) || !aligned16(B) || !aligned16(acc)) return fail(I4_ERR_ALIGN, "int4_gemm_s8s8s32: unaligned pointer");
+    i4::GemmArgs g{};
+    g.M = int32_t(M); g.Nn = int32_t(Nn); g.K = int32_t(K);
+    g.epi = i4::EPI_INT32;
+    g.out = acc;
+    return gemm(A, M, K, B, Nn, K, K, g, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

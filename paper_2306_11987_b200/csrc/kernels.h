@@ -1,0 +1,65 @@
+// Internal host-side launchers of the sm_100a kernels (not part of the C ABI;
+// the ABI is include/int4linear.h, implemented in api.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace i4 {
+
+// quant.cu --------------------------------------------------------------------
+cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
+                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s);
+cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, cudaStream_t s);
+cudaError_t launch_bitsplit(const uint16_t* g, int64_t N, int64_t C, const uint32_t* amax_bits,
+                            uint64_t seed, uint32_t call_id, int64_t token_offset, int8_t* hilo,
+                            int32_t* a_sq, float* s_down, cudaStream_t s);
+cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int8_t* dst, cudaStream_t s);
+
+// sampler.cu ------------------------------------------------------------------
+struct SamplerArgs {
+    const int32_t* a_sq;      // [2N]
+    const int32_t* x_sqnorm;  // [N]  (weight-gradient scores)
+    int32_t N;
+    int32_t mode;             // i4_lss_mode
+    uint32_t seed_lo, seed_hi, call_id;
+    int64_t token_offset;
+    int32_t* items[2];        // [0] grad_W mask, [1] grad_X mask
+    int8_t* wexp[2];
+    int32_t* count[2];
+};
+int sampler_max_tokens();
+cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
+
+// compact.cu ------------------------------------------------------------------
+cudaError_t launch_compact_rows(const int8_t* hilo, int64_t C, const int32_t* items, const int32_t* count,
+                                int64_t n_items, int8_t* out, cudaStream_t s);
+cudaError_t launch_compact_wgrad(const int8_t* hilo, const int8_t* xq, int64_t N, int64_t C, int64_t D,
+                                 const int32_t* items, const int8_t* wexp, const int32_t* count,
+                                 int64_t kcap, int8_t* a_t, int8_t* b_t, cudaStream_t s);
+
+// gemm.cu ---------------------------------------------------------------------
+enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3 };
+
+struct GemmArgs {
+    // problem: acc[M, Nn] = A[M, K] . B[Nn, K]^T; M or K may come from device memory
+    int32_t M, Nn, K;
+    const int32_t* m_dev;     // if non-null: M = roundup(*m_dev) rows are valid (dgrad)
+    const int32_t* k_dev;     // if non-null: K = *m_dev-style count of K rows (wgrad)
+    int32_t epi;
+    // outputs
+    void* out;                // int32 / fp32 / bf16 [M, Nn]
+    int32_t out_bf16;
+    float scale;              // fwd: fl32(s_x s_w); dgrad: s_w 2^{-k/2}; wgrad: s_x 2^{-k/2}
+    const float* s_down;      // dgrad / wgrad: device s_down
+    int32_t k_had;            // Hadamard exponent for the epilogue inverse transform
+    const uint32_t* mask;     // dgrad: I_X [N, Nn/32]; wgrad: I_W [M, Nn/32]
+    const int32_t* items;     // dgrad: item id of each A row
+    const int8_t* wexp;       // dgrad: weight exponent of each A row
+    int32_t n_tokens;         // dgrad: N (item id = h*N + t)
+};
+cudaError_t launch_gemm(const void* tmap_a, const void* tmap_b, const GemmArgs& g, int num_sms, cudaStream_t s);
+int gemm_block_n(int Nn);
+
+}  // namespace i4

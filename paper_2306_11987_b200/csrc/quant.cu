@@ -1,0 +1,274 @@
+// Memory-bound quantizer kernels (HBM roofline):
+//   hadamard_quant : F1+F2 / F3 -- block FWHT + LSQ (Eq. 2)
+//   amax_bf16      : B1 -- per-tensor max |grad_Y| (reading Z-9)
+//   bitsplit       : B2 -- Philox SR to the 8-bit code, split into high / low
+//                    4-bit planes, per-row integer norms
+//   transpose_i8   : W_hat -> W_hat^T (K-major B operand of the grad_X GEMM)
+//
+// Thread layout shared by the row kernels: one warp per row; the row is walked
+// in 256-column chunks, lane l owning columns [c0 + 8 l, c0 + 8 l + 8) so each
+// warp-wide 16-byte load covers 512 contiguous bytes.  Hadamard blocks of 2^k
+// <= 8 columns are transformed in registers; larger blocks (k = 4..7) add
+// xor-shuffle butterfly stages across lanes 1, 2, 4, 8 apart.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace i4 {
+
+constexpr int kRowWarps = 8;            // warps per CTA in the row kernels
+
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&v)[8]) {
+    v[0] = bf16_lo(u.x); v[1] = bf16_hi(u.x);
+    v[2] = bf16_lo(u.y); v[3] = bf16_hi(u.y);
+    v[4] = bf16_lo(u.z); v[5] = bf16_hi(u.z);
+    v[6] = bf16_lo(u.w); v[7] = bf16_hi(u.w);
+}
+
+__device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
+    return (uint32_t(a) & 0xFF) | ((uint32_t(b) & 0xFF) << 8) | ((uint32_t(c) & 0xFF) << 16) |
+           ((uint32_t(d) & 0xFF) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// hadamard_quant
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRowWarps * 32)
+hadamard_quant_kernel(const uint16_t* __restrict__ x, int64_t rows, int cols, int k, float r,
+                      int8_t* __restrict__ codes, uint32_t* __restrict__ bits,
+                      int32_t* __restrict__ sqnorm) {
+    const int lane = lane_id();
+    const int64_t warp0 = int64_t(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
+    const int64_t wstride = int64_t(gridDim.x) * kRowWarps;
+    const int words_per_row = cols >> 5;
+    for (int64_t row = warp0; row < rows; row += wstride) {
+        const uint16_t* xr = x + row * cols;
+        int sq = 0;
+        for (int c0 = 0; c0 < cols; c0 += 256) {
+            const int col = c0 + lane * 8;
+            const bool active = col < cols;
+            uint4 raw = make_uint4(0, 0, 0, 0);
+            if (active) raw = ld_nc_v4(xr + col);
+            float v[8];
+            unpack_bf16x8(raw, v);
+            // in-register butterflies: strides 1, 2, 4
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                if (s < k) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (((i >> s) & 1) == 0) {
+                            const float a = v[i], b = v[i + (1 << s)];
+                            v[i] = __fadd_rn(a, b);
+                            v[i + (1 << s)] = __fsub_rn(a, b);
+                        }
+                    }
+                }
+            }
+            // cross-lane butterflies: strides 8, 16, 32, 64 columns = lanes 1, 2, 4, 8 apart
+#pragma unroll
+            for (int s = 3; s < 7; ++s) {
+                if (s < k) {
+                    const int lm = 1 << (s - 3);
+                    const bool upper = (lane & lm) != 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float o = __shfl_xor_sync(0xFFFFFFFFu, v[i], lm);
+                        v[i] = upper ? __fsub_rn(o, v[i]) : __fadd_rn(v[i], o);
+                    }
+                }
+            }
+            // LSQ: v = fl32(t * r); code = clamp(rint(v), -7, 7); mask = -7 <= v <= 7
+            int q[8];
+            uint32_t m8 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float sv = __fmul_rn(v[i], r);
+                int c = __float2int_rn(fminf(fmaxf(sv, -7.0f), 7.0f));
+                q[i] = c;
+                m8 |= uint32_t((sv >= -7.0f) && (sv <= 7.0f)) << i;
+                sq += c * c;
+            }
+            // 32-column mask word = 4 lanes x 8 bits
+            uint32_t word = m8 << (8 * (lane & 3));
+            word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
+            word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
+            if (active) {
+                uint2 packed = make_uint2(pack4_i8(q[0], q[1], q[2], q[3]), pack4_i8(q[4], q[5], q[6], q[7]));
+                *reinterpret_cast<uint2*>(codes + row * cols + col) = packed;
+                if (bits != nullptr && (lane & 3) == 0) bits[row * words_per_row + (col >> 5)] = word;
+            }
+        }
+        if (sqnorm != nullptr) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+            if (lane == 0) sqnorm[row] = sq;
+        }
+    }
+}
+
+static int row_grid(int64_t rows) {
+    int64_t blocks = (rows + kRowWarps - 1) / kRowWarps;
+    const int64_t cap = 148 * 16;       // 16 resident CTAs of 256 threads per SM
+    return int(blocks < cap ? blocks : cap);
+}
+
+cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
+                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    hadamard_quant_kernel<<<row_grid(rows), kRowWarps * 32, 0, s>>>(x, rows, int(cols), k, r, codes, bits, sqnorm);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// amax of a bf16 tensor: max over |g| as bf16 bit patterns (non-negative bf16
+// values order like their 15-bit integers), exact and order-independent.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) amax_bf16_kernel(const uint4* __restrict__ g, int64_t n16,
+                                                        uint32_t* __restrict__ amax_bits) {
+    uint32_t m = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint4 u = ld_nc_v4(g + i);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            m = max(m, w[j] & 0x7FFFu);
+            m = max(m, (w[j] >> 16) & 0x7FFFu);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    __shared__ uint32_t red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, red[w]);
+        atomicMax(amax_bits, m);
+    }
+}
+
+cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(amax_bits, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    const int64_t n16 = n / 8;          // n is a multiple of 64 (C % 64 == 0)
+    if (n16 == 0) return cudaSuccess;
+    int64_t blocks = (n16 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    amax_bf16_kernel<<<int(blocks), 256, 0, s>>>(reinterpret_cast<const uint4*>(g), n16, amax_bits);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// bitsplit: v = clamp(fl32(g r8), -119, 119); sign-magnitude stochastic
+// rounding with Philox word u: q = sign(v) (floor|v| + [u < ceil(frac|v| 2^32)]);
+// hi = floor((q + 8) / 16), lo = q - 16 hi  (readings Z-9, Z-10, Z-11).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRowWarps * 32)
+bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t* __restrict__ amax_bits,
+                uint32_t k0, uint32_t k1, uint32_t call_id, int64_t token_offset,
+                int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, float* __restrict__ s_down_out) {
+    const int lane = lane_id();
+    const float amax = __uint_as_float(__ldg(amax_bits) << 16);
+    const bool zero = !(amax > 0.0f);
+    const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
+    const int64_t warp0 = int64_t(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
+    const int64_t wstride = int64_t(gridDim.x) * kRowWarps;
+    for (int64_t row = warp0; row < N; row += wstride) {
+        const uint16_t* gr = g + row * C;
+        int8_t* hr = hilo + row * C;
+        int8_t* lr = hilo + (N + row) * C;
+        const uint64_t tglob = uint64_t(token_offset + row);
+        int shi = 0, slo = 0;
+        for (int c0 = 0; c0 < C; c0 += 256) {
+            const int col = c0 + lane * 8;
+            if (col < C) {
+                float v[8];
+                unpack_bf16x8(ld_nc_v4(gr + col), v);
+                // Philox words for the 8 elements: L = tglob * C + col + i, block L / 4
+                const uint64_t L0 = tglob * uint64_t(C) + uint64_t(col);
+                const uint64_t b0 = L0 >> 2;
+                const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, k0, k1);
+                const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, k0, k1);
+                const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+                int hi[8], lo[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    int q = 0;
+                    if (!zero) {
+                        const float sv = fminf(fmaxf(__fmul_rn(v[i], r8), -119.0f), 119.0f);
+                        const float a = fabsf(sv);
+                        const float fl = floorf(a);
+                        const float f = __fsub_rn(a, fl);                     // exact
+                        const uint64_t T = uint64_t(ceilf(__fmul_rn(f, 4294967296.0f)));  // exact
+                        const int mag = int(fl) + int(uint64_t(u[i]) < T);
+                        q = sv < 0.0f ? -mag : mag;
+                    }
+                    hi[i] = (q + 8) >> 4;                                     // floor division
+                    lo[i] = q - 16 * hi[i];
+                    shi += hi[i] * hi[i];
+                    slo += lo[i] * lo[i];
+                }
+                *reinterpret_cast<uint2*>(hr + col) =
+                    make_uint2(pack4_i8(hi[0], hi[1], hi[2], hi[3]), pack4_i8(hi[4], hi[5], hi[6], hi[7]));
+                *reinterpret_cast<uint2*>(lr + col) =
+                    make_uint2(pack4_i8(lo[0], lo[1], lo[2], lo[3]), pack4_i8(lo[4], lo[5], lo[6], lo[7]));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            shi += __shfl_xor_sync(0xFFFFFFFFu, shi, o);
+            slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
+        }
+        if (lane == 0) {
+            a_sq[row] = shi;
+            a_sq[N + row] = slo;
+        }
+    }
+}
+
+cudaError_t launch_bitsplit(const uint16_t* g, int64_t N, int64_t C, const uint32_t* amax_bits,
+                            uint64_t seed, uint32_t call_id, int64_t token_offset, int8_t* hilo,
+                            int32_t* a_sq, float* s_down, cudaStream_t s) {
+    if (N == 0) return cudaSuccess;
+    bitsplit_kernel<<<row_grid(N), kRowWarps * 32, 0, s>>>(g, N, int(C), amax_bits, uint32_t(seed),
+                                                            uint32_t(seed >> 32), call_id, token_offset,
+                                                            hilo, a_sq, s_down);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// int8 transpose, 64 x 64 tiles through shared memory
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) transpose_i8_kernel(const int8_t* __restrict__ src, int64_t rows,
+                                                           int64_t cols, int8_t* __restrict__ dst) {
+    __shared__ int8_t tile[64][64 + 4];
+    const int64_t r0 = int64_t(blockIdx.y) * 64, c0 = int64_t(blockIdx.x) * 64;
+    // load: 64 rows x 64 bytes, 16 bytes per thread
+    {
+        const int r = threadIdx.x >> 2, seg = (threadIdx.x & 3) * 16;
+        if (r0 + r < rows && c0 + seg < cols) {
+            const uint4 u = *reinterpret_cast<const uint4*>(src + (r0 + r) * cols + c0 + seg);
+            const int8_t* b = reinterpret_cast<const int8_t*>(&u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) tile[r][seg + j] = b[j];
+        }
+    }
+    __syncthreads();
+    {
+        const int c = threadIdx.x >> 2, seg = (threadIdx.x & 3) * 16;
+        if (c0 + c < cols && r0 + seg < rows) {
+            alignas(16) int8_t b[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) b[j] = tile[seg + j][c];
+            *reinterpret_cast<uint4*>(dst + (c0 + c) * rows + r0 + seg) = *reinterpret_cast<const uint4*>(b);
+        }
+    }
+}
+
+cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int8_t* dst, cudaStream_t s) {
+    dim3 grid(unsigned((cols + 63) / 64), unsigned((rows + 63) / 64));
+    transpose_i8_kernel<<<grid, 256, 0, s>>>(src, rows, cols, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace i4

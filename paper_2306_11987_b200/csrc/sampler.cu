@@ -1,0 +1,249 @@
+// Leverage-score sampler: LSS-MM steps 2-4 for
+// the grad_W mask and the grad_X mask, one 8-CTA thread-block cluster per mask.
+//
+//   scores   integer-exact (reading Z-13): w = floor(sqrt(a b) 2^(16 + 4[h = up]))
+//            for grad_W (a = sum code^2 of the half-row, b = sum X_hat^2 of the
+//            token), w = floor(sqrt(a) 2^(16 + 4[h = up])) for
+//            grad_X.  One IEEE double sqrt per item.
+//   A.2      PAPER.md:606-610 run to its fixed point in exact integers: an item
+//            is clamped (p = 1) when R w >= W with R = budget - |S| and W the sum
+//            of the unclamped positive scores; each round is one cluster-wide
+//            reduction through distributed shared memory.  Budget = N (:269).
+//   Bernoulli  dyadic two-threshold rule (reading Z-17): e = floor(log2(W/(R w))),
+//            T2 = floor(R w 2^32 / W), T1 = 2 T2 - 2^(32-e); Philox word u of item
+//            (h, t): keep iff u < T2, weight 2^e if u < T1 else 2^(e+1); floor
+//            weight 2^E_MAX (4 for grad_W whose weights fold into int8, 24 for grad_X).
+//   compaction  ascending item ids h*N + t via block scan + cluster prefix, list
+//            padded to a multiple of 128 with the sentinel 2N; count stays on device.
+//
+// The item scores live in shared memory (16384 items per CTA -> N <= 65536,
+// the same bound the grad_W INT32 accumulator imposes).  The kernel is
+// latency-bound (it moves < 2 MB); it is not an HBM-roofline kernel.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace i4 {
+
+constexpr int kClusterCTAs = 8;
+constexpr int kSamplerThreads = 1024;
+constexpr int kItemsPerCTA = 16384;
+constexpr int kEMaxW = 4;
+constexpr int kEMaxX = 24;
+
+int sampler_max_tokens() { return kClusterCTAs * kItemsPerCTA / 2; }
+
+struct SamplerSmem {
+    uint64_t w[kItemsPerCTA];        // scores
+    uint8_t clamped[kItemsPerCTA];   // A.2 set S
+    int8_t wexp[kItemsPerCTA];       // -1: dropped, else log2 weight
+    uint64_t red_w[2][kClusterCTAs];
+    uint32_t red_c[2][kClusterCTAs];
+    uint64_t warp_w[kSamplerThreads / 32];
+    uint32_t warp_c[kSamplerThreads / 32];
+    uint32_t scan[kSamplerThreads / 32];
+    uint32_t cta_tot[kClusterCTAs];
+};
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// Cluster-wide (sum w, sum c); every thread of every CTA receives the totals.
+__device__ void cluster_sum(cg::cluster_group& cl, SamplerSmem& sm, int& parity, uint64_t w, uint32_t c,
+                            uint64_t& W, uint32_t& Cn) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    w = warp_sum_u64(w);
+    c = warp_sum_u32(c);
+    if (lane == 0) { sm.warp_w[warp] = w; sm.warp_c[warp] = c; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t bw = 0; uint32_t bc = 0;
+        for (int i = 0; i < kSamplerThreads / 32; ++i) { bw += sm.warp_w[i]; bc += sm.warp_c[i]; }
+        const unsigned me = cl.block_rank();
+        for (int r = 0; r < kClusterCTAs; ++r) {
+            uint64_t* rw = cl.map_shared_rank(&sm.red_w[parity][me], r);
+            uint32_t* rc = cl.map_shared_rank(&sm.red_c[parity][me], r);
+            *rw = bw; *rc = bc;
+        }
+    }
+    cl.sync();
+    W = 0; Cn = 0;
+#pragma unroll
+    for (int r = 0; r < kClusterCTAs; ++r) { W += sm.red_w[parity][r]; Cn += sm.red_c[parity][r]; }
+    parity ^= 1;
+}
+
+__global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kSamplerThreads, 1)
+lss_sampler_kernel(SamplerArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SamplerSmem& sm = *reinterpret_cast<SamplerSmem*>(smem_raw);
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    const int mask_id = blockIdx.y;                      // 0: grad_W, 1: grad_X
+    const int N = a.N;
+    const int n_items = 2 * N;
+    const int per = (n_items + kClusterCTAs - 1) / kClusterCTAs;
+    const int base = rank * per;
+    const int nloc = max(0, min(per, n_items - base));
+    const int ipt = (per + kSamplerThreads - 1) / kSamplerThreads;   // items per thread
+    const int t_lo = min(nloc, int(threadIdx.x) * ipt);
+    const int t_hi = min(nloc, t_lo + ipt);
+    const int e_max = mask_id == 0 ? kEMaxW : kEMaxX;
+    const uint32_t purpose = mask_id == 0 ? kPurposeMaskW : kPurposeMaskX;
+    int parity = 0;
+
+    // ---- scores -------------------------------------------------------------
+    uint64_t sum_pos = 0; uint32_t cnt_pos = 0;
+    for (int j = t_lo; j < t_hi; ++j) {
+        const int i = base + j;
+        const int h = i >= N ? 1 : 0;
+        const int t = i - h * N;
+        uint64_t w = 0;
+        if (a.mode != 2) {                                           // I4_LSS_NONE needs no scores
+            const double av = double(__ldg(a.a_sq + i));
+            double prod = av;
+            if (mask_id == 0) prod = av * double(__ldg(a.x_sqnorm + t));    // exact: < 2^53
+            const double root = __dsqrt_rn(prod);
+            w = uint64_t(root * (h == 0 ? 1048576.0 : 65536.0));   // floor(root 2^(16+4[up]))
+        }
+        sm.w[j] = w;
+        sm.clamped[j] = 0;
+        sum_pos += w;
+        cnt_pos += (w > 0);
+    }
+    uint64_t Wall; uint32_t Z;
+    cluster_sum(cl, sm, parity, sum_pos, cnt_pos, Wall, Z);
+
+    // ---- A.2 water-filling ----------------------------------------------------
+    const uint64_t B = uint64_t(N);
+    const bool bernoulli = a.mode == 0;
+    const bool binding = bernoulli && uint64_t(Z) > B;
+    uint64_t R = B, W = Wall;
+    if (binding) {
+        uint32_t s_cnt = 0;
+        for (int round = 0; round <= n_items + 1; ++round) {
+            uint64_t wun = 0; uint32_t sc = 0;
+            for (int j = t_lo; j < t_hi; ++j) {
+                const uint64_t w = sm.w[j];
+                if (w == 0) continue;
+                if (!sm.clamped[j] && R * w >= W) sm.clamped[j] = 1;
+                if (sm.clamped[j]) sc += 1; else wun += w;
+            }
+            uint64_t Wn; uint32_t Sc;
+            cluster_sum(cl, sm, parity, wun, sc, Wn, Sc);
+            if (Sc == s_cnt) break;
+            s_cnt = Sc;
+            R = B - Sc;
+            W = Wn;
+        }
+    }
+
+    // ---- Bernoulli with dyadic weights ---------------------------------------
+    uint32_t my_keep = 0;
+    for (int j = t_lo; j < t_hi; ++j) {
+        const int i = base + j;
+        const int h = i >= N ? 1 : 0;
+        const int t = i - h * N;
+        const uint64_t w = sm.w[j];
+        int8_t out = -1;
+        if (a.mode == 2) {                 // I4_LSS_NONE: every item, weight 1
+            out = 0;
+        } else if (w > 0) {
+            if (!binding || sm.clamped[j]) {
+                out = 0;                   // p = 1 (Z-16 / clamped by A.2)
+            } else {
+                const uint64_t num = R * w;                       // R w < W
+                int e = (63 - __clzll((long long)W)) - (63 - __clzll((long long)num));
+                if ((num << e) > W) --e;
+                uint64_t T1, T2;
+                if (e >= e_max) {
+                    e = e_max;
+                    T1 = T2 = 1ull << (32 - e_max);
+                } else {
+                    T2 = uint64_t(((unsigned __int128)num << 32) / W);
+                    T1 = 2 * T2 - (1ull << (32 - e));
+                }
+                const uint64_t idx = 2ull * uint64_t(a.token_offset + t) + uint64_t(h);
+                const Philox4 p = philox4x32_10(uint32_t(idx), uint32_t(idx >> 32), purpose, a.call_id,
+                                                a.seed_lo, a.seed_hi);
+                const uint64_t u = p.x;
+                if (u < T2) out = int8_t(u < T1 ? e : e + 1);
+            }
+        }
+        sm.wexp[j] = out;
+        my_keep += (out >= 0);
+    }
+
+    // ---- compaction: block exclusive scan + cluster prefix --------------------
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t incl = my_keep;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    if (lane == 31) sm.scan[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = sm.scan[lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += n;
+        }
+        sm.scan[lane] = x - v;                 // exclusive warp offsets
+        if (lane == 31) {
+            for (int r = 0; r < kClusterCTAs; ++r)
+                *cl.map_shared_rank(&sm.cta_tot[rank], r) = x;
+        }
+    }
+    cl.sync();
+    uint32_t cta_off = 0, total = 0;
+    for (int r = 0; r < kClusterCTAs; ++r) {
+        if (r < rank) cta_off += sm.cta_tot[r];
+        total += sm.cta_tot[r];
+    }
+    uint32_t pos = cta_off + sm.scan[warp] + (incl - my_keep);
+    int32_t* items = a.items[mask_id];
+    int8_t* wexp = a.wexp[mask_id];
+    for (int j = t_lo; j < t_hi; ++j) {
+        const int8_t e = sm.wexp[j];
+        if (e >= 0) {
+            items[pos] = base + j;
+            wexp[pos] = e;
+            ++pos;
+        }
+    }
+    if (rank == 0) {
+        const uint32_t padded = (total + 127u) & ~127u;
+        for (uint32_t p = total + threadIdx.x; p < padded; p += kSamplerThreads) {
+            items[p] = n_items;                // sentinel: an all-zero row
+            wexp[p] = 0;
+        }
+        if (threadIdx.x == 0) *a.count[mask_id] = int32_t(total);
+    }
+    cl.sync();                                 // keep DSMEM alive until all remote writes landed
+}
+
+cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
+    const size_t smem = sizeof(SamplerSmem);
+    cudaError_t e = cudaFuncSetAttribute(lss_sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(kClusterCTAs, 2, 1);
+    lss_sampler_kernel<<<grid, kSamplerThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace i4

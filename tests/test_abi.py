@@ -1,0 +1,60 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU, and exports every
+symbol include/*.h declares (no compute calls: CPU only)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    names = []
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        names += re.findall(r"I4_API\s+[\w\s\*]+?\b(\w+)\s*\(", src)
+    return names
+
+
+def test_header_declares_the_boundary():
+    names = set(_declared())
+    assert {"hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd"} <= names
+    assert {"int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_last_error"} <= names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2306_11987_b200 import build
+    lib_path = build.build()
+    L = ctypes.CDLL(lib_path)
+    for name in _declared():
+        assert hasattr(L, name), name
+
+
+def test_sass_is_sm100a_tcgen05():
+    # tcgen05.mma kind::i8 shows as UTCIMMA, TMA as UTMALDG, tcgen05.ld as LDTM
+    import subprocess
+    from paper_2306_11987_b200 import build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.build()], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    for mnemonic in ("UTCIMMA", "UTMALDG", "LDTM"):
+        assert mnemonic in out, mnemonic
+
+
+def test_host_validation_without_gpu():
+    # without a device every compute entry point fails loudly with a status,
+    # never silently (no CPU fallback exists)
+    import paper_2306_11987_b200 as p
+    assert p.int4_bwd_workspace_size(128, 64, 64) > 0
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        pytest.skip("host has a GPU")
+    st = p.lib.int4_gemm_s8s8s32(None, None, 1, 64, 16, None, None)
+    assert st != 0
+    assert p.lib.int4_last_error()

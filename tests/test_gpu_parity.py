@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, stage
+by stage on identical seeded inputs (SURVEY.md §8(c) parity protocol):
+  (i)   codes   X_hat / W_hat: <= 1e-6 of codes differ, none by more than 1
+                (reading Z-7); grad_Y hi/lo planes bit-exact
+  (ii)  sampler index sets, weight exponents, counts bit-exact
+  (iii) INT32 accumulators bit-exact given identical codes
+  (iv)  Y, grad_X, grad_W within 1e-5 relative Frobenius of the oracle fed the
+        GPU's intermediates
+Tolerances are written in each test."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import bitsplit as o_bs
+from oracle import gemm as o_gemm
+from oracle import hadamard as o_had
+from oracle import hq as o_hq
+from oracle import linear as o_lin
+from oracle import lss as o_lss
+
+from gpu_helpers import code_mismatch, rel_frob, to_bf16_cuda, unpack_bits
+
+pytestmark = pytest.mark.gpu
+
+FROB_TOL = 1e-5          # north star: dequantized outputs within 1e-5 rel. Frobenius
+CODE_FRAC_TOL = 1e-6     # north star: <= 1e-6 of INT4 codes differ, by at most one level
+
+
+def p():
+    import paper_2306_11987_b200 as mod
+    return mod
+
+
+# ----------------------------------------------------------------------------- (iii)
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 256, 1024), (1000, 192, 128), (77, 512, 4096),
+                                   (129, 128, 48), (4096, 3072, 768)])
+def test_gemm_int32_bit_exact(M, N, K):
+    rng = np.random.default_rng(M * 7 + N + K)
+    a = rng.integers(-8, 8, (M, K), dtype=np.int8)
+    b = rng.integers(-128, 128, (N, K), dtype=np.int8)
+    b[:, :K // 2] = np.clip(b[:, :K // 2], -112, 112)
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    acc = torch.full((M, N), -1, dtype=torch.int32, device="cuda")
+    p().int4_gemm_s8s8s32(A, B, acc)
+    torch.cuda.synchronize()
+    ref = o_gemm.int_matmul_abt(a, b)
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
+
+
+# ----------------------------------------------------------------------------- (i)
+@pytest.mark.parametrize("k", list(range(0, 8)))
+@pytest.mark.parametrize("rows,cols", [(200, 256), (64, 1024)])
+def test_hadamard_quant_codes(k, rows, cols):
+    x = synth.activations(rows, cols, seed=k)
+    s = synth.cold_start_step(x)
+    X = to_bf16_cuda(x)
+    codes = torch.empty(rows, cols, dtype=torch.int8, device="cuda")
+    bits = torch.empty(rows, cols // 32, dtype=torch.int32, device="cuda")
+    sq = torch.empty(rows, dtype=torch.int32, device="cuda")
+    p().hadamard_quant(X, k, s, codes, bits, sq)
+    torch.cuda.synchronize()
+    oc, om, osq = o_hq.hadamard_quant(x, k, s)
+    gc = codes.cpu().numpy()
+    nbad, maxdiff = code_mismatch(gc, oc)
+    assert maxdiff <= 1 and nbad <= max(CODE_FRAC_TOL * oc.size, 0)
+    gm = unpack_bits(bits, cols)
+    if nbad == 0:
+        assert np.array_equal(gm, om)
+        assert np.array_equal(sq.cpu().numpy(), osq)
+    else:
+        assert (gm != om).sum() <= nbad
+
+
+def test_hadamard_quant_no_fma_contraction_at_ties():
+    # exact .5 ties must round half-to-even identically (Z-1): x chosen so that
+    # v = t r is exactly j + 0.5 for a power-of-two r
+    k = 2
+    s = 0.25                         # r = 2^-1 / 0.25 = 2
+    x = np.zeros((4, 64), dtype=np.float32)
+    x[:, 0] = np.array([0.75, 1.25, -0.75, 3.25], dtype=np.float32)   # v = 1.5, 2.5, -1.5, 6.5
+    X = to_bf16_cuda(x)
+    codes = torch.empty(4, 64, dtype=torch.int8, device="cuda")
+    p().hadamard_quant(X, k, s, codes)
+    oc, _, _ = o_hq.hadamard_quant(x, k, s)
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    assert codes.cpu().numpy()[:, 0].tolist() == [2, 2, -2, 6]
+
+
+# ----------------------------------------------------------------------------- forward
+def _run_forward(N, D, C, k, y_dtype=torch.float32, seed=0):
+    x = synth.activations(N, D, seed=seed)
+    w = synth.weights(C, D, seed=seed)
+    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    layer = p().Int4Linear(N, D, C, k)
+    Y = torch.empty(N, C, dtype=y_dtype, device="cuda")
+    layer.forward(to_bf16_cuda(x), to_bf16_cuda(w), s_x, s_w, Y)
+    torch.cuda.synchronize()
+    return x, w, s_x, s_w, layer, Y
+
+
+@pytest.mark.parametrize("N,D,C,k", [(128, 64, 64, 4), (333, 256, 192, 5), (512, 768, 3072, 5), (256, 1024, 128, 7),
+                                     (130, 128, 256, 0)])
+def test_forward_parity(N, D, C, k):
+    x, w, s_x, s_w, layer, Y = _run_forward(N, D, C, k)
+    f = o_lin.forward(x, w, k, s_x, s_w)
+    gx, gw = layer.xq.cpu().numpy(), layer.wq.cpu().numpy()
+    for g, o in ((gx, f["xq"]), (gw, f["wq"])):
+        nbad, maxdiff = code_mismatch(g, o)
+        assert maxdiff <= 1 and nbad <= CODE_FRAC_TOL * o.size
+    assert np.array_equal(layer.wqT.cpu().numpy(), gw.T)
+    # (iii)+(iv): Y from the GPU codes, exact int acc then fp32 scale
+    acc = o_gemm.int_matmul_abt(gx, gw)
+    y_ref = acc.astype(np.float64) * (np.float64(np.float32(s_x)) * np.float64(np.float32(s_w)))
+    y = Y.cpu().numpy()
+    assert rel_frob(y, y_ref) < FROB_TOL
+    assert np.array_equal(y, (acc.astype(np.float32) * np.float32(np.float32(s_x) * np.float32(s_w))))
+    if np.array_equal(gx, f["xq"]) and np.array_equal(gw, f["wq"]):
+        assert rel_frob(y, f["y"]) < FROB_TOL                                # (v) end to end
+
+
+def test_forward_bf16_output():
+    x, w, s_x, s_w, layer, Y = _run_forward(256, 512, 512, 5, torch.bfloat16)
+    acc = o_gemm.int_matmul_abt(layer.xq.cpu().numpy(), layer.wq.cpu().numpy())
+    y_ref = acc * (np.float64(s_x) * np.float64(s_w))
+    assert rel_frob(Y.float().cpu().numpy(), y_ref) < 4e-3          # bf16 output rounding (2^-9)
+
+
+# ----------------------------------------------------------------------------- backward
+def _bwd_case(N, D, C, k, dense=False, mode=0, seed=0, call_id=3, token_offset=0, g=None):
+    x, w, s_x, s_w, layer, Y = _run_forward(N, D, C, k, seed=seed)
+    if g is None:
+        g = synth.grad_output(N, C, seed=seed, dense=dense)
+    dX = torch.empty(N, D, dtype=torch.float32, device="cuda")
+    dW = torch.empty(C, D, dtype=torch.float32, device="cuda")
+    layer.backward(to_bf16_cuda(g), dX, dW, synth.PHILOX_SEED, call_id, token_offset, mode)
+    torch.cuda.synchronize()
+    return x, w, s_x, s_w, layer, g, dX.cpu().numpy(), dW.cpu().numpy()
+
+
+def _oracle_from_gpu_codes(layer, s_x, s_w, k):
+    return dict(xq=layer.xq.cpu().numpy(), wq=layer.wq.cpu().numpy(),
+                x_mask=unpack_bits(layer.x_mask, layer.D), w_mask=unpack_bits(layer.w_mask, layer.D),
+                x_sq=layer.x_sqnorm.cpu().numpy().astype(np.int64), k=k,
+                s_x=np.float32(s_x), s_w=np.float32(s_w))
+
+
+def _check_backward(layer, g, s_x, s_w, k, dX, dW, mode, call_id=3, token_offset=0):
+    fwd = _oracle_from_gpu_codes(layer, s_x, s_w, k)
+    N, C = g.shape
+    # (i) bit split: bit-exact planes and norms
+    bs = o_bs.bit_split(g, synth.PHILOX_SEED, call_id, token_offset)
+    hilo = layer.hilo.cpu().numpy()
+    assert np.array_equal(hilo[:N], bs["hi"]) and np.array_equal(hilo[N:], bs["lo"])
+    assert np.array_equal(layer.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
+    assert layer.s_down().cpu().numpy()[0] == bs["s_down"]
+    assert np.array_equal(fwd["x_sq"], (fwd["xq"].astype(np.int64) ** 2).sum(1))
+    # (ii) sampler: index sets, weight exponents, counts bit-exact
+    mw = o_lss.sample_weight_mask(bs["a_sq"], fwd["x_sq"], synth.PHILOX_SEED, call_id, token_offset, mode)
+    mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, call_id, token_offset, mode)
+    cw, cx = [int(v) for v in layer.counts().cpu().numpy()]
+    assert cw == mw["count"] and cx == mx["count"]
+    assert np.array_equal(layer.items_w.cpu().numpy()[:cw], mw["items"])
+    assert np.array_equal(layer.wexp_w.cpu().numpy()[:cw], mw["wexp"])
+    assert np.array_equal(layer.items_x.cpu().numpy()[:cx], mx["items"])
+    assert np.array_equal(layer.wexp_x.cpu().numpy()[:cx], mx["wexp"])
+    pad_w = layer.items_w.cpu().numpy()[cw:(cw + 127) // 128 * 128]
+    assert np.all(pad_w == 2 * N)
+    # (iv) outputs from identical codes and lists
+    dx_ref, _ = o_lin.grad_x_from_items(bs, mx["items"], mx["wexp"], fwd["wq"], fwd["x_mask"], k, fwd["s_w"])
+    dw_ref, _ = o_lin.grad_w_from_items(bs, mw["items"], mw["wexp"], fwd["xq"], fwd["w_mask"], k, fwd["s_x"])
+    assert rel_frob(dX, dx_ref) < FROB_TOL
+    assert rel_frob(dW, dw_ref) < FROB_TOL
+    return mw, mx
+
+
+@pytest.mark.parametrize("mode", [o_lss.MODE_BERNOULLI, o_lss.MODE_KEEP_POSITIVE, o_lss.MODE_NONE])
+@pytest.mark.parametrize("dense", [False, True])
+def test_backward_parity_cfg1(mode, dense):
+    N, D, C, k = 128, 64, 64, 4                                     # BASELINE configs[0]
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=dense, mode=mode)
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, mode)
+
+
+@pytest.mark.parametrize("N,D,C,k,dense", [(333, 256, 192, 5, True), (1000, 512, 768, 5, False),
+                                           (512, 256, 512, 7, True), (256, 128, 256, 6, False),
+                                           (640, 192, 320, 3, True)])
+def test_backward_parity_shapes(N, D, C, k, dense):
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=dense, token_offset=17)
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, o_lss.MODE_BERNOULLI, token_offset=17)
+
+
+def test_backward_degenerate_zero_and_single_row():
+    N, D, C, k = 256, 128, 128, 5
+    g = np.zeros((N, C), dtype=np.float32)
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, g=g)
+    assert not dX.any() and not dW.any()
+    assert layer.counts().cpu().numpy().tolist() == [0, 0]
+    g = np.zeros((N, C), dtype=np.float32)
+    g[37] = synth.grad_output(1, C, dense=True)[0]
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, g=g)
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, o_lss.MODE_BERNOULLI)
+    assert not np.delete(dX, 37, axis=0).any()
+
+
+def test_backward_deterministic_bytes():
+    N, D, C, k = 512, 256, 512, 5
+    runs = [_bwd_case(N, D, C, k, dense=True) for _ in range(2)]
+    assert np.array_equal(runs[0][6], runs[1][6]) and np.array_equal(runs[0][7], runs[1][7])
+
+
+def test_shard_invariance_of_random_streams():
+    # Z-20: token t of a shard starting at token_offset draws the same Philox
+    # words as global token token_offset + t: the hi/lo planes of the second
+    # half of a batch equal those of the full batch computed with offset 0.
+    N, D, C, k = 256, 128, 128, 5
+    g = synth.grad_output(N, C, dense=True)
+    g[0, 0] = np.abs(g).max() * 2          # same amax in both halves' runs below
+    g_half = g[N // 2:].copy()
+    g_half[0, 0] = g[0, 0]
+    _, _, _, _, full, _, _, _ = _bwd_case(N, D, C, k, g=g)
+    _, _, _, _, half, _, _, _ = _bwd_case(N // 2, D, C, k, g=g_half, token_offset=N // 2)
+    hf = full.hilo.cpu().numpy()
+    hh = half.hilo.cpu().numpy()
+    assert np.array_equal(hf[N // 2 + 1:N], hh[1:N // 2])
+    assert np.array_equal(hf[N + N // 2 + 1:], hh[N // 2 + 1:])
+
+
+def test_api_errors_are_loud():
+    mod = p()
+    X = torch.zeros(128, 96, dtype=torch.bfloat16, device="cuda")
+    codes = torch.empty(128, 96, dtype=torch.int8, device="cuda")
+    with pytest.raises(mod.I4Error):
+        mod.hadamard_quant(X, 6, 0.1, codes)            # 96 % 64 != 0 -> I4_ERR_SHAPE
+    with pytest.raises(mod.I4Error):
+        mod.hadamard_quant(X[:, :64].contiguous(), 2, -1.0, codes)   # negative step -> I4_ERR_ARG
+
+
+# ----------------------------------------------------------------------------- full size
+@pytest.mark.parametrize("cfg", ["cfg3_bert_large_ffn_up", "cfg2_bert_base_ffn1"])
+def test_full_size_sampled_parity(cfg):
+    """BASELINE configs at full size in the bench's launch configuration: codes
+    and sampler lists in full, outputs on sampled rows the oracle computes one
+    by one from the GPU's intermediates."""
+    c = synth.CONFIGS[cfg]
+    N, D, C, k = c["N"], c["D"], c["C"], c["k"]
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=False)
+    xq, wq = layer.xq.cpu().numpy(), layer.wq.cpu().numpy()
+    rows = np.random.default_rng(1).choice(N, 64, replace=False)
+    # codes: sampled rows exactly vs oracle
+    oc, om, osq = o_hq.hadamard_quant(x[rows], k, s_x)
+    nbad, maxdiff = code_mismatch(xq[rows], oc)
+    assert maxdiff <= 1 and nbad <= CODE_FRAC_TOL * xq.size
+    # forward rows
+    Y = torch.empty(N, C, dtype=torch.float32, device="cuda")
+    layer.forward(to_bf16_cuda(x), to_bf16_cuda(w), s_x, s_w, Y, reuse_weight=True)
+    acc = o_gemm.int_matmul_abt(xq[rows], wq)
+    y_ref = acc * (np.float64(s_x) * np.float64(s_w))
+    assert rel_frob(Y.cpu().numpy()[rows], y_ref) < FROB_TOL
+    # backward: full sampler parity, outputs on sampled tokens / channels
+    bs = o_bs.bit_split(g, synth.PHILOX_SEED, 3, 0)
+    hilo = layer.hilo.cpu().numpy()
+    assert np.array_equal(hilo[:N], bs["hi"]) and np.array_equal(hilo[N:], bs["lo"])
+    x_sq = layer.x_sqnorm.cpu().numpy().astype(np.int64)
+    mw = o_lss.sample_weight_mask(bs["a_sq"], x_sq, synth.PHILOX_SEED, 3, 0)
+    mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 3, 0)
+    cw, cx = [int(v) for v in layer.counts().cpu().numpy()]
+    assert (cw, cx) == (mw["count"], mx["count"])
+    assert np.array_equal(layer.items_w.cpu().numpy()[:cw], mw["items"])
+    assert np.array_equal(layer.items_x.cpu().numpy()[:cx], mx["items"])
+    x_mask = unpack_bits(layer.x_mask, D)
+    w_mask = unpack_bits(layer.w_mask, D)
+    # grad_X rows of sampled tokens
+    sel = np.isin(mx["items"] % N, rows)
+    dx_ref, _ = o_lin.grad_x_from_items(bs, mx["items"][sel], mx["wexp"][sel], wq, x_mask, k, np.float32(s_w))
+    assert rel_frob(dX[rows], dx_ref[rows]) < FROB_TOL
+    # grad_W rows of sampled channels
+    ch = np.random.default_rng(2).choice(C, 32, replace=False)
+    bs_c = dict(bs, hi=bs["hi"][:, ch], lo=bs["lo"][:, ch])
+    dw_ref, _ = o_lin.grad_w_from_items(bs_c, mw["items"], mw["wexp"], xq, w_mask[ch], k, np.float32(s_x))
+    assert rel_frob(dW[ch], dw_ref) < FROB_TOL
