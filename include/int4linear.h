@@ -168,6 +168,16 @@ I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
 I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, const int8_t* B, int64_t M, int64_t Nn, int64_t K,
                             int32_t* acc, void* stream);
 
+/* Measurement hook (used by bench.py).  int4_trace_begin arms tracing on the
+ * calling thread with `capacity` caller-created cudaEvent_t handles (passed as
+ * void*): events[0] is recorded on the launch stream before the library's next
+ * launch and events[i+1] right after its i-th launch (a kernel or a memset), so
+ * consecutive events bracket each launch.  int4_trace_end disarms tracing,
+ * writes the static launch names into names[0..n) and returns n.  At most
+ * capacity - 1 launches are recorded; the events stay caller-owned. */
+I4_API i4_status int4_trace_begin(void* const* events, int32_t capacity);
+I4_API int32_t int4_trace_end(const char** names, int32_t capacity);
+
 /* Thread-local message describing the last non-OK status of this thread. */
 I4_API const char* int4_last_error(void);
 

@@ -18,7 +18,7 @@ __all__ = [
     "LIB_PATH", "lib", "I4Error", "I4FwdCache", "I4LssPlan",
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
-    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "Int4Linear",
+    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "Int4Linear", "LaunchTrace",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
@@ -72,6 +72,10 @@ def _load():
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
     L.int4_last_error.argtypes = []
     L.int4_last_error.restype = ctypes.c_char_p
+    L.int4_trace_begin.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32]
+    L.int4_trace_begin.restype = ctypes.c_int
+    L.int4_trace_end.argtypes = [ctypes.POINTER(ctypes.c_char_p), i32]
+    L.int4_trace_end.restype = i32
     return L
 
 
@@ -134,6 +138,35 @@ def int4_gemm_s8s8s32(A, B, acc, stream=None):
     M, K = A.shape
     Nn = B.shape[0]
     _check(lib.int4_gemm_s8s8s32(_ptr(A), _ptr(B), M, Nn, K, _ptr(acc), _stream(stream)))
+
+
+class LaunchTrace:
+    """Context manager around the library's launch-tracing hook: the events
+    (torch.cuda.Event, enable_timing) bracket every launch the library makes
+    on its stream while the context is open (including inside a CUDA graph
+    capture, where the records become graph nodes)."""
+
+    def __init__(self, events):
+        import torch
+        self.events = events
+        for e in events:                           # force lazy creation of the handles
+            e.record(torch.cuda.current_stream())
+        self.handles = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+        self.names = []
+
+    def __enter__(self):
+        _check(lib.int4_trace_begin(self.handles, len(self.events)))
+        return self
+
+    def __exit__(self, *exc):
+        buf = (ctypes.c_char_p * len(self.events))()
+        n = lib.int4_trace_end(buf, len(self.events))
+        self.names = [buf[i].decode() for i in range(n)]
+        return False
+
+    def durations_ms(self):
+        """[(name, ms)] of the recorded launches (events must have completed)."""
+        return [(nm, self.events[i].elapsed_time(self.events[i + 1])) for i, nm in enumerate(self.names)]
 
 
 class Int4Linear:

@@ -40,6 +40,41 @@ i4_status cuda_fail(cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(e_, where); \
     } while (0)
 
+// Launch tracing (int4_trace_begin / int4_trace_end): caller-owned events are
+// recorded on the launch stream around every kernel the library enqueues.
+constexpr int kMaxTrace = 64;
+struct TraceState {
+    bool active = false;
+    bool started = false;
+    cudaEvent_t ev[kMaxTrace + 1];
+    int cap = 0;
+    int n = 0;
+    const char* names[kMaxTrace];
+};
+thread_local TraceState g_trace;
+
+void trace_pre(cudaStream_t s) {
+    if (g_trace.active && !g_trace.started && g_trace.cap > 0) {
+        cudaEventRecordWithFlags(g_trace.ev[0], s, cudaEventRecordExternal);   // a graph node under capture
+        g_trace.started = true;
+    }
+}
+void trace_post(const char* name, cudaStream_t s) {
+    if (g_trace.active && g_trace.n + 1 < g_trace.cap) {
+        cudaEventRecordWithFlags(g_trace.ev[g_trace.n + 1], s, cudaEventRecordExternal);
+        g_trace.names[g_trace.n++] = name;
+    }
+}
+
+// Every kernel launch of the library goes through this macro.
+#define I4_LAUNCH(expr, name, stream)                       \
+    do {                                                    \
+        trace_pre(stream);                                  \
+        cudaError_t e_ = (expr);                            \
+        if (e_ != cudaSuccess) return cuda_fail(e_, name);  \
+        trace_post(name, stream);                           \
+    } while (0)
+
 struct DeviceInfo {
     bool ok = false;
     int sms = 0;
@@ -133,7 +168,8 @@ i4_status gemm(const int8_t* A, int64_t a_rows, int64_t a_pitch, const int8_t* B
     if (!make_tmap_i8(&ta, A, uint64_t(K), uint64_t(a_rows), uint64_t(a_pitch), 128) ||
         !make_tmap_i8(&tb, B, uint64_t(K), uint64_t(b_rows), uint64_t(b_pitch), uint32_t(bn)))
         return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    I4_CHECK_CUDA(i4::launch_gemm(&ta, &tb, args, device_info().sms, s), "gemm launch");
+    static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
+    I4_LAUNCH(i4::launch_gemm(&ta, &tb, args, device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
 
@@ -143,6 +179,24 @@ extern "C" {
 
 const char* int4_last_error(void) { return g_last_error.c_str(); }
 
+i4_status int4_trace_begin(void* const* events, int32_t capacity) {
+    if (!events || capacity < 2 || capacity > kMaxTrace + 1) return fail(I4_ERR_ARG, "int4_trace_begin: 2 <= capacity <= %d", kMaxTrace + 1);
+    for (int i = 0; i < capacity; ++i) g_trace.ev[i] = static_cast<cudaEvent_t>(events[i]);
+    g_trace.cap = capacity;
+    g_trace.n = 0;
+    g_trace.started = false;
+    g_trace.active = true;
+    return I4_OK;
+}
+
+int32_t int4_trace_end(const char** names, int32_t capacity) {
+    const int n = g_trace.n;
+    for (int i = 0; i < n && i < capacity; ++i) names[i] = g_trace.names[i];
+    g_trace.active = false;
+    g_trace.cap = 0;
+    return n;
+}
+
 i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t k, float step, int8_t* codes,
                          uint32_t* clamp_bits, int32_t* row_sqnorm, void* stream) {
     I4_RETURN_IF(check_device());
@@ -151,9 +205,10 @@ i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t
     I4_RETURN_IF(check_k(k, cols));
     I4_RETURN_IF(check_step(step, "step"));
     if (!aligned16(x_bf16) || !aligned16(codes)) return fail(I4_ERR_ALIGN, "hadamard_quant: pointers must be 16-byte aligned");
-    I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(x_bf16), rows, cols, k, step_recip(k, step),
-                                            codes, clamp_bits, row_sqnorm, static_cast<cudaStream_t>(stream)),
-                  "hadamard_quant");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(x_bf16), rows, cols, k, step_recip(k, step),
+                                        codes, clamp_bits, row_sqnorm, s),
+              "hadamard_quant", s);
     return I4_OK;
 }
 
@@ -174,12 +229,12 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     if (!aligned16(X) || !aligned16(W) || !aligned16(Y)) return fail(I4_ERR_ALIGN, "int4_linear_fwd: unaligned pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
-    I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(X), N, D, k, step_recip(k, s_x), cache->xq,
-                                            cache->x_mask, cache->x_sqnorm, s), "hadamard_quant(X)");
+    I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(X), N, D, k, step_recip(k, s_x), cache->xq,
+                                        cache->x_mask, cache->x_sqnorm, s), "hadamard_quant_x", s);
     if (!cache->w_valid) {
-        I4_CHECK_CUDA(i4::launch_hadamard_quant(static_cast<const uint16_t*>(W), C, D, k, step_recip(k, s_w), cache->wq,
-                                                cache->w_mask, nullptr, s), "hadamard_quant(W)");
-        I4_CHECK_CUDA(i4::launch_transpose_i8(cache->wq, C, D, cache->wqT, s), "transpose(W_hat)");
+        I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(W), C, D, k, step_recip(k, s_w), cache->wq,
+                                            cache->w_mask, nullptr, s), "hadamard_quant_w", s);
+        I4_LAUNCH(i4::launch_transpose_i8(cache->wq, C, D, cache->wqT, s), "transpose_w", s);
     }
     i4::GemmArgs g{};
     g.M = int32_t(N); g.Nn = int32_t(C); g.K = int32_t(D);
@@ -208,9 +263,9 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
     if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
     if (!aligned16(dY) || !aligned16(plan->hilo)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    I4_CHECK_CUDA(i4::launch_amax_bf16(static_cast<const uint16_t*>(dY), N * C, plan->amax_bits, s), "amax");
-    I4_CHECK_CUDA(i4::launch_bitsplit(static_cast<const uint16_t*>(dY), N, C, plan->amax_bits, seed, call_id,
-                                      token_offset, plan->hilo, plan->a_sq, plan->s_down, s), "bitsplit");
+    I4_LAUNCH(i4::launch_amax_bf16(static_cast<const uint16_t*>(dY), N * C, plan->amax_bits, s), "amax", s);
+    I4_LAUNCH(i4::launch_bitsplit(static_cast<const uint16_t*>(dY), N, C, plan->amax_bits, seed, call_id,
+                                  token_offset, plan->hilo, plan->a_sq, plan->s_down, s), "bitsplit", s);
     i4::SamplerArgs a{};
     a.a_sq = plan->a_sq;
     a.x_sqnorm = x_sqnorm;
@@ -222,7 +277,7 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
     a.token_offset = token_offset;
     a.items[0] = plan->items_w; a.wexp[0] = plan->wexp_w; a.count[0] = plan->count_w;
     a.items[1] = plan->items_x; a.wexp[1] = plan->wexp_x; a.count[1] = plan->count_x;
-    I4_CHECK_CUDA(i4::launch_lss_sampler(a, s), "lss_sampler");
+    I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
     return I4_OK;
 }
 
@@ -253,11 +308,11 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     int8_t* a_wt = a_x + round_up((2 * N + 128) * C, 256);
     int8_t* b_wt = a_wt + round_up(C * kcap, 256);
 
-    I4_CHECK_CUDA(i4::launch_compact_rows(plan->hilo, C, plan->items_x, plan->count_x, 2 * N, a_x, s), "compact_rows");
-    I4_CHECK_CUDA(i4::launch_compact_wgrad(plan->hilo, cache->xq, N, C, D, plan->items_w, plan->wexp_w, plan->count_w,
-                                           kcap, a_wt, b_wt, s), "compact_wgrad");
+    I4_LAUNCH(i4::launch_compact_rows(plan->hilo, C, plan->items_x, plan->count_x, 2 * N, a_x, s), "compact_rows", s);
+    I4_LAUNCH(i4::launch_compact_wgrad(plan->hilo, cache->xq, N, C, D, plan->items_w, plan->wexp_w, plan->count_w,
+                                       kcap, a_wt, b_wt, s), "compact_wgrad", s);
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
-    I4_CHECK_CUDA(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset dX");
+    I4_LAUNCH(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset_dx", s);
     {
         i4::GemmArgs g{};
         g.M = int32_t(2 * N + 128); g.m_dev = plan->count_x;
