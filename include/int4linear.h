@@ -71,19 +71,18 @@ typedef enum {
  * in forward propagation").  Written by int4_linear_fwd, read by
  * int4_linear_bwd.  Device buffers, caller-allocated:
  *   xq       int8  [N, D]      X_hat = <XH>_{s_X}
- *   wq       int8  [C, D]      W_hat = <WH>_{s_W}
- *   wqT      int8  [D, C]      W_hat transposed (K-major B operand of grad_X)
+ *   wq       int8  [C, D]      W_hat = <WH>_{s_W} (read K-major by the forward GEMM and
+ *                              MN-major by the grad_X GEMM: never transposed in memory)
  *   x_mask   uint32 [N, D/32]  I_X (on XH / s_X, reading Z-8)
  *   w_mask   uint32 [C, D/32]  I_W
  *   x_sqnorm int32 [N]         sum_d X_hat[t, d]^2 (leverage scores)
  * Host scalars: N, D, C, k, s_x, s_w are filled by int4_linear_fwd.  Set
- * w_valid = 1 to reuse wq / wqT / w_mask from a previous call with the same W
+ * w_valid = 1 to reuse wq / w_mask from a previous call with the same W
  * and s_w (one weight quantization per weight version); the library never
  * changes w_valid. */
 typedef struct {
     int8_t* xq;
     int8_t* wq;
-    int8_t* wqT;
     uint32_t* x_mask;
     uint32_t* w_mask;
     int32_t* x_sqnorm;
@@ -161,12 +160,13 @@ I4_API i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
 
-/* Exact INT8 x INT8 -> INT32 product acc = A B^T on the tcgen05 path used by
- * every GEMM of the operator ("Multiply the two INT4 matrices").
- * A [M, K] int8, B [Nn, K] int8, acc [M, Nn] int32; K % 16 == 0, Nn % 64 == 0.
+/* Exact INT8 x INT8 -> INT32 product acc[m, n] = sum_k A(m, k) B(n, k) on the
+ * tcgen05 path used by every GEMM of the operator ("Multiply the
+ * two INT4 matrices").  A is [M, K] (a_mn_major = 0) or [K, M] (a_mn_major = 1);
+ * B is [Nn, K] or [K, Nn]; acc [M, Nn] int32.  K % 16 == 0, Nn % 64 == 0.
  * Exposed for the bit-exact accumulator parity check. */
-I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, const int8_t* B, int64_t M, int64_t Nn, int64_t K,
-                            int32_t* acc, void* stream);
+I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B, int32_t b_mn_major, int64_t M,
+                                   int64_t Nn, int64_t K, int32_t* acc, void* stream);
 
 /* Measurement hook (used by bench.py).  int4_trace_begin arms tracing on the
  * calling thread with `capacity` caller-created cudaEvent_t handles (passed as

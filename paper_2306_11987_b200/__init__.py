@@ -36,7 +36,7 @@ class I4Error(RuntimeError):
 
 
 class I4FwdCache(ctypes.Structure):
-    _fields_ = [("xq", ctypes.c_void_p), ("wq", ctypes.c_void_p), ("wqT", ctypes.c_void_p),
+    _fields_ = [("xq", ctypes.c_void_p), ("wq", ctypes.c_void_p),
                 ("x_mask", ctypes.c_void_p), ("w_mask", ctypes.c_void_p), ("x_sqnorm", ctypes.c_void_p),
                 ("N", ctypes.c_int64), ("D", ctypes.c_int64), ("C", ctypes.c_int64),
                 ("k", ctypes.c_int32), ("s_x", ctypes.c_float), ("s_w", ctypes.c_float),
@@ -62,7 +62,7 @@ def _load():
         "bitsplit_lss": [vp, i64, i64, vp, u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp],
         "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, vp,
                             vp, ctypes.c_size_t, vp],
-        "int4_gemm_s8s8s32": [vp, vp, i64, i64, i64, vp, vp],
+        "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -133,11 +133,13 @@ def int4_bwd_workspace_size(N, D, C):
     return int(lib.int4_bwd_workspace_size(N, D, C))
 
 
-def int4_gemm_s8s8s32(A, B, acc, stream=None):
-    """acc = A B^T, int8 x int8 -> int32 on tcgen05."""
-    M, K = A.shape
-    Nn = B.shape[0]
-    _check(lib.int4_gemm_s8s8s32(_ptr(A), _ptr(B), M, Nn, K, _ptr(acc), _stream(stream)))
+def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, stream=None):
+    """acc[m, n] = sum_k A(m, k) B(n, k), int8 x int8 -> int32 on tcgen05.
+    A is [M, K] or, if a_mn_major, [K, M]; B is [Nn, K] or, if b_mn_major, [K, Nn]."""
+    M, Nn = acc.shape
+    K = A.shape[0] if a_mn_major else A.shape[1]
+    _check(lib.int4_gemm_s8s8s32(_ptr(A), int(a_mn_major), _ptr(B), int(b_mn_major), M, Nn, K, _ptr(acc),
+                                 _stream(stream)))
 
 
 class LaunchTrace:
@@ -183,11 +185,10 @@ class Int4Linear:
         i8, i32, f32 = torch.int8, torch.int32, torch.float32
         self.xq = torch.empty(N, D, dtype=i8, device=dev)
         self.wq = torch.empty(C, D, dtype=i8, device=dev)
-        self.wqT = torch.empty(D, C, dtype=i8, device=dev)
         self.x_mask = torch.empty(N, D // 32, dtype=i32, device=dev)
         self.w_mask = torch.empty(C, D // 32, dtype=i32, device=dev)
         self.x_sqnorm = torch.empty(N, dtype=i32, device=dev)
-        self.cache = I4FwdCache(xq=self.xq.data_ptr(), wq=self.wq.data_ptr(), wqT=self.wqT.data_ptr(),
+        self.cache = I4FwdCache(xq=self.xq.data_ptr(), wq=self.wq.data_ptr(),
                                 x_mask=self.x_mask.data_ptr(), w_mask=self.w_mask.data_ptr(),
                                 x_sqnorm=self.x_sqnorm.data_ptr(), w_valid=0)
         n2 = 2 * N + 128

@@ -119,7 +119,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D int8 tensor [rows, inner] with row pitch `pitch` bytes; box = 128 B x box_rows,
-// 128-byte swizzle (matches the UMMA K-major SWIZZLE_128B descriptor).
+// 128-byte swizzle (matches the UMMA SWIZZLE_128B descriptors, K- or MN-major).
 bool make_tmap_i8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t pitch, uint32_t box_rows) {
     auto fn = encode_fn();
     if (!fn) return false;
@@ -130,6 +130,23 @@ bool make_tmap_i8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Output tensor [rows, cols] of 4-byte (int32 / fp32) or 2-byte (bf16) elements;
+// box = 128 bytes x 32 rows (one epilogue warp's staging tile), 128-byte swizzle.
+bool make_tmap_out(CUtensorMap* m, void* ptr, bool bf16, bool is_int, uint64_t cols, uint64_t rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const uint32_t esz = bf16 ? 2 : 4;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * esz};
+    cuuint32_t box[2] = {128 / esz, 32};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                        : (is_int ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+    CUresult r = fn(m, dt, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -161,15 +178,23 @@ constexpr int64_t kMaxBwdTokens = 65536;
 
 #define I4_RETURN_IF(st) do { i4_status s_ = (st); if (s_ != I4_OK) return s_; } while (0)
 
-i4_status gemm(const int8_t* A, int64_t a_rows, int64_t a_pitch, const int8_t* B, int64_t b_rows, int64_t b_pitch,
-               int64_t K, const i4::GemmArgs& args, cudaStream_t s) {
-    CUtensorMap ta, tb;
-    const int bn = i4::gemm_block_n(args.Nn);
-    if (!make_tmap_i8(&ta, A, uint64_t(K), uint64_t(a_rows), uint64_t(a_pitch), 128) ||
-        !make_tmap_i8(&tb, B, uint64_t(K), uint64_t(b_rows), uint64_t(b_pitch), uint32_t(bn)))
-        return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+// One operand of a GEMM: `rows` x `inner` int8 with row pitch `pitch` bytes.
+// K-major: rows = M (or Nn), inner = K.  MN-major: rows = K, inner = M (or Nn).
+struct Operand { const int8_t* p; int64_t rows, inner, pitch; };
+
+i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s) {
+    CUtensorMap ta, tb, tc;
+    const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
+    bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), 128) &&
+              make_tmap_i8(&tb, B.p, uint64_t(B.inner), uint64_t(B.rows), uint64_t(B.pitch),
+                           args.b_mn ? 128u : uint32_t(bn));
+    if (args.epi == i4::EPI_DGRAD) tc = ta;                 // grad_X is written with red.add, no map
+    else ok = ok && make_tmap_out(&tc, args.out, args.out_bf16 != 0, args.epi == i4::EPI_INT32,
+                                  uint64_t(args.Nn), uint64_t(args.M));
+    if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
-    I4_LAUNCH(i4::launch_gemm(&ta, &tb, args, device_info().sms, s), kNames[args.epi], s);
+    const i4::GemmMaps maps{&ta, &tb, &tc};
+    I4_LAUNCH(i4::launch_gemm(maps, args, device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
 
@@ -215,7 +240,7 @@ i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t
 i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, int64_t C, int32_t k, float s_x,
                           float s_w, void* Y, i4_out_dtype y_dtype, i4_fwd_cache* cache, void* stream) {
     I4_RETURN_IF(check_device());
-    if (!X || !W || !Y || !cache || !cache->xq || !cache->wq || !cache->wqT || !cache->x_mask || !cache->w_mask ||
+    if (!X || !W || !Y || !cache || !cache->xq || !cache->wq || !cache->x_mask || !cache->w_mask ||
         !cache->x_sqnorm)
         return fail(I4_ERR_ARG, "int4_linear_fwd: NULL pointer");
     if (N <= 0 || D <= 0 || C <= 0 || D % 64 || C % 64)
@@ -234,7 +259,6 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     if (!cache->w_valid) {
         I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(W), C, D, k, step_recip(k, s_w), cache->wq,
                                             cache->w_mask, nullptr, s), "hadamard_quant_w", s);
-        I4_LAUNCH(i4::launch_transpose_i8(cache->wq, C, D, cache->wqT, s), "transpose_w", s);
     }
     i4::GemmArgs g{};
     g.M = int32_t(N); g.Nn = int32_t(C); g.K = int32_t(D);
@@ -242,7 +266,7 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     g.out = Y;
     g.out_bf16 = y_dtype == I4_OUT_BF16;
     g.scale = s_x * s_w;                      // fl32(s_x s_w), reading Z-22
-    I4_RETURN_IF(gemm(cache->xq, N, D, cache->wq, C, D, D, g, s));
+    I4_RETURN_IF(gemm(Operand{cache->xq, N, D, D}, Operand{cache->wq, C, D, D}, g, s));
     cache->N = N; cache->D = D; cache->C = C; cache->k = k; cache->s_x = s_x; cache->s_w = s_w;
     return I4_OK;
 }
@@ -305,12 +329,12 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
 
     const int64_t kcap = round_up(2 * N, 128);
     int8_t* a_x = static_cast<int8_t*>(ws);
-    int8_t* a_wt = a_x + round_up((2 * N + 128) * C, 256);
-    int8_t* b_wt = a_wt + round_up(C * kcap, 256);
+    int8_t* a_w = a_x + round_up((2 * N + 128) * C, 256);
+    int8_t* b_w = a_w + round_up(C * kcap, 256);
 
     I4_LAUNCH(i4::launch_compact_rows(plan->hilo, C, plan->items_x, plan->count_x, 2 * N, a_x, s), "compact_rows", s);
     I4_LAUNCH(i4::launch_compact_wgrad(plan->hilo, cache->xq, N, C, D, plan->items_w, plan->wexp_w, plan->count_w,
-                                       kcap, a_wt, b_wt, s), "compact_wgrad", s);
+                                       kcap, a_w, b_w, s), "compact_wgrad", s);
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
     I4_LAUNCH(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset_dx", s);
     {
@@ -326,7 +350,8 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.items = plan->items_x;
         g.wexp = plan->wexp_x;
         g.n_tokens = int32_t(N);
-        I4_RETURN_IF(gemm(a_x, 2 * N + 128, C, cache->wqT, D, C, C, g, s));
+        g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
+        I4_RETURN_IF(gemm(Operand{a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
     {
@@ -338,23 +363,28 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.s_down = plan->s_down;
         g.k_had = k;
         g.mask = cache->w_mask;
-        I4_RETURN_IF(gemm(a_wt, C, kcap, b_wt, D, kcap, kcap, g, s));
+        g.a_mn = 1; g.b_mn = 1;                  // A_W [K, C], B_W [K, D]: both MN-major
+        I4_RETURN_IF(gemm(Operand{a_w, kcap, C, C}, Operand{b_w, kcap, D, D}, g, s));
     }
     return I4_OK;
 }
 
-i4_status int4_gemm_s8s8s32(const int8_t* A, const int8_t* B, int64_t M, int64_t Nn, int64_t K, int32_t* acc,
-                            void* stream) {
+i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B, int32_t b_mn_major, int64_t M,
+                            int64_t Nn, int64_t K, int32_t* acc, void* stream) {
     I4_RETURN_IF(check_device());
     if (!A || !B || !acc) return fail(I4_ERR_ARG, "int4_gemm_s8s8s32: NULL pointer");
-    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16)
-        return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: need Nn %% 64 == 0 and K %% 16 == 0");
+    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16) || (b_mn_major && Nn % 128 && Nn > 128))
+        return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: unsupported shape M=%lld Nn=%lld K=%lld", (long long)M,
+                    (long long)Nn, (long long)K);
     if (!aligned16(A) || !aligned16(B) || !aligned16(acc)) return fail(I4_ERR_ALIGN, "int4_gemm_s8s8s32: unaligned pointer");
     i4::GemmArgs g{};
     g.M = int32_t(M); g.Nn = int32_t(Nn); g.K = int32_t(K);
+    g.a_mn = a_mn_major != 0; g.b_mn = b_mn_major != 0;
     g.epi = i4::EPI_INT32;
     g.out = acc;
-    return gemm(A, M, K, B, Nn, K, K, g, static_cast<cudaStream_t>(stream));
+    const Operand a = g.a_mn ? Operand{A, K, M, M} : Operand{A, M, K, K};
+    const Operand b = g.b_mn ? Operand{B, K, Nn, Nn} : Operand{B, Nn, K, K};
+    return gemm(a, b, g, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -119,6 +119,23 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
         : "memory");
 }
 
+// TMA store of a 2-D box from shared memory (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+                 :: "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(smem_src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05: TMEM allocation, UMMA (kind::i8), commit, TMEM -> registers
 // ---------------------------------------------------------------------------
@@ -141,8 +158,9 @@ __device__ __forceinline__ void tc_fence_after() {
 // Bit layout (PTX ISA "Instruction descriptor"): [4,6) D fmt (2 = s32),
 // [7,10) A fmt (1 = s8), [10,13) B fmt (1 = s8), [15] A major, [16] B major,
 // [17,23) N >> 3, [24,29) M >> 4.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
-    return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_mn = false, bool b_mn = false) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+           (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 // Shared-memory matrix descriptor for a K-major, 128-byte-swizzled tile whose
@@ -150,6 +168,17 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 // are 1024 bytes apart (SBO).  Version 1 (sm_100), layout type 2 = SWIZZLE_128B.
 __device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t smem_addr) {
     return (uint64_t((smem_addr >> 4) & 0x3FFFu))
+         | (uint64_t(1024u >> 4) << 32)
+         | (uint64_t(1) << 46)
+         | (uint64_t(2) << 61);
+}
+
+// Shared-memory matrix descriptor for an MN-major, 128-byte-swizzled tile:
+// 128-byte rows along MN, one row per K index; 8-row (K) core groups 1024 B
+// apart (SBO); MN atoms of 128 bytes `lbo` bytes apart (LBO).
+__device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t smem_addr, uint32_t lbo) {
+    return (uint64_t((smem_addr >> 4) & 0x3FFFu))
+         | (uint64_t((lbo >> 4) & 0x3FFFu) << 16)
          | (uint64_t(1024u >> 4) << 32)
          | (uint64_t(1) << 46)
          | (uint64_t(2) << 61);

@@ -3,21 +3,26 @@
 // codes are stored sign-extended in int8 (sm_100a has no s4 tcgen05 kind), so
 // tcgen05.mma.kind::i8 is exact for them; accumulation is int32 in TMEM.
 //
-//   acc[m, n] = sum_k A[m, k] B[n, k]      (A, B K-major: rows of K bytes)
+//   acc[m, n] = sum_k A(m, k) B(n, k)
+//   A is K-major ([M, K] rows) or MN-major ([K, M] rows); the same for B.  The
+//   UMMA descriptors read MN-major int8 directly, so no operand is ever
+//   transposed in memory (the paper's CUTLASS path needed explicit
+//   transpose+contiguous copies).
 //
 // Structure (one CTA per SM, persistent over output tiles, warp-specialised):
 //   warp 0   TMA producer: 128-byte-swizzled A (128 x 128 B) and B (BN x 128 B)
 //            tiles into a STAGES-deep shared-memory ring (mbarrier full/empty).
 //   warp 1   allocates 2 x BN TMEM columns; one lane issues tcgen05.mma
-//            (M = 128, N = BN, K = 32 per instruction, 4 per 128-byte k-block)
+//            (M = 128, N = BN, K = 32 per instruction, 4 per 128-deep k-block)
 //            and tcgen05.commit to release smem stages / publish accumulators.
-//   warps 2-5  epilogue: tcgen05.ld 32 lanes x 32 columns -> registers, then
+//   warps 2-5  epilogue: tcgen05.ld (32 lanes x 32 columns) -> registers, then
 //            EPI_INT32  raw accumulators (bit-exact parity checks)
 //            EPI_FWD    Y = fl32(acc) * fl32(s_x s_w)   (HQ-MM step 4)
+//            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; dW
+//            -> swizzled shared-memory staging -> TMA bulk tensor store
 //            EPI_DGRAD  row = kept item (h, t): v = acc * s_w s_h 2^wexp 2^{-k/2};
-//                       v = I_X[t] o v; v = v H (in-register FWHT); red.add into
-//                       dX[t] (<= 2 addends per element onto 0: order-independent)
-//            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; store dW
+//                       v = I_X[t] o v; v = v H; red.add.v4 into dX[t]
+//                       (<= 2 addends per element onto 0: order-independent)
 //   Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of
 //   tile i+1.  M (grad_X: kept items) or K (grad_W: kept items) may be read
 //   from device memory, so the sampled sizes never travel to the host.
@@ -32,6 +37,8 @@ constexpr int kBM = 128;
 constexpr int kBK = 128;                     // bytes = int8 elements along K per stage
 constexpr int kGemmThreads = 192;
 constexpr int kRingBytes = 192 * 1024;
+constexpr int kStageOutBytes = 4096;         // per epilogue warp per buffer: 32 rows x 128 B
+constexpr int kEpiWarps = 4;
 
 template <int BN>
 struct GemmCfg {
@@ -40,19 +47,27 @@ struct GemmCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = kRingBytes / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int OUT_BYTES = kEpiWarps * 2 * kStageOutBytes;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + 1024 + 256;
 };
 
-template <int BN, int EPI, int CH>
+// 16-byte chunk c of staging row r (128-byte rows, SWIZZLE_128B pattern)
+__device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
+    return buf + r * 128 + ((c ^ (r & 7)) << 4);
+}
+
+template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
     using Cfg = GemmCfg<BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_dyn[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = base;
     uint8_t* sB = base + STAGES * Cfg::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Cfg::STAGE_BYTES);
+    uint8_t* sOut = base + STAGES * Cfg::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sOut + Cfg::OUT_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -64,15 +79,16 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int M = g.m_dev ? __ldg(g.m_dev) : g.M;
     const int K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
     const int m_tiles = (M + kBM - 1) / kBM;
-    const int n_tiles = g.Nn / BN;
+    const int n_tiles = (g.Nn + BN - 1) / BN;
     const int total = m_tiles * n_tiles;
     const int nk = (K + kBK - 1) / kBK;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4 * 32); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps * 32); }
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -90,8 +106,17 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-                    tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-                    tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+                    uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+                    uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+                    if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
+                    else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 128; ++j)
+                            tma_load_2d(b_dst + j * 128 * kBK, &tmB, &full[stage], n0 + 128 * j, kb * kBK);
+                    } else {
+                        tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, n0);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -99,7 +124,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_i8(kBM, BN);
+            constexpr uint32_t idesc = idesc_i8(kBM, BN, A_MN, B_MN);
+            // descriptor advance per K = 32 MMA: K-major +32 B; MN-major +32 rows x 128 B
+            constexpr uint64_t a_step = A_MN ? (32 * 128) >> 4 : 32 >> 4;
+            constexpr uint64_t b_step = B_MN ? (32 * 128) >> 4 : 32 >> 4;
             int stage = 0; uint32_t phase = 0; int it = 0;
             for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
                 const int as = it & 1;
@@ -110,12 +138,13 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t adesc = sdesc_kmajor_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
-                    const uint64_t bdesc = sdesc_kmajor_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
+                    const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+                    const uint64_t adesc = A_MN ? sdesc_mnmajor_sw128(a_addr, 128 * kBK) : sdesc_kmajor_sw128(a_addr);
+                    const uint64_t bdesc = B_MN ? sdesc_mnmajor_sw128(b_addr, 128 * kBK) : sdesc_kmajor_sw128(b_addr);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 32; ++kk)
-                        umma_i8(d_tmem, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
-                                (kb | kk) != 0 ? 1u : 0u);
+                        umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
                     umma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -127,6 +156,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int lg = warp & 3;                       // TMEM lane group of this warp
         const int r_in_tile = lg * 32 + lane;
         const int words = g.Nn >> 5;
+        uint8_t* stg = sOut + (warp - 2) * 2 * kStageOutBytes;
+        int sbuf = 0;
         float sd = 1.0f;
         if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
         int it = 0;
@@ -154,79 +185,110 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 rscale = __fmul_rn(g.scale, sd);
             }
 
+            constexpr int CW = (EPI == EPI_FWD) ? 64 : CH;   // columns per chunk
 #pragma unroll 1
-            for (int c = 0; c < BN; c += CH) {
-                uint32_t r[CH / 32][32];
+            for (int c = 0; c < BN; c += CW) {
+                uint32_t r[CW / 32][32];
 #pragma unroll
-                for (int q = 0; q < CH / 32; ++q) tmem_ld_32x32b_x32(t_row + uint32_t(c + 32 * q), r[q]);
+                for (int q = 0; q < CW / 32; ++q) tmem_ld_32x32b_x32(t_row + uint32_t(c + 32 * q), r[q]);
                 tmem_ld_wait();
+                if (c + CW >= BN) {                   // accumulator stage drained -> MMA may reuse it
+                    tc_fence_before();
+                    mbar_arrive(&tempty[as]);
+                }
                 if (nk == 0) {
 #pragma unroll
-                    for (int q = 0; q < CH / 32; ++q)
+                    for (int q = 0; q < CW / 32; ++q)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) r[q][i] = 0;
                 }
                 const int col0 = n0 + c;
-                if (EPI == EPI_INT32) {
+                if (col0 >= g.Nn) continue;           // ragged N (MN-major B): nothing to write
+
+                if (EPI == EPI_DGRAD) {
                     if (valid) {
-                        int32_t* dst = reinterpret_cast<int32_t*>(g.out) + out_row * g.Nn + col0;
+                        float v[CW];
 #pragma unroll
-                        for (int i = 0; i < 32; i += 4)
-                            *reinterpret_cast<int4*>(dst + i) = make_int4(r[0][i], r[0][i + 1], r[0][i + 2], r[0][i + 3]);
-                    }
-                } else if (EPI == EPI_FWD) {
-                    if (valid) {
-                        float v[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = __fmul_rn(float(int32_t(r[0][i])), rscale);
-                        if (g.out_bf16) {
-                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(g.out) + out_row * g.Nn + col0;
-#pragma unroll
-                            for (int i = 0; i < 32; i += 8) {
-                                uint4 u;
-                                __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-                                __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-                                __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
-                                __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-                                u.x = *reinterpret_cast<uint32_t*>(&p0); u.y = *reinterpret_cast<uint32_t*>(&p1);
-                                u.z = *reinterpret_cast<uint32_t*>(&p2); u.w = *reinterpret_cast<uint32_t*>(&p3);
-                                *reinterpret_cast<uint4*>(dst + i) = u;
-                            }
-                        } else {
-                            float* dst = reinterpret_cast<float*>(g.out) + out_row * g.Nn + col0;
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4)
-                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                        }
-                    }
-                } else {
-                    // DGRAD / WGRAD: scale, clamp mask, inverse block Hadamard, write
-                    if (valid) {
-                        float v[CH];
-#pragma unroll
-                        for (int q = 0; q < CH / 32; ++q) {
+                        for (int q = 0; q < CW / 32; ++q) {
                             const uint32_t mw = __ldg(g.mask + out_row * words + (col0 >> 5) + q);
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
                                 v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
                         }
-                        fwht_inplace<CH>(v, g.k_had);
+                        fwht_inplace<CW>(v, g.k_had);
                         float* dst = reinterpret_cast<float*>(g.out) + out_row * g.Nn + col0;
-                        if (EPI == EPI_DGRAD) {
 #pragma unroll
-                            for (int i = 0; i < CH; i += 4)
-                                atomicAdd(reinterpret_cast<float4*>(dst + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < CH; i += 4)
-                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                        }
+                        for (int i = 0; i < CW; i += 4) red_add_v4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                     }
+                    continue;
+                }
+
+                // value transform into 32-bit words, then stage 32 x 128 B sub-tiles
+                if (EPI == EPI_FWD && g.out_bf16) {
+                    // 64 bf16 columns = one 128-byte staging row
+                    uint32_t packed[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float a = __fmul_rn(float(int32_t(r[i >> 4][(2 * i) & 31])), rscale);
+                        const float b = __fmul_rn(float(int32_t(r[i >> 4][(2 * i + 1) & 31])), rscale);
+                        __nv_bfloat162 p2 = __floats2bfloat162_rn(a, b);
+                        packed[i] = *reinterpret_cast<uint32_t*>(&p2);
+                    }
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                    uint8_t* buf = stg + sbuf * kStageOutBytes;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4*>(stage_chunk(buf, lane, q)) =
+                            make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) { tma_store_2d(&tmC, buf, col0, m0 + lg * 32); bulk_commit(); }
+                    sbuf ^= 1;
+                    continue;
+                }
+
+                uint32_t wv[CW];                      // 32-bit output words (int32 or fp32 bits)
+                if (EPI == EPI_INT32) {
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) wv[i] = r[i >> 5][i & 31];
+                } else if (EPI == EPI_FWD) {
+#pragma unroll
+                    for (int i = 0; i < CW; ++i)
+                        wv[i] = __float_as_uint(__fmul_rn(float(int32_t(r[i >> 5][i & 31])), rscale));
+                } else {                              // EPI_WGRAD
+                    float v[CW];
+                    const int64_t mrow = valid ? out_row : 0;
+#pragma unroll
+                    for (int q = 0; q < CW / 32; ++q) {
+                        const uint32_t mw = valid ? __ldg(g.mask + mrow * words + (col0 >> 5) + q) : 0u;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
+                    }
+                    fwht_inplace<CW>(v, g.k_had);
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) wv[i] = __float_as_uint(v[i]);
+                }
+#pragma unroll
+                for (int q = 0; q < CW / 32; ++q) {
+                    if (col0 + 32 * q >= g.Nn) break;
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                    uint8_t* buf = stg + sbuf * kStageOutBytes;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<uint4*>(stage_chunk(buf, lane, j)) =
+                            make_uint4(wv[32 * q + 4 * j], wv[32 * q + 4 * j + 1], wv[32 * q + 4 * j + 2], wv[32 * q + 4 * j + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) { tma_store_2d(&tmC, buf, col0 + 32 * q, m0 + lg * 32); bulk_commit(); }
+                    sbuf ^= 1;
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[as]);
         }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
     }
 
     tc_fence_before();
@@ -235,53 +297,57 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 1) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
 }
 
-int gemm_block_n(int Nn) {
+int gemm_block_n(int Nn, bool b_mn) {
     if (Nn % 256 == 0) return 256;
+    if (b_mn) return Nn > 128 ? 256 : 128;      // MN-major tiles are whole 128-byte atoms
     if (Nn % 128 == 0) return 128;
     return 64;
 }
 
-template <int BN, int EPI, int CH>
-static cudaError_t launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, int grid, cudaStream_t s) {
-    auto kern = gemm_i8_kernel<BN, EPI, CH>;
+template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
+static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
+    auto kern = gemm_i8_kernel<BN, EPI, CH, A_MN, B_MN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM, s>>>(a, b, g);
+    kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM, s>>>(*reinterpret_cast<const CUtensorMap*>(m.a),
+                                                        *reinterpret_cast<const CUtensorMap*>(m.b),
+                                                        *reinterpret_cast<const CUtensorMap*>(m.c), g);
     return cudaGetLastError();
 }
 
-template <int BN>
-static cudaError_t dispatch_epi(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, int grid, cudaStream_t s) {
-    const int ch = g.k_had >= 7 ? 128 : (g.k_had == 6 ? 64 : 32);
-    switch (g.epi) {
-        case EPI_INT32: return launch_one<BN, EPI_INT32, 32>(a, b, g, grid, s);
-        case EPI_FWD: return launch_one<BN, EPI_FWD, 32>(a, b, g, grid, s);
-        case EPI_DGRAD:
-            if (ch == 32) return launch_one<BN, EPI_DGRAD, 32>(a, b, g, grid, s);
-            if (ch == 64) return launch_one<BN, EPI_DGRAD, 64>(a, b, g, grid, s);
-            if constexpr (BN >= 128) return launch_one<BN, EPI_DGRAD, 128>(a, b, g, grid, s);
-            return cudaErrorInvalidValue;
-        case EPI_WGRAD:
-            if (ch == 32) return launch_one<BN, EPI_WGRAD, 32>(a, b, g, grid, s);
-            if (ch == 64) return launch_one<BN, EPI_WGRAD, 64>(a, b, g, grid, s);
-            if constexpr (BN >= 128) return launch_one<BN, EPI_WGRAD, 128>(a, b, g, grid, s);
-            return cudaErrorInvalidValue;
-    }
+template <int EPI, int CH, bool A_MN, bool B_MN>
+static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
+    if (bn == 256) return launch_one<256, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+    if (bn == 128) return launch_one<128, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+    if constexpr (!B_MN && CH <= 64) return launch_one<64, EPI, CH, A_MN, B_MN>(m, g, grid, s);
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_gemm(const void* tmap_a, const void* tmap_b, const GemmArgs& g, int num_sms, cudaStream_t s) {
-    const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmap_a);
-    const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmap_b);
-    const int bn = gemm_block_n(g.Nn);
-    const int64_t tiles = int64_t((g.M + kBM - 1) / kBM) * (g.Nn / bn);   // g.M = upper bound when m_dev
+template <int EPI, bool A_MN, bool B_MN>
+static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
+    if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) {
+        if (g.k_had >= 7) return dispatch_bn<EPI, 128, A_MN, B_MN>(bn, m, g, grid, s);
+        if (g.k_had == 6) return dispatch_bn<EPI, 64, A_MN, B_MN>(bn, m, g, grid, s);
+    }
+    return dispatch_bn<EPI, 32, A_MN, B_MN>(bn, m, g, grid, s);
+}
+
+cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s) {
+    const int bn = gemm_block_n(g.Nn, g.b_mn);
+    const int64_t tiles = int64_t((g.M + kBM - 1) / kBM) * ((g.Nn + bn - 1) / bn);   // g.M = bound when m_dev
     int grid = int(tiles < num_sms ? tiles : num_sms);
     if (grid < 1) grid = 1;
-    switch (bn) {
-        case 256: return dispatch_epi<256>(a, b, g, grid, s);
-        case 128: return dispatch_epi<128>(a, b, g, grid, s);
-        default: return dispatch_epi<64>(a, b, g, grid, s);
+    switch (g.epi) {
+        case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, grid, s);
+        case EPI_DGRAD: return dispatch_ch<EPI_DGRAD, false, true>(bn, m, g, grid, s);
+        case EPI_WGRAD: return dispatch_ch<EPI_WGRAD, true, true>(bn, m, g, grid, s);
+        case EPI_INT32:
+            if (!g.a_mn && !g.b_mn) return dispatch_ch<EPI_INT32, false, false>(bn, m, g, grid, s);
+            if (!g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, false, true>(bn, m, g, grid, s);
+            if (g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, true, true>(bn, m, g, grid, s);
+            return dispatch_ch<EPI_INT32, true, false>(bn, m, g, grid, s);
     }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace i4

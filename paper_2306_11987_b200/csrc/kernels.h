@@ -15,7 +15,6 @@ cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, 
 cudaError_t launch_bitsplit(const uint16_t* g, int64_t N, int64_t C, const uint32_t* amax_bits,
                             uint64_t seed, uint32_t call_id, int64_t token_offset, int8_t* hilo,
                             int32_t* a_sq, float* s_down, cudaStream_t s);
-cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int8_t* dst, cudaStream_t s);
 
 // sampler.cu ------------------------------------------------------------------
 struct SamplerArgs {
@@ -37,14 +36,15 @@ cudaError_t launch_compact_rows(const int8_t* hilo, int64_t C, const int32_t* it
                                 int64_t n_items, int8_t* out, cudaStream_t s);
 cudaError_t launch_compact_wgrad(const int8_t* hilo, const int8_t* xq, int64_t N, int64_t C, int64_t D,
                                  const int32_t* items, const int8_t* wexp, const int32_t* count,
-                                 int64_t kcap, int8_t* a_t, int8_t* b_t, cudaStream_t s);
+                                 int64_t kcap, int8_t* a_w, int8_t* b_w, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
 enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3 };
 
 struct GemmArgs {
-    // problem: acc[M, Nn] = A[M, K] . B[Nn, K]^T; M or K may come from device memory
+    // problem: acc[M, Nn] = A(M, K) . B(Nn, K)^T; M or K may come from device memory
     int32_t M, Nn, K;
+    int32_t a_mn, b_mn;       // operand stored MN-major ([K, M] / [K, Nn] rows) instead of K-major
     const int32_t* m_dev;     // if non-null: M = roundup(*m_dev) rows are valid (dgrad)
     const int32_t* k_dev;     // if non-null: K = *m_dev-style count of K rows (wgrad)
     int32_t epi;
@@ -59,7 +59,8 @@ struct GemmArgs {
     const int8_t* wexp;       // dgrad: weight exponent of each A row
     int32_t n_tokens;         // dgrad: N (item id = h*N + t)
 };
-cudaError_t launch_gemm(const void* tmap_a, const void* tmap_b, const GemmArgs& g, int num_sms, cudaStream_t s);
-int gemm_block_n(int Nn);
+struct GemmMaps { const void* a; const void* b; const void* c; };   // CUtensorMap* (host)
+cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
+int gemm_block_n(int Nn, bool b_mn);
 
 }  // namespace i4

@@ -3,7 +3,6 @@
 //   amax_bf16      : B1 -- per-tensor max |grad_Y| (reading Z-9)
 //   bitsplit       : B2 -- Philox SR to the 8-bit code, split into high / low
 //                    4-bit planes, per-row integer norms
-//   transpose_i8   : W_hat -> W_hat^T (K-major B operand of the grad_X GEMM)
 //
 // Thread layout shared by the row kernels: one warp per row; the row is walked
 // in 256-column chunks, lane l owning columns [c0 + 8 l, c0 + 8 l + 8) so each
@@ -233,41 +232,6 @@ cudaError_t launch_bitsplit(const uint16_t* g, int64_t N, int64_t C, const uint3
     bitsplit_kernel<<<row_grid(N), kRowWarps * 32, 0, s>>>(g, N, int(C), amax_bits, uint32_t(seed),
                                                             uint32_t(seed >> 32), call_id, token_offset,
                                                             hilo, a_sq, s_down);
-    return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// int8 transpose, 64 x 64 tiles through shared memory
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) transpose_i8_kernel(const int8_t* __restrict__ src, int64_t rows,
-                                                           int64_t cols, int8_t* __restrict__ dst) {
-    __shared__ int8_t tile[64][64 + 4];
-    const int64_t r0 = int64_t(blockIdx.y) * 64, c0 = int64_t(blockIdx.x) * 64;
-    // load: 64 rows x 64 bytes, 16 bytes per thread
-    {
-        const int r = threadIdx.x >> 2, seg = (threadIdx.x & 3) * 16;
-        if (r0 + r < rows && c0 + seg < cols) {
-            const uint4 u = *reinterpret_cast<const uint4*>(src + (r0 + r) * cols + c0 + seg);
-            const int8_t* b = reinterpret_cast<const int8_t*>(&u);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) tile[r][seg + j] = b[j];
-        }
-    }
-    __syncthreads();
-    {
-        const int c = threadIdx.x >> 2, seg = (threadIdx.x & 3) * 16;
-        if (c0 + c < cols && r0 + seg < rows) {
-            alignas(16) int8_t b[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) b[j] = tile[seg + j][c];
-            *reinterpret_cast<uint4*>(dst + (c0 + c) * rows + r0 + seg) = *reinterpret_cast<const uint4*>(b);
-        }
-    }
-}
-
-cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int8_t* dst, cudaStream_t s) {
-    dim3 grid(unsigned((cols + 63) / 64), unsigned((rows + 63) / 64));
-    transpose_i8_kernel<<<grid, 256, 0, s>>>(src, rows, cols, dst);
     return cudaGetLastError();
 }
 

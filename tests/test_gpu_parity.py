@@ -33,16 +33,23 @@ def p():
 
 
 # ----------------------------------------------------------------------------- (iii)
-@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 256, 1024), (1000, 192, 128), (77, 512, 4096),
-                                   (129, 128, 48), (4096, 3072, 768)])
-def test_gemm_int32_bit_exact(M, N, K):
+GEMM_SHAPES = [(128, 64, 64), (300, 256, 1024), (1000, 192, 128), (77, 512, 4096), (129, 128, 48),
+               (4096, 3072, 768), (256, 384, 256)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_int32_bit_exact(M, N, K, a_mn, b_mn):
+    if a_mn and M % 16:
+        pytest.skip("MN-major A needs 16-byte rows")
     rng = np.random.default_rng(M * 7 + N + K)
     a = rng.integers(-8, 8, (M, K), dtype=np.int8)
     b = rng.integers(-128, 128, (N, K), dtype=np.int8)
     b[:, :K // 2] = np.clip(b[:, :K // 2], -112, 112)
-    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    A = torch.from_numpy(np.ascontiguousarray(a.T) if a_mn else a).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(b.T) if b_mn else b).cuda()
     acc = torch.full((M, N), -1, dtype=torch.int32, device="cuda")
-    p().int4_gemm_s8s8s32(A, B, acc)
+    p().int4_gemm_s8s8s32(A, B, acc, a_mn_major=a_mn, b_mn_major=b_mn)
     torch.cuda.synchronize()
     ref = o_gemm.int_matmul_abt(a, b)
     assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
@@ -108,7 +115,6 @@ def test_forward_parity(N, D, C, k):
     for g, o in ((gx, f["xq"]), (gw, f["wq"])):
         nbad, maxdiff = code_mismatch(g, o)
         assert maxdiff <= 1 and nbad <= CODE_FRAC_TOL * o.size
-    assert np.array_equal(layer.wqT.cpu().numpy(), gw.T)
     # (iii)+(iv): Y from the GPU codes, exact int acc then fp32 scale
     acc = o_gemm.int_matmul_abt(gx, gw)
     y_ref = acc.astype(np.float64) * (np.float64(np.float32(s_x)) * np.float64(np.float32(s_w)))
