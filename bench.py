@@ -198,12 +198,8 @@ def algorithmic_work(name, N, D, C, kx, kw):
         return "ops", 2.0 * kx * C * D
     if name == "gemm_i8_wgrad":
         return "ops", 2.0 * kw * C * D
-    if name == "hadamard_quant_x":            # read bf16, write int8 codes + 1 bit mask + int32 norm
-        return "bytes", N * D * (2 + 1 + 1 / 8) + 4 * N
-    if name == "hadamard_quant_w":
-        return "bytes", C * D * (2 + 1 + 1 / 8)
-    if name == "transpose_w":
-        return "bytes", 2.0 * C * D
+    if name == "hadamard_quant":              # X and W: read bf16, write int8 codes + 1-bit mask (+ int32 norm)
+        return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
     if name == "amax":
         return "bytes", 2.0 * N * C
     if name == "bitsplit":                    # read bf16 grad_Y, write hi + lo planes, 2 norms

@@ -254,11 +254,17 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     if (!aligned16(X) || !aligned16(W) || !aligned16(Y)) return fail(I4_ERR_ALIGN, "int4_linear_fwd: unaligned pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
-    I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(X), N, D, k, step_recip(k, s_x), cache->xq,
-                                        cache->x_mask, cache->x_sqnorm, s), "hadamard_quant_x", s);
-    if (!cache->w_valid) {
-        I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(W), C, D, k, step_recip(k, s_w), cache->wq,
-                                            cache->w_mask, nullptr, s), "hadamard_quant_w", s);
+    {
+        // F1-F3: X and (unless cached) W quantized by one launch
+        i4::HqArgs h{};
+        h.x0 = static_cast<const uint16_t*>(X); h.rows0 = N; h.r0 = step_recip(k, s_x);
+        h.codes0 = cache->xq; h.bits0 = cache->x_mask; h.sqnorm0 = cache->x_sqnorm;
+        if (!cache->w_valid) {
+            h.x1 = static_cast<const uint16_t*>(W); h.rows1 = C; h.r1 = step_recip(k, s_w);
+            h.codes1 = cache->wq; h.bits1 = cache->w_mask; h.sqnorm1 = nullptr;
+        }
+        h.cols = D; h.k = k;
+        I4_LAUNCH(i4::launch_hadamard_quant2(h, s), "hadamard_quant", s);
     }
     i4::GemmArgs g{};
     g.M = int32_t(N); g.Nn = int32_t(C); g.K = int32_t(D);
@@ -373,7 +379,7 @@ i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B
                             int64_t Nn, int64_t K, int32_t* acc, void* stream) {
     I4_RETURN_IF(check_device());
     if (!A || !B || !acc) return fail(I4_ERR_ARG, "int4_gemm_s8s8s32: NULL pointer");
-    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16) || (b_mn_major && Nn % 128 && Nn > 128))
+    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16) || false)
         return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: unsupported shape M=%lld Nn=%lld K=%lld", (long long)M,
                     (long long)Nn, (long long)K);
     if (!aligned16(A) || !aligned16(B) || !aligned16(acc)) return fail(I4_ERR_ALIGN, "int4_gemm_s8s8s32: unaligned pointer");

@@ -14,6 +14,8 @@
 
 namespace i4 {
 
+constexpr int kGroup = 8;                 // 16-byte loads in flight per lane
+
 __global__ void __launch_bounds__(256) compact_rows_kernel(const int8_t* __restrict__ hilo, int C,
                                                            const int32_t* __restrict__ items,
                                                            const int32_t* __restrict__ count,
@@ -26,12 +28,19 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(const int8_t* __restr
          j += warps) {
         const int32_t item = __ldg(items + j);
         int8_t* dst = out + j * C;
-        if (item >= sentinel) {
-            for (int c = lane * 16; c < C; c += 512) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
-        } else {
-            const int8_t* src = hilo + int64_t(item) * C;
-            for (int c = lane * 16; c < C; c += 512)
-                *reinterpret_cast<uint4*>(dst + c) = ld_nc_v4(src + c);
+        const int8_t* src = hilo + int64_t(item < sentinel ? item : 0) * C;
+        for (int c0 = 0; c0 < C; c0 += 512 * kGroup) {
+            uint4 u[kGroup];
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) {          // all loads of the group first
+                const int c = c0 + 512 * g + lane * 16;
+                u[g] = (c < C && item < sentinel) ? ld_nc_v4(src + c) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+                const int c = c0 + 512 * g + lane * 16;
+                if (c < C) *reinterpret_cast<uint4*>(dst + c) = u[g];
+            }
         }
     }
 }
@@ -80,10 +89,25 @@ __global__ void __launch_bounds__(256) compact_wgrad_kernel(const int8_t* __rest
         const int mul_b = h == 0 ? 16 : 1;
         const int8_t* sa = hilo + int64_t(item) * C;
         const int8_t* sb = xq + int64_t(t) * D;
-        for (int c = lane * 16; c < C; c += 512)
-            *reinterpret_cast<uint4*>(da + c) = scale_i8x16(ld_nc_v4(sa + c), mul_a);
-        for (int c = lane * 16; c < D; c += 512)
-            *reinterpret_cast<uint4*>(db + c) = scale_i8x16(ld_nc_v4(sb + c), mul_b);
+        const int ca = (C + 511) / 512, cb = (D + 511) / 512;   // 16-byte pieces per lane
+        for (int p0 = 0; p0 < ca + cb; p0 += kGroup) {
+            uint4 u[kGroup];
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+                const int p = p0 + g;
+                const int c = (p < ca ? p : p - ca) * 512 + lane * 16;
+                u[g] = make_uint4(0, 0, 0, 0);
+                if (p < ca) { if (c < C) u[g] = ld_nc_v4(sa + c); }
+                else if (p < ca + cb && c < D) u[g] = ld_nc_v4(sb + c);
+            }
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) {
+                const int p = p0 + g;
+                const int c = (p < ca ? p : p - ca) * 512 + lane * 16;
+                if (p < ca) { if (c < C) *reinterpret_cast<uint4*>(da + c) = scale_i8x16(u[g], mul_a); }
+                else if (p < ca + cb && c < D) *reinterpret_cast<uint4*>(db + c) = scale_i8x16(u[g], mul_b);
+            }
+        }
     }
 }
 

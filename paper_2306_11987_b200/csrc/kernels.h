@@ -9,6 +9,12 @@
 namespace i4 {
 
 // quant.cu --------------------------------------------------------------------
+struct HqArgs {                          // two independent hadamard_quant jobs in one launch
+    const uint16_t* x0; int64_t rows0; float r0; int8_t* codes0; uint32_t* bits0; int32_t* sqnorm0;
+    const uint16_t* x1; int64_t rows1; float r1; int8_t* codes1; uint32_t* bits1; int32_t* sqnorm1;
+    int64_t cols; int k;
+};
+cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
                                   int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s);
 cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, cudaStream_t s);

@@ -55,6 +55,6 @@ def test_host_validation_without_gpu():
         has_gpu = False
     if has_gpu:
         pytest.skip("host has a GPU")
-    st = p.lib.int4_gemm_s8s8s32(None, None, 1, 64, 16, None, None)
+    st = p.lib.int4_gemm_s8s8s32(None, 0, None, 0, 1, 64, 16, None, None)
     assert st != 0
     assert p.lib.int4_last_error()
