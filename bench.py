@@ -134,7 +134,7 @@ def workload_config(args, cfg, world=1):
     return {"workload": f"{args.config}: {cfg['N']} tokens x {cfg['D']}->{cfg['C']} INT4 linear fwd+bwd, k={cfg['k']}",
             "tokens_per_gpu": cfg["N"], "global_tokens": cfg["N"] * world, "D": cfg["D"], "C": cfg["C"],
             "k": cfg["k"], "grad_y": args.grad, "lss_mode": args.mode, "parallelism": f"dp{world} (token-sharded)",
-            "l2": "flushed by a 256 MiB write before every timed step",
+            "l2": "flushed before every timed step: 256 MiB write + 256 MiB read of another buffer (cold, clean L2)",
             "graph": "step captured once in a CUDA graph, replayed"}
 
 
@@ -249,7 +249,19 @@ def run_ours(args):
     dX = torch.empty(N, D, dtype=torch.float32, device=dev)
     dW = torch.empty(C, D, dtype=torch.float32, device=dev)
     token_offset = rank * N
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(32 * 1024 * 1024, dtype=torch.int64, device=dev)
+
+    class _Flush:
+        """L2 flush before every timed step: write 256 MiB (> 126 MB L2), then read
+        another 256 MiB so the dirty lines are written back before the step
+        starts (the step begins with a cold but clean L2)."""
+
+        def zero_(self):
+            flush_w.zero_()
+            torch.sum(flush_r)
+
+    flush = _Flush()
 
     def step_body():
         layer.forward(X, W, s_x, s_w, Y)

@@ -220,6 +220,7 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
     const int64_t warp0 = int64_t(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
     const int64_t wstride = int64_t(gridDim.x) * kRowWarps;
     const int nch = (C + 255) >> 8;
+    const PhiloxKeys keys = philox_keys(k0, k1);
     for (int64_t row = warp0; row < N; row += wstride) {
         const uint16_t* gr = g + row * C;
         int8_t* hr = hilo + row * C;
@@ -241,20 +242,20 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
                 unpack_bf16x8(raw[gi], v);
                 // Philox words for the 8 elements: L = tglob * C + col + i, block L / 4
                 const uint64_t b0 = (tglob * uint64_t(C) + uint64_t(col)) >> 2;
-                const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, k0, k1);
-                const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, k0, k1);
+                const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, keys);
+                const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, keys);
                 const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
                 int hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     int q = 0;
                     if (!zero) {
+                        // A = ceil(|v| 2^32) (|v| 2^32 is exact in fp32): high word = floor|v|
+                        // (+1 when the fraction's threshold wraps to 2^32), low word =
+                        // T = ceil(frac|v| 2^32) mod 2^32; P(round up) = T / 2^32 exactly.
                         const float sv = fminf(fmaxf(__fmul_rn(v[i], r8), -119.0f), 119.0f);
-                        const float a = fabsf(sv);
-                        const float fl = floorf(a);
-                        const float f = __fsub_rn(a, fl);                     // exact
-                        const uint64_t T = uint64_t(ceilf(__fmul_rn(f, 4294967296.0f)));  // exact
-                        const int mag = int(fl) + int(uint64_t(u[i]) < T);
+                        const uint64_t A = __float2ull_ru(__fmul_rn(fabsf(sv), 4294967296.0f));
+                        const int mag = int(A >> 32) + int(u[i] < uint32_t(A));
                         q = sv < 0.0f ? -mag : mag;
                     }
                     hi[i] = (q + 8) >> 4;                                     // floor division
