@@ -210,8 +210,8 @@ def algorithmic_work(name, N, D, C, kx, kw):
         return "bytes", 2.0 * kw * (C + D)
     if name == "lss_sampler":
         return "latency", 0.0
-    if name == "memset_dx":
-        return "bytes", 4.0 * N * D
+    if name == "memsets":
+        return "bytes", 4.0 * N * D + 4
     return "bytes", 0.0
 
 
@@ -278,7 +278,7 @@ def run_ours(args):
     err = np.linalg.norm(y_got - y_ref) / np.linalg.norm(y_ref)
     assert err < 4e-3, f"parity gate failed: rel err {err}"
 
-    # ---- capture one step in a CUDA graph with launch tracing
+    # ---- capture one step in a CUDA graph (no instrumentation inside)
     stream = torch.cuda.Stream(device=dev)
     stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):
@@ -286,41 +286,40 @@ def run_ours(args):
             step_body()
     torch.cuda.current_stream().wait_stream(stream)
     torch.cuda.synchronize()
-    events = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(40)]
-    tracer = i4.LaunchTrace(events)
+    namer = i4.LaunchTrace([torch.cuda.Event(enable_timing=True) for _ in range(2)], first_launch=10 ** 6)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
-        with tracer:
+        with namer:                       # window never reached: only records launch names
             step_body()
-    names = tracer.names
-    n_launch = len(names)
-    ev_end_ar = torch.cuda.Event(enable_timing=True)
+    names = namer.names
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
 
-    def one_step():
-        graph.replay()
-        if world > 1:
-            dist.all_reduce(dW)
-        ev_end_ar.record()
+    def timed_replays(g, n_steps, other_dw=None, on_step=None):
+        """Per step: L2 flush (untimed), then CUDA events on the stream around
+        the graph replay (+ the grad_W all-reduce when N > 1)."""
+        out = []
+        for i in range(n_steps):
+            flush.zero_()
+            ev_a.record()
+            g.replay()
+            if world > 1:
+                dist.all_reduce(dW if other_dw is None else other_dw)
+            ev_b.record()
+            torch.cuda.synchronize()
+            out.append(ev_a.elapsed_time(ev_b))
+            if on_step:
+                on_step()
+        return out
 
-    for _ in range(args.warmup):
-        flush.zero_()
-        one_step()
-    torch.cuda.synchronize()
+    timed_replays(graph, args.warmup)
 
-    # ---- timed region
-    per_kernel = {nm: [] for nm in names}
-    step_ms = []
+    # ---- timed region (headline)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            one_step()
-            torch.cuda.synchronize()
-            step_ms.append(events[0].elapsed_time(ev_end_ar))
-            for nm, ms in tracer.durations_ms():
-                per_kernel[nm].append(ms)
+        step_ms = timed_replays(graph, args.steps)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -335,8 +334,6 @@ def run_ours(args):
     Yb = torch.empty(N, C, dtype=torch.bfloat16, device=dev)
     dXb = torch.empty(N, D, dtype=torch.bfloat16, device=dev)
     dWb = torch.empty(C, D, dtype=torch.bfloat16, device=dev)
-    e0 = torch.cuda.Event(enable_timing=True, external=True)
-    e1 = torch.cuda.Event(enable_timing=True, external=True)
 
     def bf16_body():
         torch.matmul(X, W.t(), out=Yb)
@@ -347,41 +344,43 @@ def run_ours(args):
         for _ in range(2):
             bf16_body()
     torch.cuda.synchronize()
-    g2 = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g2):
-        e0.record()
+    g_bf16 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_bf16):
         bf16_body()
-        e1.record()
-    bf16_ms = []
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        g2.replay()
-        if world > 1:
-            dist.all_reduce(dWb)
-        torch.cuda.synchronize()
-        if i >= args.warmup:
-            bf16_ms.append(e0.elapsed_time(e1))
-    bf16 = statistics.mean(bf16_ms)
+    timed_replays(g_bf16, args.warmup, other_dw=dWb)
+    bf16 = statistics.mean(timed_replays(g_bf16, args.steps, other_dw=dWb))
 
-    # ---- kernel breakdown + roofline of the dominant kernel
+    # ---- kernel breakdown: CUPTI kernel records (torch.profiler) over extra replays
     kx, kw = [int(v) for v in layer.counts().cpu().numpy()]
+    cupti = cupti_kernel_times(graph, flush, min(args.steps, 20))
     kernels = {}
-    for nm, lst in per_kernel.items():
-        avg = statistics.mean(lst) if lst else 0.0
+    for nm, avg_us in cupti.items():
         kind, amount = algorithmic_work(nm, N, D, C, kx, kw)
-        ent = {"avg_us": avg * 1e3, "share": avg / ms if ms else 0.0}
-        if kind == "ops" and avg > 0:
-            ent.update(achieved_tops=amount / (avg * 1e-3) / 1e12, frac_int8_peak=amount / (avg * 1e-3) / 1e12 / int8_peak)
-        elif kind == "bytes" and avg > 0 and amount > 0:
-            ent.update(achieved_gbs=amount / (avg * 1e-3) / 1e9, frac_hbm=amount / (avg * 1e-3) / 1e9 / peaks["hbm_gbs"])
+        ent = {"avg_us": avg_us, "share": avg_us * 1e-3 / ms if ms else 0.0}
+        if kind == "ops" and avg_us > 0:
+            ent.update(achieved_tops=amount / (avg_us * 1e-6) / 1e12, frac_int8_peak=amount / (avg_us * 1e-6) / 1e12 / int8_peak)
+        elif kind == "bytes" and avg_us > 0 and amount > 0:
+            ent.update(achieved_gbs=amount / (avg_us * 1e-6) / 1e9, frac_hbm=amount / (avg_us * 1e-6) / 1e9 / peaks["hbm_gbs"])
         kernels[nm] = ent
-    dom = max((nm for nm in kernels if nm != "memset_dx"), key=lambda nm: kernels[nm]["avg_us"])
+    dom = max((nm for nm in kernels if not nm.startswith("memset")), key=lambda nm: kernels[nm]["avg_us"])
+
+    # ---- dominant kernel: CUDA events bracketing its launch inside the step graph
+    dom_idx = names.index(dom)
+    dom_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+    dom_tr = i4.LaunchTrace(dom_ev, first_launch=dom_idx)
+    g_dom = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_dom):
+        with dom_tr:
+            step_body()
+    dom_ms = []
+    timed_replays(g_dom, args.warmup)
+    timed_replays(g_dom, args.steps, on_step=lambda: dom_ms.append(dom_ev[0].elapsed_time(dom_ev[1])))
+    avg_s = statistics.mean(dom_ms) * 1e-3
     kind, amount = algorithmic_work(dom, N, D, C, kx, kw)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
-    avg_s = kernels[dom]["avg_us"] * 1e-6
     if kind == "ops":
         achieved = amount / avg_s / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
@@ -393,6 +392,10 @@ def run_ours(args):
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
                 "work_per_launch": f"{amount:.4g} algorithmic bytes"}
+    roof["avg_launch_us_events"] = avg_s * 1e6
+    roof["avg_launch_us_cupti"] = kernels[dom]["avg_us"]
+    roof["timing"] = ("CUDA events recorded on the launch stream immediately before/after this kernel's "
+                      "node inside the captured step graph, averaged over the timed steps")
 
     gemm_ops = 2.0 * C * D * (N + kx + kw)
     gemm_us = sum(kernels[nm]["avg_us"] for nm in ("gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad") if nm in kernels)
@@ -439,7 +442,8 @@ def run_ours(args):
                 "speedup_vs_bf16_cublas": bf16 / ms, "bf16_cublas_ms_per_step": bf16,
                 "gemm_int8_peak_frac": gemm_ops / (gemm_us * 1e-6) / 1e12 / int8_peak if gemm_us else None,
                 "kept_items": {"grad_W": kw, "grad_X": kx, "budget": N},
-                "roofline": roof, "kernels": kernels, "gpu_launches": n_launch_ours(names) * args.steps,
+                "roofline": roof, "kernels": kernels, "kernels_timing": "CUPTI kernel records (torch.profiler) over extra flushed replays",
+                "gpu_launches": n_launch_ours(names) * args.steps,
                 "clocks": clocks.summary(), "e2e": e2e}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, args.grad, args.mode)
@@ -448,6 +452,45 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+KERNEL_NAMES = [("hadamard_quant_kernel", "hadamard_quant"), ("amax_bf16_kernel", "amax"),
+                ("bitsplit_kernel", "bitsplit"), ("lss_sampler_kernel", "lss_sampler"),
+                ("compact_rows_kernel", "compact_rows"), ("compact_wgrad_kernel", "compact_wgrad")]
+GEMM_EPI = {"0": "gemm_i8_int32", "1": "gemm_i8_fwd", "2": "gemm_i8_dgrad", "3": "gemm_i8_wgrad"}
+
+
+def short_kernel_name(full):
+    if "gemm_i8_kernel<" in full:
+        epi = full.split("gemm_i8_kernel<", 1)[1].split(",")[1].strip()
+        return GEMM_EPI.get(epi, "gemm_i8")
+    for key, short in KERNEL_NAMES:
+        if key in full:
+            return short
+    if "memset" in full.lower():
+        return "memsets"                 # cudaMemsetAsync: zeroed grad_X + the 4-byte amax word
+    return None
+
+
+def cupti_kernel_times(graph, flush, n):
+    """Average device duration (us) of each of our kernels per replay, from the
+    CUPTI activity records torch.profiler collects (kernels inside graphs too)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    acc = {}
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(n):
+            flush.zero_()
+            graph.replay()
+            torch.cuda.synchronize()
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA":
+            continue
+        nm = short_kernel_name(ev.name)
+        if nm is None:
+            continue
+        acc.setdefault(nm, []).append(ev.device_time_total)
+    return {nm: sum(v) / n for nm, v in acc.items()}
 
 
 def n_launch_ours(names):

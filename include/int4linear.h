@@ -170,12 +170,14 @@ I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const in
 
 /* Measurement hook (used by bench.py).  int4_trace_begin arms tracing on the
  * calling thread with `capacity` caller-created cudaEvent_t handles (passed as
- * void*): events[0] is recorded on the launch stream before the library's next
- * launch and events[i+1] right after its i-th launch (a kernel or a memset), so
- * consecutive events bracket each launch.  int4_trace_end disarms tracing,
- * writes the static launch names into names[0..n) and returns n.  At most
- * capacity - 1 launches are recorded; the events stay caller-owned. */
-I4_API i4_status int4_trace_begin(void* const* events, int32_t capacity);
+ * void*) for a window of launches starting at the library's `first_launch`-th
+ * launch (0-based, counted from this call): events[0] is recorded on the launch
+ * stream just before that launch and events[i+1] right after the window's i-th
+ * launch, so consecutive events bracket each launch of the window (under
+ * stream capture the records become graph event nodes).  int4_trace_end
+ * disarms tracing, writes the static names of all launches seen into
+ * names[0..n) and returns n.  The events stay caller-owned. */
+I4_API i4_status int4_trace_begin(void* const* events, int32_t capacity, int32_t first_launch);
 I4_API int32_t int4_trace_end(const char** names, int32_t capacity);
 
 /* Thread-local message describing the last non-OK status of this thread. */

@@ -72,7 +72,7 @@ def _load():
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
     L.int4_last_error.argtypes = []
     L.int4_last_error.restype = ctypes.c_char_p
-    L.int4_trace_begin.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32]
+    L.int4_trace_begin.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32]
     L.int4_trace_begin.restype = ctypes.c_int
     L.int4_trace_end.argtypes = [ctypes.POINTER(ctypes.c_char_p), i32]
     L.int4_trace_end.restype = i32
@@ -144,31 +144,35 @@ def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, stream=None
 
 class LaunchTrace:
     """Context manager around the library's launch-tracing hook: the events
-    (torch.cuda.Event, enable_timing) bracket every launch the library makes
-    on its stream while the context is open (including inside a CUDA graph
-    capture, where the records become graph nodes)."""
+    (torch.cuda.Event, enable_timing) bracket the library launches
+    first_launch, first_launch + 1, ... made on its stream while the context is
+    open (inside a CUDA graph capture the records become graph nodes; create
+    the events with external=True then).  `names` lists every launch seen."""
 
-    def __init__(self, events):
+    def __init__(self, events, first_launch=0):
         import torch
         self.events = events
+        self.first = first_launch
         for e in events:                           # force lazy creation of the handles
             e.record(torch.cuda.current_stream())
+        torch.cuda.current_stream().synchronize()
         self.handles = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
         self.names = []
 
     def __enter__(self):
-        _check(lib.int4_trace_begin(self.handles, len(self.events)))
+        _check(lib.int4_trace_begin(self.handles, len(self.events), self.first))
         return self
 
     def __exit__(self, *exc):
-        buf = (ctypes.c_char_p * len(self.events))()
-        n = lib.int4_trace_end(buf, len(self.events))
+        buf = (ctypes.c_char_p * 64)()
+        n = lib.int4_trace_end(buf, 64)
         self.names = [buf[i].decode() for i in range(n)]
         return False
 
     def durations_ms(self):
-        """[(name, ms)] of the recorded launches (events must have completed)."""
-        return [(nm, self.events[i].elapsed_time(self.events[i + 1])) for i, nm in enumerate(self.names)]
+        """[(name, ms)] of the launches inside the window (events must have completed)."""
+        win = self.names[self.first:self.first + len(self.events) - 1]
+        return [(nm, self.events[i].elapsed_time(self.events[i + 1])) for i, nm in enumerate(win)]
 
 
 class Int4Linear:

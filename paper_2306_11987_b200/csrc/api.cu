@@ -41,29 +41,33 @@ i4_status cuda_fail(cudaError_t e, const char* where) {
     } while (0)
 
 // Launch tracing (int4_trace_begin / int4_trace_end): caller-owned events are
-// recorded on the launch stream around every kernel the library enqueues.
+// recorded on the launch stream around a window of the library's launches.
 constexpr int kMaxTrace = 64;
 struct TraceState {
     bool active = false;
-    bool started = false;
     cudaEvent_t ev[kMaxTrace + 1];
-    int cap = 0;
-    int n = 0;
+    int cap = 0;                 // events available
+    int first = 0;               // index of the first launch inside the window
+    int n = 0;                   // launches seen since int4_trace_begin
     const char* names[kMaxTrace];
 };
 thread_local TraceState g_trace;
 
+void trace_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);  // graph node
+    else cudaEventRecord(e, s);
+}
 void trace_pre(cudaStream_t s) {
-    if (g_trace.active && !g_trace.started && g_trace.cap > 0) {
-        cudaEventRecordWithFlags(g_trace.ev[0], s, cudaEventRecordExternal);   // a graph node under capture
-        g_trace.started = true;
-    }
+    if (g_trace.active && g_trace.n == g_trace.first && g_trace.cap > 0) trace_record(g_trace.ev[0], s);
 }
 void trace_post(const char* name, cudaStream_t s) {
-    if (g_trace.active && g_trace.n + 1 < g_trace.cap) {
-        cudaEventRecordWithFlags(g_trace.ev[g_trace.n + 1], s, cudaEventRecordExternal);
-        g_trace.names[g_trace.n++] = name;
-    }
+    if (!g_trace.active) return;
+    const int w = g_trace.n - g_trace.first;                 // position inside the window
+    if (w >= 0 && w + 1 < g_trace.cap) trace_record(g_trace.ev[w + 1], s);
+    if (g_trace.n < kMaxTrace) g_trace.names[g_trace.n] = name;
+    ++g_trace.n;
 }
 
 // Every kernel launch of the library goes through this macro.
@@ -204,18 +208,19 @@ extern "C" {
 
 const char* int4_last_error(void) { return g_last_error.c_str(); }
 
-i4_status int4_trace_begin(void* const* events, int32_t capacity) {
-    if (!events || capacity < 2 || capacity > kMaxTrace + 1) return fail(I4_ERR_ARG, "int4_trace_begin: 2 <= capacity <= %d", kMaxTrace + 1);
+i4_status int4_trace_begin(void* const* events, int32_t capacity, int32_t first_launch) {
+    if (!events || capacity < 2 || capacity > kMaxTrace + 1 || first_launch < 0)
+        return fail(I4_ERR_ARG, "int4_trace_begin: 2 <= capacity <= %d, first_launch >= 0", kMaxTrace + 1);
     for (int i = 0; i < capacity; ++i) g_trace.ev[i] = static_cast<cudaEvent_t>(events[i]);
     g_trace.cap = capacity;
+    g_trace.first = first_launch;
     g_trace.n = 0;
-    g_trace.started = false;
     g_trace.active = true;
     return I4_OK;
 }
 
 int32_t int4_trace_end(const char** names, int32_t capacity) {
-    const int n = g_trace.n;
+    const int n = g_trace.n < kMaxTrace ? g_trace.n : kMaxTrace;
     for (int i = 0; i < n && i < capacity; ++i) names[i] = g_trace.names[i];
     g_trace.active = false;
     g_trace.cap = 0;
