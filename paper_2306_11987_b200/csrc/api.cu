@@ -191,7 +191,7 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
     const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
     bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), 128) &&
               make_tmap_i8(&tb, B.p, uint64_t(B.inner), uint64_t(B.rows), uint64_t(B.pitch),
-                           args.b_mn ? 128u : uint32_t(bn));
+                           args.b_mn ? 128u : uint32_t(bn / i4::kGemmCG));
     if (args.epi == i4::EPI_DGRAD) tc = ta;                 // grad_X is written with red.add, no map
     else ok = ok && make_tmap_out(&tc, args.out, args.out_bf16 != 0, args.epi == i4::EPI_INT32,
                                   uint64_t(args.Nn), uint64_t(args.M));

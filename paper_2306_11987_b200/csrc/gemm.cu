@@ -9,12 +9,18 @@
 //   transposed in memory (the paper's CUTLASS path needed explicit
 //   transpose+contiguous copies).
 //
-// Structure (one CTA per SM, persistent over output tiles, warp-specialised):
-//   warp 0   TMA producer: 128-byte-swizzled A (128 x 128 B) and B (BN x 128 B)
-//            tiles into a STAGES-deep shared-memory ring (mbarrier full/empty).
-//   warp 1   allocates 2 x BN TMEM columns; one lane issues tcgen05.mma
-//            (M = 128, N = BN, K = 32 per instruction, 4 per 128-deep k-block)
-//            and tcgen05.commit to release smem stages / publish accumulators.
+// Structure (one CTA per SM, persistent over output tiles, warp-specialised).
+// CG = 2 (default): a CTA pair (thread-block cluster of 2 on one TPC) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2: each CTA stages its 128 rows of
+// A and BN/2 rows of B, so per-SM operand traffic is half that of a 1-SM
+// 128 x BN tile; the leader CTA issues the MMAs for both.
+//   warp 0   TMA producer: 128-byte-swizzled A (128 x 128 B) and B (BN/CG x 128 B)
+//            tiles into a STAGES-deep shared-memory ring; completion counted on
+//            the leader's mbarrier (2-SM TMA), slots released by a multicast commit.
+//   warp 1   allocates 2 x BN TMEM columns (cta_group::CG); the leader's lane 0
+//            issues tcgen05.mma (M = 128 CG, N = BN, K = 32 per instruction, 4 per
+//            128-deep k-block) and tcgen05.commit to release stages / publish
+//            accumulators to both CTAs.
 //   warps 2-5  epilogue: tcgen05.ld (32 lanes x 32 columns) -> registers, then
 //            EPI_INT32  raw accumulators (bit-exact parity checks)
 //            EPI_FWD    Y = fl32(acc) * fl32(s_x s_w)   (HQ-MM step 4)
@@ -40,10 +46,10 @@ constexpr int kRingBytes = 192 * 1024;
 constexpr int kStageOutBytes = 4096;         // per epilogue warp per buffer: 32 rows x 128 B
 constexpr int kEpiWarps = 4;
 
-template <int BN>
+template <int BN, int CG>
 struct GemmCfg {
     static constexpr int A_BYTES = kBM * kBK;
-    static constexpr int B_BYTES = BN * kBK;
+    static constexpr int B_BYTES = (BN / CG) * kBK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = kRingBytes / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
@@ -56,11 +62,13 @@ __device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
     return buf + r * 128 + ((c ^ (r & 7)) << 4);
 }
 
-template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
+template <int BN, int EPI, int CH, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, CG>;
+    constexpr int BMP = kBM * CG;                // rows per (pair) tile
+    constexpr int BNC = BN / CG;                 // B rows / columns staged by this CTA
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_dyn[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -74,11 +82,14 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int unit0 = int(blockIdx.x) / CG, n_units = int(gridDim.x) / CG;
 
     // problem size (possibly data-dependent)
     const int M = g.m_dev ? __ldg(g.m_dev) : g.M;
     const int K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
-    const int m_tiles = (M + kBM - 1) / kBM;
+    const int m_tiles = (M + BMP - 1) / BMP;
     const int n_tiles = (g.Nn + BN - 1) / BN;
     const int total = m_tiles * n_tiles;
     const int nk = (K + kBK - 1) / kBK;
@@ -88,12 +99,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         tma_prefetch_desc(&tmB);
         if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps * 32); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CG * kEpiWarps); }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    if (warp == 1) tmem_alloc<CG>(tmem_slot, Cfg::TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -101,35 +112,49 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // ------------------------------------------------------------- producer
         if (lane == 0) {
             int stage = 0; uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
+            for (int tile = unit0; tile < total; tile += n_units) {
+                const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
+                const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
                     uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
                     uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
-                    if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
-                    else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
-                    if (B_MN) {
+                    if constexpr (CG == 2) {
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (A_MN) tma_load_2d_2sm(a_dst, &tmA, fb, m0, kb * kBK);
+                        else      tma_load_2d_2sm(a_dst, &tmA, fb, kb * kBK, m0);
+                        if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 128; ++j)
-                            tma_load_2d(b_dst + j * 128 * kBK, &tmB, &full[stage], n0 + 128 * j, kb * kBK);
+                            for (int j = 0; j < BNC / 128; ++j)
+                                tma_load_2d_2sm(b_dst + j * 128 * kBK, &tmB, fb, nb + 128 * j, kb * kBK);
+                        } else {
+                            tma_load_2d_2sm(b_dst, &tmB, fb, kb * kBK, nb);
+                        }
                     } else {
-                        tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, n0);
+                        if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
+                        else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
+                        if (B_MN) {
+#pragma unroll
+                            for (int j = 0; j < BNC / 128; ++j)
+                                tma_load_2d(b_dst + j * 128 * kBK, &tmB, &full[stage], nb + 128 * j, kb * kBK);
+                        } else {
+                            tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, nb);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_i8(kBM, BN, A_MN, B_MN);
+        // ------------------------------------------------------------- MMA issuer (leader CTA)
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = idesc_i8(BMP, BN, A_MN, B_MN);
             // descriptor advance per K = 32 MMA: K-major +32 B; MN-major +32 rows x 128 B
             constexpr uint64_t a_step = A_MN ? (32 * 128) >> 4 : 32 >> 4;
             constexpr uint64_t b_step = B_MN ? (32 * 128) >> 4 : 32 >> 4;
             int stage = 0; uint32_t phase = 0; int it = 0;
-            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+            for (int tile = unit0; tile < total; tile += n_units, ++it) {
                 const int as = it & 1;
                 const uint32_t ap = (it >> 1) & 1;
                 mbar_wait(&tempty[as], ap ^ 1);
@@ -143,12 +168,16 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const uint64_t adesc = A_MN ? sdesc_mnmajor_sw128(a_addr, 128 * kBK) : sdesc_kmajor_sw128(a_addr);
                     const uint64_t bdesc = B_MN ? sdesc_mnmajor_sw128(b_addr, 128 * kBK) : sdesc_kmajor_sw128(b_addr);
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 32; ++kk)
-                        umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
-                    umma_commit(&empty[stage]);
+                    for (int kk = 0; kk < kBK / 32; ++kk) {
+                        if constexpr (CG == 2)
+                            umma_i8_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        else
+                            umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    if constexpr (CG == 2) umma_commit_2sm(&empty[stage]); else umma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                umma_commit(&tfull[as]);
+                if constexpr (CG == 2) umma_commit_2sm(&tfull[as]); else umma_commit(&tfull[as]);
             }
         }
     } else {
@@ -161,10 +190,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         float sd = 1.0f;
         if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
         int it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        for (int tile = unit0; tile < total; tile += n_units, ++it) {
             const int as = it & 1;
             const uint32_t ap = (it >> 1) & 1;
-            const int m0 = (tile / n_tiles) * kBM, n0 = (tile % n_tiles) * BN;
+            const int m0 = (tile / n_tiles) * BMP + kBM * int(rank), n0 = (tile % n_tiles) * BN;
             const int row = m0 + r_in_tile;
             mbar_wait(&tfull[as], ap);
             tc_fence_after();
@@ -194,7 +223,11 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 tmem_ld_wait();
                 if (c + CW >= BN) {                   // accumulator stage drained -> MMA may reuse it
                     tc_fence_before();
-                    mbar_arrive(&tempty[as]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+                        else mbar_arrive(&tempty[as]);
+                    }
                 }
                 if (nk == 0) {
 #pragma unroll
@@ -292,34 +325,46 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (warp == 1) tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
 }
 
 int gemm_block_n(int Nn, bool b_mn) {
-    if (Nn % 256 == 0) return 256;
-    if (b_mn) return Nn > 128 ? 256 : 128;      // MN-major tiles are whole 128-byte atoms
+    if (Nn % 256 == 0 || b_mn) return 256;      // MN-major B halves are whole 128-byte atoms
     if (Nn % 128 == 0) return 128;
     return 64;
 }
 
+constexpr int kCG = kGemmCG;                    // CTA pairs (cta_group::2) for every GEMM
+
 template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
 static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    auto kern = gemm_i8_kernel<BN, EPI, CH, A_MN, B_MN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
+    auto kern = gemm_i8_kernel<BN, EPI, CH, A_MN, B_MN, kCG>;
+    constexpr int smem = GemmCfg<BN, kCG>::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kGemmThreads, GemmCfg<BN>::SMEM, s>>>(*reinterpret_cast<const CUtensorMap*>(m.a),
-                                                        *reinterpret_cast<const CUtensorMap*>(m.b),
-                                                        *reinterpret_cast<const CUtensorMap*>(m.c), g);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(m.a),
+                              *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c), g);
 }
 
 template <int EPI, int CH, bool A_MN, bool B_MN>
 static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
     if (bn == 256) return launch_one<256, EPI, CH, A_MN, B_MN>(m, g, grid, s);
-    if (bn == 128) return launch_one<128, EPI, CH, A_MN, B_MN>(m, g, grid, s);
-    if constexpr (!B_MN && CH <= 64) return launch_one<64, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+    if constexpr (!B_MN) {
+        if (bn == 128) return launch_one<128, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+        if constexpr (CH <= 64) return launch_one<64, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+    }
     return cudaErrorInvalidValue;
 }
 
@@ -334,9 +379,10 @@ static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, int
 
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s) {
     const int bn = gemm_block_n(g.Nn, g.b_mn);
-    const int64_t tiles = int64_t((g.M + kBM - 1) / kBM) * ((g.Nn + bn - 1) / bn);   // g.M = bound when m_dev
-    int grid = int(tiles < num_sms ? tiles : num_sms);
-    if (grid < 1) grid = 1;
+    const int64_t tiles = int64_t((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
+    const int64_t pairs = num_sms / kCG;
+    int grid = kCG * int(tiles < pairs ? tiles : pairs);
+    if (grid < kCG) grid = kCG;
     switch (g.epi) {
         case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, grid, s);
         case EPI_DGRAD: return dispatch_ch<EPI_DGRAD, false, true>(bn, m, g, grid, s);

@@ -65,6 +65,7 @@ struct GemmArgs {
     const int8_t* wexp;       // dgrad: weight exponent of each A row
     int32_t n_tokens;         // dgrad: N (item id = h*N + t)
 };
+constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
 struct GemmMaps { const void* a; const void* b; const void* c; };   // CUtensorMap* (host)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
 int gemm_block_n(int Nn, bool b_mn);

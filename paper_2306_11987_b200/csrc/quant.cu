@@ -50,9 +50,9 @@ struct HqJob {
     int blocks;                          // CTAs assigned to this job
 };
 
-constexpr int kHqGroup = 8;              // chunks (of 256 columns) loaded per group
+constexpr int kHqGroup = 4;              // chunks (of 256 columns) loaded per group
 
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, 4)
 hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k) {
     const bool second = int(blockIdx.x) >= j0.blocks;
     const HqJob& J = second ? j1 : j0;
@@ -98,11 +98,11 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k) {
                 for (int s = 3; s < 7; ++s) {
                     if (s < k) {
                         const int lm = 1 << (s - 3);
-                        const bool upper = (lane & lm) != 0;
+                        const float sgn = (lane & lm) ? -1.0f : 1.0f;   // upper lane: o - v, lower: v + o
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const float o = __shfl_xor_sync(0xFFFFFFFFu, v[i], lm);
-                            v[i] = upper ? __fsub_rn(o, v[i]) : __fadd_rn(v[i], o);
+                            v[i] = __fmaf_rn(sgn, v[i], o);              // one rounding, = the add/sub
                         }
                     }
                 }
@@ -114,7 +114,7 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k) {
                     const float sv = __fmul_rn(v[i], J.r);
                     const int c = __float2int_rn(fminf(fmaxf(sv, -7.0f), 7.0f));
                     q[i] = c;
-                    m8 |= uint32_t((sv >= -7.0f) && (sv <= 7.0f)) << i;
+                    m8 |= uint32_t(fabsf(sv) <= 7.0f) << i;
                     sq += c * c;
                 }
                 // 32-column mask word = 4 lanes x 8 bits
@@ -208,7 +208,7 @@ cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, 
 // ---------------------------------------------------------------------------
 constexpr int kBsGroup = 4;
 
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, 4)
 bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t* __restrict__ amax_bits,
                 uint32_t k0, uint32_t k1, uint32_t call_id, int64_t token_offset,
                 int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, float* __restrict__ s_down_out) {
@@ -253,9 +253,12 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
                         // A = ceil(|v| 2^32) (|v| 2^32 is exact in fp32): high word = floor|v|
                         // (+1 when the fraction's threshold wraps to 2^32), low word =
                         // T = ceil(frac|v| 2^32) mod 2^32; P(round up) = T / 2^32 exactly.
-                        const float sv = fminf(fmaxf(__fmul_rn(v[i], r8), -119.0f), 119.0f);
-                        const uint64_t A = __float2ull_ru(__fmul_rn(fabsf(sv), 4294967296.0f));
-                        const int mag = int(A >> 32) + int(u[i] < uint32_t(A));
+                        // a = min(|g r8|, 119); floor / fraction exact in fp32; T = ceil(f 2^32) < 2^32
+                        const float sv = __fmul_rn(v[i], r8);
+                        const float a = fminf(fabsf(sv), 119.0f);
+                        const float fl = floorf(a);
+                        const uint32_t T = __float2uint_ru(__fmul_rn(__fsub_rn(a, fl), 4294967296.0f));
+                        const int mag = int(fl) + int(u[i] < T);
                         q = sv < 0.0f ? -mag : mag;
                     }
                     hi[i] = (q + 8) >> 4;                                     // floor division
