@@ -282,8 +282,9 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     return I4_OK;
 }
 
-i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed, uint32_t call_id,
-                       int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* stream) {
+static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed,
+                            uint32_t call_id, int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan,
+                            cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words) {
     I4_RETURN_IF(check_device());
     if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->items_w ||
         !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x)
@@ -297,7 +298,6 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
                     (long long)kMaxBwdTokens);
     if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
     if (!aligned16(dY) || !aligned16(plan->hilo)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     I4_LAUNCH(i4::launch_amax_bf16(static_cast<const uint16_t*>(dY), N * C, plan->amax_bits, s), "amax", s);
     I4_LAUNCH(i4::launch_bitsplit(static_cast<const uint16_t*>(dY), N, C, plan->amax_bits, seed, call_id,
                                   token_offset, plan->hilo, plan->a_sq, plan->s_down, s), "bitsplit", s);
@@ -312,17 +312,59 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
     a.token_offset = token_offset;
     a.items[0] = plan->items_w; a.wexp[0] = plan->wexp_w; a.count[0] = plan->count_w;
     a.items[1] = plan->items_x; a.wexp[1] = plan->wexp_x; a.count[1] = plan->count_x;
+    a.zero_words = zero_words; a.n_zero_words = n_zero_words;
     I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
     return I4_OK;
 }
 
-size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) {
-    const int64_t kcap = round_up(2 * N, 128);
-    const int64_t ax = round_up((2 * N + 128) * C, 256);
-    const int64_t aw = round_up(C * kcap, 256);
-    const int64_t bw = round_up(D * kcap, 256);
-    return size_t(ax + aw + bw);
+i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed, uint32_t call_id,
+                       int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* stream) {
+    return bitsplit_lss_impl(dY, N, C, x_sqnorm, seed, call_id, token_offset, mode, plan,
+                             static_cast<cudaStream_t>(stream), nullptr, 0);
 }
+
+}  // extern "C"
+
+namespace {
+
+// Backward workspace layout (bytes, each region 256-aligned):
+//   A_X [2N + 128, C] | A_W [kcap, C] | B_W [kcap, D] | split-K partials (dgrad, wgrad) | split-K flags
+struct BwdWs {
+    int8_t* a_x; int8_t* a_w; int8_t* b_w;
+    int32_t* part_x; int32_t* part_w; uint32_t* flags_x; uint32_t* flags_w;
+    size_t total;
+};
+
+BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
+    const int64_t kcap = round_up(2 * N, 128);
+    BwdWs w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += size_t(round_up(int64_t(bytes), 256)); return o; };
+    const size_t o_ax = take(size_t((2 * N + 128) * C));
+    const size_t o_aw = take(size_t(C * kcap));
+    const size_t o_bw = take(size_t(D * kcap));
+    const size_t o_px = take(i4::gemm_split_partial_bytes());
+    const size_t o_pw = take(i4::gemm_split_partial_bytes());
+    const size_t o_f = take(2 * i4::gemm_split_flag_words() * sizeof(uint32_t));
+    w.total = off;
+    if (ws) {
+        uint8_t* b = static_cast<uint8_t*>(ws);
+        w.a_x = reinterpret_cast<int8_t*>(b + o_ax);
+        w.a_w = reinterpret_cast<int8_t*>(b + o_aw);
+        w.b_w = reinterpret_cast<int8_t*>(b + o_bw);
+        w.part_x = reinterpret_cast<int32_t*>(b + o_px);
+        w.part_w = reinterpret_cast<int32_t*>(b + o_pw);
+        w.flags_x = reinterpret_cast<uint32_t*>(b + o_f);
+        w.flags_w = w.flags_x + i4::gemm_split_flag_words();
+    }
+    return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) { return carve_bwd_ws(nullptr, N, D, C).total; }
 
 i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                           int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, float* dX, float* dW,
@@ -335,13 +377,19 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     if (ws_bytes < int4_bwd_workspace_size(N, D, C))
         return fail(I4_ERR_WORKSPACE, "int4_linear_bwd: ws_bytes %zu < %zu", ws_bytes, int4_bwd_workspace_size(N, D, C));
     if (!aligned16(dX) || !aligned16(dW) || !aligned16(ws)) return fail(I4_ERR_ALIGN, "int4_linear_bwd: unaligned pointer");
-    I4_RETURN_IF(bitsplit_lss(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, stream));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    {
+        const BwdWs w0 = carve_bwd_ws(ws, N, D, C);
+        // the sampler launch also zeroes the split-K flags of the two GEMMs below
+        I4_RETURN_IF(bitsplit_lss_impl(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, s,
+                                       w0.flags_x, int32_t(2 * i4::gemm_split_flag_words())));
+    }
 
     const int64_t kcap = round_up(2 * N, 128);
-    int8_t* a_x = static_cast<int8_t*>(ws);
-    int8_t* a_w = a_x + round_up((2 * N + 128) * C, 256);
-    int8_t* b_w = a_w + round_up(C * kcap, 256);
+    const BwdWs w = carve_bwd_ws(ws, N, D, C);
+    int8_t* a_x = w.a_x;
+    int8_t* a_w = w.a_w;
+    int8_t* b_w = w.b_w;
 
     I4_LAUNCH(i4::launch_compact_rows(plan->hilo, C, plan->items_x, plan->count_x, 2 * N, a_x, s), "compact_rows", s);
     I4_LAUNCH(i4::launch_compact_wgrad(plan->hilo, cache->xq, N, C, D, plan->items_w, plan->wexp_w, plan->count_w,
@@ -362,6 +410,8 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.wexp = plan->wexp_x;
         g.n_tokens = int32_t(N);
         g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
+        g.partial = w.part_x; g.flags = w.flags_x;
+        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;
         I4_RETURN_IF(gemm(Operand{a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
@@ -375,27 +425,40 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.k_had = k;
         g.mask = cache->w_mask;
         g.a_mn = 1; g.b_mn = 1;                  // A_W [K, C], B_W [K, D]: both MN-major
+        g.partial = w.part_w; g.flags = w.flags_w;
+        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;
         I4_RETURN_IF(gemm(Operand{a_w, kcap, C, C}, Operand{b_w, kcap, D, D}, g, s));
     }
     return I4_OK;
 }
 
 i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B, int32_t b_mn_major, int64_t M,
-                            int64_t Nn, int64_t K, int32_t* acc, void* stream) {
+                            int64_t Nn, int64_t K, int32_t* acc, void* ws, size_t ws_bytes, void* stream) {
     I4_RETURN_IF(check_device());
     if (!A || !B || !acc) return fail(I4_ERR_ARG, "int4_gemm_s8s8s32: NULL pointer");
-    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16) || false)
+    if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16))
         return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: unsupported shape M=%lld Nn=%lld K=%lld", (long long)M,
                     (long long)Nn, (long long)K);
+    if (ws && ws_bytes < int4_gemm_workspace_size()) return fail(I4_ERR_WORKSPACE, "int4_gemm_s8s8s32: ws too small");
     if (!aligned16(A) || !aligned16(B) || !aligned16(acc)) return fail(I4_ERR_ALIGN, "int4_gemm_s8s8s32: unaligned pointer");
     i4::GemmArgs g{};
     g.M = int32_t(M); g.Nn = int32_t(Nn); g.K = int32_t(K);
     g.a_mn = a_mn_major != 0; g.b_mn = b_mn_major != 0;
     g.epi = i4::EPI_INT32;
     g.out = acc;
+    if (ws) {                                    // deterministic split-K over the caller's zeroed workspace
+        g.partial = static_cast<int32_t*>(ws);
+        g.flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + i4::gemm_split_partial_bytes());
+        g.max_tiles_split = i4::kSplitMaxTiles;
+        g.max_splits = i4::kSplitMaxK;
+    }
     const Operand a = g.a_mn ? Operand{A, K, M, M} : Operand{A, M, K, K};
     const Operand b = g.b_mn ? Operand{B, K, Nn, Nn} : Operand{B, Nn, K, K};
     return gemm(a, b, g, static_cast<cudaStream_t>(stream));
+}
+
+size_t int4_gemm_workspace_size(void) {
+    return i4::gemm_split_partial_bytes() + i4::gemm_split_flag_words() * sizeof(uint32_t);
 }
 
 }  // extern "C"

@@ -62,6 +62,33 @@ __device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
     return buf + r * 128 + ((c ^ (r & 7)) << 4);
 }
 
+// Deterministic split-K (used when there are fewer output tiles than CTA pairs,
+// e.g. the grad_W GEMM whose K is the sampled-item count): S splits of the K
+// range are separate work units; the unit of the highest K split writes its raw
+// INT32 accumulators to a workspace tile, each lower split waits for it, adds
+// its own accumulators (integer adds: exact and order-independent) and passes
+// it on, and split 0 runs the real epilogue.  Units are numbered so that a unit
+// only ever waits on a lower-numbered one, so a persistent grid of co-resident
+// CTAs cannot deadlock.
+__device__ __forceinline__ int choose_splits(int tiles, int pairs, int nk, int max_splits) {
+    int best = 1, best_cost = ((tiles + pairs - 1) / pairs) * nk;
+    for (int s = 2; s <= max_splits; ++s) {
+        if (nk < 2 * s) break;
+        const int cost = ((s * tiles + pairs - 1) / pairs) * ((nk + s - 1) / s);
+        if (cost < best_cost) { best = s; best_cost = cost; }
+    }
+    return best;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 template <int BN, int EPI, int CH, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -84,15 +111,22 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
-    const int unit0 = int(blockIdx.x) / CG, n_units = int(gridDim.x) / CG;
+    const int pair0 = int(blockIdx.x) / CG, n_pairs = int(gridDim.x) / CG;
 
-    // problem size (possibly data-dependent)
+    // problem size (possibly data-dependent) and work units
     const int M = g.m_dev ? __ldg(g.m_dev) : g.M;
     const int K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
     const int m_tiles = (M + BMP - 1) / BMP;
     const int n_tiles = (g.Nn + BN - 1) / BN;
-    const int total = m_tiles * n_tiles;
+    const int T = m_tiles * n_tiles;
     const int nk = (K + kBK - 1) / kBK;
+    const int S = (g.partial != nullptr && T <= g.max_tiles_split) ? choose_splits(T, n_pairs, nk, g.max_splits) : 1;
+    const int units = S * T;
+    // unit u: tile = u % T; split s = S - 1 - u / T (s = 0 is the final one), k-blocks [kb0, kb1)
+#define UNIT_DECODE(u)                                          \
+    const int tile = (u) % T;                                   \
+    const int split = S - 1 - (u) / T;                          \
+    const int kb0 = split * nk / S, kb1 = (split + 1) * nk / S;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -112,10 +146,11 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // ------------------------------------------------------------- producer
         if (lane == 0) {
             int stage = 0; uint32_t phase = 0;
-            for (int tile = unit0; tile < total; tile += n_units) {
+            for (int u = pair0; u < units; u += n_pairs) {
+                UNIT_DECODE(u)
                 const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
                 const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
                     uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
@@ -154,13 +189,15 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             constexpr uint64_t a_step = A_MN ? (32 * 128) >> 4 : 32 >> 4;
             constexpr uint64_t b_step = B_MN ? (32 * 128) >> 4 : 32 >> 4;
             int stage = 0; uint32_t phase = 0; int it = 0;
-            for (int tile = unit0; tile < total; tile += n_units, ++it) {
+            for (int u = pair0; u < units; u += n_pairs, ++it) {
+                UNIT_DECODE(u)
+                (void)tile;
                 const int as = it & 1;
                 const uint32_t ap = (it >> 1) & 1;
                 mbar_wait(&tempty[as], ap ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(as * BN);
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -169,10 +206,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const uint64_t bdesc = B_MN ? sdesc_mnmajor_sw128(b_addr, 128 * kBK) : sdesc_kmajor_sw128(b_addr);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 32; ++kk) {
-                        if constexpr (CG == 2)
-                            umma_i8_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
-                        else
-                            umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+                        if constexpr (CG == 2) umma_i8_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, acc);
+                        else umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, acc);
                     }
                     if constexpr (CG == 2) umma_commit_2sm(&empty[stage]); else umma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -190,11 +226,24 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         float sd = 1.0f;
         if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
         int it = 0;
-        for (int tile = unit0; tile < total; tile += n_units, ++it) {
+        for (int u = pair0; u < units; u += n_pairs, ++it) {
+            UNIT_DECODE(u)
             const int as = it & 1;
             const uint32_t ap = (it >> 1) & 1;
             const int m0 = (tile / n_tiles) * BMP + kBM * int(rank), n0 = (tile % n_tiles) * BN;
             const int row = m0 + r_in_tile;
+            const bool no_acc = kb1 == kb0;            // empty K range: accumulator is zero
+            // split-K bookkeeping for this warp's 32 rows of the tile
+            int32_t* part = nullptr;
+            uint32_t* flag = nullptr;
+            if (S > 1) {
+                part = g.partial + (int64_t(tile) * BMP + kBM * int(rank) + r_in_tile) * BN;
+                flag = g.flags + (tile * CG + int(rank)) * kEpiWarps + lg;
+                if (split < S - 1) {                   // wait until the higher splits are in `part`
+                    if (lane == 0) while (ld_acquire_u32(flag) < uint32_t(S - 1 - split)) { }
+                    __syncwarp();
+                }
+            }
             mbar_wait(&tfull[as], ap);
             tc_fence_after();
             const uint32_t t_row = tmem_base + (uint32_t(lg * 32) << 16) + uint32_t(as * BN);
@@ -229,11 +278,33 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         else mbar_arrive(&tempty[as]);
                     }
                 }
-                if (nk == 0) {
+                if (nk == 0 || no_acc) {
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) r[q][i] = 0;
+                }
+                if (S > 1) {
+                    int32_t* pc = part + c;
+                    if (split < S - 1) {               // add the higher splits' partial sums (exact)
+#pragma unroll
+                        for (int q = 0; q < CW / 32; ++q)
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4) {
+                                const int4 v = __ldcg(reinterpret_cast<const int4*>(pc + 32 * q + i));
+                                r[q][i] += uint32_t(v.x); r[q][i + 1] += uint32_t(v.y);
+                                r[q][i + 2] += uint32_t(v.z); r[q][i + 3] += uint32_t(v.w);
+                            }
+                    }
+                    if (split > 0) {                   // pass the running sum on; no output yet
+#pragma unroll
+                        for (int q = 0; q < CW / 32; ++q)
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4)
+                                __stcg(reinterpret_cast<int4*>(pc + 32 * q + i),
+                                       make_int4(int(r[q][i]), int(r[q][i + 1]), int(r[q][i + 2]), int(r[q][i + 3])));
+                        continue;
+                    }
                 }
                 const int col0 = n0 + c;
                 if (col0 >= g.Nn) continue;           // ragged N (MN-major B): nothing to write
@@ -319,7 +390,17 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     sbuf ^= 1;
                 }
             }
+            if (S > 1) {
+                __syncwarp();
+                if (split > 0) {                       // publish: this warp's rows now hold S - split splits
+                    __threadfence();
+                    if (lane == 0) st_release_u32(flag, uint32_t(S - split));
+                } else if (lane == 0) {
+                    *flag = 0u;                        // consumed: reset for the next launch
+                }
+            }
         }
+#undef UNIT_DECODE
         if (lane == 0) bulk_wait<0>();
         __syncwarp();
     }
@@ -329,6 +410,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tc_fence_after();
     if (warp == 1) tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
 }
+
+size_t gemm_split_partial_bytes() { return size_t(kSplitMaxTiles) * (kBM * kGemmCG) * 256 * sizeof(int32_t); }
+size_t gemm_split_flag_words() { return size_t(kSplitMaxTiles) * kGemmCG * kEpiWarps; }
 
 int gemm_block_n(int Nn, bool b_mn) {
     if (Nn % 256 == 0 || b_mn) return 256;      // MN-major B halves are whole 128-byte atoms

@@ -33,6 +33,8 @@ struct SamplerArgs {
     int32_t* items[2];        // [0] grad_W mask, [1] grad_X mask
     int8_t* wexp[2];
     int32_t* count[2];
+    uint32_t* zero_words;     // optional: words zeroed by the launch (split-K flags of the GEMMs)
+    int32_t n_zero_words;
 };
 int sampler_max_tokens();
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
@@ -64,7 +66,16 @@ struct GemmArgs {
     const int32_t* items;     // dgrad: item id of each A row
     const int8_t* wexp;       // dgrad: weight exponent of each A row
     int32_t n_tokens;         // dgrad: N (item id = h*N + t)
+    // deterministic split-K (optional): INT32 partial tiles + per-warp flags (zeroed before use)
+    int32_t* partial;         // [max_tiles_split, 128 CG, BN] int32, or null (no split-K)
+    uint32_t* flags;          // [max_tiles_split, CG, 4]
+    int32_t max_tiles_split;  // split only when the tile count is at most this
+    int32_t max_splits;
 };
+constexpr int kSplitMaxTiles = 96;        // workspace tiles reserved for split-K
+constexpr int kSplitMaxK = 4;
+size_t gemm_split_partial_bytes();        // bytes of one GEMM's split-K partial workspace
+size_t gemm_split_flag_words();
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
 struct GemmMaps { const void* a; const void* b; const void* c; };   // CUtensorMap* (host)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);

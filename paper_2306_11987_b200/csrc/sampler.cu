@@ -102,6 +102,8 @@ lss_sampler_kernel(SamplerArgs a) {
     const int e_max = mask_id == 0 ? kEMaxW : kEMaxX;
     const uint32_t purpose = mask_id == 0 ? kPurposeMaskW : kPurposeMaskX;
     int parity = 0;
+    if (blockIdx.y == 0 && rank == 0)
+        for (int i = threadIdx.x; i < a.n_zero_words; i += kSamplerThreads) a.zero_words[i] = 0u;
 
     // ---- scores -------------------------------------------------------------
     uint64_t sum_pos = 0; uint32_t cnt_pos = 0;
