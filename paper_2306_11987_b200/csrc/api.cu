@@ -411,7 +411,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.n_tokens = int32_t(N);
         g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
         g.partial = w.part_x; g.flags = w.flags_x;
-        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;
+        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
         I4_RETURN_IF(gemm(Operand{a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
@@ -426,7 +426,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.mask = cache->w_mask;
         g.a_mn = 1; g.b_mn = 1;                  // A_W [K, C], B_W [K, D]: both MN-major
         g.partial = w.part_w; g.flags = w.flags_w;
-        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;
+        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
         I4_RETURN_IF(gemm(Operand{a_w, kcap, C, C}, Operand{b_w, kcap, D, D}, g, s));
     }
     return I4_OK;
