@@ -220,14 +220,12 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2306_11987_b200 as i4
+    from paper_2306_11987_b200 import dist as pdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = pdist.env_world()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    pdist.init("nccl", device=dev)
     cfg = synth.CONFIGS[args.config]
     N, D, C, k = cfg["N"], cfg["D"], cfg["C"], cfg["k"]
     mode = MODES[args.mode]
@@ -248,7 +246,7 @@ def run_ours(args):
     Y = torch.empty(N, C, dtype=torch.bfloat16, device=dev)
     dX = torch.empty(N, D, dtype=torch.float32, device=dev)
     dW = torch.empty(C, D, dtype=torch.float32, device=dev)
-    token_offset = rank * N
+    token_offset = pdist.token_offset(rank, N)           # global token index of this shard
     flush_w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     flush_r = torch.ones(32 * 1024 * 1024, dtype=torch.int64, device=dev)
 
@@ -303,8 +301,8 @@ def run_ours(args):
             flush.zero_()
             ev_a.record()
             g.replay()
-            if world > 1:
-                dist.all_reduce(dW if other_dw is None else other_dw)
+            if world > 1:                                 # the one exchange: sum of grad_W partials
+                pdist.allreduce_grad_w(dW if other_dw is None else other_dw)
             ev_b.record()
             torch.cuda.synchronize()
             out.append(ev_a.elapsed_time(ev_b))
@@ -324,10 +322,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = statistics.mean(step_ms)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = pdist.max_over_ranks(ms, dev)
     value = 6.0 * N * C * D * world / (ms_max * 1e-3) / 1e12
 
     # ---- cuBLAS BF16 baseline (same protocol): Y = X W^T, dX = dY W, dW = dY^T X
@@ -418,19 +413,17 @@ def run_ours(args):
             X.copy_(hx, non_blocking=True); W.copy_(hw, non_blocking=True); G.copy_(hg, non_blocking=True)
             step_body()
             if world > 1:
-                dist.all_reduce(dW)
+                pdist.allreduce_grad_w(dW)
             hY.copy_(Y, non_blocking=True); hdX.copy_(dX, non_blocking=True); hdW.copy_(dW, non_blocking=True)
             a1.record()
             torch.cuda.synchronize()
             if i >= args.warmup:
                 e2e_ms.append(a0.elapsed_time(a1))
-        t_e2e = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        e2e = {"value": 6.0 * N * C * D * world / (float(t_e2e.item()) * 1e-3) / 1e12, "unit": UNIT,
+        t_e2e = pdist.max_over_ranks(statistics.mean(e2e_ms), dev)
+        e2e = {"value": 6.0 * N * C * D * world / (t_e2e * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(hx.numel() * 2 + hw.numel() * 2 + hg.numel() * 2),
                "d2h_bytes_per_step": int(hY.numel() * 2 + hdX.numel() * 4 + hdW.numel() * 4),
-               "ms_per_step": float(t_e2e.item()),
+               "ms_per_step": t_e2e,
                "path": "pinned host X, W, grad_Y -> device; Int4Linear.forward/backward (C ABI); Y, grad_X, grad_W -> pinned host"}
 
     line = None
