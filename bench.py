@@ -200,10 +200,8 @@ def algorithmic_work(name, N, D, C, kx, kw):
         return "ops", 2.0 * kw * C * D
     if name == "hadamard_quant":              # X and W: read bf16, write int8 codes + 1-bit mask (+ int32 norm)
         return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
-    if name == "amax":
-        return "bytes", 2.0 * N * C
-    if name == "bitsplit":                    # read bf16 grad_Y, write hi + lo planes, 2 norms
-        return "bytes", N * C * (2 + 2) + 8 * N
+    if name == "grad_split":                  # amax + SR + bit split: read bf16 grad_Y once (the amax
+        return "bytes", N * C * (2 + 2) + 8 * N  # pass's re-read is an implementation cost), write hi + lo planes
     if name == "compact_rows":
         return "bytes", 2.0 * kx * C
     if name == "compact_wgrad":
@@ -447,8 +445,8 @@ def run_ours(args):
     return 0
 
 
-KERNEL_NAMES = [("hadamard_quant_kernel", "hadamard_quant"), ("amax_bf16_kernel", "amax"),
-                ("bitsplit_kernel", "bitsplit"), ("lss_sampler_kernel", "lss_sampler"),
+KERNEL_NAMES = [("hadamard_quant_kernel", "hadamard_quant"), ("grad_split_kernel", "grad_split"),
+                ("lss_sampler_kernel", "lss_sampler"),
                 ("compact_rows_kernel", "compact_rows"), ("compact_wgrad_kernel", "compact_wgrad")]
 GEMM_EPI = {"0": "gemm_i8_int32", "1": "gemm_i8_fwd", "2": "gemm_i8_dgrad", "3": "gemm_i8_wgrad"}
 

@@ -96,8 +96,9 @@ typedef struct {
  * caller-allocated, written by bitsplit_lss:
  *   hilo     int8  [2N, C]     rows 0..N-1 = grad_up (high 4 bits), N..2N-1 = grad_down
  *   a_sq     int32 [2N]        sum_c code^2 per row of hilo
- *   amax_bits uint32 [1]       bf16 bit pattern of max |grad_Y| (scratch)
- *   s_down   float [1]         s_down = amax / 119 (s_up = 16 s_down), reading Z-9
+ *   amax_bits uint32 [1]       out: bf16 bit pattern of max |grad_Y|
+ *   s_down   float [1]         out: s_down = amax / 119 (s_up = 16 s_down), reading Z-9
+ *   scratch  uint32 [2048]     scratch (per-CTA partial maxima of the fused amax pass)
  *   items_w  int32 [2N + 128]  kept items of the grad_W mask, ascending ids h*N + t,
  *                              padded with the sentinel 2N up to a multiple of 128
  *   wexp_w   int8  [2N + 128]  log2 of each kept item's weight (~ m_i / p_i)
@@ -108,6 +109,7 @@ typedef struct {
     int32_t* a_sq;
     uint32_t* amax_bits;
     float* s_down;
+    uint32_t* scratch;
     int32_t* items_w;
     int8_t* wexp_w;
     int32_t* count_w;

@@ -45,7 +45,8 @@ class I4FwdCache(ctypes.Structure):
 
 class I4LssPlan(ctypes.Structure):
     _fields_ = [("hilo", ctypes.c_void_p), ("a_sq", ctypes.c_void_p), ("amax_bits", ctypes.c_void_p),
-                ("s_down", ctypes.c_void_p), ("items_w", ctypes.c_void_p), ("wexp_w", ctypes.c_void_p),
+                ("s_down", ctypes.c_void_p), ("scratch", ctypes.c_void_p), ("items_w", ctypes.c_void_p),
+                ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
                 ("count_x", ctypes.c_void_p)]
 
@@ -207,12 +208,14 @@ class Int4Linear:
         self.hilo = torch.empty(2 * N, C, dtype=i8, device=dev)
         self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
         self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
+        self.scratch = torch.zeros(2048, dtype=i32, device=dev)  # fused-amax block maxima
         self.items_w = torch.empty(n2, dtype=i32, device=dev)
         self.wexp_w = torch.empty(n2, dtype=i8, device=dev)
         self.items_x = torch.empty(n2, dtype=i32, device=dev)
         self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
         sp = self.scalars.data_ptr()
         self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
+                              scratch=self.scratch.data_ptr(),
                               items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
                               items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12)
         self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)

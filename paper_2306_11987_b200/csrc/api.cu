@@ -286,7 +286,7 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
                             uint32_t call_id, int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan,
                             cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words) {
     I4_RETURN_IF(check_device());
-    if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->items_w ||
+    if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
         !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x)
         return fail(I4_ERR_ARG, "bitsplit_lss: NULL pointer");
     if (mode != I4_LSS_BERNOULLI && mode != I4_LSS_KEEP_POSITIVE && mode != I4_LSS_NONE)
@@ -298,9 +298,8 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
                     (long long)kMaxBwdTokens);
     if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
     if (!aligned16(dY) || !aligned16(plan->hilo)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
-    I4_LAUNCH(i4::launch_amax_bf16(static_cast<const uint16_t*>(dY), N * C, plan->amax_bits, s), "amax", s);
-    I4_LAUNCH(i4::launch_bitsplit(static_cast<const uint16_t*>(dY), N, C, plan->amax_bits, seed, call_id,
-                                  token_offset, plan->hilo, plan->a_sq, plan->s_down, s), "bitsplit", s);
+    I4_LAUNCH(i4::launch_grad_split(static_cast<const uint16_t*>(dY), N, C, plan->scratch, seed, call_id, token_offset,
+                                    plan->hilo, plan->a_sq, plan->s_down, plan->amax_bits, s), "grad_split", s);
     i4::SamplerArgs a{};
     a.a_sq = plan->a_sq;
     a.x_sqnorm = x_sqnorm;

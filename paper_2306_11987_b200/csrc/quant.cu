@@ -12,6 +12,8 @@
 // latency per group instead of one per chunk).  Hadamard blocks of 2^k <= 8
 // columns are transformed in registers; larger blocks (k = 4..7) add
 // xor-shuffle butterfly stages across lanes 1, 2, 4, 8 apart.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -156,71 +158,93 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 }
 
 // ---------------------------------------------------------------------------
-// amax of a bf16 tensor: max over |g| as bf16 bit patterns (non-negative bf16
-// values order like their 15-bit integers), exact and order-independent.
+// B1 + B2 fused: grad_split_kernel (cooperative launch, one grid barrier).
+//   phase 1  amax of grad_Y: max over |g| as bf16 bit patterns (non-negative bf16
+//            values order like their 15-bit integers), exact and
+//            order-independent; one slot per CTA, no atomics.
+//   --- grid.sync() ---
+//   phase 2  every CTA reduces the slots to amax; s_down = fl32(amax / 119),
+//            r8 = fl32(119 / amax); v = fl32(g r8), a = min(|v|, 119);
+//            A = ceil(a 2^32) (a 2^32 is exact in fp32, the conversion rounds up):
+//            high word = floor(a) (+1 when frac's threshold wraps), low word =
+//            T = ceil(frac(a) 2^32) mod 2^32; q = sign(v) (hi(A) + [u < lo(A)])
+//            with u the element's Philox word: P(round up) = frac(a) exactly
+//            (reading Z-10); hi = floor((q+8)/16), lo = q - 16 hi (Z-11);
+//            per-row sum hi^2, sum lo^2 (the leverage scores' INT data).
+//            grad_Y is re-read right after phase 1, mostly from L2.
 // ---------------------------------------------------------------------------
+constexpr int kSplitThreads = 256;
+constexpr int kBsGroup = 4;
 constexpr int kAmaxUnroll = 4;
 
-__global__ void __launch_bounds__(256) amax_bf16_kernel(const uint4* __restrict__ g, int64_t n8,
-                                                        uint32_t* __restrict__ amax_bits) {
-    uint32_t m = 0;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n8; i0 += stride * kAmaxUnroll) {
-        uint4 u[kAmaxUnroll];
-#pragma unroll
-        for (int j = 0; j < kAmaxUnroll; ++j) {
-            const int64_t i = i0 + j * stride;
-            u[j] = i < n8 ? ld_nc_v4(g + i) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int j = 0; j < kAmaxUnroll; ++j) {
-            const uint32_t w[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) m = max(m, max(w[q] & 0x7FFFu, (w[q] >> 16) & 0x7FFFu));
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-    __shared__ uint32_t red[8];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < int(blockDim.x >> 5); ++w) m = max(m, red[w]);
-        atomicMax(amax_bits, m);
-    }
+__device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t w) {
+    return max(w & 0x7FFFu, (w >> 16) & 0x7FFFu);
 }
 
-cudaError_t launch_amax_bf16(const uint16_t* g, int64_t n, uint32_t* amax_bits, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(amax_bits, 0, sizeof(uint32_t), s);
-    if (e != cudaSuccess) return e;
-    const int64_t n8 = n / 8;           // n is a multiple of 64 (C % 64 == 0)
-    if (n8 == 0) return cudaSuccess;
-    int64_t blocks = (n8 + 256 * kAmaxUnroll - 1) / (256 * kAmaxUnroll);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    amax_bf16_kernel<<<int(blocks), 256, 0, s>>>(reinterpret_cast<const uint4*>(g), n8, amax_bits);
-    return cudaGetLastError();
+// pack the low bytes of 8 ints into 8 bytes
+__device__ __forceinline__ uint2 pack8_i8(const int (&v)[8]) {
+    const uint32_t a = __byte_perm(uint32_t(v[0]), uint32_t(v[1]), 0x0040);   // [v0, v1, 0, 0]
+    const uint32_t b = __byte_perm(uint32_t(v[2]), uint32_t(v[3]), 0x0040);
+    const uint32_t c = __byte_perm(uint32_t(v[4]), uint32_t(v[5]), 0x0040);
+    const uint32_t d = __byte_perm(uint32_t(v[6]), uint32_t(v[7]), 0x0040);
+    return make_uint2(__byte_perm(a, b, 0x5410), __byte_perm(c, d, 0x5410));
 }
 
-// ---------------------------------------------------------------------------
-// bitsplit: v = clamp(fl32(g r8), -119, 119); sign-magnitude stochastic
-// rounding with Philox word u: q = sign(v) (floor|v| + [u < ceil(frac|v| 2^32)]);
-// hi = floor((q + 8) / 16), lo = q - 16 hi  (readings Z-9, Z-10, Z-11).
-// ---------------------------------------------------------------------------
-constexpr int kBsGroup = 4;
-
-__global__ void __launch_bounds__(kRowWarps * 32, 4)
-bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t* __restrict__ amax_bits,
-                uint32_t k0, uint32_t k1, uint32_t call_id, int64_t token_offset,
-                int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, float* __restrict__ s_down_out) {
+__global__ void __launch_bounds__(kSplitThreads, 4)
+grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ block_max,
+                  uint32_t k0, uint32_t k1, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
+                  int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out) {
+    namespace cgrp = cooperative_groups;
+    cgrp::grid_group grid = cgrp::this_grid();
     const int lane = lane_id();
-    const float amax = __uint_as_float(__ldg(amax_bits) << 16);
+    const int warp = threadIdx.x >> 5;
+
+    // ---- phase 1: amax ----------------------------------------------------
+    {
+        const uint4* g4 = reinterpret_cast<const uint4*>(g);
+        const int64_t n8 = N * int64_t(C) / 8;
+        const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+        uint32_t m = 0;
+        for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n8; i0 += stride * kAmaxUnroll) {
+            uint4 u[kAmaxUnroll];
+#pragma unroll
+            for (int j = 0; j < kAmaxUnroll; ++j) {
+                const int64_t i = i0 + j * stride;
+                u[j] = i < n8 ? __ldg(g4 + i) : make_uint4(0, 0, 0, 0);    // L1/L2-cached: re-read in phase 2
+            }
+#pragma unroll
+            for (int j = 0; j < kAmaxUnroll; ++j)
+                m = max(m, max(max(bf16x2_absmax(u[j].x), bf16x2_absmax(u[j].y)),
+                               max(bf16x2_absmax(u[j].z), bf16x2_absmax(u[j].w))));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        __shared__ uint32_t red[kSplitThreads / 32];
+        if (lane == 0) red[warp] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kSplitThreads / 32; ++w) m = max(m, red[w]);
+            block_max[blockIdx.x] = m;
+        }
+    }
+    grid.sync();
+    uint32_t amax_b = 0;
+    for (int i = lane; i < int(gridDim.x); i += 32) amax_b = max(amax_b, __ldcg(block_max + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax_b = max(amax_b, __shfl_xor_sync(0xFFFFFFFFu, amax_b, o));
+    const float amax = __uint_as_float(amax_b << 16);
     const bool zero = !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
-    const int64_t warp0 = int64_t(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
-    const int64_t wstride = int64_t(gridDim.x) * kRowWarps;
-    const int nch = (C + 255) >> 8;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
+        *amax_out = amax_b;
+    }
+
+    // ---- phase 2: SR + bit split, one warp per row ------------------------
     const PhiloxKeys keys = philox_keys(k0, k1);
+    const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
+    const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
+    const int nch = (C + 255) >> 8;
     for (int64_t row = warp0; row < N; row += wstride) {
         const uint16_t* gr = g + row * C;
         int8_t* hr = hilo + row * C;
@@ -240,7 +264,7 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
                 if (g0 + gi >= nch || col >= C) continue;
                 float v[8];
                 unpack_bf16x8(raw[gi], v);
-                // Philox words for the 8 elements: L = tglob * C + col + i, block L / 4
+                // Philox words for the 8 elements: L = tglob * C + col + i, block L / 4 (Z-20)
                 const uint64_t b0 = (tglob * uint64_t(C) + uint64_t(col)) >> 2;
                 const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, keys);
                 const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, keys);
@@ -248,28 +272,18 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
                 int hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    int q = 0;
-                    if (!zero) {
-                        // A = ceil(|v| 2^32) (|v| 2^32 is exact in fp32): high word = floor|v|
-                        // (+1 when the fraction's threshold wraps to 2^32), low word =
-                        // T = ceil(frac|v| 2^32) mod 2^32; P(round up) = T / 2^32 exactly.
-                        // a = min(|g r8|, 119); floor / fraction exact in fp32; T = ceil(f 2^32) < 2^32
-                        const float sv = __fmul_rn(v[i], r8);
-                        const float a = fminf(fabsf(sv), 119.0f);
-                        const float fl = floorf(a);
-                        const uint32_t T = __float2uint_ru(__fmul_rn(__fsub_rn(a, fl), 4294967296.0f));
-                        const int mag = int(fl) + int(u[i] < T);
-                        q = sv < 0.0f ? -mag : mag;
-                    }
-                    hi[i] = (q + 8) >> 4;                                     // floor division
+                    const float sv = __fmul_rn(v[i], r8);
+                    const float a = fminf(fabsf(sv), 119.0f);
+                    const uint64_t A = __float2ull_ru(__fmul_rn(a, 4294967296.0f));   // exact ceil(a 2^32)
+                    const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
+                    const int q = sv < 0.0f ? -mag : mag;
+                    hi[i] = (q + 8) >> 4;                                             // floor division
                     lo[i] = q - 16 * hi[i];
                     shi += hi[i] * hi[i];
                     slo += lo[i] * lo[i];
                 }
-                *reinterpret_cast<uint2*>(hr + col) =
-                    make_uint2(pack4_i8(hi[0], hi[1], hi[2], hi[3]), pack4_i8(hi[4], hi[5], hi[6], hi[7]));
-                *reinterpret_cast<uint2*>(lr + col) =
-                    make_uint2(pack4_i8(lo[0], lo[1], lo[2], lo[3]), pack4_i8(lo[4], lo[5], lo[6], lo[7]));
+                *reinterpret_cast<uint2*>(hr + col) = pack8_i8(hi);
+                *reinterpret_cast<uint2*>(lr + col) = pack8_i8(lo);
             }
         }
 #pragma unroll
@@ -284,14 +298,32 @@ bitsplit_kernel(const uint16_t* __restrict__ g, int64_t N, int C, const uint32_t
     }
 }
 
-cudaError_t launch_bitsplit(const uint16_t* g, int64_t N, int64_t C, const uint32_t* amax_bits,
-                            uint64_t seed, uint32_t call_id, int64_t token_offset, int8_t* hilo,
-                            int32_t* a_sq, float* s_down, cudaStream_t s) {
+int grad_split_max_blocks() {
+    static int cached = 0;
+    if (cached == 0) {
+        int per_sm = 0, sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel, kSplitThreads, 0);
+        cached = per_sm * sms;
+    }
+    return cached;
+}
+
+cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
+                              uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
+                              uint32_t* amax_out, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
-    bitsplit_kernel<<<row_grid(N), kRowWarps * 32, 0, s>>>(g, N, int(C), amax_bits, uint32_t(seed),
-                                                            uint32_t(seed >> 32), call_id, token_offset,
-                                                            hilo, a_sq, s_down);
-    return cudaGetLastError();
+    int blocks = grad_split_max_blocks();
+    const int64_t want = (N + 7) / 8;                       // one warp per row at most
+    if (want < blocks) blocks = int(want);
+    if (blocks > kGradSplitMaxBlocks) blocks = kGradSplitMaxBlocks;
+    const uint32_t k0 = uint32_t(seed), k1 = uint32_t(seed >> 32);
+    void* args[] = {(void*)&g, (void*)&N, (void*)&C, (void*)&block_max, (void*)&k0, (void*)&k1, (void*)&call_id,
+                    (void*)&token_offset, (void*)&hilo, (void*)&a_sq, (void*)&s_down, (void*)&amax_out};
+    int Ci = int(C);
+    args[2] = (void*)&Ci;
+    return cudaLaunchCooperativeKernel((const void*)grad_split_kernel, dim3(blocks), dim3(kSplitThreads), args, 0, s);
 }
 
 }  // namespace i4
