@@ -231,7 +231,8 @@ i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t
                          uint32_t* clamp_bits, int32_t* row_sqnorm, void* stream) {
     I4_RETURN_IF(check_device());
     if (!x_bf16 || !codes) return fail(I4_ERR_ARG, "hadamard_quant: NULL input/output");
-    if (rows < 0 || cols <= 0 || cols % 32 != 0) return fail(I4_ERR_SHAPE, "hadamard_quant: cols = %lld must be a positive multiple of 32", (long long)cols);
+    if (rows < 0 || cols <= 0 || cols % 32 != 0 || cols > 8192)
+        return fail(I4_ERR_SHAPE, "hadamard_quant: cols = %lld must be a multiple of 32 in [32, 8192]", (long long)cols);
     I4_RETURN_IF(check_k(k, cols));
     I4_RETURN_IF(check_step(step, "step"));
     if (!aligned16(x_bf16) || !aligned16(codes)) return fail(I4_ERR_ALIGN, "hadamard_quant: pointers must be 16-byte aligned");
@@ -248,7 +249,7 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     if (!X || !W || !Y || !cache || !cache->xq || !cache->wq || !cache->x_mask || !cache->w_mask ||
         !cache->x_sqnorm)
         return fail(I4_ERR_ARG, "int4_linear_fwd: NULL pointer");
-    if (N <= 0 || D <= 0 || C <= 0 || D % 64 || C % 64)
+    if (N <= 0 || D <= 0 || C <= 0 || D % 64 || C % 64 || D > 8192)
         return fail(I4_ERR_SHAPE, "int4_linear_fwd: need N > 0 and D, C positive multiples of 64 (N=%lld D=%lld C=%lld)",
                     (long long)N, (long long)D, (long long)C);
     if (N > (int64_t(1) << 31) / 2) return fail(I4_ERR_SHAPE, "int4_linear_fwd: N too large");

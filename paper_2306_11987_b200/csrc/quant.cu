@@ -40,7 +40,12 @@ static int row_grid(int64_t rows) {
 }
 
 // ---------------------------------------------------------------------------
-// hadamard_quant
+// hadamard_quant: one thread per 32-column block of a row (32 bf16 loaded as
+// 4 x 16 B, 32 int8 codes stored as 2 x 16 B, one mask word), so Hadamard
+// blocks of up to 2^5 columns are transformed entirely in registers; k = 6, 7
+// add one / two xor-shuffle stages between neighbouring threads of the row.
+// A CTA holds R whole rows (R * cols/32 threads); row norms are reduced in
+// shared memory.  X and W are two row jobs of one launch.
 // ---------------------------------------------------------------------------
 struct HqJob {
     const uint16_t* x;
@@ -52,100 +57,95 @@ struct HqJob {
     int blocks;                          // CTAs assigned to this job
 };
 
-constexpr int kHqGroup = 4;              // chunks (of 256 columns) loaded per group
+constexpr int kHqMaxThreads = 256;
 
-__global__ void __launch_bounds__(kRowWarps * 32, 4)
-hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k) {
+__global__ void __launch_bounds__(kHqMaxThreads)
+hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k, int rows_per_cta) {
     const bool second = int(blockIdx.x) >= j0.blocks;
     const HqJob& J = second ? j1 : j0;
     const int bid = second ? int(blockIdx.x) - j0.blocks : int(blockIdx.x);
-    const int lane = lane_id();
-    const int64_t warp0 = int64_t(bid) * kRowWarps + (threadIdx.x >> 5);
-    const int64_t wstride = int64_t(J.blocks) * kRowWarps;
-    const int words_per_row = cols >> 5;
-    const int nch = (cols + 255) >> 8;
-    for (int64_t row = warp0; row < J.rows; row += wstride) {
-        const uint16_t* xr = J.x + row * cols;
+    const int tpr = cols >> 5;                       // threads (32-column blocks) per row
+    const int r_local = int(threadIdx.x) / tpr;
+    const int blk = int(threadIdx.x) - r_local * tpr;
+    const int64_t row = int64_t(bid) * rows_per_cta + r_local;
+    const bool active = r_local < rows_per_cta && row < J.rows;
+    __shared__ int sq_row[kHqMaxThreads];
+    if (threadIdx.x < rows_per_cta) sq_row[threadIdx.x] = 0;
+
+    float v[32];
+    {
+        const uint16_t* src = J.x + (active ? row * cols + blk * 32 : 0);
+        uint4 raw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) raw[q] = active ? ld_nc_v4(src + 8 * q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float t[8];
+            unpack_bf16x8(raw[q], t);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * q + i] = t[i];
+        }
+    }
+    fwht_inplace<32>(v, k < 5 ? k : 5);              // strides 1 .. 16: registers only
+#pragma unroll
+    for (int s = 5; s < 7; ++s) {                      // strides 32, 64 columns: partner thread blk ^ 1, ^ 2
+        if (s < k) {
+            const int lm = 1 << (s - 5);
+            const float sgn = (blk & lm) ? -1.0f : 1.0f;   // upper block: o - v, lower: v + o
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float o = __shfl_xor_sync(0xFFFFFFFFu, v[i], lm);
+                v[i] = __fmaf_rn(sgn, v[i], o);             // one rounding = the add / sub
+            }
+        }
+    }
+    __syncthreads();                                   // sq_row initialised
+    if (active) {
+        // LSQ: v = fl32(t r); code = clamp(rint(v), -7, 7); mask = |v| <= 7
+        int q[32];
+        uint32_t mask = 0;
         int sq = 0;
-        for (int g0 = 0; g0 < nch; g0 += kHqGroup) {
-            uint4 raw[kHqGroup];
 #pragma unroll
-            for (int g = 0; g < kHqGroup; ++g) {
-                const int col = (g0 + g) * 256 + lane * 8;
-                raw[g] = (g0 + g < nch && col < cols) ? ld_nc_v4(xr + col) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int g = 0; g < kHqGroup; ++g) {
-                if (g0 + g >= nch) break;
-                const int col = (g0 + g) * 256 + lane * 8;
-                const bool active = col < cols;
-                float v[8];
-                unpack_bf16x8(raw[g], v);
-                // in-register butterflies: strides 1, 2, 4
-#pragma unroll
-                for (int s = 0; s < 3; ++s) {
-                    if (s < k) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            if (((i >> s) & 1) == 0) {
-                                const float a = v[i], b = v[i + (1 << s)];
-                                v[i] = __fadd_rn(a, b);
-                                v[i + (1 << s)] = __fsub_rn(a, b);
-                            }
-                        }
-                    }
-                }
-                // cross-lane butterflies: strides 8, 16, 32, 64 columns = lanes 1, 2, 4, 8 apart
-#pragma unroll
-                for (int s = 3; s < 7; ++s) {
-                    if (s < k) {
-                        const int lm = 1 << (s - 3);
-                        const float sgn = (lane & lm) ? -1.0f : 1.0f;   // upper lane: o - v, lower: v + o
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float o = __shfl_xor_sync(0xFFFFFFFFu, v[i], lm);
-                            v[i] = __fmaf_rn(sgn, v[i], o);              // one rounding, = the add/sub
-                        }
-                    }
-                }
-                // LSQ: v = fl32(t * r); code = clamp(rint(v), -7, 7); mask = -7 <= v <= 7
-                int q[8];
-                uint32_t m8 = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float sv = __fmul_rn(v[i], J.r);
-                    const int c = __float2int_rn(fminf(fmaxf(sv, -7.0f), 7.0f));
-                    q[i] = c;
-                    m8 |= uint32_t(fabsf(sv) <= 7.0f) << i;
-                    sq += c * c;
-                }
-                // 32-column mask word = 4 lanes x 8 bits
-                uint32_t word = m8 << (8 * (lane & 3));
-                word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
-                word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
-                if (active) {
-                    *reinterpret_cast<uint2*>(J.codes + row * cols + col) =
-                        make_uint2(pack4_i8(q[0], q[1], q[2], q[3]), pack4_i8(q[4], q[5], q[6], q[7]));
-                    if (J.bits != nullptr && (lane & 3) == 0) J.bits[row * words_per_row + (col >> 5)] = word;
-                }
-            }
+        for (int i = 0; i < 32; ++i) {
+            const float sv = __fmul_rn(v[i], J.r);
+            q[i] = __float2int_rn(fminf(fmaxf(sv, -7.0f), 7.0f));
+            mask |= uint32_t(fabsf(sv) <= 7.0f) << i;
         }
-        if (J.sqnorm != nullptr) {
+        uint32_t w[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
-            if (lane == 0) J.sqnorm[row] = sq;
+        for (int i = 0; i < 8; ++i) {
+            w[i] = __byte_perm(__byte_perm(uint32_t(q[4 * i]), uint32_t(q[4 * i + 1]), 0x0040),
+                               __byte_perm(uint32_t(q[4 * i + 2]), uint32_t(q[4 * i + 3]), 0x0040), 0x5410);
+            sq = __dp4a(int(w[i]), int(w[i]), sq);     // sum of squared codes, 4 per instruction
         }
+        int8_t* dst = J.codes + row * cols + blk * 32;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (J.bits != nullptr) J.bits[row * tpr + blk] = mask;
+        if (J.sqnorm != nullptr) atomicAdd(&sq_row[r_local], sq);
+    }
+    if (J.sqnorm != nullptr) {
+        __syncthreads();
+        if (active && blk == 0) J.sqnorm[row] = sq_row[r_local];
     }
 }
 
+static int hq_rows_per_cta(int64_t cols) {
+    const int tpr = int(cols / 32);
+    return tpr >= kHqMaxThreads ? 1 : kHqMaxThreads / tpr;
+}
+
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
+    if (a.cols / 32 > kHqMaxThreads) return cudaErrorInvalidValue;   // cols > 8192: not supported
+    const int R = hq_rows_per_cta(a.cols);
     HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, 0};
     HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, 0};
-    j0.blocks = a.rows0 > 0 ? row_grid(a.rows0) : 0;
-    j1.blocks = a.rows1 > 0 ? row_grid(a.rows1) : 0;
+    j0.blocks = int((a.rows0 + R - 1) / R);
+    j1.blocks = int((a.rows1 + R - 1) / R);
     const int grid = j0.blocks + j1.blocks;
     if (grid == 0) return cudaSuccess;
-    hadamard_quant_kernel<<<grid, kRowWarps * 32, 0, s>>>(j0, j1, int(a.cols), a.k);
+    const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
+    hadamard_quant_kernel<<<grid, threads, 0, s>>>(j0, j1, int(a.cols), a.k, R);
     return cudaGetLastError();
 }
 
@@ -278,12 +278,13 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                     const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
                     const int q = sv < 0.0f ? -mag : mag;
                     hi[i] = (q + 8) >> 4;                                             // floor division
-                    lo[i] = q - 16 * hi[i];
-                    shi += hi[i] * hi[i];
-                    slo += lo[i] * lo[i];
+                    lo[i] = q - (hi[i] << 4);
                 }
-                *reinterpret_cast<uint2*>(hr + col) = pack8_i8(hi);
-                *reinterpret_cast<uint2*>(lr + col) = pack8_i8(lo);
+                const uint2 ph = pack8_i8(hi), pl = pack8_i8(lo);
+                shi = __dp4a(int(ph.x), int(ph.x), __dp4a(int(ph.y), int(ph.y), shi));   // sum of squares
+                slo = __dp4a(int(pl.x), int(pl.x), __dp4a(int(pl.y), int(pl.y), slo));
+                *reinterpret_cast<uint2*>(hr + col) = ph;
+                *reinterpret_cast<uint2*>(lr + col) = pl;
             }
         }
 #pragma unroll
