@@ -202,10 +202,8 @@ def algorithmic_work(name, N, D, C, kx, kw):
         return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
     if name == "grad_split":                  # amax + SR + bit split: read bf16 grad_Y once (the amax
         return "bytes", N * C * (2 + 2) + 8 * N  # pass's re-read is an implementation cost), write hi + lo planes
-    if name == "compact_rows":
-        return "bytes", 2.0 * kx * C
-    if name == "compact_wgrad":
-        return "bytes", 2.0 * kw * (C + D)
+    if name == "compact_wgrad":               # B_W = 2^wexp X_hat rows: read + write D bytes per kept item
+        return "bytes", 2.0 * kw * D
     if name == "lss_sampler":
         return "latency", 0.0
     if name == "memsets":

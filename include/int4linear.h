@@ -94,8 +94,10 @@ typedef struct {
 
 /* Bit-split + sampling plan (Procedure LSS-MM steps 1-4).  Device buffers,
  * caller-allocated, written by bitsplit_lss:
- *   hilo     int8  [2N, C]     rows 0..N-1 = grad_up (high 4 bits), N..2N-1 = grad_down
- *   a_sq     int32 [2N]        sum_c code^2 per row of hilo
+ *   hilo     int8  [2N+1, C]   the bit-split plane: row t = 16 grad_up[t] (the high 4 bits,
+ *                              scaled so that s_up = 16 s_down is folded in; |.| <= 112),
+ *                              row N + t = grad_down[t] (low 4 bits), row 2N = zeros
+ *   a_sq     int32 [2N]        sum_c code^2 per half-row (unscaled codes hi, lo)
  *   amax_bits uint32 [1]       out: bf16 bit pattern of max |grad_Y|
  *   s_down   float [1]         out: s_down = amax / 119 (s_up = 16 s_down), reading Z-9
  *   scratch  uint32 [2048]     scratch (per-CTA partial maxima of the fused amax pass)

@@ -205,7 +205,7 @@ class Int4Linear:
                                 x_mask=self.x_mask.data_ptr(), w_mask=self.w_mask.data_ptr(),
                                 x_sqnorm=self.x_sqnorm.data_ptr(), w_valid=0)
         n2 = 2 * N + 128
-        self.hilo = torch.empty(2 * N, C, dtype=i8, device=dev)
+        self.hilo = torch.empty(2 * N + 1, C, dtype=i8, device=dev)   # row 2N: zero pad
         self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
         self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
         self.scratch = torch.zeros(2048, dtype=i32, device=dev)  # fused-amax block maxima

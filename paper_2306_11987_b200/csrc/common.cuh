@@ -189,6 +189,26 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* tmap
         : "memory");
 }
 
+// TMA row gather: 4 rows (row indices r0..r3) x 128 bytes starting at column c0
+// land as 4 consecutive 128-byte rows at smem_dst.  CG = 2: completion counted
+// on the leader CTA's barrier (bar = shared::cluster address).
+template <int CG>
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const void* tmap, uint32_t bar, int32_t c0,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+    if constexpr (CG == 2)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.cta_group::2"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+            :: "r"(smem_u32(smem_dst)), "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+            :: "r"(smem_u32(smem_dst)), "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+            : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05: TMEM allocation, UMMA (kind::i8), commit, TMEM -> registers
 // ---------------------------------------------------------------------------

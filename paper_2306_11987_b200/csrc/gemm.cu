@@ -26,7 +26,8 @@
 //            EPI_FWD    Y = fl32(acc) * fl32(s_x s_w)   (HQ-MM step 4)
 //            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; dW
 //            -> swizzled shared-memory staging -> TMA bulk tensor store
-//            EPI_DGRAD  row = kept item (h, t): v = acc * s_w s_h 2^wexp 2^{-k/2};
+//            EPI_DGRAD  row = kept item (h, t): v = acc * s_w s_down 2^wexp 2^{-k/2} (the
+//                       plane row holds 16 hi or lo, so s_up = 16 s_down is folded in);
 //                       v = I_X[t] o v; v = v H; red.add.v4 into dX[t]
 //                       (<= 2 addends per element onto 0: order-independent)
 //   Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of
@@ -143,22 +144,51 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ------------------------------------------------------------- producer
-        if (lane == 0) {
-            int stage = 0; uint32_t phase = 0;
-            for (int u = pair0; u < units; u += n_pairs) {
-                UNIT_DECODE(u)
-                const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
-                const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
-                for (int kb = kb0; kb < kb1; ++kb) {
+        // ------------------------------------------------------------- producer (warp 0)
+        // lane 0 issues the TMA; with a gathered A the 32 lanes first fetch the
+        // 128 row indices of the stage (4 per lane) and hand them out by shuffles.
+        const bool gather = g.a_gather != nullptr;
+        const int gcount = gather ? __ldg(g.gather_count) : 0;
+        auto load_idx4 = [&](int r) {
+            int4 v;
+            v.x = r + 0 < gcount ? __ldg(g.a_gather + r + 0) : g.gather_zero_row;
+            v.y = r + 1 < gcount ? __ldg(g.a_gather + r + 1) : g.gather_zero_row;
+            v.z = r + 2 < gcount ? __ldg(g.a_gather + r + 2) : g.gather_zero_row;
+            v.w = r + 3 < gcount ? __ldg(g.a_gather + r + 3) : g.gather_zero_row;
+            return v;
+        };
+        int stage = 0; uint32_t phase = 0;
+        for (int u = pair0; u < units; u += n_pairs) {
+            UNIT_DECODE(u)
+            const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
+            const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
+            int4 gidx = make_int4(0, 0, 0, 0);
+            if (gather && !A_MN) gidx = load_idx4(m0 + 4 * lane);       // rows of the tile (grad_X)
+            for (int kb = kb0; kb < kb1; ++kb) {
+                if (gather && A_MN) gidx = load_idx4(kb * kBK + 4 * lane); // K rows of the stage (grad_W)
+                if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
-                    uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
-                    uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+                }
+                __syncwarp();
+                uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+                uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+                const uint32_t fb = CG == 2 ? mapa_shared(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+                if (gather) {
+                    const int c0 = A_MN ? m0 : kb * kBK;
+#pragma unroll 8
+                    for (int q = 0; q < 32; ++q) {
+                        const int r0 = __shfl_sync(0xFFFFFFFFu, gidx.x, q), r1 = __shfl_sync(0xFFFFFFFFu, gidx.y, q);
+                        const int r2 = __shfl_sync(0xFFFFFFFFu, gidx.z, q), r3 = __shfl_sync(0xFFFFFFFFu, gidx.w, q);
+                        if (lane == 0) tma_gather4<CG>(a_dst + q * 4 * 128, &tmA, fb, c0, r0, r1, r2, r3);
+                    }
+                }
+                if (lane == 0) {
                     if constexpr (CG == 2) {
-                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (A_MN) tma_load_2d_2sm(a_dst, &tmA, fb, m0, kb * kBK);
-                        else      tma_load_2d_2sm(a_dst, &tmA, fb, kb * kBK, m0);
+                        if (!gather) {
+                            if (A_MN) tma_load_2d_2sm(a_dst, &tmA, fb, m0, kb * kBK);
+                            else      tma_load_2d_2sm(a_dst, &tmA, fb, kb * kBK, m0);
+                        }
                         if (B_MN) {
 #pragma unroll
                             for (int j = 0; j < BNC / 128; ++j)
@@ -167,8 +197,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             tma_load_2d_2sm(b_dst, &tmB, fb, kb * kBK, nb);
                         }
                     } else {
-                        if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
-                        else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
+                        if (!gather) {
+                            if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
+                            else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
+                        }
                         if (B_MN) {
 #pragma unroll
                             for (int j = 0; j < BNC / 128; ++j)
@@ -177,8 +209,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, nb);
                         }
                     }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
@@ -258,7 +290,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
                 const int e = valid ? int(__ldg(g.wexp + row)) : 0;
-                rscale = ldexpf(__fmul_rn(g.scale, sd), e + (h == 0 ? 4 : 0));
+                rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
             } else if (EPI == EPI_WGRAD) {
                 rscale = __fmul_rn(g.scale, sd);
             }

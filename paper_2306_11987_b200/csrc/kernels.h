@@ -40,11 +40,8 @@ int sampler_max_tokens();
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
 
 // compact.cu ------------------------------------------------------------------
-cudaError_t launch_compact_rows(const int8_t* hilo, int64_t C, const int32_t* items, const int32_t* count,
-                                int64_t n_items, int8_t* out, cudaStream_t s);
-cudaError_t launch_compact_wgrad(const int8_t* hilo, const int8_t* xq, int64_t N, int64_t C, int64_t D,
-                                 const int32_t* items, const int8_t* wexp, const int32_t* count,
-                                 int64_t kcap, int8_t* a_w, int8_t* b_w, cudaStream_t s);
+cudaError_t launch_compact_wgrad(const int8_t* xq, int64_t N, int64_t D, const int32_t* items, const int8_t* wexp,
+                                 const int32_t* count, int64_t kcap, int8_t* b_w, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
 enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3 };
@@ -64,6 +61,11 @@ struct GemmArgs {
     int32_t k_had;            // Hadamard exponent for the epilogue inverse transform
     const uint32_t* mask;     // dgrad: I_X [N, Nn/32]; wgrad: I_W [M, Nn/32]
     const int32_t* items;     // dgrad: item id of each A row
+    // A rows gathered by TMA (tile::gather4) from a row list: along M for a K-major A
+    // (grad_X: the kept items' plane rows), along K for an MN-major A (grad_W)
+    const int32_t* a_gather;  // row indices, or null (plain tiles)
+    const int32_t* gather_count;   // indices at positions >= *gather_count read the zero row
+    int32_t gather_zero_row;
     const int8_t* wexp;       // dgrad: weight exponent of each A row
     int32_t n_tokens;         // dgrad: N (item id = h*N + t)
     // deterministic split-K (optional): INT32 partial tiles + per-warp flags (zeroed before use)

@@ -169,7 +169,8 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 //            high word = floor(a) (+1 when frac's threshold wraps), low word =
 //            T = ceil(frac(a) 2^32) mod 2^32; q = sign(v) (hi(A) + [u < lo(A)])
 //            with u the element's Philox word: P(round up) = frac(a) exactly
-//            (reading Z-10); hi = floor((q+8)/16), lo = q - 16 hi (Z-11);
+//            (reading Z-10); hi = floor((q+8)/16), lo = q - 16 hi (Z-11); the
+//            plane stores 16 hi (s_up = 16 s_down folded in) and lo;
 //            per-row sum hi^2, sum lo^2 (the leverage scores' INT data).
 //            grad_Y is re-read right after phase 1, mostly from L2.
 // ---------------------------------------------------------------------------
@@ -241,6 +242,9 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     }
 
     // ---- phase 2: SR + bit split, one warp per row ------------------------
+    if (blockIdx.x == gridDim.x - 1)                      // plane row 2N: the all-zero gather pad
+        for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
+            *reinterpret_cast<uint4*>(hilo + 2 * N * C + c) = make_uint4(0, 0, 0, 0);
     const PhiloxKeys keys = philox_keys(k0, k1);
     const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
     const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
@@ -283,7 +287,8 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 const uint2 ph = pack8_i8(hi), pl = pack8_i8(lo);
                 shi = __dp4a(int(ph.x), int(ph.x), __dp4a(int(ph.y), int(ph.y), shi));   // sum of squares
                 slo = __dp4a(int(pl.x), int(pl.x), __dp4a(int(pl.y), int(pl.y), slo));
-                *reinterpret_cast<uint2*>(hr + col) = ph;
+                // the high plane stores 16 hi (per byte: low nibble moved up; |16 hi| <= 112)
+                *reinterpret_cast<uint2*>(hr + col) = make_uint2((ph.x << 4) & 0xF0F0F0F0u, (ph.y << 4) & 0xF0F0F0F0u);
                 *reinterpret_cast<uint2*>(lr + col) = pl;
             }
         }

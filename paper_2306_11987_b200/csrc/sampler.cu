@@ -1,5 +1,6 @@
 // Leverage-score sampler: LSS-MM steps 2-4 for
-// the grad_W mask and the grad_X mask, one 8-CTA thread-block cluster per mask.
+// the grad_W mask and the grad_X mask: one CTA per mask (N <= 8192), or one
+// 8-CTA thread-block cluster per mask with distributed-shared-memory reductions.
 //
 //   scores   integer-exact (reading Z-13): w = floor(sqrt(a b) 2^(16 + 4[h = up]))
 //            for grad_W (a = sum code^2 of the half-row, b = sum X_hat^2 of the
@@ -59,8 +60,24 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
     return v;
 }
 
-// Cluster-wide (sum w, sum c); every thread of every CTA receives the totals.
-__device__ void cluster_sum(cg::cluster_group& cl, SamplerSmem& sm, int& parity, uint64_t w, uint32_t c,
+// CTA group of one mask: a single CTA (2N <= 16384 items) or an 8-CTA cluster
+// sharing partial sums through distributed shared memory.
+template <int CL> struct Group;
+template <> struct Group<1> {
+    __device__ unsigned rank() const { return 0; }
+    __device__ void sync() const { __syncthreads(); }
+    template <class T> __device__ T* map(T* p, int) const { return p; }
+};
+template <> struct Group<kClusterCTAs> {
+    cg::cluster_group g = cg::this_cluster();
+    __device__ unsigned rank() const { return g.block_rank(); }
+    __device__ void sync() const { g.sync(); }
+    template <class T> __device__ T* map(T* p, int r) const { return g.map_shared_rank(p, r); }
+};
+
+// Group-wide (sum w, sum c); every thread of every CTA receives the totals.
+template <int CL>
+__device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, uint64_t w, uint32_t c,
                             uint64_t& W, uint32_t& Cn) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     w = warp_sum_u64(w);
@@ -70,30 +87,31 @@ __device__ void cluster_sum(cg::cluster_group& cl, SamplerSmem& sm, int& parity,
     if (threadIdx.x == 0) {
         uint64_t bw = 0; uint32_t bc = 0;
         for (int i = 0; i < kSamplerThreads / 32; ++i) { bw += sm.warp_w[i]; bc += sm.warp_c[i]; }
-        const unsigned me = cl.block_rank();
-        for (int r = 0; r < kClusterCTAs; ++r) {
-            uint64_t* rw = cl.map_shared_rank(&sm.red_w[parity][me], r);
-            uint32_t* rc = cl.map_shared_rank(&sm.red_c[parity][me], r);
+        const unsigned me = cl.rank();
+        for (int r = 0; r < CL; ++r) {
+            uint64_t* rw = cl.map(&sm.red_w[parity][me], r);
+            uint32_t* rc = cl.map(&sm.red_c[parity][me], r);
             *rw = bw; *rc = bc;
         }
     }
     cl.sync();
     W = 0; Cn = 0;
 #pragma unroll
-    for (int r = 0; r < kClusterCTAs; ++r) { W += sm.red_w[parity][r]; Cn += sm.red_c[parity][r]; }
+    for (int r = 0; r < CL; ++r) { W += sm.red_w[parity][r]; Cn += sm.red_c[parity][r]; }
     parity ^= 1;
 }
 
-__global__ void __cluster_dims__(kClusterCTAs, 1, 1) __launch_bounds__(kSamplerThreads, 1)
+template <int CL>
+__global__ void __launch_bounds__(kSamplerThreads, 1)
 lss_sampler_kernel(SamplerArgs a) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SamplerSmem& sm = *reinterpret_cast<SamplerSmem*>(smem_raw);
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = int(cl.block_rank());
+    const Group<CL> cl;
+    const int rank = int(cl.rank());
     const int mask_id = blockIdx.y;                      // 0: grad_W, 1: grad_X
     const int N = a.N;
     const int n_items = 2 * N;
-    const int per = (n_items + kClusterCTAs - 1) / kClusterCTAs;
+    const int per = (n_items + CL - 1) / CL;
     const int base = rank * per;
     const int nloc = max(0, min(per, n_items - base));
     const int ipt = (per + kSamplerThreads - 1) / kSamplerThreads;   // items per thread
@@ -207,13 +225,13 @@ lss_sampler_kernel(SamplerArgs a) {
         }
         sm.scan[lane] = x - v;                 // exclusive warp offsets
         if (lane == 31) {
-            for (int r = 0; r < kClusterCTAs; ++r)
-                *cl.map_shared_rank(&sm.cta_tot[rank], r) = x;
+            for (int r = 0; r < CL; ++r)
+                *cl.map(&sm.cta_tot[rank], r) = x;
         }
     }
     cl.sync();
     uint32_t cta_off = 0, total = 0;
-    for (int r = 0; r < kClusterCTAs; ++r) {
+    for (int r = 0; r < CL; ++r) {
         if (r < rank) cta_off += sm.cta_tot[r];
         total += sm.cta_tot[r];
     }
@@ -239,13 +257,30 @@ lss_sampler_kernel(SamplerArgs a) {
     cl.sync();                                 // keep DSMEM alive until all remote writes landed
 }
 
-cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
+template <int CL>
+static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
     const size_t smem = sizeof(SamplerSmem);
-    cudaError_t e = cudaFuncSetAttribute(lss_sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    auto kern = lss_sampler_kernel<CL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid(kClusterCTAs, 2, 1);
-    lss_sampler_kernel<<<grid, kSamplerThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask
+    cfg.blockDim = dim3(kSamplerThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CL > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
+    // one CTA per mask while the 2N scores fit its shared memory (no cluster barriers
+    // in the A.2 rounds), an 8-CTA cluster beyond that
+    if (2 * int64_t(a.N) <= kItemsPerCTA) return launch_cl<1>(a, s);
+    return launch_cl<kClusterCTAs>(a, s);
 }
 
 }  // namespace i4

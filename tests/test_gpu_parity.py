@@ -164,8 +164,9 @@ def _check_backward(layer, g, s_x, s_w, k, dX, dW, mode, call_id=3, token_offset
     N, C = g.shape
     # (i) bit split: bit-exact planes and norms
     bs = o_bs.bit_split(g, synth.PHILOX_SEED, call_id, token_offset)
-    hilo = layer.hilo.cpu().numpy()
-    assert np.array_equal(hilo[:N], bs["hi"]) and np.array_equal(hilo[N:], bs["lo"])
+    hilo = layer.hilo.cpu().numpy().astype(np.int64)
+    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64))       # plane stores 16 hi
+    assert np.array_equal(hilo[N:2 * N], bs["lo"]) and not hilo[2 * N].any()
     assert np.array_equal(layer.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
     assert layer.s_down().cpu().numpy()[0] == bs["s_down"]
     assert np.array_equal(fwd["x_sq"], (fwd["xq"].astype(np.int64) ** 2).sum(1))
@@ -237,7 +238,7 @@ def test_shard_invariance_of_random_streams():
     hf = full.hilo.cpu().numpy()
     hh = half.hilo.cpu().numpy()
     assert np.array_equal(hf[N // 2 + 1:N], hh[1:N // 2])
-    assert np.array_equal(hf[N + N // 2 + 1:], hh[N // 2 + 1:])
+    assert np.array_equal(hf[N + N // 2 + 1:2 * N], hh[N // 2 + 1:N])
 
 
 def test_api_errors_are_loud():
@@ -273,8 +274,8 @@ def test_full_size_sampled_parity(cfg):
     assert rel_frob(Y.cpu().numpy()[rows], y_ref) < FROB_TOL
     # backward: full sampler parity, outputs on sampled tokens / channels
     bs = o_bs.bit_split(g, synth.PHILOX_SEED, 3, 0)
-    hilo = layer.hilo.cpu().numpy()
-    assert np.array_equal(hilo[:N], bs["hi"]) and np.array_equal(hilo[N:], bs["lo"])
+    hilo = layer.hilo.cpu().numpy().astype(np.int64)
+    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64)) and np.array_equal(hilo[N:2 * N], bs["lo"])
     x_sq = layer.x_sqnorm.cpu().numpy().astype(np.int64)
     mw = o_lss.sample_weight_mask(bs["a_sq"], x_sq, synth.PHILOX_SEED, 3, 0)
     mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 3, 0)
