@@ -162,10 +162,14 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             UNIT_DECODE(u)
             const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
             const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
-            int4 gidx = make_int4(0, 0, 0, 0);
+            int4 gidx = make_int4(0, 0, 0, 0), gnext = make_int4(0, 0, 0, 0);
             if (gather && !A_MN) gidx = load_idx4(m0 + 4 * lane);       // rows of the tile (grad_X)
+            if (gather && A_MN && kb0 < kb1) gnext = load_idx4(kb0 * kBK + 4 * lane);   // K rows (grad_W)
             for (int kb = kb0; kb < kb1; ++kb) {
-                if (gather && A_MN) gidx = load_idx4(kb * kBK + 4 * lane); // K rows of the stage (grad_W)
+                if (gather && A_MN) {                 // indices of this stage; prefetch the next stage's
+                    gidx = gnext;
+                    if (kb + 1 < kb1) gnext = load_idx4((kb + 1) * kBK + 4 * lane);
+                }
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
@@ -174,15 +178,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
                 uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
                 const uint32_t fb = CG == 2 ? mapa_shared(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
-                if (gather) {
-                    const int c0 = A_MN ? m0 : kb * kBK;
-#pragma unroll 8
-                    for (int q = 0; q < 32; ++q) {
-                        const int r0 = __shfl_sync(0xFFFFFFFFu, gidx.x, q), r1 = __shfl_sync(0xFFFFFFFFu, gidx.y, q);
-                        const int r2 = __shfl_sync(0xFFFFFFFFu, gidx.z, q), r3 = __shfl_sync(0xFFFFFFFFu, gidx.w, q);
-                        if (lane == 0) tma_gather4<CG>(a_dst + q * 4 * 128, &tmA, fb, c0, r0, r1, r2, r3);
-                    }
-                }
+                if (gather)                            // every lane issues the gather of its own 4 rows
+                    tma_gather4<CG>(a_dst + lane * 4 * 128, &tmA, fb, A_MN ? m0 : kb * kBK,
+                                    gidx.x, gidx.y, gidx.z, gidx.w);
                 if (lane == 0) {
                     if constexpr (CG == 2) {
                         if (!gather) {

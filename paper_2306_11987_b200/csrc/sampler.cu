@@ -277,9 +277,10 @@ static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
-    // one CTA per mask while the 2N scores fit its shared memory (no cluster barriers
-    // in the A.2 rounds), an 8-CTA cluster beyond that
-    if (2 * int64_t(a.N) <= kItemsPerCTA) return launch_cl<1>(a, s);
+    // an 8-CTA cluster per mask: the A.2 rounds are dominated by the per-item
+    // work, which the cluster spreads over 8 SMs (a single CTA measured 6x slower
+    // on binding budgets); tiny problems use one CTA
+    if (2 * int64_t(a.N) <= 2048) return launch_cl<1>(a, s);
     return launch_cl<kClusterCTAs>(a, s);
 }
 
