@@ -202,8 +202,8 @@ def algorithmic_work(name, N, D, C, kx, kw):
         return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
     if name == "grad_split":                  # amax + SR + bit split: read bf16 grad_Y once (the amax
         return "bytes", N * C * (2 + 2) + 8 * N  # pass's re-read is an implementation cost), write hi + lo planes
-    if name == "compact_wgrad":               # B_W = 2^wexp X_hat rows: read + write D bytes per kept item
-        return "bytes", 2.0 * kw * D
+    if name == "compact":                     # A_X, A_W (plane rows) and B_W rows: read + write
+        return "bytes", 2.0 * (kx * C + kw * (C + D))
     if name == "lss_sampler":
         return "latency", 0.0
     if name == "memsets":
@@ -445,7 +445,7 @@ def run_ours(args):
 
 KERNEL_NAMES = [("hadamard_quant_kernel", "hadamard_quant"), ("grad_split_kernel", "grad_split"),
                 ("lss_sampler_kernel", "lss_sampler"),
-                ("compact_rows_kernel", "compact_rows"), ("compact_wgrad_kernel", "compact_wgrad")]
+                ("compact_kernel", "compact")]
 GEMM_EPI = {"0": "gemm_i8_int32", "1": "gemm_i8_fwd", "2": "gemm_i8_dgrad", "3": "gemm_i8_wgrad"}
 
 

@@ -328,20 +328,20 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
 namespace {
 
 // Backward workspace layout (bytes, each region 256-aligned):
-//   B_W [kcap, D] | split-K partials (dgrad, wgrad) | split-K flags
-// (the GEMMs gather the bit-split plane rows themselves: no A copies)
+//   A_X [2N+128, C] | A_W [kcap, C] | B_W [kcap, D] | split-K partials (dgrad, wgrad) | split-K flags
 struct BwdWs {
-    int8_t* b_w;
+    int8_t* a_x; int8_t* a_w; int8_t* b_w;
     int32_t* part_x; int32_t* part_w; uint32_t* flags_x; uint32_t* flags_w;
     size_t total;
 };
 
 BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
-    (void)C;
     const int64_t kcap = round_up(2 * N, 128);
     BwdWs w{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += size_t(round_up(int64_t(bytes), 256)); return o; };
+    const size_t o_ax = take(size_t((2 * N + 128) * C));
+    const size_t o_aw = take(size_t(C * kcap));
     const size_t o_bw = take(size_t(D * kcap));
     const size_t o_px = take(i4::gemm_split_partial_bytes());
     const size_t o_pw = take(i4::gemm_split_partial_bytes());
@@ -349,6 +349,8 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
     w.total = off;
     if (ws) {
         uint8_t* b = static_cast<uint8_t*>(ws);
+        w.a_x = reinterpret_cast<int8_t*>(b + o_ax);
+        w.a_w = reinterpret_cast<int8_t*>(b + o_aw);
         w.b_w = reinterpret_cast<int8_t*>(b + o_bw);
         w.part_x = reinterpret_cast<int32_t*>(b + o_px);
         w.part_w = reinterpret_cast<int32_t*>(b + o_pw);
@@ -385,11 +387,15 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
 
     const int64_t kcap = round_up(2 * N, 128);
     const BwdWs w = carve_bwd_ws(ws, N, D, C);
-    const int64_t plane_rows = 2 * N + 1;                // row 2N is the all-zero pad row
-
-    // B_W[j] = 2^wexp_j X_hat[t_j]: the only operand copy left (the plane rows are gathered)
-    I4_LAUNCH(i4::launch_compact_wgrad(cache->xq, N, D, plan->items_w, plan->wexp_w, plan->count_w, kcap, w.b_w, s),
-              "compact_wgrad", s);
+    {
+        i4::CompactArgs ca{};
+        ca.plane = plan->hilo; ca.xq = cache->xq;
+        ca.N = int32_t(N); ca.C = int32_t(C); ca.D = int32_t(D);
+        ca.items_x = plan->items_x; ca.count_x = plan->count_x;
+        ca.items_w = plan->items_w; ca.wexp_w = plan->wexp_w; ca.count_w = plan->count_w;
+        ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
+        I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
+    }
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
     I4_LAUNCH(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset_dx", s);
     {
@@ -405,12 +411,10 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.items = plan->items_x;
         g.wexp = plan->wexp_x;
         g.n_tokens = int32_t(N);
-        g.a_gather = plan->items_x; g.gather_count = plan->count_x; g.gather_zero_row = int32_t(2 * N);
         g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
         g.partial = w.part_x; g.flags = w.flags_x;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
-        Operand a{plan->hilo, plane_rows, C, C, true};   // A rows = kept items' plane rows (TMA gather4)
-        I4_RETURN_IF(gemm(a, Operand{cache->wq, C, D, D}, g, s));
+        I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
     {
@@ -422,12 +426,10 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.s_down = plan->s_down;
         g.k_had = k;
         g.mask = cache->w_mask;
-        g.a_gather = plan->items_w; g.gather_count = plan->count_w; g.gather_zero_row = int32_t(2 * N);
-        g.a_mn = 1; g.b_mn = 1;                  // A = plane rows [K items, C], B_W [K, D]: both MN-major
+        g.a_mn = 1; g.b_mn = 1;                  // A_W [K items, C], B_W [K, D]: both MN-major
         g.partial = w.part_w; g.flags = w.flags_w;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
-        Operand a{plan->hilo, plane_rows, C, C, true};   // K rows = kept items' plane rows (TMA gather4)
-        I4_RETURN_IF(gemm(a, Operand{w.b_w, kcap, D, D}, g, s));
+        I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, s));
     }
     return I4_OK;
 }

@@ -2,9 +2,9 @@
 // grad_Y and X_hat given the masks"; zero padding of the
 // sampled K / M to the MMA tile).  HBM-bound gathers.
 //
-//   The grad_X and grad_W GEMMs gather the kept items' bit-split plane rows
-//   themselves (TMA tile::gather4); the only copy left is the grad_W B operand,
-//   which carries the item weights.
+//   compact_kernel builds the grad_X GEMM's A and the grad_W GEMM's A and B in
+//   one launch (row copies; TMA tile::gather4 inside the GEMM producers measured
+//   ~3x slower than these copies on B200).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -12,11 +12,13 @@ namespace i4 {
 
 constexpr int kGroup = 8;                 // 16-byte loads in flight per lane
 
-// One warp per kept item j of the grad_W mask (row gather + shift):
-//   B_W[j, :] = 2^wexp_j X_hat[t_j, :]      (D bytes, |.| <= 16 * 7 = 112)
-// The A operand (the item's plane row, which holds 16 hi or lo) is gathered by
-// the GEMM itself, so acc[c, d] = sum_j plane[item_j, c] B_W[j, d] is the
+// One launch builds all three compacted operands; one warp per output row:
+//   A_X[j, :] = plane[items_x[j], :]              (C bytes; grad_X GEMM A, K-major)
+//   A_W[j, :] = plane[items_w[j], :]              (C bytes; grad_W GEMM A, MN-major)
+//   B_W[j, :] = 2^wexp_w[j] X_hat[t(items_w[j]), :]   (D bytes, |.| <= 112; grad_W GEMM B)
+// The plane rows hold 16 hi or lo, so acc[c, d] = sum_j A_W[j, c] B_W[j, d] is the
 // weighted bit-split product with s_up = 16 s_down folded in (reading Z-17).
+// Rows past a list's count, up to its multiple of 128, are zero (the MMA pad).
 __device__ __forceinline__ uint4 scale_i8x16(uint4 u, int mul) {
     int8_t* b = reinterpret_cast<int8_t*>(&u);
 #pragma unroll
@@ -24,42 +26,55 @@ __device__ __forceinline__ uint4 scale_i8x16(uint4 u, int mul) {
     return u;
 }
 
-__global__ void __launch_bounds__(256) compact_wgrad_kernel(const int8_t* __restrict__ xq, int N, int D,
-                                                            const int32_t* __restrict__ items,
-                                                            const int8_t* __restrict__ wexp,
-                                                            const int32_t* __restrict__ count,
-                                                            int8_t* __restrict__ b_w) {
-    const int64_t padded = (int64_t(__ldg(count)) + 127) & ~int64_t(127);
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < padded; j += warps) {
-        const int32_t item = __ldg(items + j);
-        int8_t* db = b_w + j * D;
-        const bool pad = item >= 2 * N;
-        const int t = pad ? 0 : (item >= N ? item - N : item);
-        const int mul = pad ? 0 : (1 << __ldg(wexp + j));
-        const int8_t* sb = xq + int64_t(t) * D;
-        for (int c0 = 0; c0 < D; c0 += 512 * kGroup) {
-            uint4 u[kGroup];
+__device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t* __restrict__ dst, int n, int lane,
+                                         bool zero, int mul) {
+    for (int c0 = 0; c0 < n; c0 += 512 * kGroup) {
+        uint4 u[kGroup];
 #pragma unroll
-            for (int gq = 0; gq < kGroup; ++gq) {          // all loads of the group first
-                const int c = c0 + 512 * gq + lane * 16;
-                u[gq] = (c < D && !pad) ? ld_nc_v4(sb + c) : make_uint4(0, 0, 0, 0);
-            }
+        for (int gq = 0; gq < kGroup; ++gq) {          // all loads of the group first
+            const int c = c0 + 512 * gq + lane * 16;
+            u[gq] = (c < n && !zero) ? ld_nc_v4(src + c) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-            for (int gq = 0; gq < kGroup; ++gq) {
-                const int c = c0 + 512 * gq + lane * 16;
-                if (c < D) *reinterpret_cast<uint4*>(db + c) = scale_i8x16(u[gq], mul);
-            }
+        for (int gq = 0; gq < kGroup; ++gq) {
+            const int c = c0 + 512 * gq + lane * 16;
+            if (c < n) *reinterpret_cast<uint4*>(dst + c) = mul == 1 ? u[gq] : scale_i8x16(u[gq], mul);
         }
     }
 }
 
-cudaError_t launch_compact_wgrad(const int8_t* xq, int64_t N, int64_t D, const int32_t* items, const int8_t* wexp,
-                                 const int32_t* count, int64_t kcap, int8_t* b_w, cudaStream_t s) {
-    int64_t blocks = (kcap + 7) / 8;
+__global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
+    const int64_t pad_x = (int64_t(__ldg(a.count_x)) + 127) & ~int64_t(127);
+    const int64_t pad_w = (int64_t(__ldg(a.count_w)) + 127) & ~int64_t(127);
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int64_t total = pad_x + 2 * pad_w;
+    const int two_n = 2 * a.N;
+    for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
+        if (j < pad_x) {
+            const int32_t item = __ldg(a.items_x + j);
+            const bool pad = item >= two_n;
+            copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1);
+        } else if (j < pad_x + pad_w) {
+            const int64_t r = j - pad_x;
+            const int32_t item = __ldg(a.items_w + r);
+            const bool pad = item >= two_n;
+            copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_w + r * a.C, a.C, lane, pad, 1);
+        } else {
+            const int64_t r = j - pad_x - pad_w;
+            const int32_t item = __ldg(a.items_w + r);
+            const bool pad = item >= two_n;
+            const int t = pad ? 0 : (item >= a.N ? item - a.N : item);
+            copy_row(a.xq + int64_t(t) * a.D, a.b_w + r * a.D, a.D, lane, pad, pad ? 1 : (1 << __ldg(a.wexp_w + r)));
+        }
+    }
+}
+
+cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
+    const int64_t rows = (2 * int64_t(a.N) + 128) * 3;       // upper bound of pad_x + 2 pad_w
+    int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    compact_wgrad_kernel<<<int(blocks), 256, 0, s>>>(xq, int(N), int(D), items, wexp, count, b_w);
+    compact_kernel<<<int(blocks), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -40,8 +40,17 @@ int sampler_max_tokens();
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
 
 // compact.cu ------------------------------------------------------------------
-cudaError_t launch_compact_wgrad(const int8_t* xq, int64_t N, int64_t D, const int32_t* items, const int8_t* wexp,
-                                 const int32_t* count, int64_t kcap, int8_t* b_w, cudaStream_t s);
+struct CompactArgs {
+    const int8_t* plane;      // [2N+1, C] bit-split plane (16 hi / lo / zero row)
+    const int8_t* xq;         // [N, D] X_hat
+    int32_t N, C, D;
+    const int32_t* items_x; const int32_t* count_x;
+    const int32_t* items_w; const int8_t* wexp_w; const int32_t* count_w;
+    int8_t* a_x;              // [2N+128, C]
+    int8_t* a_w;              // [kcap, C]
+    int8_t* b_w;              // [kcap, D]
+};
+cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
 enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3 };
