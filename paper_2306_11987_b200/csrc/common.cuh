@@ -53,12 +53,12 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
     return {c0, c1, c2, c3};
 }
 
-// Philox with the 10 round keys precomputed once per thread (bulk generation).
+// Philox with the 10 round keys precomputed on the host and passed as a kernel
+// parameter (they sit in the constant bank: each round is 2 IMAD.WIDE + 2 LOP3).
 struct PhiloxKeys { uint32_t k0[10], k1[10]; };
 
-__device__ __forceinline__ PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+__host__ __device__ inline PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
     PhiloxKeys K;
-#pragma unroll
     for (int r = 0; r < 10; ++r) { K.k0[r] = k0; K.k1[r] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
     return K;
 }

@@ -176,7 +176,7 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 // ---------------------------------------------------------------------------
 constexpr int kSplitThreads = 256;
 constexpr int kBsGroup = 4;
-constexpr int kAmaxUnroll = 4;
+constexpr int kAmaxUnroll = 8;
 
 __device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t w) {
     return max(w & 0x7FFFu, (w >> 16) & 0x7FFFu);
@@ -193,7 +193,7 @@ __device__ __forceinline__ uint2 pack8_i8(const int (&v)[8]) {
 
 __global__ void __launch_bounds__(kSplitThreads, 4)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ block_max,
-                  uint32_t k0, uint32_t k1, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
+                  const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out) {
     namespace cgrp = cooperative_groups;
     cgrp::grid_group grid = cgrp::this_grid();
@@ -245,7 +245,6 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     if (blockIdx.x == gridDim.x - 1)                      // plane row 2N: the all-zero gather pad
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(hilo + 2 * N * C + c) = make_uint4(0, 0, 0, 0);
-    const PhiloxKeys keys = philox_keys(k0, k1);
     const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
     const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
     const int nch = (C + 255) >> 8;
@@ -324,8 +323,8 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     const int64_t want = (N + 7) / 8;                       // one warp per row at most
     if (want < blocks) blocks = int(want);
     if (blocks > kGradSplitMaxBlocks) blocks = kGradSplitMaxBlocks;
-    const uint32_t k0 = uint32_t(seed), k1 = uint32_t(seed >> 32);
-    void* args[] = {(void*)&g, (void*)&N, (void*)&C, (void*)&block_max, (void*)&k0, (void*)&k1, (void*)&call_id,
+    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
+    void* args[] = {(void*)&g, (void*)&N, (void*)&C, (void*)&block_max, (void*)&keys, (void*)&call_id,
                     (void*)&token_offset, (void*)&hilo, (void*)&a_sq, (void*)&s_down, (void*)&amax_out};
     int Ci = int(C);
     args[2] = (void*)&Ci;
