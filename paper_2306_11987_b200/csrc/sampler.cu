@@ -47,19 +47,8 @@ struct SamplerSmem {
     uint32_t warp_c[kSamplerThreads / 32];
     uint32_t scan[kSamplerThreads / 32];
     uint32_t cta_tot[kClusterCTAs];
-    // log-bucket histogram of the scores (water-filling pre-pass)
-    uint32_t hcnt[512];
-    uint64_t hsum[512];
-    uint64_t hmax[512];
-    int32_t b_clamp;
 };
 
-// 512 log-spaced buckets: 8 per octave (msb position and the next 3 bits).
-__device__ __forceinline__ int score_bucket(uint64_t w) {
-    const int e = 63 - __clzll((long long)w);
-    const uint32_t f3 = e >= 3 ? uint32_t(w >> (e - 3)) & 7u : uint32_t(w << (3 - e)) & 7u;
-    return e * 8 + int(f3);
-}
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
@@ -86,6 +75,19 @@ template <> struct Group<kClusterCTAs> {
     __device__ void sync() const { g.sync(); }
     template <class T> __device__ T* map(T* p, int r) const { return g.map_shared_rank(p, r); }
 };
+
+// Exact floor(num 2^32 / W) for 0 < num < W < 2^64 without a 128-bit division:
+// a double-precision estimate (relative error < 2^-52, so off by at most a few
+// units) corrected by exact 128-bit products.
+__device__ __forceinline__ uint64_t floor_mul2_32_div(uint64_t num, uint64_t W) {
+    const unsigned __int128 lhs = (unsigned __int128)num << 32;
+    double est = (double(num) / double(W)) * 4294967296.0;
+    uint64_t q = uint64_t(est);
+    if (q > 0) q -= 1;                                  // start at or below the true quotient
+    while ((unsigned __int128)(q + 1) * W <= lhs) ++q;  // at most a few steps
+    while ((unsigned __int128)q * W > lhs) --q;
+    return q;
+}
 
 // Group-wide (sum w, sum c); every thread of every CTA receives the totals.
 template <int CL>
@@ -163,67 +165,6 @@ lss_sampler_kernel(SamplerArgs a) {
     const bool binding = bernoulli && uint64_t(Z) > B;
     uint64_t R = B, W = Wall;
     if (binding) {
-        // Pre-pass (exact): with S_b = {items in buckets > b}, the predicate
-        // f(b) = (B - |S_b|) * max{w in buckets <= b} < sum{w in buckets <= b}
-        // is monotone in b (SURVEY.md §8(c) O-8'); the A.2 fixed point satisfies
-        // S_{b1+1} (subset of) S* (subset of) S_{b1} for b1 = max{b : f(b)}, so every
-        // bucket above b1 + 1 is clamped up front and the A.2 rounds below only
-        // settle the items of bucket b1 + 1.
-        for (int b = threadIdx.x; b < 512; b += kSamplerThreads) { sm.hcnt[b] = 0; sm.hsum[b] = 0; sm.hmax[b] = 0; }
-        cl.sync();
-        for (int j = t_lo; j < t_hi; ++j) {
-            const uint64_t w = sm.w[j];
-            if (w == 0) continue;
-            const int b = score_bucket(w);
-            atomicAdd(&sm.hcnt[b], 1u);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&sm.hsum[b]), (unsigned long long)w);
-            atomicMax(reinterpret_cast<unsigned long long*>(&sm.hmax[b]), (unsigned long long)w);
-        }
-        __syncthreads();
-        if (rank != 0) {                                  // merge into CTA 0's histogram (DSMEM atomics)
-            for (int b = threadIdx.x; b < 512; b += kSamplerThreads) {
-                if (sm.hcnt[b] == 0) continue;
-                atomicAdd(cl.map(&sm.hcnt[b], 0), sm.hcnt[b]);
-                atomicAdd(reinterpret_cast<unsigned long long*>(cl.map(&sm.hsum[b], 0)), (unsigned long long)sm.hsum[b]);
-                atomicMax(reinterpret_cast<unsigned long long*>(cl.map(&sm.hmax[b], 0)), (unsigned long long)sm.hmax[b]);
-            }
-        }
-        cl.sync();
-        if (rank == 0 && threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            // lane owns buckets [16 lane, 16 lane + 16): counts / sums of all higher
-            // buckets and the max of all lower buckets (exact, 32 x 16 values)
-            uint32_t c_hi = 0; uint64_t s_hi = 0, m_lo = 0;
-            for (int l2 = 0; l2 < 32; ++l2) {
-                uint32_t c2 = 0; uint64_t s2 = 0, m2 = 0;
-                for (int q = 0; q < 16; ++q) { const int b = 16 * l2 + q; c2 += sm.hcnt[b]; s2 += sm.hsum[b]; m2 = max(m2, sm.hmax[b]); }
-                if (l2 > lane) { c_hi += c2; s_hi += s2; }
-                if (l2 < lane) m_lo = max(m_lo, m2);
-            }
-            // walk this lane's buckets from the top: S_b = buckets > b
-            int best = -1;
-            uint32_t cnt_above = c_hi; uint64_t sum_above = s_hi;
-            for (int q = 15; q >= 0; --q) {
-                const int b = 16 * lane + q;
-                uint64_t m_below = m_lo;                             // max over buckets <= b
-                for (int q2 = 0; q2 <= q; ++q2) m_below = max(m_below, sm.hmax[16 * lane + q2]);
-                const uint64_t Rb = B - uint64_t(cnt_above);
-                const uint64_t Wb = Wall - sum_above;
-                if (cnt_above <= B && m_below > 0 && Rb * m_below < Wb) best = max(best, b);
-                cnt_above += sm.hcnt[b]; sum_above += sm.hsum[b];
-            }
-            for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
-            if (lane == 0) {
-                const int bc = best + 1;                             // clamp buckets > bc
-                for (int r = 0; r < CL; ++r) *cl.map(&sm.b_clamp, r) = bc;
-            }
-        }
-        cl.sync();
-        const int bc = sm.b_clamp;
-        for (int j = t_lo; j < t_hi; ++j) {
-            const uint64_t w = sm.w[j];
-            if (w > 0 && score_bucket(w) > bc) sm.clamped[j] = 1;
-        }
         uint32_t s_cnt = 0;
         for (int round = 0; round <= n_items + 1; ++round) {
             uint64_t wun = 0; uint32_t sc = 0;
@@ -264,7 +205,7 @@ lss_sampler_kernel(SamplerArgs a) {
                     e = e_max;
                     T1 = T2 = 1ull << (32 - e_max);
                 } else {
-                    T2 = uint64_t(((unsigned __int128)num << 32) / W);
+                    T2 = floor_mul2_32_div(num, W);
                     T1 = 2 * T2 - (1ull << (32 - e));
                 }
                 const uint64_t idx = 2ull * uint64_t(a.token_offset + t) + uint64_t(h);
