@@ -105,7 +105,9 @@ typedef struct {
  *                              padded with the sentinel 2N up to a multiple of 128
  *   wexp_w   int8  [2N + 128]  log2 of each kept item's weight (~ m_i / p_i)
  *   count_w  int32 [1]         number of kept items (device)
- *   items_x, wexp_x, count_x   the same for the grad_X mask */
+ *   items_x, wexp_x, count_x   the same for the grad_X mask, in token-major order
+ *                              (slot 2t + h: a token's two items are adjacent)
+ *   x_touched uint8 [N]        1 if token t has a kept grad_X item */
 typedef struct {
     int8_t* hilo;
     int32_t* a_sq;
@@ -118,6 +120,7 @@ typedef struct {
     int32_t* items_x;
     int8_t* wexp_x;
     int32_t* count_x;
+    uint8_t* x_touched;
 } i4_lss_plan;
 
 /* F1+F2 / F3: block-Hadamard transform + LSQ quantize of a bf16 matrix

@@ -152,13 +152,26 @@ def dyadic_thresholds(p, e_max):
     return e, T1, T2
 
 
-def sample(w, budget, u, mode, e_max):
-    """Masks m_i and weights for all 2N items, compacted in ascending item order.
+def sample(w, budget, u, mode, e_max, token_major=False):
+    """Masks m_i and weights for all 2N items, compacted in ascending item order
+    (ids h*N + t), or token-major (t, h) when `token_major` (the order of the
+    grad_X list; the estimator does not depend on the order).
 
     w: uint64 [2, N] scores, u: uint64 [2, N] Philox words (row h).
     Returns dict(items int64 [K], wexp int64 [K], count K, p list, e, T1, T2).
     """
     w = np.asarray(w)
+    two, N = w.shape
+    out = _sample_item_order(w, budget, u, mode, e_max)
+    if token_major and out["count"]:
+        key = (out["items"] % N) * 2 + out["items"] // N
+        order = np.argsort(key, kind="stable")
+        out["items"] = out["items"][order]
+        out["wexp"] = out["wexp"][order]
+    return out
+
+
+def _sample_item_order(w, budget, u, mode, e_max):
     two, N = w.shape
     wf = [int(x) for x in w.reshape(-1)]          # item id i = h*N + t
     uf = [int(x) for x in np.asarray(u).reshape(-1)]
@@ -195,10 +208,11 @@ def sample_weight_mask(a_sq, b_sq, seed, call_id, token_offset, mode=MODE_BERNOU
 
 
 def sample_activation_mask(a_sq, seed, call_id, token_offset, mode=MODE_BERNOULLI):
-    """LSS mask of the activation gradient, purpose-3 stream."""
+    """LSS mask of the activation gradient (PAPER.md:619-632), purpose-3 stream;
+    list in token-major order (t, h)."""
     N = np.asarray(a_sq).shape[1]
     w = activation_scores(a_sq)
     u = mask_uniforms(seed, call_id, token_offset, N, PURPOSE_MASK_X)
-    out = sample(w, N, u, mode, E_MAX_X)
+    out = sample(w, N, u, mode, E_MAX_X, token_major=True)
     out["w"] = w
     return out

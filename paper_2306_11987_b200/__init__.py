@@ -48,7 +48,7 @@ class I4LssPlan(ctypes.Structure):
                 ("s_down", ctypes.c_void_p), ("scratch", ctypes.c_void_p), ("items_w", ctypes.c_void_p),
                 ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
-                ("count_x", ctypes.c_void_p)]
+                ("count_x", ctypes.c_void_p), ("x_touched", ctypes.c_void_p)]
 
 
 def _load():
@@ -213,11 +213,13 @@ class Int4Linear:
         self.wexp_w = torch.empty(n2, dtype=i8, device=dev)
         self.items_x = torch.empty(n2, dtype=i32, device=dev)
         self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
+        self.x_touched = torch.empty(N, dtype=torch.uint8, device=dev)
         sp = self.scalars.data_ptr()
         self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
                               scratch=self.scratch.data_ptr(),
                               items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
-                              items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12)
+                              items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12,
+                              x_touched=self.x_touched.data_ptr())
         self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
 
     def forward(self, X, W, s_x, s_w, Y, reuse_weight=False, stream=None):

@@ -288,7 +288,7 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
                             cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words) {
     I4_RETURN_IF(check_device());
     if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
-        !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x)
+        !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x || !plan->x_touched)
         return fail(I4_ERR_ARG, "bitsplit_lss: NULL pointer");
     if (mode != I4_LSS_BERNOULLI && mode != I4_LSS_KEEP_POSITIVE && mode != I4_LSS_NONE)
         return fail(I4_ERR_ARG, "bitsplit_lss: bad mode");
@@ -313,6 +313,7 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
     a.items[0] = plan->items_w; a.wexp[0] = plan->wexp_w; a.count[0] = plan->count_w;
     a.items[1] = plan->items_x; a.wexp[1] = plan->wexp_x; a.count[1] = plan->count_x;
     a.zero_words = zero_words; a.n_zero_words = n_zero_words;
+    a.x_touched = plan->x_touched;
     I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
     return I4_OK;
 }
@@ -394,10 +395,10 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         ca.items_x = plan->items_x; ca.count_x = plan->count_x;
         ca.items_w = plan->items_w; ca.wexp_w = plan->wexp_w; ca.count_w = plan->count_w;
         ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
+        ca.x_touched = plan->x_touched; ca.dx = dX;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
-    I4_LAUNCH(cudaMemsetAsync(dX, 0, size_t(N * D) * sizeof(float), s), "memset_dx", s);
     {
         i4::GemmArgs g{};
         g.M = int32_t(2 * N + 128); g.m_dev = plan->count_x;

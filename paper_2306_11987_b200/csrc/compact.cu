@@ -43,15 +43,35 @@ __device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t*
     }
 }
 
+__device__ __forceinline__ void zero_row_f32(float* dst, int n, int lane) {
+    for (int c = lane * 4; c < n; c += 128) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
-    const int64_t pad_x = (int64_t(__ldg(a.count_x)) + 127) & ~int64_t(127);
+    const int64_t cnt_x = __ldg(a.count_x);
+    const int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
     const int64_t pad_w = (int64_t(__ldg(a.count_w)) + 127) & ~int64_t(127);
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int64_t total = pad_x + 2 * pad_w;
+    const int64_t n_straddle = (cnt_x + 31) / 32;            // candidate positions 31, 63, ...
+    const int64_t total = pad_x + 2 * pad_w + a.N + n_straddle;
     const int two_n = 2 * a.N;
     for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
-        if (j < pad_x) {
+        if (j >= pad_x + 2 * pad_w) {
+            // grad_X rows the GEMM epilogue does not store: tokens without a kept
+            // item, and tokens whose two items straddle a 32-row group (both red.add)
+            const int64_t r = j - pad_x - 2 * pad_w;
+            if (r < a.N) {
+                if (__ldg(a.x_touched + r) == 0) zero_row_f32(a.dx + r * a.D, a.D, lane);
+            } else {
+                const int64_t p = 32 * (r - a.N) + 31;
+                if (p + 1 < cnt_x) {
+                    const int32_t i0 = __ldg(a.items_x + p), i1 = __ldg(a.items_x + p + 1);
+                    const int t0 = i0 >= a.N ? i0 - a.N : i0, t1 = i1 >= a.N ? i1 - a.N : i1;
+                    if (t0 == t1) zero_row_f32(a.dx + int64_t(t0) * a.D, a.D, lane);
+                }
+            }
+        } else if (j < pad_x) {
             const int32_t item = __ldg(a.items_x + j);
             const bool pad = item >= two_n;
             copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1);
@@ -71,7 +91,7 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
 }
 
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
-    const int64_t rows = (2 * int64_t(a.N) + 128) * 3;       // upper bound of pad_x + 2 pad_w
+    const int64_t rows = (2 * int64_t(a.N) + 128) * 3 + a.N;  // upper bound of the row count
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 8) blocks = 148 * 8;
     compact_kernel<<<int(blocks), 256, 0, s>>>(a);

@@ -28,8 +28,10 @@
 //            -> swizzled shared-memory staging -> TMA bulk tensor store
 //            EPI_DGRAD  row = kept item (h, t): v = acc * s_w s_down 2^wexp 2^{-k/2} (the
 //                       plane row holds 16 hi or lo, so s_up = 16 s_down is folded in);
-//                       v = I_X[t] o v; v = v H; red.add.v4 into dX[t]
-//                       (<= 2 addends per element onto 0: order-independent)
+//                       v = I_X[t] o v; v = v H; rows are token-major, so a token's
+//                       two items are adjacent lanes: summed by a shuffle and stored
+//                       once (pairs straddling a 32-row group: red.add.v4 of 2
+//                       addends onto a zeroed row -- order-independent)
 //   Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of
 //   tile i+1.  M (grad_X: kept items) or K (grad_W: kept items) may be read
 //   from device memory, so the sampled sizes never travel to the host.
@@ -282,13 +284,25 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             bool valid = row < M;
             int64_t out_row = row;
             float rscale = g.scale;
+            // grad_X rows are token-major kept items: a token's two items are adjacent
+            // rows; the first adds its neighbour's values (shuffle) and stores plainly;
+            // pairs straddling a 32-row group use red.add onto rows zeroed beforehand
+            int dmode = 0;                             // 0 store, 1 store pair sum, 2 skip, 3 red.add
             if (EPI == EPI_DGRAD) {
-                const int item = valid ? __ldg(g.items + row) : 2 * g.n_tokens;
-                valid = valid && item < 2 * g.n_tokens;
+                const int two_n = 2 * g.n_tokens;
+                const int item = valid ? __ldg(g.items + row) : two_n;
+                valid = valid && item < two_n;
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
                 const int e = valid ? int(__ldg(g.wexp + row)) : 0;
                 rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
+                const int inext = (valid && row + 1 < M) ? __ldg(g.items + row + 1) : two_n;
+                const int iprev = (valid && row > 0) ? __ldg(g.items + row - 1) : two_n;
+                const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;
+                const bool second = iprev < two_n && (iprev >= g.n_tokens ? iprev - g.n_tokens : iprev) == out_row;
+                if ((first && lane == 31) || (second && lane == 0)) dmode = 3;
+                else if (second) dmode = 2;
+                else if (first) dmode = 1;
             } else if (EPI == EPI_WGRAD) {
                 rscale = __fmul_rn(g.scale, sd);
             }
@@ -340,19 +354,29 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if (col0 >= g.Nn) continue;           // ragged N (MN-major B): nothing to write
 
                 if (EPI == EPI_DGRAD) {
-                    if (valid) {
-                        float v[CW];
+                    float v[CW];
+                    const int64_t mrow = valid ? out_row : 0;
 #pragma unroll
-                        for (int q = 0; q < CW / 32; ++q) {
-                            const uint32_t mw = __ldg(g.mask + out_row * words + (col0 >> 5) + q);
+                    for (int q = 0; q < CW / 32; ++q) {
+                        const uint32_t mw = valid ? __ldg(g.mask + mrow * words + (col0 >> 5) + q) : 0u;
 #pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
-                        }
-                        fwht_inplace<CW>(v, g.k_had);
-                        float* dst = reinterpret_cast<float*>(g.out) + out_row * g.Nn + col0;
+                        for (int i = 0; i < 32; ++i)
+                            v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
+                    }
+                    fwht_inplace<CW>(v, g.k_had);
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) {         // warp-wide: every lane takes part
+                        const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
+                        if (dmode == 1) v[i] = __fadd_rn(v[i], o);
+                    }
+                    float* dst = reinterpret_cast<float*>(g.out) + mrow * g.Nn + col0;
+                    if (valid && dmode == 3) {
 #pragma unroll
                         for (int i = 0; i < CW; i += 4) red_add_v4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    } else if (valid && dmode != 2) {
+#pragma unroll
+                        for (int i = 0; i < CW; i += 4)
+                            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                     }
                     continue;
                 }

@@ -33,6 +33,7 @@ struct SamplerArgs {
     int32_t* items[2];        // [0] grad_W mask, [1] grad_X mask
     int8_t* wexp[2];
     int32_t* count[2];
+    uint8_t* x_touched;       // [N]: 1 if the token has a kept grad_X item (optional)
     uint32_t* zero_words;     // optional: words zeroed by the launch (split-K flags of the GEMMs)
     int32_t n_zero_words;
 };
@@ -46,6 +47,8 @@ struct CompactArgs {
     int32_t N, C, D;
     const int32_t* items_x; const int32_t* count_x;
     const int32_t* items_w; const int8_t* wexp_w; const int32_t* count_w;
+    const uint8_t* x_touched; // [N]
+    float* dx;                // [N, D]: rows of untouched tokens and of straddling pairs are zeroed here
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]

@@ -133,6 +133,10 @@ lss_sampler_kernel(SamplerArgs a) {
     const int t_hi = min(nloc, t_lo + ipt);
     const int e_max = mask_id == 0 ? kEMaxW : kEMaxX;
     const uint32_t purpose = mask_id == 0 ? kPurposeMaskW : kPurposeMaskX;
+    // slot -> item id: the grad_W list is in item order h*N + t; the grad_X list is
+    // token-major (slot 2t + h) so that a token's two items are adjacent rows of
+    // the grad_X GEMM and combine in its epilogue without atomics
+    auto item_of = [&](int slot) { return mask_id == 0 ? slot : (slot & 1) * N + (slot >> 1); };
     int parity = 0;
     if (blockIdx.y == 0 && rank == 0)
         for (int i = threadIdx.x; i < a.n_zero_words; i += kSamplerThreads) a.zero_words[i] = 0u;
@@ -140,9 +144,10 @@ lss_sampler_kernel(SamplerArgs a) {
     // ---- scores -------------------------------------------------------------
     uint64_t sum_pos = 0; uint32_t cnt_pos = 0;
     for (int j = t_lo; j < t_hi; ++j) {
-        const int i = base + j;
+        const int i = item_of(base + j);
         const int h = i >= N ? 1 : 0;
         const int t = i - h * N;
+        if (mask_id == 1 && h == 0 && a.x_touched) a.x_touched[t] = 0;   // set below for kept items
         uint64_t w = 0;
         if (a.mode != 2) {                                           // I4_LSS_NONE needs no scores
             const double av = double(__ldg(a.a_sq + i));
@@ -186,7 +191,7 @@ lss_sampler_kernel(SamplerArgs a) {
     // ---- Bernoulli with dyadic weights ---------------------------------------
     uint32_t my_keep = 0;
     for (int j = t_lo; j < t_hi; ++j) {
-        const int i = base + j;
+        const int i = item_of(base + j);
         const int h = i >= N ? 1 : 0;
         const int t = i - h * N;
         const uint64_t w = sm.w[j];
@@ -217,6 +222,7 @@ lss_sampler_kernel(SamplerArgs a) {
         }
         sm.wexp[j] = out;
         my_keep += (out >= 0);
+        if (mask_id == 1 && out >= 0 && a.x_touched) a.x_touched[t] = 1;
     }
 
     // ---- compaction: block exclusive scan + cluster prefix --------------------
@@ -255,7 +261,7 @@ lss_sampler_kernel(SamplerArgs a) {
     for (int j = t_lo; j < t_hi; ++j) {
         const int8_t e = sm.wexp[j];
         if (e >= 0) {
-            items[pos] = base + j;
+            items[pos] = item_of(base + j);
             wexp[pos] = e;
             ++pos;
         }
