@@ -240,8 +240,8 @@ def run_ours(args):
     X, W, G = up(x), up(w), up(g)
     layer = i4.Int4Linear(N, D, C, k, device=dev)
     Y = torch.empty(N, C, dtype=torch.bfloat16, device=dev)
-    dX = torch.empty(N, D, dtype=torch.float32, device=dev)
-    dW = torch.empty(C, D, dtype=torch.float32, device=dev)
+    dX = torch.empty(N, D, dtype=torch.bfloat16, device=dev)   # perf mode: bf16 Y and grad_X (Z-24)
+    dW = torch.empty(C, D, dtype=torch.float32, device=dev)    # fp32 grad_W (all-reduce operand)
     token_offset = pdist.token_offset(rank, N)           # global token index of this shard
     flush_w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     flush_r = torch.ones(32 * 1024 * 1024, dtype=torch.int64, device=dev)
@@ -398,7 +398,7 @@ def run_ours(args):
         hw = torch.from_numpy(synth.bf16_bits(w).view(np.int16).copy()).view(torch.bfloat16).pin_memory()
         hg = torch.from_numpy(synth.bf16_bits(g).view(np.int16).copy()).view(torch.bfloat16).pin_memory()
         hY = torch.empty(N, C, dtype=torch.bfloat16).pin_memory()
-        hdX = torch.empty(N, D, dtype=torch.float32).pin_memory()
+        hdX = torch.empty(N, D, dtype=torch.bfloat16).pin_memory()
         hdW = torch.empty(C, D, dtype=torch.float32).pin_memory()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e2e_ms = []
@@ -418,7 +418,7 @@ def run_ours(args):
         t_e2e = pdist.max_over_ranks(statistics.mean(e2e_ms), dev)
         e2e = {"value": 6.0 * N * C * D * world / (t_e2e * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": int(hx.numel() * 2 + hw.numel() * 2 + hg.numel() * 2),
-               "d2h_bytes_per_step": int(hY.numel() * 2 + hdX.numel() * 4 + hdW.numel() * 4),
+               "d2h_bytes_per_step": int(hY.numel() * 2 + hdX.numel() * 2 + hdW.numel() * 4),
                "ms_per_step": t_e2e,
                "path": "pinned host X, W, grad_Y -> device; Int4Linear.forward/backward (C ABI); Y, grad_X, grad_W -> pinned host"}
 

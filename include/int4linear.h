@@ -155,14 +155,17 @@ I4_API i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_
                        void* stream);
 
 /* Full LSS-MM backward (Eq. 4):
- *   grad_X = [I_X o (s_W sum_kept w_i s_h code_i W_hat)] H^T   -> dX [N, D] fp32
+ *   grad_X = [I_X o (s_W sum_kept w_i s_h code_i W_hat)] H^T   -> dX [N, D]
  *   grad_W = s_X [(sum_kept w_i s_h code_i (x) X_hat_t) o I_W] H^T -> dW [C, D] fp32
  * Runs bitsplit_lss into *plan, then the compaction and the two INT32 GEMMs
  * whose epilogues apply scale, mask and the inverse transform (reading Z-23).
- * ws: device scratch of int4_bwd_workspace_size(N, D, C) bytes. */
+ * dX is fp32 (dx_dtype = I4_OUT_F32, parity mode) or bf16 (I4_OUT_BF16, perf
+ * mode as the cuBLAS BF16 baseline; reading Z-24); dW stays fp32 (the data-
+ * parallel all-reduce operand).  ws: device scratch of
+ * int4_bwd_workspace_size(N, D, C) bytes. */
 I4_API i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
-                          int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, float* dX,
-                          float* dW, void* ws, size_t ws_bytes, void* stream);
+                                 int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
+                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream);
 
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);

@@ -61,8 +61,8 @@ def _load():
         "hadamard_quant": [vp, i64, i64, i32, f32, vp, vp, vp, vp],
         "int4_linear_fwd": [vp, vp, i64, i64, i64, i32, f32, f32, vp, i32, ctypes.POINTER(I4FwdCache), vp],
         "bitsplit_lss": [vp, i64, i64, vp, u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp],
-        "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, vp,
-                            vp, ctypes.c_size_t, vp],
+        "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, i32,
+                            vp, vp, ctypes.c_size_t, vp],
         "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
@@ -126,10 +126,12 @@ def bitsplit_lss(dY, x_sqnorm, seed, call_id, token_offset, mode, plan, stream=N
 
 
 def int4_linear_bwd(dY, cache, seed, call_id, token_offset, mode, plan, dX, dW, ws, stream=None):
-    """LSS-MM backward."""
+    """LSS-MM backward; dX fp32 or bf16, dW fp32."""
+    import torch
+    dx_dtype = OUT_BF16 if dX.dtype == torch.bfloat16 else OUT_F32
     _check(lib.int4_linear_bwd(_ptr(dY), ctypes.byref(cache), int(seed), int(call_id), int(token_offset), int(mode),
-                               ctypes.byref(plan), _ptr(dX), _ptr(dW), _ptr(ws), ws.numel() * ws.element_size(),
-                               _stream(stream)))
+                               ctypes.byref(plan), _ptr(dX), dx_dtype, _ptr(dW), _ptr(ws),
+                               ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def int4_bwd_workspace_size(N, D, C):

@@ -368,10 +368,11 @@ extern "C" {
 size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) { return carve_bwd_ws(nullptr, N, D, C).total; }
 
 i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
-                          int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, float* dX, float* dW,
-                          void* ws, size_t ws_bytes, void* stream) {
+                          int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
+                          i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream) {
     I4_RETURN_IF(check_device());
     if (!cache || !dX || !dW || !ws) return fail(I4_ERR_ARG, "int4_linear_bwd: NULL pointer");
+    if (dx_dtype != I4_OUT_F32 && dx_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "int4_linear_bwd: bad dx_dtype");
     const int64_t N = cache->N, D = cache->D, C = cache->C;
     const int32_t k = cache->k;
     if (N <= 0 || D <= 0 || C <= 0) return fail(I4_ERR_ARG, "int4_linear_bwd: cache not filled by int4_linear_fwd");
@@ -395,7 +396,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         ca.items_x = plan->items_x; ca.count_x = plan->count_x;
         ca.items_w = plan->items_w; ca.wexp_w = plan->wexp_w; ca.count_w = plan->count_w;
         ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
-        ca.x_touched = plan->x_touched; ca.dx = dX;
+        ca.x_touched = plan->x_touched; ca.dx = dX; ca.dx_bf16 = dx_dtype == I4_OUT_BF16;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
@@ -405,6 +406,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.Nn = int32_t(D); g.K = int32_t(C);
         g.epi = i4::EPI_DGRAD;
         g.out = dX;
+        g.out_bf16 = dx_dtype == I4_OUT_BF16;
         g.scale = cache->s_w * inv_sqrt_block(k);
         g.s_down = plan->s_down;
         g.k_had = k;

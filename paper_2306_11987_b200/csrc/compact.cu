@@ -43,8 +43,10 @@ __device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t*
     }
 }
 
-__device__ __forceinline__ void zero_row_f32(float* dst, int n, int lane) {
-    for (int c = lane * 4; c < n; c += 128) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+__device__ __forceinline__ void zero_row(void* base, int64_t row, int n, bool bf16, int lane) {
+    uint8_t* dst = static_cast<uint8_t*>(base) + row * n * (bf16 ? 2 : 4);
+    const int bytes = n * (bf16 ? 2 : 4);
+    for (int c = lane * 16; c < bytes; c += 512) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
 }
 
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
@@ -62,13 +64,13 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
             // item, and tokens whose two items straddle a 32-row group (both red.add)
             const int64_t r = j - pad_x - 2 * pad_w;
             if (r < a.N) {
-                if (__ldg(a.x_touched + r) == 0) zero_row_f32(a.dx + r * a.D, a.D, lane);
+                if (__ldg(a.x_touched + r) == 0) zero_row(a.dx, r, a.D, a.dx_bf16, lane);
             } else {
                 const int64_t p = 32 * (r - a.N) + 31;
                 if (p + 1 < cnt_x) {
                     const int32_t i0 = __ldg(a.items_x + p), i1 = __ldg(a.items_x + p + 1);
                     const int t0 = i0 >= a.N ? i0 - a.N : i0, t1 = i1 >= a.N ? i1 - a.N : i1;
-                    if (t0 == t1) zero_row_f32(a.dx + int64_t(t0) * a.D, a.D, lane);
+                    if (t0 == t1) zero_row(a.dx, t0, a.D, a.dx_bf16, lane);
                 }
             }
         } else if (j < pad_x) {

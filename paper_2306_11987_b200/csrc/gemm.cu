@@ -369,6 +369,24 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
                         if (dmode == 1) v[i] = __fadd_rn(v[i], o);
                     }
+                    if (g.out_bf16) {                       // perf mode: bf16 grad_X (reading Z-24)
+                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(g.out) + mrow * g.Nn + col0;
+                        uint32_t pk[CW / 2];
+#pragma unroll
+                        for (int i = 0; i < CW / 2; ++i) {
+                            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                            pk[i] = *reinterpret_cast<uint32_t*>(&p2);
+                        }
+                        if (valid && dmode == 3) {          // 2 bf16 addends onto 0: order-independent
+#pragma unroll
+                            for (int i = 0; i < CW / 2; ++i) red_add_bf16x2(dst + 2 * i, pk[i]);
+                        } else if (valid && dmode != 2) {
+#pragma unroll
+                            for (int i = 0; i < CW / 2; i += 4)
+                                *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
+                        }
+                        continue;
+                    }
                     float* dst = reinterpret_cast<float*>(g.out) + mrow * g.Nn + col0;
                     if (valid && dmode == 3) {
 #pragma unroll

@@ -48,7 +48,8 @@ struct CompactArgs {
     const int32_t* items_x; const int32_t* count_x;
     const int32_t* items_w; const int8_t* wexp_w; const int32_t* count_w;
     const uint8_t* x_touched; // [N]
-    float* dx;                // [N, D]: rows of untouched tokens and of straddling pairs are zeroed here
+    void* dx;                 // [N, D] fp32 or bf16: rows of untouched tokens / straddling pairs zeroed here
+    int32_t dx_bf16;
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]

@@ -218,6 +218,18 @@ def test_backward_degenerate_zero_and_single_row():
     assert not np.delete(dX, 37, axis=0).any()
 
 
+def test_backward_bf16_grad_x():
+    # perf mode (reading Z-24): bf16 grad_X equals the fp32 result rounded once
+    N, D, C, k = 512, 256, 512, 5
+    x, w, s_x, s_w, layer, g, dX32, dW32 = _bwd_case(N, D, C, k, dense=True)
+    dX = torch.empty(N, D, dtype=torch.bfloat16, device="cuda")
+    dW = torch.empty(C, D, dtype=torch.float32, device="cuda")
+    layer.backward(to_bf16_cuda(g), dX, dW, synth.PHILOX_SEED, 3, 0, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(dW.cpu().numpy(), dW32)
+    assert rel_frob(dX.float().cpu().numpy(), dX32) < 4e-3
+
+
 def test_backward_deterministic_bytes():
     N, D, C, k = 512, 256, 512, 5
     runs = [_bwd_case(N, D, C, k, dense=True) for _ in range(2)]
