@@ -175,7 +175,13 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 //            grad_Y is re-read right after phase 1, mostly from L2.
 // ---------------------------------------------------------------------------
 constexpr int kSplitThreads = 256;
-constexpr int kBsGroup = 4;
+#ifndef I4_BS_GROUP
+#define I4_BS_GROUP 4
+#endif
+#ifndef I4_BS_MINB
+#define I4_BS_MINB 4
+#endif
+constexpr int kBsGroup = I4_BS_GROUP;
 constexpr int kAmaxUnroll = 8;
 
 __device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t w) {
@@ -191,7 +197,7 @@ __device__ __forceinline__ uint2 pack8_i8(const int (&v)[8]) {
     return make_uint2(__byte_perm(a, b, 0x5410), __byte_perm(c, d, 0x5410));
 }
 
-__global__ void __launch_bounds__(kSplitThreads, 4)
+__global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ block_max,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out) {
