@@ -211,6 +211,47 @@ def algorithmic_work(name, N, D, C, kx, kw):
     return "bytes", 0.0
 
 
+def dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels):
+    """roofline entry of the dominant kernel: CUDA events around its node in the step graph."""
+    import torch
+
+    import paper_2306_11987_b200 as i4
+
+    # ---- dominant kernel: CUDA events bracketing its launch inside the step graph
+    dom_idx = names.index(dom)
+    dom_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
+    dom_tr = i4.LaunchTrace(dom_ev, first_launch=dom_idx)
+    g_dom = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_dom):
+        with dom_tr:
+            step_body()
+    dom_ms = []
+    timed_replays(g_dom, args.warmup)
+    timed_replays(g_dom, args.steps, on_step=lambda: dom_ms.append(dom_ev[0].elapsed_time(dom_ev[1])))
+    avg_s = statistics.mean(dom_ms) * 1e-3
+    kind, amount = algorithmic_work(dom, N, D, C, kx, kw)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+    if kind == "ops":
+        achieved = amount / avg_s / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+                "frac": achieved / int8_peak, "traffic": traffic,
+                "peak_source": f"{peaks['source']}: bf16 {peaks['bf16_tflops']} TF/s x nominal INT8:BF16 = 2 (int8 TOPS)",
+                "work_per_launch": f"2*M*N*K = {amount:.4g} int ops"}
+    else:
+        achieved = amount / avg_s / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
+                "work_per_launch": f"{amount:.4g} algorithmic bytes"}
+    roof["avg_launch_us_events"] = avg_s * 1e6
+    roof["avg_launch_us_cupti"] = kernels[dom]["avg_us"]
+    roof["timing"] = ("CUDA events recorded on the launch stream immediately before/after this kernel's "
+                      "node inside the captured step graph, averaged over the timed steps")
+    return roof
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -353,41 +394,11 @@ def run_ours(args):
         elif kind == "bytes" and avg_us > 0 and amount > 0:
             ent.update(achieved_gbs=amount / (avg_us * 1e-6) / 1e9, frac_hbm=amount / (avg_us * 1e-6) / 1e9 / peaks["hbm_gbs"])
         kernels[nm] = ent
-    dom = max((nm for nm in kernels if not nm.startswith("memset")), key=lambda nm: kernels[nm]["avg_us"])
-
-    # ---- dominant kernel: CUDA events bracketing its launch inside the step graph
-    dom_idx = names.index(dom)
-    dom_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2)]
-    dom_tr = i4.LaunchTrace(dom_ev, first_launch=dom_idx)
-    g_dom = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_dom):
-        with dom_tr:
-            step_body()
-    dom_ms = []
-    timed_replays(g_dom, args.warmup)
-    timed_replays(g_dom, args.steps, on_step=lambda: dom_ms.append(dom_ev[0].elapsed_time(dom_ev[1])))
-    avg_s = statistics.mean(dom_ms) * 1e-3
-    kind, amount = algorithmic_work(dom, N, D, C, kx, kw)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
-    if kind == "ops":
-        achieved = amount / avg_s / 1e12
-        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
-                "frac": achieved / int8_peak, "traffic": traffic,
-                "peak_source": f"{peaks['source']}: bf16 {peaks['bf16_tflops']} TF/s x nominal INT8:BF16 = 2 (int8 TOPS)",
-                "work_per_launch": f"2*M*N*K = {amount:.4g} int ops"}
-    else:
-        achieved = amount / avg_s / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
-                "work_per_launch": f"{amount:.4g} algorithmic bytes"}
-    roof["avg_launch_us_events"] = avg_s * 1e6
-    roof["avg_launch_us_cupti"] = kernels[dom]["avg_us"]
-    roof["timing"] = ("CUDA events recorded on the launch stream immediately before/after this kernel's "
-                      "node inside the captured step graph, averaged over the timed steps")
-
+    dom = max((nm for nm in kernels if not nm.startswith("memset")), key=lambda nm: kernels[nm]["avg_us"],
+              default=None)   # None when CUPTI is unavailable (e.g. the run is under ncu)
+    roof = None
+    if dom is not None:
+        roof = dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels)
     gemm_ops = 2.0 * C * D * (N + kx + kw)
     gemm_us = sum(kernels[nm]["avg_us"] for nm in ("gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad") if nm in kernels)
 

@@ -181,6 +181,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t ra
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(cluster_addr) : "memory");
 }
+// Relaxed remote arrive: no memory ordering (no fence that waits for this
+// thread's outstanding global stores).  Enough when the barrier only orders
+// tcgen05 operations (tcgen05.fence::before_thread_sync precedes it), e.g.
+// "this accumulator stage has been read out of TMEM".
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" :: "r"(cluster_addr) : "memory");
+}
 // 2-SM TMA load: data lands in this CTA's smem, completion is counted on the
 // mbarrier at `bar_cluster_addr` (the leader CTA's barrier).
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* tmap, uint32_t bar_cluster_addr,

@@ -21,7 +21,8 @@
 //            issues tcgen05.mma (M = 128 CG, N = BN, K = 32 per instruction, 4 per
 //            128-deep k-block) and tcgen05.commit to release stages / publish
 //            accumulators to both CTAs.
-//   warps 2-5  epilogue: tcgen05.ld (32 lanes x 32 columns) -> registers, then
+//   warps 2-5 (2-9)  epilogue, one (two) per TMEM lane group -- with 8 warps each
+//            takes half of the tile's columns: tcgen05.ld (32 lanes x 32 columns) -> registers, then
 //            EPI_INT32  raw accumulators (bit-exact parity checks)
 //            EPI_FWD    Y = fl32(acc) * fl32(s_x s_w)   (HQ-MM step 4)
 //            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; dW
@@ -44,19 +45,30 @@ namespace i4 {
 
 constexpr int kBM = 128;
 constexpr int kBK = 128;                     // bytes = int8 elements along K per stage
-constexpr int kGemmThreads = 192;
-constexpr int kRingBytes = 192 * 1024;
 constexpr int kStageOutBytes = 4096;         // per epilogue warp per buffer: 32 rows x 128 B
-constexpr int kEpiWarps = 4;
+constexpr int kMaxEpiWarps = 8;
 
-template <int BN, int CG>
+// Epilogue warps: 4 (one per TMEM lane group) or 8 (two per lane group, each
+// taking one half of the tile's columns) -- the epilogue (tcgen05.ld, scaling,
+// masking, the k-level FWHT, stores) is the bottleneck for short-K tiles, so
+// it gets twice the warps whenever the register budget of a chunk allows.
+template <int BN, int EPI, int CH>
+struct EpiShape {
+    static constexpr int CW = (EPI == EPI_FWD) ? 64 : CH;          // columns per chunk
+    static constexpr int WARPS = (CH <= 64 && BN / 2 >= CW) ? 8 : 4;
+    static constexpr int COLS = BN / (WARPS / 4);                    // columns per warp
+    static constexpr int THREADS = 64 + 32 * WARPS;
+};
+
+template <int BN, int CG, int EPW>
 struct GemmCfg {
     static constexpr int A_BYTES = kBM * kBK;
     static constexpr int B_BYTES = (BN / CG) * kBK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = kRingBytes / STAGE_BYTES;
+    static constexpr int RING = EPW == 8 ? 160 * 1024 : 192 * 1024;
+    static constexpr int STAGES = RING / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int OUT_BYTES = kEpiWarps * 2 * kStageOutBytes;
+    static constexpr int OUT_BYTES = EPW * 2 * kStageOutBytes;
     static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + 1024 + 256;
 };
 
@@ -83,6 +95,17 @@ __device__ __forceinline__ int choose_splits(int tiles, int pairs, int nk, int m
     return best;
 }
 
+// mask word j of a warp's preloaded column range (j is a compile-time index
+// after unrolling the chunk loop only when the range is one chunk; otherwise a
+// small select chain keeps the array in registers)
+template <int NW>
+__device__ __forceinline__ uint32_t mask_word(const uint32_t (&mw)[NW], int j) {
+    uint32_t v = mw[0];
+#pragma unroll
+    for (int q = 1; q < NW; ++q) v = j == q ? mw[q] : v;
+    return v;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -93,10 +116,12 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 }
 
 template <int BN, int EPI, int CH, bool A_MN, bool B_MN, int CG>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(EpiShape<BN, EPI, CH>::THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
-    using Cfg = GemmCfg<BN, CG>;
+    using Epi = EpiShape<BN, EPI, CH>;
+    constexpr int kEpiWarps = Epi::WARPS;
+    using Cfg = GemmCfg<BN, CG, kEpiWarps>;
     constexpr int BMP = kBM * CG;                // rows per (pair) tile
     constexpr int BNC = BN / CG;                 // B rows / columns staged by this CTA
     constexpr int STAGES = Cfg::STAGES;
@@ -251,15 +276,63 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     } else {
         // ------------------------------------------------------------- epilogue
         const int lg = warp & 3;                       // TMEM lane group of this warp
+        const int ew = warp - 2;                       // epilogue warp index
+        const int cbeg = (ew >> 2) * Epi::COLS;        // this warp's column range [cbeg, cbeg + COLS)
         const int r_in_tile = lg * 32 + lane;
         const int words = g.Nn >> 5;
         uint8_t* stg = sOut + (warp - 2) * 2 * kStageOutBytes;
         int sbuf = 0;
         float sd = 1.0f;
         if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
+        // Row metadata (kept item, its neighbours, its weight exponent) and the mask
+        // words of this warp's columns are loaded two / one tile(s) ahead: the mask
+        // row of a grad_X item depends on the item index, and both loads would
+        // otherwise sit as two dependent global-memory latencies on every tile.
+        constexpr bool kMask = EPI == EPI_DGRAD || EPI == EPI_WGRAD;
+        constexpr int NW = kMask ? Epi::COLS / 32 : 1;
+        const int two_n = 2 * g.n_tokens;
+        struct RowInfo { int item, inext, iprev, e; };
+        auto load_ri = [&](int u) {
+            RowInfo x{two_n, two_n, two_n, 0};
+            if (EPI == EPI_DGRAD && u < units) {
+                const int tl = u % T;
+                const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+                if (rw < M) {
+                    x.item = __ldg(g.items + rw);
+                    x.e = int(__ldg(g.wexp + rw));
+                    if (rw + 1 < M) x.inext = __ldg(g.items + rw + 1);
+                    if (rw > 0) x.iprev = __ldg(g.items + rw - 1);
+                }
+            }
+            return x;
+        };
+        auto load_mask = [&](int u, const RowInfo& x, uint32_t (&mw)[NW]) {
+#pragma unroll
+            for (int q = 0; q < NW; ++q) mw[q] = 0u;
+            if (!kMask || u >= units) return;
+            const int tl = u % T;
+            const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+            int64_t mrow = rw;
+            if (EPI == EPI_DGRAD) {
+                if (x.item >= two_n) return;
+                mrow = x.item >= g.n_tokens ? x.item - g.n_tokens : x.item;
+            } else if (rw >= M) {
+                return;
+            }
+            const int cw0 = ((tl % n_tiles) * BN + cbeg) >> 5;
+#pragma unroll
+            for (int q = 0; q < NW; ++q)
+                if (cw0 + q < words) mw[q] = __ldg(g.mask + mrow * words + cw0 + q);
+        };
+        RowInfo ri_cur = load_ri(pair0), ri_next = load_ri(pair0 + n_pairs);
+        uint32_t mw_cur[NW];
+        load_mask(pair0, ri_cur, mw_cur);
         int it = 0;
         for (int u = pair0; u < units; u += n_pairs, ++it) {
             UNIT_DECODE(u)
+            uint32_t mw_next[NW];
+            load_mask(u + n_pairs, ri_next, mw_next);  // ri_next arrived during the previous tile
+            const RowInfo ri_next2 = load_ri(u + 2 * n_pairs);
             const int as = it & 1;
             const uint32_t ap = (it >> 1) & 1;
             const int m0 = (tile / n_tiles) * BMP + kBM * int(rank), n0 = (tile % n_tiles) * BN;
@@ -270,15 +343,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t* flag = nullptr;
             if (S > 1) {
                 part = g.partial + (int64_t(tile) * BMP + kBM * int(rank) + r_in_tile) * BN;
-                flag = g.flags + (tile * CG + int(rank)) * kEpiWarps + lg;
+                flag = g.flags + (tile * CG + int(rank)) * kMaxEpiWarps + ew;
                 if (split < S - 1) {                   // wait until the higher splits are in `part`
                     if (lane == 0) while (ld_acquire_u32(flag) < uint32_t(S - 1 - split)) { }
                     __syncwarp();
                 }
             }
-            mbar_wait(&tfull[as], ap);
-            tc_fence_after();
-            const uint32_t t_row = tmem_base + (uint32_t(lg * 32) << 16) + uint32_t(as * BN);
 
             // per-row setup
             bool valid = row < M;
@@ -289,15 +359,14 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             // pairs straddling a 32-row group use red.add onto rows zeroed beforehand
             int dmode = 0;                             // 0 store, 1 store pair sum, 2 skip, 3 red.add
             if (EPI == EPI_DGRAD) {
-                const int two_n = 2 * g.n_tokens;
-                const int item = valid ? __ldg(g.items + row) : two_n;
+                const int item = ri_cur.item;
                 valid = valid && item < two_n;
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
-                const int e = valid ? int(__ldg(g.wexp + row)) : 0;
+                const int e = valid ? ri_cur.e : 0;
                 rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
-                const int inext = (valid && row + 1 < M) ? __ldg(g.items + row + 1) : two_n;
-                const int iprev = (valid && row > 0) ? __ldg(g.items + row - 1) : two_n;
+                const int inext = valid ? ri_cur.inext : two_n;
+                const int iprev = valid ? ri_cur.iprev : two_n;
                 const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;
                 const bool second = iprev < two_n && (iprev >= g.n_tokens ? iprev - g.n_tokens : iprev) == out_row;
                 if ((first && lane == 31) || (second && lane == 0)) dmode = 3;
@@ -306,19 +375,22 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             } else if (EPI == EPI_WGRAD) {
                 rscale = __fmul_rn(g.scale, sd);
             }
+            mbar_wait(&tfull[as], ap);
+            tc_fence_after();
+            const uint32_t t_row = tmem_base + (uint32_t(lg * 32) << 16) + uint32_t(as * BN);
 
-            constexpr int CW = (EPI == EPI_FWD) ? 64 : CH;   // columns per chunk
+            constexpr int CW = Epi::CW;
 #pragma unroll 1
-            for (int c = 0; c < BN; c += CW) {
+            for (int c = cbeg; c < cbeg + Epi::COLS; c += CW) {
                 uint32_t r[CW / 32][32];
 #pragma unroll
                 for (int q = 0; q < CW / 32; ++q) tmem_ld_32x32b_x32(t_row + uint32_t(c + 32 * q), r[q]);
                 tmem_ld_wait();
-                if (c + CW >= BN) {                   // accumulator stage drained -> MMA may reuse it
+                if (c + CW >= cbeg + Epi::COLS) {     // this warp's part drained -> MMA may reuse it
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
-                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+                        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty[as]), 0));
                         else mbar_arrive(&tempty[as]);
                     }
                 }
@@ -358,7 +430,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     const int64_t mrow = valid ? out_row : 0;
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q) {
-                        const uint32_t mw = valid ? __ldg(g.mask + mrow * words + (col0 >> 5) + q) : 0u;
+                        const uint32_t mw = mask_word(mw_cur, (c - cbeg) / 32 + q);
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
@@ -434,10 +506,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         wv[i] = __float_as_uint(__fmul_rn(float(int32_t(r[i >> 5][i & 31])), rscale));
                 } else {                              // EPI_WGRAD
                     float v[CW];
-                    const int64_t mrow = valid ? out_row : 0;
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q) {
-                        const uint32_t mw = valid ? __ldg(g.mask + mrow * words + (col0 >> 5) + q) : 0u;
+                        const uint32_t mw = mask_word(mw_cur, (c - cbeg) / 32 + q);
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
@@ -462,6 +533,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     sbuf ^= 1;
                 }
             }
+            ri_cur = ri_next; ri_next = ri_next2;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) mw_cur[q] = mw_next[q];
             if (S > 1) {
                 __syncwarp();
                 if (split > 0) {                       // publish: this warp's rows now hold S - split splits
@@ -484,7 +558,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 size_t gemm_split_partial_bytes() { return size_t(kSplitMaxTiles) * (kBM * kGemmCG) * 256 * sizeof(int32_t); }
-size_t gemm_split_flag_words() { return size_t(kSplitMaxTiles) * kGemmCG * kEpiWarps; }
+size_t gemm_split_flag_words() { return size_t(kSplitMaxTiles) * kGemmCG * kMaxEpiWarps; }
 
 int gemm_block_n(int Nn, bool b_mn) {
     if (Nn % 256 == 0 || b_mn) return 256;      // MN-major B halves are whole 128-byte atoms
@@ -497,12 +571,13 @@ constexpr int kCG = kGemmCG;                    // CTA pairs (cta_group::2) for 
 template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
 static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
     auto kern = gemm_i8_kernel<BN, EPI, CH, A_MN, B_MN, kCG>;
-    constexpr int smem = GemmCfg<BN, kCG>::SMEM;
+    using Epi = EpiShape<BN, EPI, CH>;
+    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(Epi::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
