@@ -22,6 +22,8 @@ __all__ = [
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
+# development knob: time a compile variant of the same library (tools/exp_bwd.py)
+LIB_PATH = os.environ.get("I4_LIB_OVERRIDE", LIB_PATH)
 
 LSS_BERNOULLI, LSS_KEEP_POSITIVE, LSS_NONE = 0, 1, 2
 OUT_F32, OUT_BF16 = 0, 1

@@ -431,7 +431,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.mask = cache->w_mask;
         g.a_mn = 1; g.b_mn = 1;                  // A_W [K items, C], B_W [K, D]: both MN-major
         g.partial = w.part_w; g.flags = w.flags_w;
-        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
+        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;   // few (C/256 x D/256) tiles, long sampled K
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, s));
     }
     return I4_OK;

@@ -99,6 +99,24 @@ __device__ __forceinline__ void fwht_inplace(float (&v)[CH], int k) {
     }
 }
 
+// Same transform with k fixed at compile time: every stage runs unconditionally,
+// so the butterflies ping-pong between registers with no moves or branches.
+template <int CH, int K>
+__device__ __forceinline__ void fwht_static(float (&v)[CH]) {
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const int h = 1 << s;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            if (((i >> s) & 1) == 0 && i + h < CH) {
+                const float a = v[i], b = v[i + h];
+                v[i] = __fadd_rn(a, b);
+                v[i + h] = __fsub_rn(a, b);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier
 // ---------------------------------------------------------------------------
@@ -145,6 +163,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
                  :: "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(smem_src)) : "memory");
+}
+// plain (non-tensor) bulk copy shared -> global; bytes and both addresses 16-B aligned
+__device__ __forceinline__ void bulk_copy_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"(smem_u32(smem_src)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>

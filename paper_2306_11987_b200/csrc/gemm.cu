@@ -52,6 +52,10 @@ constexpr int kMaxEpiWarps = 8;
 // taking one half of the tile's columns) -- the epilogue (tcgen05.ld, scaling,
 // masking, the k-level FWHT, stores) is the bottleneck for short-K tiles, so
 // it gets twice the warps whenever the register budget of a chunk allows.
+// columns per epilogue chunk for Hadamard order 2^KH (one row's block must be
+// in one thread's registers)
+constexpr int kh_ch(int KH) { return KH <= 5 ? 32 : (1 << KH); }
+
 template <int BN, int EPI, int CH>
 struct EpiShape {
     static constexpr int CW = (EPI == EPI_FWD) ? 64 : CH;          // columns per chunk
@@ -60,16 +64,18 @@ struct EpiShape {
     static constexpr int THREADS = 64 + 32 * WARPS;
 };
 
-template <int BN, int CG, int EPW>
+template <int BN, int CG, int EPW, int EPI, int COLS>
 struct GemmCfg {
     static constexpr int A_BYTES = kBM * kBK;
     static constexpr int B_BYTES = (BN / CG) * kBK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int RING = EPW == 8 ? 160 * 1024 : 192 * 1024;
-    static constexpr int STAGES = RING / STAGE_BYTES;
+    static constexpr int OUT_BYTES = EPI == EPI_DGRAD ? 0 : EPW * 2 * kStageOutBytes;   // grad_X: direct stores
+    static constexpr int MAX_SMEM = 232448 - 1024 - 256;
+    static constexpr int STAGES_FIT = (MAX_SMEM - OUT_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT < 6 ? STAGES_FIT : 6;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int OUT_BYTES = EPW * 2 * kStageOutBytes;
     static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + 1024 + 256;
+    static_assert(STAGES >= 3, "shared memory ring too shallow");
 };
 
 // 16-byte chunk c of staging row r (128-byte rows, SWIZZLE_128B pattern)
@@ -85,11 +91,14 @@ __device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
 // it on, and split 0 runs the real epilogue.  Units are numbered so that a unit
 // only ever waits on a lower-numbered one, so a persistent grid of co-resident
 // CTAs cannot deadlock.
+// The partial-sum hand-over costs about kSplitHandoverKb k-blocks of MMA time
+// (measured: a 2-way split of a 32-k-block grad_W took longer than none).
+constexpr int kSplitHandoverKb = 24;
 __device__ __forceinline__ int choose_splits(int tiles, int pairs, int nk, int max_splits) {
     int best = 1, best_cost = ((tiles + pairs - 1) / pairs) * nk;
     for (int s = 2; s <= max_splits; ++s) {
         if (nk < 2 * s) break;
-        const int cost = ((s * tiles + pairs - 1) / pairs) * ((nk + s - 1) / s);
+        const int cost = ((s * tiles + pairs - 1) / pairs) * ((nk + s - 1) / s) + kSplitHandoverKb;
         if (cost < best_cost) { best = s; best_cost = cost; }
     }
     return best;
@@ -115,13 +124,15 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
-template <int BN, int EPI, int CH, bool A_MN, bool B_MN, int CG>
-__global__ void __launch_bounds__(EpiShape<BN, EPI, CH>::THREADS, 1)
+// KH: Hadamard order k of the grad epilogues (compile-time, 0 for FWD / INT32)
+template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG>
+__global__ void __launch_bounds__(EpiShape<BN, EPI, kh_ch(KH)>::THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+    constexpr int CH = kh_ch(KH);
     using Epi = EpiShape<BN, EPI, CH>;
     constexpr int kEpiWarps = Epi::WARPS;
-    using Cfg = GemmCfg<BN, CG, kEpiWarps>;
+    using Cfg = GemmCfg<BN, CG, kEpiWarps, EPI, Epi::COLS>;
     constexpr int BMP = kBM * CG;                // rows per (pair) tile
     constexpr int BNC = BN / CG;                 // B rows / columns staged by this CTA
     constexpr int STAGES = Cfg::STAGES;
@@ -280,7 +291,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int cbeg = (ew >> 2) * Epi::COLS;        // this warp's column range [cbeg, cbeg + COLS)
         const int r_in_tile = lg * 32 + lane;
         const int words = g.Nn >> 5;
-        uint8_t* stg = sOut + (warp - 2) * 2 * kStageOutBytes;
+        uint8_t* stg = sOut + (warp - 2) * (Cfg::OUT_BYTES / kEpiWarps);
         int sbuf = 0;
         float sd = 1.0f;
         if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
@@ -427,7 +438,6 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
                 if (EPI == EPI_DGRAD) {
                     float v[CW];
-                    const int64_t mrow = valid ? out_row : 0;
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q) {
                         const uint32_t mw = mask_word(mw_cur, (c - cbeg) / 32 + q);
@@ -435,20 +445,20 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         for (int i = 0; i < 32; ++i)
                             v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
                     }
-                    fwht_inplace<CW>(v, g.k_had);
+                    fwht_static<CW, KH>(v);
 #pragma unroll
                     for (int i = 0; i < CW; ++i) {         // warp-wide: every lane takes part
                         const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
                         if (dmode == 1) v[i] = __fadd_rn(v[i], o);
                     }
                     if (g.out_bf16) {                       // perf mode: bf16 grad_X (reading Z-24)
-                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(g.out) + mrow * g.Nn + col0;
                         uint32_t pk[CW / 2];
 #pragma unroll
                         for (int i = 0; i < CW / 2; ++i) {
                             __nv_bfloat162 p2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
                             pk[i] = *reinterpret_cast<uint32_t*>(&p2);
                         }
+                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(g.out) + (valid ? out_row : 0) * g.Nn + col0;
                         if (valid && dmode == 3) {          // 2 bf16 addends onto 0: order-independent
 #pragma unroll
                             for (int i = 0; i < CW / 2; ++i) red_add_bf16x2(dst + 2 * i, pk[i]);
@@ -459,6 +469,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                         continue;
                     }
+                    const int64_t mrow = valid ? out_row : 0;
                     float* dst = reinterpret_cast<float*>(g.out) + mrow * g.Nn + col0;
                     if (valid && dmode == 3) {
 #pragma unroll
@@ -513,7 +524,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         for (int i = 0; i < 32; ++i)
                             v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
                     }
-                    fwht_inplace<CW>(v, g.k_had);
+                    fwht_static<CW, KH>(v);
 #pragma unroll
                     for (int i = 0; i < CW; ++i) wv[i] = __float_as_uint(v[i]);
                 }
@@ -547,7 +558,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
         }
 #undef UNIT_DECODE
-        if (lane == 0) bulk_wait<0>();
+        bulk_wait<0>();                                // every lane: its own copies are done
         __syncwarp();
     }
 
@@ -568,11 +579,11 @@ int gemm_block_n(int Nn, bool b_mn) {
 
 constexpr int kCG = kGemmCG;                    // CTA pairs (cta_group::2) for every GEMM
 
-template <int BN, int EPI, int CH, bool A_MN, bool B_MN>
+template <int BN, int EPI, int KH, bool A_MN, bool B_MN>
 static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    auto kern = gemm_i8_kernel<BN, EPI, CH, A_MN, B_MN, kCG>;
-    using Epi = EpiShape<BN, EPI, CH>;
-    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS>::SMEM;
+    auto kern = gemm_i8_kernel<BN, EPI, KH, A_MN, B_MN, kCG>;
+    using Epi = EpiShape<BN, EPI, kh_ch(KH)>;
+    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS, EPI, Epi::COLS>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
@@ -589,30 +600,42 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cu
                               *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c), g);
 }
 
-template <int EPI, int CH, bool A_MN, bool B_MN>
+template <int EPI, int KH, bool A_MN, bool B_MN>
 static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    if (bn == 256) return launch_one<256, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+    if (bn == 256) return launch_one<256, EPI, KH, A_MN, B_MN>(m, g, grid, s);
     if constexpr (!B_MN) {
-        if (bn == 128) return launch_one<128, EPI, CH, A_MN, B_MN>(m, g, grid, s);
-        if constexpr (CH <= 64) return launch_one<64, EPI, CH, A_MN, B_MN>(m, g, grid, s);
+        if (bn == 128) return launch_one<128, EPI, KH, A_MN, B_MN>(m, g, grid, s);
+        if constexpr (kh_ch(KH) <= 64) return launch_one<64, EPI, KH, A_MN, B_MN>(m, g, grid, s);
     }
     return cudaErrorInvalidValue;
 }
 
 template <int EPI, bool A_MN, bool B_MN>
 static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) {
-        if (g.k_had >= 7) return dispatch_bn<EPI, 128, A_MN, B_MN>(bn, m, g, grid, s);
-        if (g.k_had == 6) return dispatch_bn<EPI, 64, A_MN, B_MN>(bn, m, g, grid, s);
+    if constexpr (EPI == EPI_DGRAD || EPI == EPI_WGRAD) {
+        switch (g.k_had) {
+            case 0: return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, grid, s);
+            case 1: return dispatch_bn<EPI, 1, A_MN, B_MN>(bn, m, g, grid, s);
+            case 2: return dispatch_bn<EPI, 2, A_MN, B_MN>(bn, m, g, grid, s);
+            case 3: return dispatch_bn<EPI, 3, A_MN, B_MN>(bn, m, g, grid, s);
+            case 4: return dispatch_bn<EPI, 4, A_MN, B_MN>(bn, m, g, grid, s);
+            case 5: return dispatch_bn<EPI, 5, A_MN, B_MN>(bn, m, g, grid, s);
+            case 6: return dispatch_bn<EPI, 6, A_MN, B_MN>(bn, m, g, grid, s);
+            case 7: return dispatch_bn<EPI, 7, A_MN, B_MN>(bn, m, g, grid, s);
+            default: return cudaErrorInvalidValue;
+        }
+    } else {
+        return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, grid, s);
     }
-    return dispatch_bn<EPI, 32, A_MN, B_MN>(bn, m, g, grid, s);
 }
 
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s) {
     const int bn = gemm_block_n(g.Nn, g.b_mn);
     const int64_t tiles = int64_t((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
     const int64_t pairs = num_sms / kCG;
-    int grid = kCG * int(tiles < pairs ? tiles : pairs);
+    // split-K turns each of few tiles into several work units: size the grid for those
+    const int64_t units = (g.partial != nullptr && tiles <= g.max_tiles_split) ? tiles * g.max_splits : tiles;
+    int grid = kCG * int(units < pairs ? units : pairs);
     if (grid < kCG) grid = kCG;
     switch (g.epi) {
         case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, grid, s);

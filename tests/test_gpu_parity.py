@@ -39,7 +39,7 @@ GEMM_SHAPES = [(128, 64, 64), (300, 256, 1024), (1000, 192, 128), (77, 512, 4096
 
 @pytest.mark.parametrize("split_ws", [False, True])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
-@pytest.mark.parametrize("M,N,K", GEMM_SHAPES + [(128, 64, 8192), (512, 256, 3008)])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES + [(128, 64, 8192), (512, 256, 3008), (300, 256, 12288)])
 def test_gemm_int32_bit_exact(M, N, K, a_mn, b_mn, split_ws):
     if a_mn and M % 16:
         pytest.skip("MN-major A needs 16-byte rows")
@@ -59,7 +59,7 @@ def test_gemm_int32_bit_exact(M, N, K, a_mn, b_mn, split_ws):
         ref = o_gemm.int_matmul_abt(a, b)
         assert np.array_equal(acc.cpu().numpy().astype(np.int64), ref)
     if ws is not None:
-        flags = ws[-(96 * 2 * 4 * 4):].view(torch.int32)
+        flags = ws[-(96 * 2 * 8 * 4):].view(torch.int32)   # kSplitMaxTiles x CG x 8 warps
         assert int(flags.abs().sum()) == 0
 
 
