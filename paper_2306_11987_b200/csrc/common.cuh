@@ -117,6 +117,73 @@ __device__ __forceinline__ void fwht_static(float (&v)[CH]) {
     }
 }
 
+// Packed fp32x2 arithmetic (sm_100a add/sub/mul.rn.f32x2 -> FADD2 / FMUL2): each
+// lane of the pair is an ordinary IEEE fp32 op with round-to-nearest, so results
+// are bit-identical to the scalar __fadd_rn / __fsub_rn / __fmul_rn.
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// The same FWHT stages (same order, same roundings) on CH values held as CH/2
+// pairs q[i] = (v[i], v[i + CH/2]): every stage with stride h < CH/2 pairs
+// q[i] with q[i + h] and runs as packed FADD2/FADD2(sub); the stride-CH/2 stage
+// combines the two halves of each pair with scalar ops.
+template <int CH, int K>
+__device__ __forceinline__ void fwht_pairs(uint64_t (&q)[CH / 2]) {
+    constexpr int HALF = CH / 2;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const int h = 1 << s;
+        if (h < HALF) {
+#pragma unroll
+            for (int i = 0; i < HALF; ++i) {
+                if (((i >> s) & 1) == 0) {
+                    const uint64_t a = q[i], b = q[i + h];
+                    q[i] = f2_add(a, b);
+                    q[i + h] = f2_sub(a, b);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < HALF; ++i) {
+                float a, b;
+                f2_unpack(q[i], a, b);
+                q[i] = f2_pack(__fadd_rn(a, b), __fsub_rn(a, b));
+            }
+        }
+    }
+}
+template <int CH, int K>
+__device__ __forceinline__ void fwht_static2(float (&v)[CH]) {
+    constexpr int HALF = CH / 2;
+    uint64_t q[HALF];
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) q[i] = f2_pack(v[i], v[i + HALF]);
+    fwht_pairs<CH, K>(q);
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) f2_unpack(q[i], v[i], v[i + HALF]);
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier
 // ---------------------------------------------------------------------------

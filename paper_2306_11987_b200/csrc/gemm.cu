@@ -115,6 +115,31 @@ __device__ __forceinline__ uint32_t mask_word(const uint32_t (&mw)[NW], int j) {
     return v;
 }
 
+// v = H_k (I o (acc * rscale)) for one CW-column chunk of a row: the mask is
+// applied to the integer accumulators, the scale and the butterflies run on
+// fp32 pairs (element j with element j + CW/2); same roundings as the scalar
+// formula fl(fl(acc) * rscale) followed by the FWHT stages in order.
+template <int CW, int KH, int NW>
+__device__ __forceinline__ void masked_scaled_fwht(const uint32_t (&r)[CW / 32][32], const uint32_t (&mw)[NW],
+                                                   int w0, float rscale, float (&v)[CW]) {
+    constexpr int HALF = CW / 2;
+    uint32_t m[CW / 32];
+#pragma unroll
+    for (int q = 0; q < CW / 32; ++q) m[q] = mask_word(mw, w0 + q);
+    const uint64_t rs2 = f2_pack(rscale, rscale);
+    uint64_t p[HALF];
+#pragma unroll
+    for (int j = 0; j < HALF; ++j) {
+        const int e0 = j, e1 = j + HALF;
+        const int32_t a = ((m[e0 >> 5] >> (e0 & 31)) & 1u) ? int32_t(r[e0 >> 5][e0 & 31]) : 0;
+        const int32_t b = ((m[e1 >> 5] >> (e1 & 31)) & 1u) ? int32_t(r[e1 >> 5][e1 & 31]) : 0;
+        p[j] = f2_mul(f2_pack(float(a), float(b)), rs2);
+    }
+    fwht_pairs<CW, KH>(p);
+#pragma unroll
+    for (int j = 0; j < HALF; ++j) f2_unpack(p[j], v[j], v[j + HALF]);
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -438,14 +463,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
                 if (EPI == EPI_DGRAD) {
                     float v[CW];
-#pragma unroll
-                    for (int q = 0; q < CW / 32; ++q) {
-                        const uint32_t mw = mask_word(mw_cur, (c - cbeg) / 32 + q);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
-                    }
-                    fwht_static<CW, KH>(v);
+                    masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
 #pragma unroll
                     for (int i = 0; i < CW; ++i) {         // warp-wide: every lane takes part
                         const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
@@ -517,14 +535,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         wv[i] = __float_as_uint(__fmul_rn(float(int32_t(r[i >> 5][i & 31])), rscale));
                 } else {                              // EPI_WGRAD
                     float v[CW];
-#pragma unroll
-                    for (int q = 0; q < CW / 32; ++q) {
-                        const uint32_t mw = mask_word(mw_cur, (c - cbeg) / 32 + q);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            v[32 * q + i] = ((mw >> i) & 1u) ? __fmul_rn(float(int32_t(r[q][i])), rscale) : 0.0f;
-                    }
-                    fwht_static<CW, KH>(v);
+                    masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
 #pragma unroll
                     for (int i = 0; i < CW; ++i) wv[i] = __float_as_uint(v[i]);
                 }

@@ -1,17 +1,12 @@
-// Memory-bound quantizer kernels (HBM roofline):
+// Quantizer kernels (HBM roofline; instruction issue is the co-limiter):
 //   hadamard_quant : F1+F2 / F3 -- block FWHT + LSQ (Eq. 2);
-//                    X and W are quantized by ONE launch (two row jobs)
-//   amax_bf16      : B1 -- per-tensor max |grad_Y| (reading Z-9)
-//   bitsplit       : B2 -- Philox SR to the 8-bit code, split into high / low
-//                    4-bit planes, per-row integer norms
-//
-// Thread layout shared by the row kernels: one warp per row; the row is walked
-// in 256-column chunks, lane l owning columns [c0 + 8 l, c0 + 8 l + 8) so each
-// warp-wide 16-byte load covers 512 contiguous bytes.  All loads of a group of
-// chunks are issued before any is consumed (memory-level parallelism: one DRAM
-// latency per group instead of one per chunk).  Hadamard blocks of 2^k <= 8
-// columns are transformed in registers; larger blocks (k = 4..7) add
-// xor-shuffle butterfly stages across lanes 1, 2, 4, 8 apart.
+//                    X and W are quantized by ONE launch (two row jobs); one
+//                    thread per 32-column block, Hadamard order k compile-time,
+//                    butterflies and scaling on fp32 pairs (FADD2 / FMUL2)
+//   grad_split     : B1 + B2 -- per-tensor max |grad_Y| (reading
+//                    Z-9), then Philox SR to the 8-bit code, split into high /
+//                    low 4-bit planes, per-row integer norms (PAPER.md:234-239,
+//                    :680); one cooperative launch with one grid barrier
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -19,7 +14,6 @@
 
 namespace i4 {
 
-constexpr int kRowWarps = 8;            // warps per CTA in the row kernels
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&v)[8]) {
     v[0] = bf16_lo(u.x); v[1] = bf16_hi(u.x);
@@ -31,12 +25,6 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&v)[8]) {
 __device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
     return (uint32_t(a) & 0xFF) | ((uint32_t(b) & 0xFF) << 8) | ((uint32_t(c) & 0xFF) << 16) |
            ((uint32_t(d) & 0xFF) << 24);
-}
-
-static int row_grid(int64_t rows) {
-    int64_t blocks = (rows + kRowWarps - 1) / kRowWarps;
-    const int64_t cap = 148 * 8;        // 8 resident CTAs of 256 threads per SM
-    return int(blocks < cap ? blocks : cap);
 }
 
 // ---------------------------------------------------------------------------
@@ -59,8 +47,9 @@ struct HqJob {
 
 constexpr int kHqMaxThreads = 256;
 
+template <int K>
 __global__ void __launch_bounds__(kHqMaxThreads)
-hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k, int rows_per_cta) {
+hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     const bool second = int(blockIdx.x) >= j0.blocks;
     const HqJob& J = second ? j1 : j0;
     const int bid = second ? int(blockIdx.x) - j0.blocks : int(blockIdx.x);
@@ -72,12 +61,15 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k, int rows_per_cta) {
     __shared__ int sq_row[kHqMaxThreads];
     if (threadIdx.x < rows_per_cta) sq_row[threadIdx.x] = 0;
 
-    float v[32];
+    // column pairs (j, j + 16) in fp32x2 registers: the in-register FWHT stages
+    // (strides 1 .. 8) and the LSQ scaling run as packed FADD2 / FMUL2
+    uint64_t p[16];
     {
         const uint16_t* src = J.x + (active ? row * cols + blk * 32 : 0);
         uint4 raw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) raw[q] = active ? ld_nc_v4(src + 8 * q) : make_uint4(0, 0, 0, 0);
+        float v[32];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             float t[8];
@@ -85,31 +77,39 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int k, int rows_per_cta) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[8 * q + i] = t[i];
         }
-    }
-    fwht_inplace<32>(v, k < 5 ? k : 5);              // strides 1 .. 16: registers only
 #pragma unroll
-    for (int s = 5; s < 7; ++s) {                      // strides 32, 64 columns: partner thread blk ^ 1, ^ 2
-        if (s < k) {
+        for (int j = 0; j < 16; ++j) p[j] = f2_pack(v[j], v[j + 16]);
+    }
+    fwht_pairs<32, (K < 5 ? K : 5)>(p);              // strides 1 .. 16: registers only
+    if constexpr (K > 5) {                           // strides 32, 64 columns: partner thread blk ^ 1, ^ 2
+#pragma unroll
+        for (int s = 5; s < K; ++s) {
             const int lm = 1 << (s - 5);
             const float sgn = (blk & lm) ? -1.0f : 1.0f;   // upper block: o - v, lower: v + o
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const float o = __shfl_xor_sync(0xFFFFFFFFu, v[i], lm);
-                v[i] = __fmaf_rn(sgn, v[i], o);             // one rounding = the add / sub
+            for (int j = 0; j < 16; ++j) {
+                float a, b;
+                f2_unpack(p[j], a, b);
+                const float oa = __shfl_xor_sync(0xFFFFFFFFu, a, lm);
+                const float ob = __shfl_xor_sync(0xFFFFFFFFu, b, lm);
+                p[j] = f2_pack(__fmaf_rn(sgn, a, oa), __fmaf_rn(sgn, b, ob));   // one rounding = the add / sub
             }
         }
     }
     __syncthreads();                                   // sq_row initialised
     if (active) {
         // LSQ: v = fl32(t r); code = clamp(rint(v), -7, 7); mask = |v| <= 7
+        const uint64_t r2 = f2_pack(J.r, J.r);
         int q[32];
         uint32_t mask = 0;
         int sq = 0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const float sv = __fmul_rn(v[i], J.r);
-            q[i] = __float2int_rn(fminf(fmaxf(sv, -7.0f), 7.0f));
-            mask |= uint32_t(fabsf(sv) <= 7.0f) << i;
+        for (int j = 0; j < 16; ++j) {
+            float s0, s1;
+            f2_unpack(f2_mul(p[j], r2), s0, s1);
+            q[j] = __float2int_rn(fminf(fmaxf(s0, -7.0f), 7.0f));
+            q[j + 16] = __float2int_rn(fminf(fmaxf(s1, -7.0f), 7.0f));
+            mask |= (uint32_t(fabsf(s0) <= 7.0f) << j) | (uint32_t(fabsf(s1) <= 7.0f) << (j + 16));
         }
         uint32_t w[8];
 #pragma unroll
@@ -145,7 +145,17 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     const int grid = j0.blocks + j1.blocks;
     if (grid == 0) return cudaSuccess;
     const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
-    hadamard_quant_kernel<<<grid, threads, 0, s>>>(j0, j1, int(a.cols), a.k, R);
+    switch (a.k) {
+        case 0: hadamard_quant_kernel<0><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 1: hadamard_quant_kernel<1><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 2: hadamard_quant_kernel<2><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 3: hadamard_quant_kernel<3><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 4: hadamard_quant_kernel<4><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 5: hadamard_quant_kernel<5><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 6: hadamard_quant_kernel<6><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 7: hadamard_quant_kernel<7><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
