@@ -245,10 +245,25 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         }
     }
     grid.sync();
-    uint32_t amax_b = 0;
-    for (int i = lane; i < int(gridDim.x); i += 32) amax_b = max(amax_b, __ldcg(block_max + i));
+    // reduce the per-CTA slots: warp 0 only, all loads in flight at once, then
+    // broadcast through shared memory
+    __shared__ uint32_t amax_sh;
+    if (warp == 0) {
+        uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i0 = lane; i0 < int(gridDim.x); i0 += 32 * 8) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax_b = max(amax_b, __shfl_xor_sync(0xFFFFFFFFu, amax_b, o));
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + 32 * j;
+                m8[j] = max(m8[j], i < int(gridDim.x) ? __ldcg(block_max + i) : 0u);
+            }
+        }
+        uint32_t m = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])), max(max(m8[4], m8[5]), max(m8[6], m8[7])));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (lane == 0) amax_sh = m;
+    }
+    __syncthreads();
+    const uint32_t amax_b = amax_sh;
     const float amax = __uint_as_float(amax_b << 16);
     const bool zero = !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
