@@ -303,23 +303,34 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, keys);
                 const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, keys);
                 const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-                int hi[8], lo[8];
+                int qv[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const float sv = __fmul_rn(v[i], r8);
                     const float a = fminf(fabsf(sv), 119.0f);
                     const uint64_t A = __float2ull_ru(__fmul_rn(a, 4294967296.0f));   // exact ceil(a 2^32)
                     const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
-                    const int q = sv < 0.0f ? -mag : mag;
-                    hi[i] = (q + 8) >> 4;                                             // floor division
-                    lo[i] = q - (hi[i] << 4);
+                    qv[i] = sv < 0.0f ? -mag : mag;
                 }
-                const uint2 ph = pack8_i8(hi), pl = pack8_i8(lo);
-                shi = __dp4a(int(ph.x), int(ph.x), __dp4a(int(ph.y), int(ph.y), shi));   // sum of squares
-                slo = __dp4a(int(pl.x), int(pl.x), __dp4a(int(pl.y), int(pl.y), slo));
-                // the high plane stores 16 hi (per byte: low nibble moved up; |16 hi| <= 112)
-                *reinterpret_cast<uint2*>(hr + col) = make_uint2((ph.x << 4) & 0xF0F0F0F0u, (ph.y << 4) & 0xF0F0F0F0u);
-                *reinterpret_cast<uint2*>(lr + col) = pl;
+                // bit split on 4 packed codes at a time: t = (q + 128) + 8 per byte (no
+                // carries: q + 136 <= 255); hi = floor((q + 8) / 16) = (t >> 4) - 8, so the
+                // high plane byte 16 hi = (t & 0xF0) - 128 = (t & 0xF0) ^ 0x80; the low
+                // nibble t & 15 = lo + 8, i.e. lo in 4-bit two's complement after ^ 8,
+                // sign-extended to a byte by adding 0xF0 when its bit 3 is set
+                const uint2 qp = pack8_i8(qv);
+                uint32_t ph[2], pl[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t t = ((h ? qp.y : qp.x) ^ 0x80808080u) + 0x08080808u;
+                    ph[h] = (t & 0xF0F0F0F0u) ^ 0x80808080u;
+                    const uint32_t x = (t & 0x0F0F0F0Fu) ^ 0x08080808u;
+                    pl[h] = (x & 0x08080808u) * 0x1Eu + x;
+                }
+                // sums of squares: the high plane holds 16 hi, so its dp4a sum is 256 sum hi^2
+                shi = __dp4a(int(ph[0]), int(ph[0]), __dp4a(int(ph[1]), int(ph[1]), shi));
+                slo = __dp4a(int(pl[0]), int(pl[0]), __dp4a(int(pl[1]), int(pl[1]), slo));
+                *reinterpret_cast<uint2*>(hr + col) = make_uint2(ph[0], ph[1]);
+                *reinterpret_cast<uint2*>(lr + col) = make_uint2(pl[0], pl[1]);
             }
         }
 #pragma unroll
@@ -328,7 +339,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
         }
         if (lane == 0) {
-            a_sq[row] = shi;
+            a_sq[row] = shi >> 8;                             // exact: every term is 256 hi^2
             a_sq[N + row] = slo;
         }
     }
