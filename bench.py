@@ -135,7 +135,7 @@ def workload_config(args, cfg, world=1):
             "tokens_per_gpu": cfg["N"], "global_tokens": cfg["N"] * world, "D": cfg["D"], "C": cfg["C"],
             "k": cfg["k"], "grad_y": args.grad, "lss_mode": args.mode, "parallelism": f"dp{world} (token-sharded)",
             "l2": "flushed before every timed step: 256 MiB write + 256 MiB read of another buffer (cold, clean L2)",
-            "graph": "step captured once in a CUDA graph, replayed"}
+            "graph": "step captured once in a CUDA graph, replayed; kernels chained by programmatic dependent launch (per-kernel breakdown from a PDL-off capture)"}
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -384,7 +384,13 @@ def run_ours(args):
 
     # ---- kernel breakdown: CUPTI kernel records (torch.profiler) over extra replays
     kx, kw = [int(v) for v in layer.counts().cpu().numpy()]
-    cupti = cupti_kernel_times(graph, flush, min(args.steps, 20))
+    # per-kernel numbers come from a PDL-off capture of the same step: with PDL a
+    # kernel launches early and its duration would include the wait on its predecessor
+    prev_pdl = i4.int4_set_pdl(False)
+    graph_serial = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_serial):
+        step_body()
+    cupti = cupti_kernel_times(graph_serial, flush, min(args.steps, 20))
     kernels = {}
     for nm, avg_us in cupti.items():
         kind, amount = algorithmic_work(nm, N, D, C, kx, kw)
@@ -399,6 +405,7 @@ def run_ours(args):
     roof = None
     if dom is not None:
         roof = dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels)
+    i4.int4_set_pdl(prev_pdl)
     gemm_ops = 2.0 * C * D * (N + kx + kw)
     gemm_us = sum(kernels[nm]["avg_us"] for nm in ("gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad") if nm in kernels)
 

@@ -194,6 +194,15 @@ I4_API size_t int4_gemm_workspace_size(void);
 I4_API i4_status int4_trace_begin(void* const* events, int32_t capacity, int32_t first_launch);
 I4_API int32_t int4_trace_end(const char** names, int32_t capacity);
 
+/* Programmatic dependent launch: every kernel of the library is launched so that
+ * the next kernel in the stream may start launching while it drains (each kernel
+ * waits for its predecessor's completion before touching its data).  On by
+ * default (environment I4_PDL=0 turns it off); int4_set_pdl(0/1) switches it
+ * process-wide and returns the previous setting.  Timing per kernel (bench.py's
+ * breakdown) is taken with it off, since an early-launched kernel's duration
+ * includes its wait. */
+I4_API int32_t int4_set_pdl(int32_t enable);
+
 /* Thread-local message describing the last non-OK status of this thread. */
 I4_API const char* int4_last_error(void);
 

@@ -18,7 +18,7 @@ __all__ = [
     "LIB_PATH", "lib", "I4Error", "I4FwdCache", "I4LssPlan",
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
-    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "Int4Linear", "LaunchTrace",
+    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "Int4Linear", "LaunchTrace",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
@@ -75,6 +75,8 @@ def _load():
     L.int4_gemm_workspace_size.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
+    L.int4_set_pdl.argtypes = [i32]
+    L.int4_set_pdl.restype = i32
     L.int4_last_error.argtypes = []
     L.int4_last_error.restype = ctypes.c_char_p
     L.int4_trace_begin.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32]
@@ -153,6 +155,11 @@ def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, ws=None, st
 
 def int4_gemm_workspace_size():
     return int(lib.int4_gemm_workspace_size())
+
+
+def int4_set_pdl(enable):
+    """Switch programmatic dependent launch for all library launches; returns the previous setting."""
+    return bool(lib.int4_set_pdl(1 if enable else 0))
 
 
 class LaunchTrace:

@@ -15,6 +15,23 @@
 #include "../../include/int4linear.h"
 #include "kernels.h"
 
+#include <atomic>
+#include <cstdlib>
+
+namespace i4 {
+// process-wide PDL switch: on unless I4_PDL=0; int4_set_pdl() overrides it
+static std::atomic<int> g_pdl{-1};
+bool pdl_enabled() {
+    int v = g_pdl.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char* e = std::getenv("I4_PDL");
+        v = (e != nullptr && e[0] == '0') ? 0 : 1;
+        g_pdl.store(v, std::memory_order_relaxed);
+    }
+    return v != 0;
+}
+}  // namespace i4
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -207,6 +224,12 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
 extern "C" {
 
 const char* int4_last_error(void) { return g_last_error.c_str(); }
+
+int32_t int4_set_pdl(int32_t enable) {
+    const int32_t prev = i4::pdl_enabled() ? 1 : 0;
+    i4::g_pdl.store(enable ? 1 : 0, std::memory_order_relaxed);
+    return prev;
+}
 
 i4_status int4_trace_begin(void* const* events, int32_t capacity, int32_t first_launch) {
     if (!events || capacity < 2 || capacity > kMaxTrace + 1 || first_launch < 0)

@@ -185,6 +185,17 @@ __device__ __forceinline__ void fwht_static2(float (&v)[CH]) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel of the library is launched
+// with programmatic stream serialization: it signals at its start that the next
+// kernel in the stream may begin launching (its CTAs fill SMs as this grid
+// drains), and it waits for the previous kernel's completion and memory flush
+// before touching any data the previous kernel may write.  Without the launch
+// attribute both instructions are no-ops.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // mbarrier
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

@@ -50,6 +50,8 @@ __device__ __forceinline__ void zero_row(void* base, int64_t row, int n, bool bf
 }
 
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
+    pdl_trigger();
+    pdl_wait();                                               // counts / lists of the sampler
     const int64_t cnt_x = __ldg(a.count_x);
     const int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
     const int64_t pad_w = (int64_t(__ldg(a.count_w)) + 127) & ~int64_t(127);
@@ -96,8 +98,14 @@ cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
     const int64_t rows = (2 * int64_t(a.N) + 128) * 3 + a.N;  // upper bound of the row count
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    compact_kernel<<<int(blocks), 256, 0, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 0);
+    return cudaLaunchKernelEx(&cfg, compact_kernel, a);
 }
 
 }  // namespace i4

@@ -177,7 +177,23 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const bool leader = rank == 0;
     const int pair0 = int(blockIdx.x) / CG, n_pairs = int(gridDim.x) / CG;
 
-    // problem size (possibly data-dependent) and work units
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CG * kEpiWarps); }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<CG>(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();                                  // operands / metadata of the previous kernels
+
+    // problem size (possibly data-dependent, so read after the PDL wait) and work units
     const int M = g.m_dev ? __ldg(g.m_dev) : g.M;
     const int K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
     const int m_tiles = (M + BMP - 1) / BMP;
@@ -192,19 +208,6 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int split = S - 1 - (u) / T;                          \
     const int kb0 = split * nk / S, kb1 = (split + 1) * nk / S;
 
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-        if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CG * kEpiWarps); }
-        fence_mbar_init();
-    }
-    if (warp == 1) tmem_alloc<CG>(tmem_slot, Cfg::TMEM_COLS);
-    tc_fence_before();
-    if (CG == 2) cluster_sync_all(); else __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer (warp 0)
@@ -602,11 +605,11 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cu
     cfg.blockDim = dim3(Epi::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = add_pdl_attr(attr, 1);
     return cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(m.a),
                               *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c), g);
 }

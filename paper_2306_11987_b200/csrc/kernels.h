@@ -8,6 +8,18 @@
 
 namespace i4 {
 
+// Programmatic dependent launch attribute for every launch of the library
+// (disabled with the environment variable I4_PDL=0, for A/B timing).
+bool pdl_enabled();
+inline int add_pdl_attr(cudaLaunchAttribute* attrs, int n) {
+    if (pdl_enabled()) {
+        attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    return n;
+}
+
 // quant.cu --------------------------------------------------------------------
 struct HqArgs {                          // two independent hadamard_quant jobs in one launch
     const uint16_t* x0; int64_t rows0; float r0; int8_t* codes0; uint32_t* bits0; int32_t* sqnorm0;

@@ -58,6 +58,8 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     const int blk = int(threadIdx.x) - r_local * tpr;
     const int64_t row = int64_t(bid) * rows_per_cta + r_local;
     const bool active = r_local < rows_per_cta && row < J.rows;
+    pdl_trigger();
+    pdl_wait();                                        // X / W may be written by the previous kernel
     __shared__ int sq_row[kHqMaxThreads];
     if (threadIdx.x < rows_per_cta) sq_row[threadIdx.x] = 0;
 
@@ -145,17 +147,26 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     const int grid = j0.blocks + j1.blocks;
     if (grid == 0) return cudaSuccess;
     const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
+    void (*kern)(HqJob, HqJob, int, int) = nullptr;
     switch (a.k) {
-        case 0: hadamard_quant_kernel<0><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 1: hadamard_quant_kernel<1><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 2: hadamard_quant_kernel<2><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 3: hadamard_quant_kernel<3><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 4: hadamard_quant_kernel<4><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 5: hadamard_quant_kernel<5><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 6: hadamard_quant_kernel<6><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
-        case 7: hadamard_quant_kernel<7><<<grid, threads, 0, s>>>(j0, j1, int(a.cols), R); break;
+        case 0: kern = hadamard_quant_kernel<0>; break;
+        case 1: kern = hadamard_quant_kernel<1>; break;
+        case 2: kern = hadamard_quant_kernel<2>; break;
+        case 3: kern = hadamard_quant_kernel<3>; break;
+        case 4: kern = hadamard_quant_kernel<4>; break;
+        case 5: kern = hadamard_quant_kernel<5>; break;
+        case 6: kern = hadamard_quant_kernel<6>; break;
+        case 7: kern = hadamard_quant_kernel<7>; break;
         default: return cudaErrorInvalidValue;
     }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 0);
+    return cudaLaunchKernelEx(&cfg, kern, j0, j1, int(a.cols), R);
     return cudaGetLastError();
 }
 
@@ -215,6 +226,8 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     cgrp::grid_group grid = cgrp::this_grid();
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
+    pdl_trigger();
+    pdl_wait();
 
     // ---- phase 1: amax ----------------------------------------------------
     {
@@ -366,11 +379,25 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     if (want < blocks) blocks = int(want);
     if (blocks > kGradSplitMaxBlocks) blocks = kGradSplitMaxBlocks;
     const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
-    void* args[] = {(void*)&g, (void*)&N, (void*)&C, (void*)&block_max, (void*)&keys, (void*)&call_id,
-                    (void*)&token_offset, (void*)&hilo, (void*)&a_sq, (void*)&s_down, (void*)&amax_out};
     int Ci = int(C);
-    args[2] = (void*)&Ci;
-    return cudaLaunchCooperativeKernel((const void*)grad_split_kernel, dim3(blocks), dim3(kSplitThreads), args, 0, s);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(blocks));
+    cfg.blockDim = dim3(kSplitThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 1);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel, g, N, Ci, block_max, keys, call_id, token_offset,
+                                       hilo, a_sq, s_down, amax_out);
+    if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
+        (void)cudaGetLastError();
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, grad_split_kernel, g, N, Ci, block_max, keys, call_id, token_offset,
+                               hilo, a_sq, s_down, amax_out);
+    }
+    return e;
 }
 
 }  // namespace i4

@@ -118,6 +118,8 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
 template <int CL>
 __global__ void __launch_bounds__(kSamplerThreads, 1)
 lss_sampler_kernel(SamplerArgs a) {
+    pdl_trigger();
+    pdl_wait();                                   // a_sq / s_down of grad_split
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SamplerSmem& sm = *reinterpret_cast<SamplerSmem*>(smem_raw);
     const Group<CL> cl;
@@ -288,11 +290,13 @@ static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
     cfg.blockDim = dim3(kSamplerThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = CL > 1 ? 1 : 0;
+    int n = CL > 1 ? 1 : 0;
+    if (CL == 1) attr[0] = attr[1];
+    cfg.numAttrs = add_pdl_attr(attr, n);
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -58,6 +58,7 @@ def main():
     libs = [None] + sorted(glob.glob(os.path.join(ROOT, "build_variants", "*.so")))
     for lib in libs:
         env = dict(os.environ, I4_EXP_CHILD="1")
+        env.setdefault("I4_PDL", "0")             # per-kernel durations without early-launch waits
         if lib:
             env["I4_LIB_OVERRIDE"] = lib
         subprocess.run([sys.executable, __file__, cfg], env=env, timeout=300)
