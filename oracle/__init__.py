@@ -25,7 +25,9 @@ Modules
   lss       leverage scores, A.2 probability normalisation, Bernoulli masks,
             compaction (PAPER.md:244-336, :339-371, :606-610; Z-12..Z-19).
   linear    HQ-MM forward and LSS-MM backward composed (PAPER.md:140-158,
-            :199-212, :320-334, :619-632).
+            :199-212, :320-334, :619-632), step-size gradients (A.3).
+  lsq_grad  LSQ step-size gradient pieces delta, g and the cold-start step
+            (A.3 / A.4; readings Z-27..Z-29).
 
 Pins: every function here is checked in `tests/test_oracle_*.py` against
 closed forms, paper invariants, worked examples (tests/golden/) or brute

@@ -43,8 +43,10 @@ def _item_rows(bs, items):
     return codes, t, h
 
 
-def grad_x_from_items(bs, items, wexp, wq, x_mask, k, s_w):
-    """grad_X = [I_X o (s_W sum_i w_i s_h code_i W_hat)] H   (PAPER.md:366-371)."""
+def grad_x_product(bs, items, wexp, wq, s_w):
+    """The sampled estimate of s_W grad_Y W_hat (before the mask
+    and the inverse transform): row t = s_W sum_{kept i = (h, t)} w_i s_h code_i W_hat.
+    Returns (G float64 [N, D], acc int64 [K, D])."""
     N, C = bs["hi"].shape
     D = wq.shape[1]
     codes, t, h = _item_rows(bs, items)
@@ -54,6 +56,13 @@ def grad_x_from_items(bs, items, wexp, wq, x_mask, k, s_w):
     scale = np.float64(np.float32(s_w)) * s_h * np.ldexp(1.0, np.asarray(wexp, dtype=np.int64))
     G = np.zeros((N, D), dtype=np.float64)
     np.add.at(G, t, acc.astype(np.float64) * scale[:, None])
+    return G, acc
+
+
+def grad_x_from_items(bs, items, wexp, wq, x_mask, k, s_w):
+    """grad_X = [I_X o (s_W sum_i w_i s_h code_i W_hat)] H   (PAPER.md:366-371)."""
+    D = wq.shape[1]
+    G, acc = grad_x_product(bs, items, wexp, wq, s_w)
     G = G * x_mask                                                  # mask first (Z-23)
     return G @ block_diag_hadamard(D, k), acc
 
@@ -75,6 +84,25 @@ def grad_w_from_items(bs, items, wexp, xq, w_mask, k, s_x):
     G = acc.astype(np.float64) * (np.float64(np.float32(s_x)) * np.float64(bs["s_down"]))
     G = G * w_mask
     return G @ block_diag_hadamard(D, k), acc
+
+
+def step_size_grads(x, w, fwd, bwd, n_elem_x=None, n_elem_w=None):
+    """A.3 step-size gradients (readings Z-27, Z-28, Z-29) from
+    the forward cache and the backward's sampled products.  Returns (gs_x, gs_w)."""
+    from . import lsq_grad
+    from .hq import transformed_scaled
+    k = fwd["k"]
+    N, D = np.asarray(x).shape
+    C = np.asarray(w).shape[0]
+    bs = bwd["bs"]
+    mx, mw = bwd["mask_x"], bwd["mask_w"]
+    Gx, _ = grad_x_product(bs, mx["items"], mx["wexp"], fwd["wq"], fwd["s_w"])
+    Gw = bwd["acc_w"].astype(np.float64) * (np.float64(fwd["s_x"]) * np.float64(bs["s_down"]))
+    dx = lsq_grad.delta(transformed_scaled(x, k, fwd["s_x"]))
+    dw = lsq_grad.delta(transformed_scaled(w, k, fwd["s_w"]))
+    gs_x = lsq_grad.step_size_grad(Gx, dx, N * D if n_elem_x is None else n_elem_x)
+    gs_w = lsq_grad.step_size_grad(Gw, dw, C * D if n_elem_w is None else n_elem_w)
+    return gs_x, gs_w
 
 
 def backward(g, fwd, seed, call_id, token_offset=0, mode=lss_mod.MODE_BERNOULLI):
