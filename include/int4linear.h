@@ -76,10 +76,14 @@ typedef enum {
  *   x_mask   uint32 [N, D/32]  I_X (on XH / s_X, reading Z-8)
  *   w_mask   uint32 [C, D/32]  I_W
  *   x_sqnorm int32 [N]         sum_d X_hat[t, d]^2 (leverage scores)
+ *   x_delta  float [N, D]      nullable: delta_X = <v> - I_X o v of the quantizer input
+ *                              v = XH / s_X (A.3, reading Z-27), exact
+ *                              in fp32; needed only for the step-size gradients
+ *   w_delta  float [C, D]      nullable: delta_W, the same for W
  * Host scalars: N, D, C, k, s_x, s_w are filled by int4_linear_fwd.  Set
- * w_valid = 1 to reuse wq / w_mask from a previous call with the same W
- * and s_w (one weight quantization per weight version); the library never
- * changes w_valid. */
+ * w_valid = 1 to reuse wq / w_mask (/ w_delta) from a previous call with the
+ * same W and s_w (one weight quantization per weight version); the library
+ * never changes w_valid. */
 typedef struct {
     int8_t* xq;
     int8_t* wq;
@@ -90,6 +94,8 @@ typedef struct {
     int32_t k;
     float s_x, s_w;
     int32_t w_valid;
+    float* x_delta;
+    float* w_delta;
 } i4_fwd_cache;
 
 /* Bit-split + sampling plan (Procedure LSS-MM steps 1-4).  Device buffers,
@@ -107,7 +113,12 @@ typedef struct {
  *   count_w  int32 [1]         number of kept items (device)
  *   items_x, wexp_x, count_x   the same for the grad_X mask, in token-major order
  *                              (slot 2t + h: a token's two items are adjacent)
- *   x_touched uint8 [N]        1 if token t has a kept grad_X item */
+ *   x_touched uint8 [N]        1 if token t has a kept grad_X item
+ *   grad_s   float [2]         nullable out (int4_linear_bwd): the LSQ step-size gradients
+ *                              {grad s_X, grad s_W} (A.3; readings
+ *                              Z-27..Z-29), computed when the cache holds x_delta and w_delta
+ *   n_elem_x, n_elem_w         host: N_X, N_W of g(s) = 1/sqrt(Q_P N) (0 = this call's
+ *                              N*D and C*D; a token-sharded caller passes the global counts) */
 typedef struct {
     int8_t* hilo;
     int32_t* a_sq;
@@ -121,6 +132,8 @@ typedef struct {
     int8_t* wexp_x;
     int32_t* count_x;
     uint8_t* x_touched;
+    float* grad_s;
+    int64_t n_elem_x, n_elem_w;
 } i4_lss_plan;
 
 /* F1+F2 / F3: block-Hadamard transform + LSQ quantize of a bf16 matrix
@@ -162,10 +175,26 @@ I4_API i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_
  * dX is fp32 (dx_dtype = I4_OUT_F32, parity mode) or bf16 (I4_OUT_BF16, perf
  * mode as the cuBLAS BF16 baseline; reading Z-24); dW stays fp32 (the data-
  * parallel all-reduce operand).  ws: device scratch of
- * int4_bwd_workspace_size(N, D, C) bytes. */
+ * int4_bwd_workspace_size(N, D, C) bytes.
+ * Step-size gradients (A.3): if plan->grad_s is non-NULL and the cache holds
+ * x_delta and w_delta, the two GEMM epilogues also reduce sum(acc o delta) over
+ * their tiles (fp32 per 32-column chunk, fp64 across chunks, per-CTA partials)
+ * and a final one-CTA launch writes
+ *   grad_s[0] = g(N_X) s_W s_down sum_{kept i} w_i sum_d acc_i[d] delta_X[t_i, d]
+ *   grad_s[1] = g(N_W) s_X s_down sum_{c,d} acc_W[c, d] delta_W[c, d]
+ * (reading Z-28: the partner step size is included, the sum runs over all
+ * elements).  Deterministic: fixed tile-to-CTA assignment and fixed-order sums. */
 I4_API i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                                  int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
                                  i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream);
+
+/* Cold-start step size (A.4; reading Z-25): step = fl32(2 mean|x| /
+ * sqrt(Q_P)) over the n bf16 values of x_bf16 (one fixed-order fp64 reduction,
+ * deterministic).  step: device float out.  ws: zero-initialised device scratch of
+ * lsq_cold_start_workspace_size() bytes, left zeroed on return. */
+I4_API i4_status lsq_cold_start_step(const void* x_bf16, int64_t n, float* step, void* ws, size_t ws_bytes,
+                                     void* stream);
+I4_API size_t lsq_cold_start_workspace_size(void);
 
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);

@@ -18,7 +18,8 @@ __all__ = [
     "LIB_PATH", "lib", "I4Error", "I4FwdCache", "I4LssPlan",
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
-    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "Int4Linear", "LaunchTrace",
+    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step",
+    "lsq_cold_start_workspace_size", "Int4Linear", "LaunchTrace",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
@@ -42,7 +43,7 @@ class I4FwdCache(ctypes.Structure):
                 ("x_mask", ctypes.c_void_p), ("w_mask", ctypes.c_void_p), ("x_sqnorm", ctypes.c_void_p),
                 ("N", ctypes.c_int64), ("D", ctypes.c_int64), ("C", ctypes.c_int64),
                 ("k", ctypes.c_int32), ("s_x", ctypes.c_float), ("s_w", ctypes.c_float),
-                ("w_valid", ctypes.c_int32)]
+                ("w_valid", ctypes.c_int32), ("x_delta", ctypes.c_void_p), ("w_delta", ctypes.c_void_p)]
 
 
 class I4LssPlan(ctypes.Structure):
@@ -50,7 +51,8 @@ class I4LssPlan(ctypes.Structure):
                 ("s_down", ctypes.c_void_p), ("scratch", ctypes.c_void_p), ("items_w", ctypes.c_void_p),
                 ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
-                ("count_x", ctypes.c_void_p), ("x_touched", ctypes.c_void_p)]
+                ("count_x", ctypes.c_void_p), ("x_touched", ctypes.c_void_p), ("grad_s", ctypes.c_void_p),
+                ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64)]
 
 
 def _load():
@@ -66,6 +68,7 @@ def _load():
         "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, i32,
                             vp, vp, ctypes.c_size_t, vp],
         "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp, ctypes.c_size_t, vp],
+        "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -73,6 +76,8 @@ def _load():
         fn.restype = ctypes.c_int
     L.int4_gemm_workspace_size.argtypes = []
     L.int4_gemm_workspace_size.restype = ctypes.c_size_t
+    L.lsq_cold_start_workspace_size.argtypes = []
+    L.lsq_cold_start_workspace_size.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
     L.int4_set_pdl.argtypes = [i32]
@@ -157,6 +162,18 @@ def int4_gemm_workspace_size():
     return int(lib.int4_gemm_workspace_size())
 
 
+def lsq_cold_start_workspace_size():
+    return int(lib.lsq_cold_start_workspace_size())
+
+
+def lsq_cold_start_step(x, step, ws, stream=None):
+    """A.4 cold start: step[0] = fl32(2 mean|x| / sqrt(7)) on the device.
+    x: bf16 tensor; step: float32 device tensor; ws: zeroed uint8 tensor of
+    lsq_cold_start_workspace_size() bytes (left zeroed)."""
+    _check(lib.lsq_cold_start_step(_ptr(x), x.numel(), _ptr(step), _ptr(ws), ws.numel() * ws.element_size(),
+                                   _stream(stream)))
+
+
 def int4_set_pdl(enable):
     """Switch programmatic dependent launch for all library launches; returns the previous setting."""
     return bool(lib.int4_set_pdl(1 if enable else 0))
@@ -202,7 +219,9 @@ class Int4Linear:
     backward workspace once; forward / backward then only launch kernels.
     """
 
-    def __init__(self, N, D, C, k, device="cuda"):
+    def __init__(self, N, D, C, k, device="cuda", step_grads=False):
+        """step_grads: also keep the A.3 deltas in the forward cache and return the
+        step-size gradients {grad s_X, grad s_W} from backward (see grad_s())."""
         import torch
         self.N, self.D, self.C, self.k = N, D, C, k
         dev = torch.device(device)
@@ -232,6 +251,14 @@ class Int4Linear:
                               items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12,
                               x_touched=self.x_touched.data_ptr())
         self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
+        self.step_grads = bool(step_grads)
+        if self.step_grads:
+            self.x_delta = torch.empty(N, D, dtype=f32, device=dev)
+            self.w_delta = torch.empty(C, D, dtype=f32, device=dev)
+            self.grad_s_buf = torch.zeros(2, dtype=f32, device=dev)
+            self.cache.x_delta = self.x_delta.data_ptr()
+            self.cache.w_delta = self.w_delta.data_ptr()
+            self.plan.grad_s = self.grad_s_buf.data_ptr()
 
     def forward(self, X, W, s_x, s_w, Y, reuse_weight=False, stream=None):
         self.cache.w_valid = 1 if reuse_weight else 0
@@ -246,3 +273,9 @@ class Int4Linear:
 
     def counts(self):
         return self.scalars[2:4]
+
+    def grad_s(self):
+        """{grad s_X, grad s_W} of the last backward (A.3), a float32 device tensor."""
+        if not self.step_grads:
+            raise RuntimeError("Int4Linear(step_grads=True) is required for step-size gradients")
+        return self.grad_s_buf

@@ -280,7 +280,8 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     I4_RETURN_IF(check_step(s_x, "s_x"));
     I4_RETURN_IF(check_step(s_w, "s_w"));
     if (y_dtype != I4_OUT_F32 && y_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "bad y_dtype");
-    if (!aligned16(X) || !aligned16(W) || !aligned16(Y)) return fail(I4_ERR_ALIGN, "int4_linear_fwd: unaligned pointer");
+    if (!aligned16(X) || !aligned16(W) || !aligned16(Y) || !aligned16(cache->x_delta) || !aligned16(cache->w_delta))
+        return fail(I4_ERR_ALIGN, "int4_linear_fwd: unaligned pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
     {
@@ -288,9 +289,11 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
         i4::HqArgs h{};
         h.x0 = static_cast<const uint16_t*>(X); h.rows0 = N; h.r0 = step_recip(k, s_x);
         h.codes0 = cache->xq; h.bits0 = cache->x_mask; h.sqnorm0 = cache->x_sqnorm;
+        h.delta0 = cache->x_delta;              // A.3 deltas only when the caller asks for them
         if (!cache->w_valid) {
             h.x1 = static_cast<const uint16_t*>(W); h.rows1 = C; h.r1 = step_recip(k, s_w);
             h.codes1 = cache->wq; h.bits1 = cache->w_mask; h.sqnorm1 = nullptr;
+            h.delta1 = cache->w_delta;
         }
         h.cols = D; h.k = k;
         I4_LAUNCH(i4::launch_hadamard_quant2(h, s), "hadamard_quant", s);
@@ -356,6 +359,7 @@ namespace {
 struct BwdWs {
     int8_t* a_x; int8_t* a_w; int8_t* b_w;
     int32_t* part_x; int32_t* part_w; uint32_t* flags_x; uint32_t* flags_w;
+    double* lsq_x; double* lsq_w;        // A.3 fp64 partials (zeroed with the flags by the sampler)
     size_t total;
 };
 
@@ -369,7 +373,8 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
     const size_t o_bw = take(size_t(D * kcap));
     const size_t o_px = take(i4::gemm_split_partial_bytes());
     const size_t o_pw = take(i4::gemm_split_partial_bytes());
-    const size_t o_f = take(2 * i4::gemm_split_flag_words() * sizeof(uint32_t));
+    // split-K flags and the A.3 partials are one contiguous region: the sampler zeroes it
+    const size_t o_f = take(2 * i4::gemm_split_flag_words() * sizeof(uint32_t) + 2 * i4::kLsqPartials * sizeof(double));
     w.total = off;
     if (ws) {
         uint8_t* b = static_cast<uint8_t*>(ws);
@@ -380,6 +385,8 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
         w.part_w = reinterpret_cast<int32_t*>(b + o_pw);
         w.flags_x = reinterpret_cast<uint32_t*>(b + o_f);
         w.flags_w = w.flags_x + i4::gemm_split_flag_words();
+        w.lsq_x = reinterpret_cast<double*>(w.flags_w + i4::gemm_split_flag_words());
+        w.lsq_w = w.lsq_x + i4::kLsqPartials;
     }
     return w;
 }
@@ -403,11 +410,17 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         return fail(I4_ERR_WORKSPACE, "int4_linear_bwd: ws_bytes %zu < %zu", ws_bytes, int4_bwd_workspace_size(N, D, C));
     if (!aligned16(dX) || !aligned16(dW) || !aligned16(ws)) return fail(I4_ERR_ALIGN, "int4_linear_bwd: unaligned pointer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool want_lsq = plan && plan->grad_s != nullptr;
+    if (want_lsq && (!cache->x_delta || !cache->w_delta))
+        return fail(I4_ERR_ARG, "int4_linear_bwd: plan->grad_s needs cache->x_delta and cache->w_delta");
     {
         const BwdWs w0 = carve_bwd_ws(ws, N, D, C);
-        // the sampler launch also zeroes the split-K flags of the two GEMMs below
+        // the sampler launch also zeroes the split-K flags of the two GEMMs below (and
+        // the A.3 partial slots that follow them)
+        const int32_t words = int32_t(2 * i4::gemm_split_flag_words() +
+                                      (want_lsq ? 2 * i4::kLsqPartials * sizeof(double) / sizeof(uint32_t) : 0));
         I4_RETURN_IF(bitsplit_lss_impl(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, s,
-                                       w0.flags_x, int32_t(2 * i4::gemm_split_flag_words())));
+                                       w0.flags_x, words));
     }
 
     const int64_t kcap = round_up(2 * N, 128);
@@ -440,6 +453,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
         g.partial = w.part_x; g.flags = w.flags_x;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
+        if (want_lsq) { g.delta = cache->x_delta; g.lsq_part = w.lsq_x; }
         I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
@@ -455,8 +469,30 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.a_mn = 1; g.b_mn = 1;                  // A_W [K items, C], B_W [K, D]: both MN-major
         g.partial = w.part_w; g.flags = w.flags_w;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;   // few (C/256 x D/256) tiles, long sampled K
+        if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, s));
     }
+    if (want_lsq) {
+        // A.3: g(s) = 1 / sqrt(Q_P N_elem), Q_P = 7 (reading Z-29 for N_elem)
+        const double nx = double(plan->n_elem_x > 0 ? plan->n_elem_x : N * D);
+        const double nw = double(plan->n_elem_w > 0 ? plan->n_elem_w : C * D);
+        I4_LAUNCH(i4::launch_lsq_finalize(w.lsq_x, w.lsq_w, plan->s_down, cache->s_x, cache->s_w,
+                                          1.0 / std::sqrt(7.0 * nx), 1.0 / std::sqrt(7.0 * nw), plan->grad_s, s),
+                  "lsq_finalize", s);
+    }
+    return I4_OK;
+}
+
+size_t lsq_cold_start_workspace_size(void) { return i4::lsq_cold_start_ws_bytes(); }
+
+i4_status lsq_cold_start_step(const void* x_bf16, int64_t n, float* step, void* ws, size_t ws_bytes, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!x_bf16 || !step || !ws) return fail(I4_ERR_ARG, "lsq_cold_start_step: NULL pointer");
+    if (n <= 0) return fail(I4_ERR_SHAPE, "lsq_cold_start_step: n must be positive");
+    if (ws_bytes < i4::lsq_cold_start_ws_bytes()) return fail(I4_ERR_WORKSPACE, "lsq_cold_start_step: ws too small");
+    if (!aligned16(x_bf16) || !aligned16(ws)) return fail(I4_ERR_ALIGN, "lsq_cold_start_step: unaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    I4_LAUNCH(i4::launch_lsq_cold_start(static_cast<const uint16_t*>(x_bf16), n, step, ws, s), "lsq_cold_start", s);
     return I4_OK;
 }
 

@@ -366,6 +366,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         RowInfo ri_cur = load_ri(pair0), ri_next = load_ri(pair0 + n_pairs);
         uint32_t mw_cur[NW];
         load_mask(pair0, ri_cur, mw_cur);
+        double lsq_acc = 0.0;                          // A.3 partial of this lane
         int it = 0;
         for (int u = pair0; u < units; u += n_pairs, ++it) {
             UNIT_DECODE(u)
@@ -397,12 +398,14 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             // rows; the first adds its neighbour's values (shuffle) and stores plainly;
             // pairs straddling a 32-row group use red.add onto rows zeroed beforehand
             int dmode = 0;                             // 0 store, 1 store pair sum, 2 skip, 3 red.add
+            int row_e = 0;                             // dgrad: log2 of the item's weight
             if (EPI == EPI_DGRAD) {
                 const int item = ri_cur.item;
                 valid = valid && item < two_n;
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
                 const int e = valid ? ri_cur.e : 0;
+                row_e = e;
                 rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
                 const int inext = valid ? ri_cur.inext : two_n;
                 const int iprev = valid ? ri_cur.iprev : two_n;
@@ -463,6 +466,23 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 const int col0 = n0 + c;
                 if (col0 >= g.Nn) continue;           // ragged N (MN-major B): nothing to write
+                if (kMask && g.lsq_part != nullptr && valid) {
+                    // A.3 step-size gradient: sum_d acc[d] delta[row, d] (fp32 in column order,
+                    // then fp64 across chunks; the dgrad item weight 2^e applied exactly)
+                    const float* dp = g.delta + (EPI == EPI_DGRAD ? out_row : int64_t(row)) * g.Nn + col0;
+                    float cs = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < CW / 32; ++q)
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            const float4 d4 = __ldg(reinterpret_cast<const float4*>(dp + 32 * q + i));
+                            cs = __fmaf_rn(float(int32_t(r[q][i])), d4.x, cs);
+                            cs = __fmaf_rn(float(int32_t(r[q][i + 1])), d4.y, cs);
+                            cs = __fmaf_rn(float(int32_t(r[q][i + 2])), d4.z, cs);
+                            cs = __fmaf_rn(float(int32_t(r[q][i + 3])), d4.w, cs);
+                        }
+                    lsq_acc += EPI == EPI_DGRAD ? ldexp(double(cs), row_e) : double(cs);
+                }
 
                 if (EPI == EPI_DGRAD) {
                     float v[CW];
@@ -572,6 +592,11 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
         }
 #undef UNIT_DECODE
+        if (kMask && g.lsq_part != nullptr) {          // fixed-order warp sum -> this warp's slot
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lsq_acc += __shfl_xor_sync(0xFFFFFFFFu, lsq_acc, o);
+            if (lane == 0) g.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc;
+        }
         bulk_wait<0>();                                // every lane: its own copies are done
         __syncwarp();
     }

@@ -25,6 +25,7 @@ struct HqArgs {                          // two independent hadamard_quant jobs 
     const uint16_t* x0; int64_t rows0; float r0; int8_t* codes0; uint32_t* bits0; int32_t* sqnorm0;
     const uint16_t* x1; int64_t rows1; float r1; int8_t* codes1; uint32_t* bits1; int32_t* sqnorm1;
     int64_t cols; int k;
+    float* delta0; float* delta1;        // optional A.3 delta = <v> - I o v (fp32, exact)
 };
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
@@ -98,6 +99,9 @@ struct GemmArgs {
     uint32_t* flags;          // [max_tiles_split, CG, 4]
     int32_t max_tiles_split;  // split only when the tile count is at most this
     int32_t max_splits;
+    // LSQ step-size gradient (A.3), optional: sum(acc o delta) per CTA epilogue warp
+    const float* delta;       // dgrad: delta_X [N, Nn] (row = token); wgrad: delta_W [M, Nn]
+    double* lsq_part;         // [gridDim.x * 8] fp64 partials (entries of absent CTAs pre-zeroed)
 };
 constexpr int kSplitMaxTiles = 96;        // workspace tiles reserved for split-K
 constexpr int kSplitMaxK = 4;
@@ -107,5 +111,12 @@ constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_grou
 struct GemmMaps { const void* a; const void* b; const void* c; };   // CUtensorMap* (host)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
 int gemm_block_n(int Nn, bool b_mn);
+
+// lsq.cu ----------------------------------------------------------------------
+constexpr int kLsqPartials = 2048;        // fp64 partial slots per GEMM (>= max grid x 8 warps)
+cudaError_t launch_lsq_finalize(const double* part_x, const double* part_w, const float* s_down, float s_x,
+                                float s_w, double g_x, double g_w, float* grad_s, cudaStream_t s);
+size_t lsq_cold_start_ws_bytes();
+cudaError_t launch_lsq_cold_start(const uint16_t* x, int64_t n, float* step, void* ws, cudaStream_t s);
 
 }  // namespace i4

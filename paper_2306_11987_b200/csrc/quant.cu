@@ -42,6 +42,7 @@ struct HqJob {
     int8_t* codes;
     uint32_t* bits;
     int32_t* sqnorm;
+    float* delta;                        // optional: A.3 delta = code - I o v (fp32, exact)
     int blocks;                          // CTAs assigned to this job
 };
 
@@ -105,13 +106,22 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
         int q[32];
         uint32_t mask = 0;
         int sq = 0;
+        float dl[32];                                   // A.3 delta, if requested
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             float s0, s1;
             f2_unpack(f2_mul(p[j], r2), s0, s1);
             q[j] = __float2int_rn(fminf(fmaxf(s0, -7.0f), 7.0f));
             q[j + 16] = __float2int_rn(fminf(fmaxf(s1, -7.0f), 7.0f));
-            mask |= (uint32_t(fabsf(s0) <= 7.0f) << j) | (uint32_t(fabsf(s1) <= 7.0f) << (j + 16));
+            const bool in0 = fabsf(s0) <= 7.0f, in1 = fabsf(s1) <= 7.0f;
+            mask |= (uint32_t(in0) << j) | (uint32_t(in1) << (j + 16));
+            dl[j] = in0 ? __fsub_rn(float(q[j]), s0) : float(q[j]);          // exact (|.| <= 1/2)
+            dl[j + 16] = in1 ? __fsub_rn(float(q[j + 16]), s1) : float(q[j + 16]);
+        }
+        if (J.delta != nullptr) {
+            float4* dd = reinterpret_cast<float4*>(J.delta + row * cols + blk * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dd[i] = make_float4(dl[4 * i], dl[4 * i + 1], dl[4 * i + 2], dl[4 * i + 3]);
         }
         uint32_t w[8];
 #pragma unroll
@@ -140,8 +150,8 @@ static int hq_rows_per_cta(int64_t cols) {
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     if (a.cols / 32 > kHqMaxThreads) return cudaErrorInvalidValue;   // cols > 8192: not supported
     const int R = hq_rows_per_cta(a.cols);
-    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, 0};
-    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, 0};
+    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0};
+    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0};
     j0.blocks = int((a.rows0 + R - 1) / R);
     j1.blocks = int((a.rows1 + R - 1) / R);
     const int grid = j0.blocks + j1.blocks;
