@@ -196,6 +196,19 @@ I4_API i4_status lsq_cold_start_step(const void* x_bf16, int64_t n, float* step,
                                      void* stream);
 I4_API size_t lsq_cold_start_workspace_size(void);
 
+/* Adaptive Hadamard block size (A.5; reading Z-30): for every
+ * k in [k_min, k_max] the reconstructions X_bar_k = s_X <XH>_{s_X} H^T and W_bar_k
+ * (the forward path's quantizer) are compared with X and W;
+ *   mse[2k] = MSE(X_bar_k, X), mse[2k+1] = MSE(W_bar_k, W)   (device double [16]),
+ *   *k_best = argmin_k mse[2k] mse[2k+1], ties to the smaller k (device int32).
+ * X [N, D], W [C, D] bf16; D % 64 == 0, D % 2^k_max == 0, 0 <= k_min <= k_max <= 7.
+ * ws: zero-initialised scratch of hq_select_k_workspace_size() bytes, left zeroed.
+ * One launch per candidate k plus one selection launch; deterministic. */
+I4_API i4_status hq_select_k(const void* X, int64_t N, const void* W, int64_t C, int64_t D, float s_x, float s_w,
+                             int32_t k_min, int32_t k_max, int32_t* k_best, double* mse, void* ws,
+                             size_t ws_bytes, void* stream);
+I4_API size_t hq_select_k_workspace_size(void);
+
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
 

@@ -18,7 +18,7 @@ __all__ = [
     "LIB_PATH", "lib", "I4Error", "I4FwdCache", "I4LssPlan",
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
-    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step",
+    "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step", "hq_select_k", "hq_select_k_workspace_size",
     "lsq_cold_start_workspace_size", "Int4Linear", "LaunchTrace",
 ]
 
@@ -69,6 +69,7 @@ def _load():
                             vp, vp, ctypes.c_size_t, vp],
         "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp, ctypes.c_size_t, vp],
         "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
+        "hq_select_k": [vp, i64, vp, i64, i64, f32, f32, i32, i32, vp, vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -78,6 +79,8 @@ def _load():
     L.int4_gemm_workspace_size.restype = ctypes.c_size_t
     L.lsq_cold_start_workspace_size.argtypes = []
     L.lsq_cold_start_workspace_size.restype = ctypes.c_size_t
+    L.hq_select_k_workspace_size.argtypes = []
+    L.hq_select_k_workspace_size.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
     L.int4_set_pdl.argtypes = [i32]
@@ -160,6 +163,19 @@ def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, ws=None, st
 
 def int4_gemm_workspace_size():
     return int(lib.int4_gemm_workspace_size())
+
+
+def hq_select_k_workspace_size():
+    return int(lib.hq_select_k_workspace_size())
+
+
+def hq_select_k(X, W, s_x, s_w, k_min, k_max, k_best, mse, ws, stream=None):
+    """A.5: per-k reconstruction MSEs of X and W into mse (float64
+    device [16]) and the argmin of their product into k_best (int32 device [1])."""
+    N, D = X.shape
+    C = W.shape[0]
+    _check(lib.hq_select_k(_ptr(X), N, _ptr(W), C, D, float(s_x), float(s_w), int(k_min), int(k_max),
+                           _ptr(k_best), _ptr(mse), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def lsq_cold_start_workspace_size():

@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libint4linear.so")
-SOURCES = ["api.cu", "quant.cu", "sampler.cu", "compact.cu", "gemm.cu", "lsq.cu"]
+SOURCES = ["api.cu", "quant.cu", "sampler.cu", "compact.cu", "gemm.cu", "lsq.cu", "adaptive_k.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

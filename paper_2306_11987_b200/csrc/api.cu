@@ -483,6 +483,37 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     return I4_OK;
 }
 
+size_t hq_select_k_workspace_size(void) { return i4::select_k_ws_bytes(); }
+
+i4_status hq_select_k(const void* X, int64_t N, const void* W, int64_t C, int64_t D, float s_x, float s_w,
+                      int32_t k_min, int32_t k_max, int32_t* k_best, double* mse, void* ws, size_t ws_bytes,
+                      void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!X || !W || !k_best || !mse || !ws) return fail(I4_ERR_ARG, "hq_select_k: NULL pointer");
+    if (N <= 0 || C <= 0 || D <= 0 || D % 64 || D > 8192)
+        return fail(I4_ERR_SHAPE, "hq_select_k: need N, C > 0 and D a positive multiple of 64 (<= 8192)");
+    if (k_min < 0 || k_max > 7 || k_min > k_max) return fail(I4_ERR_SHAPE, "hq_select_k: need 0 <= k_min <= k_max <= 7");
+    I4_RETURN_IF(check_k(k_max, D));
+    I4_RETURN_IF(check_step(s_x, "s_x"));
+    I4_RETURN_IF(check_step(s_w, "s_w"));
+    if (ws_bytes < i4::select_k_ws_bytes()) return fail(I4_ERR_WORKSPACE, "hq_select_k: ws too small");
+    if (!aligned16(X) || !aligned16(W) || !aligned16(ws) || (reinterpret_cast<uintptr_t>(mse) & 7u))
+        return fail(I4_ERR_ALIGN, "hq_select_k: unaligned pointer");
+    float r_x[8], r_w[8];
+    double c_x[8], c_w[8];
+    for (int k = 0; k < 8; ++k) {
+        r_x[k] = step_recip(k, s_x);                    // the forward path's quantizer (Z-4)
+        r_w[k] = step_recip(k, s_w);
+        c_x[k] = double(s_x) * std::pow(2.0, -double(k) / 2.0);   // x_bar = s 2^{-k/2} (codes H_pm1)
+        c_w[k] = double(s_w) * std::pow(2.0, -double(k) / 2.0);
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    I4_LAUNCH(i4::launch_select_k(static_cast<const uint16_t*>(X), N, static_cast<const uint16_t*>(W), C, D, r_x, r_w,
+                                  c_x, c_w, k_min, k_max, k_best, mse, ws, s),
+              "hq_select_k", s);
+    return I4_OK;
+}
+
 size_t lsq_cold_start_workspace_size(void) { return i4::lsq_cold_start_ws_bytes(); }
 
 i4_status lsq_cold_start_step(const void* x_bf16, int64_t n, float* step, void* ws, size_t ws_bytes, void* stream) {

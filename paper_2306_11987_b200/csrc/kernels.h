@@ -119,4 +119,10 @@ cudaError_t launch_lsq_finalize(const double* part_x, const double* part_w, cons
 size_t lsq_cold_start_ws_bytes();
 cudaError_t launch_lsq_cold_start(const uint16_t* x, int64_t n, float* step, void* ws, cudaStream_t s);
 
+// adaptive_k.cu -----------------------------------------------------------------
+size_t select_k_ws_bytes();
+cudaError_t launch_select_k(const uint16_t* x, int64_t n, const uint16_t* w, int64_t c, int64_t d, float r_x[8],
+                            float r_w[8], double c_x[8], double c_w[8], int k_min, int k_max, int32_t* k_best,
+                            double* mse, void* ws, cudaStream_t s);
+
 }  // namespace i4

@@ -49,9 +49,9 @@ def launches(r):
     ours = [k for k in order if not k.startswith("cuBLAS")]
     tot = sum(statistics.median(per[k]) for k in ours)
     lines = [f"# {r}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)", "",
-             "Command: `python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e` (default workload, "
-             "BERT-base FFN1 4096 x 768 -> 3072, fwd + bwd).  Per-launch times under ncu are cold-cache and "
-             "serialised: compare SHARES with the bench's CUPTI breakdown, not absolutes.", "",
+             f"Command: `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 3 "
+             f"--warmup 1 --no-cpu-baseline --no-e2e --config {CONFIG}` (fwd + bwd).  Per-launch times under ncu are "
+             "cold-cache and serialised: compare SHARES with the bench's CUPTI breakdown, not absolutes.", "",
              "| kernel | launches | median us | share of our step |", "|---|---|---|---|"]
     for k in order:
         med = statistics.median(per[k])
@@ -97,7 +97,8 @@ def full(r):
         res.append(d)
     lines = [f"# {r}: ncu --set full (one launch each, cold cache, --clock-control none)", "",
              "Command: `ncu --set full --clock-control none --import-source on -k regex:\"grad_split|gemm_i8|"
-             "hadamard_quant|lss_sampler|compact\" -s 9 -c 7 python bench.py --steps 1 --warmup 1 ...`", "",
+             f"hadamard_quant|lss_sampler|compact\" -s 7 -c 7 python bench.py --steps 1 --warmup 1 --config {CONFIG} ...` "
+             "(tools/profile_round.sh).  DRAM write bytes stay in L2 within one replayed launch.", "",
              "| kernel | us | DRAM read MB | DRAM write MB | DRAM % | L2 % | INT8 tensor % | issue active % | warps active % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in res:
@@ -110,9 +111,12 @@ def full(r):
     return "\n".join(lines) + "\n", res
 
 
+CONFIG = sys.argv[2] if len(sys.argv) > 2 else "cfg2_bert_base_ffn1"
+
+
 def main():
     r = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    config = sys.argv[2] if len(sys.argv) > 2 else "cfg2_bert_base_ffn1"
+    config = CONFIG
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md, _ = launches(r)
     open(os.path.join(ROOT, "profiles", f"{r}_launches.md"), "w").write(md)
