@@ -28,6 +28,8 @@ Modules
             :199-212, :320-334, :619-632), step-size gradients (A.3).
   lsq_grad  LSQ step-size gradient pieces delta, g and the cold-start step
             (A.3 / A.4; readings Z-27..Z-29).
+  bmm       BMM in attention as B independent HQ-MM / LSS-MM problems
+            (A.1; reading Z-31).
   adaptive_k  reconstruction error MSE(X_bar_k) x MSE(W_bar_k) and the argmin
             over k (A.5; reading Z-30).
 
