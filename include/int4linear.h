@@ -209,6 +209,40 @@ I4_API i4_status hq_select_k(const void* X, int64_t N, const void* W, int64_t C,
                              size_t ws_bytes, void* stream);
 I4_API size_t hq_select_k_workspace_size(void);
 
+/* BMM in attention (A.1; reading Z-31): T = BMM(Q, K^T) with
+ * Q [B, N, M], K [B, P, M] bf16 and per-batch step sizes s_q[B], s_k[B] (HOST
+ * float arrays).  Batch b is the linear operator above with
+ * X = Q_b, W = K_b (D = M, C = P): T_b = s_q[b] s_k[b] Q_hat_b K_hat_b^T.  The
+ * cache holds all batches (device buffers, caller-allocated):
+ *   qq int8 [B, N, M], kq int8 [B, P, M], q_mask uint32 [B, N, M/32],
+ *   k_mask uint32 [B, P, M/32], q_sqnorm int32 [B, N];
+ * B, N, P, M, k are filled by int4_bmm_fwd.  Shape rules as for the linear
+ * operator (M, P multiples of 64; N <= 65536 for the backward).
+ * This version runs the per-batch operator for b = 0 .. B-1 on `stream` (every
+ * step in the library's kernels; the batch loop is host orchestration). */
+typedef struct {
+    int8_t* qq;
+    int8_t* kq;
+    uint32_t* q_mask;
+    uint32_t* k_mask;
+    int32_t* q_sqnorm;
+    int64_t B, N, P, M;
+    int32_t k;
+} i4_bmm_cache;
+
+/* T [B, N, P] fp32 or bf16. */
+I4_API i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64_t P, int64_t M, int32_t k,
+                              const float* s_q, const float* s_k, void* T, i4_out_dtype t_dtype, i4_bmm_cache* cache,
+                              void* stream);
+
+/* Per-batch LSS-MM backward: dQ [B, N, M] (fp32 or bf16), dK [B, P, M] fp32.  Batch b
+ * uses token_offset = b N (its Philox streams are distinct, reading Z-31), its own
+ * amax and budget N.  plan: an i4_lss_plan sized for ONE batch (N tokens, C = P),
+ * reused batch after batch; ws: int4_bwd_workspace_size(N, M, P) bytes. */
+I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k,
+                              uint64_t seed, uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plan, void* dQ,
+                              i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes, void* stream);
+
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
 

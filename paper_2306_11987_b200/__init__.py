@@ -19,6 +19,7 @@ __all__ = [
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
     "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step", "hq_select_k", "hq_select_k_workspace_size",
+    "int4_bmm_fwd", "int4_bmm_bwd", "Int4BMM", "I4BmmCache",
     "lsq_cold_start_workspace_size", "Int4Linear", "LaunchTrace",
 ]
 
@@ -55,6 +56,13 @@ class I4LssPlan(ctypes.Structure):
                 ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64)]
 
 
+class I4BmmCache(ctypes.Structure):
+    _fields_ = [("qq", ctypes.c_void_p), ("kq", ctypes.c_void_p), ("q_mask", ctypes.c_void_p),
+                ("k_mask", ctypes.c_void_p), ("q_sqnorm", ctypes.c_void_p),
+                ("B", ctypes.c_int64), ("N", ctypes.c_int64), ("P", ctypes.c_int64), ("M", ctypes.c_int64),
+                ("k", ctypes.c_int32)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -70,6 +78,9 @@ def _load():
         "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp, ctypes.c_size_t, vp],
         "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
         "hq_select_k": [vp, i64, vp, i64, i64, f32, f32, i32, i32, vp, vp, vp, ctypes.c_size_t, vp],
+        "int4_bmm_fwd": [vp, vp, i64, i64, i64, i64, i32, vp, vp, vp, i32, ctypes.POINTER(I4BmmCache), vp],
+        "int4_bmm_bwd": [vp, ctypes.POINTER(I4BmmCache), vp, vp, u64, u32, i32, ctypes.POINTER(I4LssPlan), vp, i32,
+                         vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -228,6 +239,34 @@ class LaunchTrace:
         return [(nm, self.events[i].elapsed_time(self.events[i + 1])) for i, nm in enumerate(win)]
 
 
+class _PlanBuffers:
+    """Device buffers of one i4_lss_plan (N tokens, C output features)."""
+
+    def __init__(self, N, C, dev):
+        import torch
+        i8, i32 = torch.int8, torch.int32
+        n2 = 2 * N + 128
+        self.hilo = torch.empty(2 * N + 1, C, dtype=i8, device=dev)   # row 2N: zero pad
+        self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
+        self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
+        self.scratch = torch.zeros(2048, dtype=i32, device=dev)  # fused-amax block maxima
+        self.items_w = torch.empty(n2, dtype=i32, device=dev)
+        self.wexp_w = torch.empty(n2, dtype=i8, device=dev)
+        self.items_x = torch.empty(n2, dtype=i32, device=dev)
+        self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
+        self.x_touched = torch.empty(N, dtype=torch.uint8, device=dev)
+        sp = self.scalars.data_ptr()
+        self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
+                              scratch=self.scratch.data_ptr(),
+                              items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
+                              items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12,
+                              x_touched=self.x_touched.data_ptr())
+
+    def views(self):
+        return {k: getattr(self, k) for k in ("hilo", "a_sq", "scalars", "scratch", "items_w", "wexp_w",
+                                              "items_x", "wexp_x", "x_touched")}
+
+
 class Int4Linear:
     """Caller-side buffers of one INT4 linear layer shape [N, D] x [C, D].
 
@@ -250,22 +289,9 @@ class Int4Linear:
         self.cache = I4FwdCache(xq=self.xq.data_ptr(), wq=self.wq.data_ptr(),
                                 x_mask=self.x_mask.data_ptr(), w_mask=self.w_mask.data_ptr(),
                                 x_sqnorm=self.x_sqnorm.data_ptr(), w_valid=0)
-        n2 = 2 * N + 128
-        self.hilo = torch.empty(2 * N + 1, C, dtype=i8, device=dev)   # row 2N: zero pad
-        self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
-        self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
-        self.scratch = torch.zeros(2048, dtype=i32, device=dev)  # fused-amax block maxima
-        self.items_w = torch.empty(n2, dtype=i32, device=dev)
-        self.wexp_w = torch.empty(n2, dtype=i8, device=dev)
-        self.items_x = torch.empty(n2, dtype=i32, device=dev)
-        self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
-        self.x_touched = torch.empty(N, dtype=torch.uint8, device=dev)
-        sp = self.scalars.data_ptr()
-        self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
-                              scratch=self.scratch.data_ptr(),
-                              items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
-                              items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12,
-                              x_touched=self.x_touched.data_ptr())
+        self._plan_bufs = _PlanBuffers(N, C, dev)
+        self.__dict__.update(self._plan_bufs.views())
+        self.plan = self._plan_bufs.plan
         self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
         self.step_grads = bool(step_grads)
         if self.step_grads:
@@ -295,3 +321,55 @@ class Int4Linear:
         if not self.step_grads:
             raise RuntimeError("Int4Linear(step_grads=True) is required for step-size gradients")
         return self.grad_s_buf
+
+
+def int4_bmm_fwd(Q, K, k, s_q, s_k, T, cache, stream=None):
+    """A.1 BMM forward: per-batch HQ-MM; s_q, s_k host float32 arrays."""
+    import numpy as np
+    import torch
+    B, N, M = Q.shape
+    P = K.shape[1]
+    sq = np.ascontiguousarray(s_q, dtype=np.float32)
+    sk = np.ascontiguousarray(s_k, dtype=np.float32)
+    t_dtype = OUT_BF16 if T.dtype == torch.bfloat16 else OUT_F32
+    _check(lib.int4_bmm_fwd(_ptr(Q), _ptr(K), B, N, P, M, k, sq.ctypes.data, sk.ctypes.data, _ptr(T), t_dtype,
+                            ctypes.byref(cache), _stream(stream)))
+
+
+def int4_bmm_bwd(dT, cache, s_q, s_k, seed, call_id, mode, plan, dQ, dK, ws, stream=None):
+    """A.1 BMM backward: per-batch LSS-MM with token offsets b N (reading Z-31)."""
+    import numpy as np
+    import torch
+    sq = np.ascontiguousarray(s_q, dtype=np.float32)
+    sk = np.ascontiguousarray(s_k, dtype=np.float32)
+    dq_dtype = OUT_BF16 if dQ.dtype == torch.bfloat16 else OUT_F32
+    _check(lib.int4_bmm_bwd(_ptr(dT), ctypes.byref(cache), sq.ctypes.data, sk.ctypes.data, int(seed), int(call_id),
+                            int(mode), ctypes.byref(plan), _ptr(dQ), dq_dtype, _ptr(dK), _ptr(ws),
+                            ws.numel() * ws.element_size(), _stream(stream)))
+
+
+class Int4BMM:
+    """Caller-side buffers of one attention BMM shape T = BMM(Q [B,N,M], K [B,P,M]^T)."""
+
+    def __init__(self, B, N, P, M, k, device="cuda"):
+        import torch
+        self.B, self.N, self.P, self.M, self.k = B, N, P, M, k
+        dev = torch.device(device)
+        i8, i32 = torch.int8, torch.int32
+        self.qq = torch.empty(B, N, M, dtype=i8, device=dev)
+        self.kq = torch.empty(B, P, M, dtype=i8, device=dev)
+        self.q_mask = torch.empty(B, N, M // 32, dtype=i32, device=dev)
+        self.k_mask = torch.empty(B, P, M // 32, dtype=i32, device=dev)
+        self.q_sqnorm = torch.empty(B, N, dtype=i32, device=dev)
+        self.cache = I4BmmCache(qq=self.qq.data_ptr(), kq=self.kq.data_ptr(), q_mask=self.q_mask.data_ptr(),
+                                k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr())
+        self._plan_bufs = _PlanBuffers(N, P, dev)            # one batch's plan, reused batch after batch
+        self.plan = self._plan_bufs.plan
+        self.ws = torch.empty(int4_bwd_workspace_size(N, M, P), dtype=torch.uint8, device=dev)
+
+    def forward(self, Q, K, s_q, s_k, T, stream=None):
+        self.s_q, self.s_k = s_q, s_k
+        int4_bmm_fwd(Q, K, self.k, s_q, s_k, T, self.cache, stream)
+
+    def backward(self, dT, dQ, dK, seed, call_id=0, mode=LSS_BERNOULLI, stream=None):
+        int4_bmm_bwd(dT, self.cache, self.s_q, self.s_k, seed, call_id, mode, self.plan, dQ, dK, self.ws, stream)

@@ -483,6 +483,56 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     return I4_OK;
 }
 
+namespace {
+i4_fwd_cache bmm_view(const i4_bmm_cache* c, int64_t b, float s_q, float s_k) {
+    i4_fwd_cache v{};
+    const int64_t N = c->N, P = c->P, M = c->M;
+    v.xq = c->qq + b * N * M;
+    v.wq = c->kq + b * P * M;
+    v.x_mask = c->q_mask + b * N * (M / 32);
+    v.w_mask = c->k_mask + b * P * (M / 32);
+    v.x_sqnorm = c->q_sqnorm + b * N;
+    v.N = N; v.D = M; v.C = P; v.k = c->k; v.s_x = s_q; v.s_w = s_k;
+    return v;
+}
+}  // namespace
+
+i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64_t P, int64_t M, int32_t k,
+                       const float* s_q, const float* s_k, void* T, i4_out_dtype t_dtype, i4_bmm_cache* cache,
+                       void* stream) {
+    if (!Q || !K || !T || !cache || !s_q || !s_k || !cache->qq || !cache->kq || !cache->q_mask || !cache->k_mask ||
+        !cache->q_sqnorm)
+        return fail(I4_ERR_ARG, "int4_bmm_fwd: NULL pointer");
+    if (B <= 0) return fail(I4_ERR_SHAPE, "int4_bmm_fwd: B must be positive");
+    if (N <= 0 || P <= 0 || M <= 0 || M % 64 || P % 64)
+        return fail(I4_ERR_SHAPE, "int4_bmm_fwd: need N > 0 and M, P positive multiples of 64");
+    cache->B = B; cache->N = N; cache->P = P; cache->M = M; cache->k = k;
+    const size_t ob = t_dtype == I4_OUT_BF16 ? 2 : 4;
+    for (int64_t b = 0; b < B; ++b) {
+        i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
+        I4_RETURN_IF(int4_linear_fwd(static_cast<const uint16_t*>(Q) + b * N * M, static_cast<const uint16_t*>(K) + b * P * M,
+                                     N, M, P, k, s_q[b], s_k[b], static_cast<uint8_t*>(T) + size_t(b * N * P) * ob, t_dtype,
+                                     &v, stream));
+    }
+    return I4_OK;
+}
+
+i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k, uint64_t seed,
+                       uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plan, void* dQ, i4_out_dtype dq_dtype,
+                       float* dK, void* ws, size_t ws_bytes, void* stream) {
+    if (!dT || !cache || !s_q || !s_k || !dQ || !dK) return fail(I4_ERR_ARG, "int4_bmm_bwd: NULL pointer");
+    if (cache->B <= 0) return fail(I4_ERR_ARG, "int4_bmm_bwd: cache not filled by int4_bmm_fwd");
+    const int64_t B = cache->B, N = cache->N, P = cache->P, M = cache->M;
+    const size_t oq = dq_dtype == I4_OUT_BF16 ? 2 : 4;
+    for (int64_t b = 0; b < B; ++b) {
+        const i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
+        I4_RETURN_IF(int4_linear_bwd(static_cast<const uint16_t*>(dT) + b * N * P, &v, seed, call_id, b * N, mode, plan,
+                                     static_cast<uint8_t*>(dQ) + size_t(b * N * M) * oq, dq_dtype, dK + b * P * M, ws,
+                                     ws_bytes, stream));
+    }
+    return I4_OK;
+}
+
 size_t hq_select_k_workspace_size(void) { return i4::select_k_ws_bytes(); }
 
 i4_status hq_select_k(const void* X, int64_t N, const void* W, int64_t C, int64_t D, float s_x, float s_w,
