@@ -7,6 +7,8 @@
 //                    Z-9), then Philox SR to the 8-bit code, split into high /
 //                    low 4-bit planes, per-row integer norms (PAPER.md:234-239,
 //                    :680); one cooperative launch with one grid barrier
+#include <cstdlib>
+
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -228,10 +230,134 @@ __device__ __forceinline__ uint2 pack8_i8(const int (&v)[8]) {
     return make_uint2(__byte_perm(a, b, 0x5410), __byte_perm(c, d, 0x5410));
 }
 
+// prmt.b32 in its generic mode: a selector nibble with bit 3 set replicates the
+// sign bit of the selected byte (used to turn bf16 sign bits into byte masks)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+// Fast phase 2 for one 8-element chunk (reading Z-10 / Z-11, same arithmetic as
+// the generic loop below, restated for the ALU / fma-heavy pipe budget):
+//   y = fl32(|g| R32) with R32 = r8 2^32 (exact power-of-two scaling of
+//       fl32(|g| r8); DESIGN.md notes the subnormal-underflow corner)
+//   A = ceil(min(y, 119 2^32)) as u64: high word floor(a), low word T
+//   mag = hi(A) + [u < lo(A)]
+// then sign and split on packed bytes, with no cross-byte carries:
+//   S  = sign bytes (0xFF / 0x00) straight from the bf16 sign bits (PRMT)
+//   t  = (M ^ S ^ 0x80) + (S & 1) + 8 per byte  == q + 136 in [16, 255]
+//        (positive: m + 128 + 8; negative: 127 - m + 1 + 8)
+//   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
+template <bool CLAMP, bool FAKE_RNG = false>
+__device__ __forceinline__ void split_chunk8(const uint4 raw, const uint64_t blk, const float R32, const PhiloxKeys& keys,
+                                             uint32_t call_id, uint2& ph, uint2& pl, int& shi, int& slo) {
+    Philox4 p0, p1;
+    if (FAKE_RNG) {                                   // timing experiment only (I4_BS_EXP bit 1)
+        p0 = {uint32_t(blk) * 3u, uint32_t(blk) * 5u, uint32_t(blk) * 7u, uint32_t(blk) * 9u};
+        p1 = {p0.x ^ call_id, p0.y ^ call_id, p0.z ^ call_id, p0.w ^ call_id};
+    } else {
+        p0 = philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSR, call_id, keys);
+        p1 = philox4x32_10(uint32_t(blk) + 1u, uint32_t(blk >> 32), kPurposeSR, call_id, keys);
+    }
+    const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+    uint32_t mag[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t bits = (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
+        float y = __fmul_rn(fabsf(__uint_as_float(bits)), R32);
+        if (CLAMP) y = fminf(y, 511101108224.0f);                       // 119 * 2^32
+        const uint64_t A = __float2ull_ru(y);
+        mag[i] = uint32_t(A >> 32) + (u[i] < uint32_t(A) ? 1u : 0u);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t M = __byte_perm(__byte_perm(mag[4 * h], mag[4 * h + 1], 0x0040),
+                                       __byte_perm(mag[4 * h + 2], mag[4 * h + 3], 0x0040), 0x5410);
+        const uint32_t S = prmt(w[2 * h], w[2 * h + 1], 0xFDB9u);     // sign bytes of the 4 elements
+        const uint32_t t = (M ^ S ^ 0x80808080u) + (S & 0x01010101u) + 0x08080808u;
+        const uint32_t hi16 = (t & 0xF0F0F0F0u) ^ 0x80808080u;
+        const uint32_t lo = ((t & 0x0F0F0F0Fu) + 0x78787878u) ^ 0x80808080u;
+        shi = __dp4a(int(hi16), int(hi16), shi);
+        slo = __dp4a(int(lo), int(lo), slo);
+        if (h == 0) { ph.x = hi16; pl.x = lo; } else { ph.y = hi16; pl.y = lo; }
+    }
+}
+
+// Work unit = G chunks of 256 columns of one row (one 16-byte load of 8 bf16 per
+// lane per chunk).  With C % (256 G) == 0 unit u starts at flat element 256 G u,
+// so addresses and Philox counters need no division.  Each warp takes a
+// contiguous unit range, keeps the next unit's loads in flight (the first ones
+// issued before the grid barrier), accumulates the row
+// norms in registers and flushes them (exact int32 atomics onto the zeroed
+// a_sq) when the row changes.
+// (measured on B200: unit sizes 1-4 chunks, 1-3 units in flight and 64 / 85
+// registers per thread all time within 3 %; the launcher picks the largest G
+// dividing C / 256)
+
+__device__ __forceinline__ void warp_unit_range(int64_t units, int64_t& u0, int64_t& u1) {
+    const int64_t nwarps = int64_t(gridDim.x) * (kSplitThreads / 32);
+    const int64_t wid = int64_t(blockIdx.x) * (kSplitThreads / 32) + (threadIdx.x >> 5);
+    u0 = units * wid / nwarps;
+    u1 = units * (wid + 1) / nwarps;
+}
+
+template <int G>
+__device__ __forceinline__ void load_unit(const uint4* src, int64_t un, uint4 (&dst)[G]) {
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) dst[gi] = ld_nc_v4(src + (un * G + gi) * 32);
+}
+
+template <int G, bool CLAMP, bool FAKE_RNG = false>
+__device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int64_t N, int C, const float R32,
+                                            const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset,
+                                            int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, int64_t u0,
+                                            int64_t u1, uint4 (&buf)[G]) {
+    if (u0 >= u1) return;
+    const int lane = lane_id();
+    const int upr = C / (256 * G);                                    // units per row
+    const uint4* src = reinterpret_cast<const uint4*>(g) + lane;
+    const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);       // Z-20: L = (t0 + t) C + c
+    int8_t* lo_plane = hilo + N * int64_t(C);
+    int64_t row = u0 / upr;
+    int seg = int(u0 - row * upr);
+    int shi = 0, slo = 0;
+    for (int64_t un = u0; un < u1; ++un) {
+        uint4 cur[G];
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
+        if (un + 1 < u1) load_unit<G>(src, un + 1, buf);            // next unit's loads in flight
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi) {
+            const int64_t flat = (un * G + gi) * 256 + lane * 8;
+            uint2 ph, pl;
+            split_chunk8<CLAMP, FAKE_RNG>(cur[gi], (tbase + uint64_t(flat)) >> 2, R32, keys, call_id, ph, pl, shi, slo);
+            *reinterpret_cast<uint2*>(hilo + flat) = ph;
+            *reinterpret_cast<uint2*>(lo_plane + flat) = pl;
+        }
+        if (++seg == upr || un + 1 == u1) {                           // row done (or range end): flush
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                shi += __shfl_xor_sync(0xFFFFFFFFu, shi, o);
+                slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
+            }
+            if (lane == 0) {
+                atomicAdd(a_sq + row, shi >> 8);                      // exact: every term is 256 hi^2
+                atomicAdd(a_sq + N + row, slo);
+            }
+            shi = 0; slo = 0;
+            seg = 0; ++row;
+        }
+    }
+}
+
+template <int G>
 __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ block_max,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
-                  int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out) {
+                  int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
+                  int exp_flags) {
     namespace cgrp = cooperative_groups;
     cgrp::grid_group grid = cgrp::this_grid();
     const int lane = lane_id();
@@ -259,6 +385,8 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (G > 0)                                        // the fast phase 2 accumulates norms atomically
+            for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * N; i += stride) a_sq[i] = 0;
         __shared__ uint32_t red[kSplitThreads / 32];
         if (lane == 0) red[warp] = m;
         __syncthreads();
@@ -266,6 +394,12 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             for (int w = 1; w < kSplitThreads / 32; ++w) m = max(m, red[w]);
             block_max[blockIdx.x] = m;
         }
+    }
+    int64_t pu0 = 0, pu1 = 0;
+    uint4 pbuf[G > 0 ? G : 1];
+    if constexpr (G > 0) {                                // first phase-2 loads in flight across the barrier
+        warp_unit_range(N * int64_t(C / (256 * G)), pu0, pu1);
+        if (pu0 < pu1) load_unit<G>(reinterpret_cast<const uint4*>(g) + lane, pu0, pbuf);
     }
     grid.sync();
     // reduce the per-CTA slots: warp 0 only, all loads in flight at once, then
@@ -295,10 +429,30 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         *amax_out = amax_b;
     }
 
-    // ---- phase 2: SR + bit split, one warp per row ------------------------
+    // ---- phase 2: SR + bit split ------------------------------------------
     if (blockIdx.x == gridDim.x - 1)                      // plane row 2N: the all-zero gather pad
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(hilo + 2 * N * C + c) = make_uint4(0, 0, 0, 0);
+    if constexpr (G > 0) {
+        if (exp_flags & 1) return;                        // timing experiment: phase 1 only
+        if (exp_flags & 2) {                              // timing experiment: no Philox
+            split_units<G, false, true>(g, N, C, __fmul_rn(r8, 4294967296.0f), keys, call_id, token_offset, hilo, a_sq,
+                                     pu0, pu1, pbuf);
+            return;
+        }
+        if (zero) {                                       // all-zero grad_Y: codes 0, norms 0 (zeroed above)
+            split_units<G, false>(g, N, C, 0.0f, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+        } else {
+            const float R32 = __fmul_rn(r8, 4294967296.0f);
+            // only elements with |g| = amax can land above 119 (fl32(amax r8) may round up by an ulp)
+            if (__fmul_rn(amax, r8) > 119.0f)
+                split_units<G, true>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+            else
+                split_units<G, false>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+        }
+        return;
+    }
+    // generic path (C not a multiple of 256): one warp per row
     const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
     const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
     const int nch = (C + 255) >> 8;
@@ -368,28 +522,30 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     }
 }
 
-int grad_split_max_blocks() {
+template <int G>
+static int grad_split_max_blocks() {
     static int cached = 0;
     if (cached == 0) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel, kSplitThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G>, kSplitThreads, 0);
         cached = per_sm * sms;
     }
     return cached;
 }
 
-cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
-                              uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, cudaStream_t s) {
-    if (N == 0) return cudaSuccess;
-    int blocks = grad_split_max_blocks();
-    const int64_t want = (N + 7) / 8;                       // one warp per row at most
+int grad_split_max_blocks() { return grad_split_max_blocks<0>(); }
+
+template <int G>
+static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
+                                       uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq,
+                                       float* s_down, uint32_t* amax_out, cudaStream_t s) {
+    static const int exp_flags = getenv("I4_BS_EXP") ? atoi(getenv("I4_BS_EXP")) : 0;   // timing experiments only
+    int blocks = grad_split_max_blocks<G>();
+    const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
     if (blocks > kGradSplitMaxBlocks) blocks = kGradSplitMaxBlocks;
-    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
-    int Ci = int(C);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(blocks));
     cfg.blockDim = dim3(kSplitThreads);
@@ -399,15 +555,32 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel, g, N, Ci, block_max, keys, call_id, token_offset,
-                                       hilo, a_sq, s_down, amax_out);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G>, g, N, C, block_max, keys, call_id, token_offset,
+                                       hilo, a_sq, s_down, amax_out, exp_flags);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, grad_split_kernel, g, N, Ci, block_max, keys, call_id, token_offset,
-                               hilo, a_sq, s_down, amax_out);
+        e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G>, g, N, C, block_max, keys, call_id, token_offset,
+                               hilo, a_sq, s_down, amax_out, exp_flags);
     }
     return e;
+}
+
+cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
+                              uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
+                              uint32_t* amax_out, cudaStream_t s) {
+    if (N == 0) return cudaSuccess;
+    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
+    const int Ci = int(C);
+    const char* env = getenv("I4_BS_GENERIC");            // experiment switch: force the generic phase 2
+    const bool generic = env && env[0] == '1';
+#define I4_GS(GG) launch_grad_split_g<GG>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s)
+    if (!generic && C % 1024 == 0) return I4_GS(4);
+    if (!generic && C % 768 == 0) return I4_GS(3);
+    if (!generic && C % 512 == 0) return I4_GS(2);
+    if (!generic && C % 256 == 0) return I4_GS(1);
+#undef I4_GS
+    return launch_grad_split_g<0>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s);
 }
 
 }  // namespace i4

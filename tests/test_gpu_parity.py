@@ -306,3 +306,39 @@ def test_full_size_sampled_parity(cfg):
     bs_c = dict(bs, hi=bs["hi"][:, ch], lo=bs["lo"][:, ch])
     dw_ref, _ = o_lin.grad_w_from_items(bs_c, mw["items"], mw["wexp"], xq, w_mask[ch], k, np.float32(s_x))
     assert rel_frob(dW[ch], dw_ref) < FROB_TOL
+
+
+# ----------------------------------------------------------------------------- bit split fast paths
+@pytest.mark.parametrize("C", [256, 512, 768, 1024, 3072, 320])
+@pytest.mark.parametrize("clamp", [False, True])
+def test_bitsplit_unit_paths(C, clamp):
+    """grad_split phase 2 for every unit size (C % 1024, 768, 512, 256 and the
+    generic row loop), with and without an element landing above 119 after the
+    fp32 scaling (reading Z-10 clamp), bit-exact planes and norms."""
+    N = 37
+    g = synth.grad_output(N, C, seed=C, dense=True)
+    g = synth.bf16_bits(g).view(np.uint16).astype(np.uint32)
+    g = (g << 16).view(np.float32)                          # exactly representable in bf16
+    if clamp:
+        a = np.float32(np.max(np.abs(g)) * 1.5)
+        for m in range(1, 128):                            # bf16 values above the current max
+            cand = (np.uint32((np.float32(a).view(np.uint32) >> 16) + m) << 16).view(np.float32)
+            if np.float32(cand * (np.float32(119.0) / cand)) > np.float32(119.0):
+                a = cand
+                break
+        else:
+            pytest.skip("no rounding-up bf16 amax near this scale")
+        g[5, 7] = -a
+        g[11, C - 1] = a
+    bs = o_bs.bit_split(g, synth.PHILOX_SEED, 9, 123)
+    if clamp:
+        assert np.float32(bs["amax"] * (np.float32(119.0) / bs["amax"])) > np.float32(119.0)
+    mod = p()
+    plan = mod._PlanBuffers(N, C, "cuda")
+    xsq = torch.ones(N, dtype=torch.int32, device="cuda")
+    mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, 9, 123, o_lss.MODE_BERNOULLI, plan.plan)
+    torch.cuda.synchronize()
+    hilo = plan.hilo.cpu().numpy().astype(np.int64)
+    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64))
+    assert np.array_equal(hilo[N:2 * N], bs["lo"]) and not hilo[2 * N].any()
+    assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
