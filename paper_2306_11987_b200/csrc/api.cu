@@ -225,6 +225,11 @@ extern "C" {
 
 const char* int4_last_error(void) { return g_last_error.c_str(); }
 
+// timing-experiment hook (tools/gs_stamps.py), not part of the documented ABI
+__attribute__((visibility("default"))) int32_t int4_debug_grad_split_stamps(unsigned long long* host, int32_t n) {
+    return i4::grad_split_stamps(host, n);
+}
+
 int32_t int4_set_pdl(int32_t enable) {
     const int32_t prev = i4::pdl_enabled() ? 1 : 0;
     i4::g_pdl.store(enable ? 1 : 0, std::memory_order_relaxed);

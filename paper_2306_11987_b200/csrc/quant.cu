@@ -191,12 +191,13 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 }
 
 // ---------------------------------------------------------------------------
-// B1 + B2 fused: grad_split_kernel (cooperative launch, one grid barrier).
+// B1 + B2 fused: grad_split_kernel (cooperative launch: all CTAs co-resident).
 //   phase 1  amax of grad_Y: max over |g| as bf16 bit patterns (non-negative bf16
 //            values order like their 15-bit integers), exact and
-//            order-independent; one slot per CTA, no atomics.
-//   --- grid.sync() ---
-//   phase 2  every CTA reduces the slots to amax; s_down = fl32(amax / 119),
+//            order-independent; each CTA folds its maximum into one scratch
+//            word (atomicMax) and counts itself in (fence + atomicAdd)
+//   --- every CTA spins until all arrived (one acquire load per poll) ---
+//   phase 2  s_down = fl32(amax / 119),
 //            r8 = fl32(119 / amax); v = fl32(g r8), a = min(|v|, 119);
 //            A = ceil(a 2^32) (a 2^32 is exact in fp32, the conversion rounds up):
 //            high word = floor(a) (+1 when frac's threshold wraps), low word =
@@ -212,10 +213,13 @@ constexpr int kSplitThreads = 256;
 #define I4_BS_GROUP 4
 #endif
 #ifndef I4_BS_MINB
-#define I4_BS_MINB 4
+#define I4_BS_MINB 3
 #endif
 constexpr int kBsGroup = I4_BS_GROUP;
-constexpr int kAmaxUnroll = 8;
+#ifndef I4_BS_AMAX_UNROLL
+#define I4_BS_AMAX_UNROLL 4
+#endif
+constexpr int kAmaxUnroll = I4_BS_AMAX_UNROLL;
 
 __device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t w) {
     return max(w & 0x7FFFu, (w >> 16) & 0x7FFFu);
@@ -238,6 +242,38 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return r;
 }
 
+// Philox4x32-10 of the SR stream (purpose word c2 = 1) for counters whose high
+// word c1 is 0 (block index L/4 < 2^32, checked on the host): round 0's
+// multiply of c2 is the constant M1, and round 1 multiplies c0 = k0[0], a
+// kernel constant the compiler hoists -- 18 IMAD.WIDE per call instead of 20.
+// Same function as philox4x32_10(c0, 0, 1, call_id, K), restated.
+__device__ __forceinline__ Philox4 philox_sr_c1z(uint32_t c0, uint32_t call_id, const PhiloxKeys& K) {
+    const uint64_t p0 = uint64_t(0xD2511F53u) * c0;
+    uint32_t x0 = K.k0[0], x1 = 0xCD9E8D57u;                 // hi(M1 * 1) ^ c1 ^ k0 ; lo(M1 * 1)
+    uint32_t x2 = uint32_t(p0 >> 32) ^ call_id ^ K.k1[0], x3 = uint32_t(p0);
+#pragma unroll
+    for (int r = 1; r < 10; ++r) {
+        const uint64_t q0 = uint64_t(0xD2511F53u) * x0;
+        const uint64_t q1 = uint64_t(0xCD9E8D57u) * x2;
+        const uint32_t n0 = uint32_t(q1 >> 32) ^ x1 ^ K.k0[r], n2 = uint32_t(q0 >> 32) ^ x3 ^ K.k1[r];
+        x0 = n0; x1 = uint32_t(q1); x2 = n2; x3 = uint32_t(q0);
+    }
+    return {x0, x1, x2, x3};
+}
+
+// The two Philox blocks of an 8-element chunk starting at stream block blk (even).
+template <bool C1Z>
+__device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const PhiloxKeys& keys, Philox4& p0,
+                                         Philox4& p1) {
+    if (C1Z) {
+        p0 = philox_sr_c1z(uint32_t(blk), call_id, keys);
+        p1 = philox_sr_c1z(uint32_t(blk) + 1u, call_id, keys);
+    } else {                                          // blk even: blk + 1 never carries into the high word
+        p0 = philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSR, call_id, keys);
+        p1 = philox4x32_10(uint32_t(blk) + 1u, uint32_t(blk >> 32), kPurposeSR, call_id, keys);
+    }
+}
+
 // Fast phase 2 for one 8-element chunk (reading Z-10 / Z-11, same arithmetic as
 // the generic loop below, restated for the ALU / fma-heavy pipe budget):
 //   y = fl32(|g| R32) with R32 = r8 2^32 (exact power-of-two scaling of
@@ -249,17 +285,9 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 //   t  = (M ^ S ^ 0x80) + (S & 1) + 8 per byte  == q + 136 in [16, 255]
 //        (positive: m + 128 + 8; negative: 127 - m + 1 + 8)
 //   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
-template <bool CLAMP, bool FAKE_RNG = false>
-__device__ __forceinline__ void split_chunk8(const uint4 raw, const uint64_t blk, const float R32, const PhiloxKeys& keys,
-                                             uint32_t call_id, uint2& ph, uint2& pl, int& shi, int& slo) {
-    Philox4 p0, p1;
-    if (FAKE_RNG) {                                   // timing experiment only (I4_BS_EXP bit 1)
-        p0 = {uint32_t(blk) * 3u, uint32_t(blk) * 5u, uint32_t(blk) * 7u, uint32_t(blk) * 9u};
-        p1 = {p0.x ^ call_id, p0.y ^ call_id, p0.z ^ call_id, p0.w ^ call_id};
-    } else {
-        p0 = philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSR, call_id, keys);
-        p1 = philox4x32_10(uint32_t(blk) + 1u, uint32_t(blk >> 32), kPurposeSR, call_id, keys);
-    }
+template <bool CLAMP>
+__device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float R32,
+                                             uint2& ph, uint2& pl, int& shi, int& slo) {
     const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t mag[8];
@@ -287,20 +315,37 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const uint64_t blk
 
 // Work unit = G chunks of 256 columns of one row (one 16-byte load of 8 bf16 per
 // lane per chunk).  With C % (256 G) == 0 unit u starts at flat element 256 G u,
-// so addresses and Philox counters need no division.  Each warp takes a
-// contiguous unit range, keeps the next unit's loads in flight (the first ones
-// issued before the grid barrier), accumulates the row
-// norms in registers and flushes them (exact int32 atomics onto the zeroed
-// a_sq) when the row changes.
-// (measured on B200: unit sizes 1-4 chunks, 1-3 units in flight and 64 / 85
-// registers per thread all time within 3 %; the launcher picks the largest G
-// dividing C / 256)
+// so addresses and Philox counters need no division.
+//
+// Each warp takes a contiguous unit range (keeps the next unit's loads in flight,
+// the first ones issued before the phase-1 -> phase-2 wait), accumulates the row
+// norms in registers and flushes them (exact int32 atomics onto the zeroed a_sq)
+// when the row changes.  (Measured and dropped: a dynamic pool of units claimed
+// from a counter -- the per-CTA finish spread is not load imbalance; and Philox
+// words precomputed into shared memory during phase 1 -- no gain.)
 
-__device__ __forceinline__ void warp_unit_range(int64_t units, int64_t& u0, int64_t& u1) {
-    const int64_t nwarps = int64_t(gridDim.x) * (kSplitThreads / 32);
-    const int64_t wid = int64_t(blockIdx.x) * (kSplitThreads / 32) + (threadIdx.x >> 5);
-    u0 = units * wid / nwarps;
-    u1 = units * (wid + 1) / nwarps;
+// scratch words (uint32 [kGradSplitMaxBlocks], zero before the first call; every
+// launch returns them to zero): amax word, arrival / departure counters
+constexpr int kAmaxWord = kGradSplitMaxBlocks - 8, kArriveWord = kAmaxWord + 1, kDepartWord = kAmaxWord + 2;
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// last CTA out returns the counters to zero for the next launch (every CTA read
+// the amax word and the arrival count before it departed)
+__device__ __forceinline__ void depart(uint32_t* scratch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(scratch + kDepartWord, 1u) == gridDim.x - 1) {
+            scratch[kAmaxWord] = 0u;
+            scratch[kArriveWord] = 0u;
+            scratch[kDepartWord] = 0u;
+        }
+    }
 }
 
 template <int G>
@@ -309,61 +354,93 @@ __device__ __forceinline__ void load_unit(const uint4* src, int64_t un, uint4 (&
     for (int gi = 0; gi < G; ++gi) dst[gi] = ld_nc_v4(src + (un * G + gi) * 32);
 }
 
-template <int G, bool CLAMP, bool FAKE_RNG = false>
+// One unit: SR words (Philox, or a fake stream for the timing experiment),
+// split, plane stores, norms into shi / slo.
+template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG>
+__device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, const float R32, const PhiloxKeys& keys,
+                                           uint32_t call_id, uint64_t tbase, int8_t* __restrict__ hilo,
+                                           int8_t* __restrict__ lo_plane, int& shi, int& slo) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+        const int64_t flat = (un * G + gi) * 256 + lane * 8;
+        Philox4 p0, p1;
+        if (FAKE_RNG) {
+            const uint32_t blk = uint32_t(flat);
+            p0 = {blk * 3u, blk * 5u, blk * 7u, blk * 9u};
+            p1 = {p0.x ^ call_id, p0.y ^ call_id, p0.z ^ call_id, p0.w ^ call_id};
+        } else {
+            sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
+        }
+        uint2 ph, pl;
+        split_chunk8<CLAMP>(cur[gi], p0, p1, R32, ph, pl, shi, slo);
+        *reinterpret_cast<uint2*>(hilo + flat) = ph;
+        *reinterpret_cast<uint2*>(lo_plane + flat) = pl;
+    }
+}
+
+__device__ __forceinline__ void flush_norms(int& shi, int& slo, int32_t* __restrict__ a_sq, int64_t N, int64_t row) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        shi += __shfl_xor_sync(0xFFFFFFFFu, shi, o);
+        slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
+    }
+    if (lane_id() == 0) {
+        atomicAdd(a_sq + row, shi >> 8);                              // exact: every term is 256 hi^2
+        atomicAdd(a_sq + N + row, slo);
+    }
+    shi = 0; slo = 0;
+}
+
+template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG = false>
 __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int64_t N, int C, const float R32,
                                             const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset,
                                             int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, int64_t u0,
                                             int64_t u1, uint4 (&buf)[G]) {
-    if (u0 >= u1) return;
-    const int lane = lane_id();
     const int upr = C / (256 * G);                                    // units per row
-    const uint4* src = reinterpret_cast<const uint4*>(g) + lane;
+    const uint4* src = reinterpret_cast<const uint4*>(g) + lane_id();
     const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);       // Z-20: L = (t0 + t) C + c
     int8_t* lo_plane = hilo + N * int64_t(C);
-    int64_t row = u0 / upr;
-    int seg = int(u0 - row * upr);
     int shi = 0, slo = 0;
-    for (int64_t un = u0; un < u1; ++un) {
-        uint4 cur[G];
+    // range [u0, u1): its first unit's loads were issued before the phase-1 wait
+    if (u0 < u1) {
+        int64_t row = u0 / upr;
+        int seg = int(u0 - row * upr);
+        for (int64_t un = u0; un < u1; ++un) {
+            uint4 cur[G];
 #pragma unroll
-        for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
-        if (un + 1 < u1) load_unit<G>(src, un + 1, buf);            // next unit's loads in flight
-#pragma unroll
-        for (int gi = 0; gi < G; ++gi) {
-            const int64_t flat = (un * G + gi) * 256 + lane * 8;
-            uint2 ph, pl;
-            split_chunk8<CLAMP, FAKE_RNG>(cur[gi], (tbase + uint64_t(flat)) >> 2, R32, keys, call_id, ph, pl, shi, slo);
-            *reinterpret_cast<uint2*>(hilo + flat) = ph;
-            *reinterpret_cast<uint2*>(lo_plane + flat) = pl;
-        }
-        if (++seg == upr || un + 1 == u1) {                           // row done (or range end): flush
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                shi += __shfl_xor_sync(0xFFFFFFFFu, shi, o);
-                slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
+            for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
+            if (un + 1 < u1) load_unit<G>(src, un + 1, buf);        // next unit's loads in flight
+            split_unit<G, CLAMP, C1Z, FAKE_RNG>(cur, un, R32, keys, call_id, tbase, hilo, lo_plane, shi, slo);
+            if (++seg == upr || un + 1 == u1) {                       // row done (or range end): flush
+                flush_norms(shi, slo, a_sq, N, row);
+                seg = 0; ++row;
             }
-            if (lane == 0) {
-                atomicAdd(a_sq + row, shi >> 8);                      // exact: every term is 256 hi^2
-                atomicAdd(a_sq + N + row, slo);
-            }
-            shi = 0; slo = 0;
-            seg = 0; ++row;
         }
     }
 }
 
-template <int G>
+// timing experiment (I4_BS_EXP bit 3): per-CTA globaltimer stamps -- start,
+// phase 1 done, barrier passed, amax known, phase 2 done (max over warps)
+__device__ unsigned long long g_gs_stamp[5][kGradSplitMaxBlocks];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int G, bool C1Z>
 __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
-grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ block_max,
+grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ scratch,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
                   int exp_flags) {
-    namespace cgrp = cooperative_groups;
-    cgrp::grid_group grid = cgrp::this_grid();
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     pdl_trigger();
     pdl_wait();
+    const bool stamp = exp_flags & 8;
+    if (stamp && threadIdx.x == 0) g_gs_stamp[0][blockIdx.x] = gtimer();
 
     // ---- phase 1: amax ----------------------------------------------------
     {
@@ -392,38 +469,38 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int w = 1; w < kSplitThreads / 32; ++w) m = max(m, red[w]);
-            block_max[blockIdx.x] = m;
+            // arrive: fold the CTA maximum into the amax word, then count this CTA
+            // (the fence orders this CTA's a_sq zeroing and the max before the count)
+            atomicMax(scratch + kAmaxWord, m);
+            __threadfence();
+            atomicAdd(scratch + kArriveWord, 1u);
+            if (stamp) g_gs_stamp[1][blockIdx.x] = gtimer();
         }
     }
+    // unit range of this warp; its first loads go in flight across the wait
     int64_t pu0 = 0, pu1 = 0;
     uint4 pbuf[G > 0 ? G : 1];
-    if constexpr (G > 0) {                                // first phase-2 loads in flight across the barrier
-        warp_unit_range(N * int64_t(C / (256 * G)), pu0, pu1);
+    if constexpr (G > 0) {
+        const int64_t units = N * int64_t(C / (256 * G));
+        const int64_t nwarps = int64_t(gridDim.x) * (kSplitThreads / 32);
+        const int64_t wid = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
+        pu0 = units * wid / nwarps;
+        pu1 = units * (wid + 1) / nwarps;
         if (pu0 < pu1) load_unit<G>(reinterpret_cast<const uint4*>(g) + lane, pu0, pbuf);
     }
-    grid.sync();
-    // reduce the per-CTA slots: warp 0 only, all loads in flight at once, then
-    // broadcast through shared memory
+    // wait until every CTA arrived (co-resident: cooperative launch), read amax
     __shared__ uint32_t amax_sh;
-    if (warp == 0) {
-        uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i0 = lane; i0 < int(gridDim.x); i0 += 32 * 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int i = i0 + 32 * j;
-                m8[j] = max(m8[j], i < int(gridDim.x) ? __ldcg(block_max + i) : 0u);
-            }
-        }
-        uint32_t m = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])), max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-        if (lane == 0) amax_sh = m;
+    if (threadIdx.x == 0) {
+        while (ld_acquire_gpu(scratch + kArriveWord) < gridDim.x) __nanosleep(32);
+        amax_sh = ld_acquire_gpu(scratch + kAmaxWord);
+        if (stamp) g_gs_stamp[2][blockIdx.x] = gtimer();
     }
     __syncthreads();
     const uint32_t amax_b = amax_sh;
     const float amax = __uint_as_float(amax_b << 16);
     const bool zero = !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
+    if (stamp && threadIdx.x == 0) { g_gs_stamp[3][blockIdx.x] = gtimer(); g_gs_stamp[4][blockIdx.x] = 0; }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
         *amax_out = amax_b;
@@ -434,22 +511,25 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(hilo + 2 * N * C + c) = make_uint4(0, 0, 0, 0);
     if constexpr (G > 0) {
-        if (exp_flags & 1) return;                        // timing experiment: phase 1 only
-        if (exp_flags & 2) {                              // timing experiment: no Philox
-            split_units<G, false, true>(g, N, C, __fmul_rn(r8, 4294967296.0f), keys, call_id, token_offset, hilo, a_sq,
-                                     pu0, pu1, pbuf);
+        if (exp_flags & 3) {                              // timing experiments: phase 1 only / no Philox
+            if (exp_flags & 2)
+                split_units<G, false, C1Z, true>(g, N, C, __fmul_rn(r8, 4294967296.0f), keys, call_id, token_offset,
+                                                 hilo, a_sq, pu0, pu1, pbuf);
+            depart(scratch);
             return;
         }
         if (zero) {                                       // all-zero grad_Y: codes 0, norms 0 (zeroed above)
-            split_units<G, false>(g, N, C, 0.0f, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+            split_units<G, false, C1Z>(g, N, C, 0.0f, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
         } else {
             const float R32 = __fmul_rn(r8, 4294967296.0f);
             // only elements with |g| = amax can land above 119 (fl32(amax r8) may round up by an ulp)
             if (__fmul_rn(amax, r8) > 119.0f)
-                split_units<G, true>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+                split_units<G, true, C1Z>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
             else
-                split_units<G, false>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+                split_units<G, false, C1Z>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
         }
+        if (stamp && lane == 0) atomicMax(&g_gs_stamp[4][blockIdx.x], gtimer());
+        depart(scratch);
         return;
     }
     // generic path (C not a multiple of 256): one warp per row
@@ -520,32 +600,33 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             a_sq[N + row] = slo;
         }
     }
+    depart(scratch);
 }
 
-template <int G>
+template <int G, bool C1Z>
 static int grad_split_max_blocks() {
     static int cached = 0;
     if (cached == 0) {
         int per_sm = 0, sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G>, kSplitThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z>, kSplitThreads, 0);
         cached = per_sm * sms;
     }
     return cached;
 }
 
-int grad_split_max_blocks() { return grad_split_max_blocks<0>(); }
+int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
 
-template <int G>
+template <int G, bool C1Z>
 static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
                                        uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq,
                                        float* s_down, uint32_t* amax_out, cudaStream_t s) {
     static const int exp_flags = getenv("I4_BS_EXP") ? atoi(getenv("I4_BS_EXP")) : 0;   // timing experiments only
-    int blocks = grad_split_max_blocks<G>();
+    int blocks = grad_split_max_blocks<G, C1Z>();
     const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
-    if (blocks > kGradSplitMaxBlocks) blocks = kGradSplitMaxBlocks;
+    if (blocks > kAmaxWord) blocks = kAmaxWord;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(blocks));
     cfg.blockDim = dim3(kSplitThreads);
@@ -555,15 +636,28 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G>, g, N, C, block_max, keys, call_id, token_offset,
-                                       hilo, a_sq, s_down, amax_out, exp_flags);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id,
+                                       token_offset, hilo, a_sq, s_down, amax_out, exp_flags);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G>, g, N, C, block_max, keys, call_id, token_offset,
+        e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id, token_offset,
                                hilo, a_sq, s_down, amax_out, exp_flags);
     }
     return e;
+}
+
+template <int G>
+static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint32_t* block_max,
+                                       const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* hilo,
+                                       int32_t* a_sq, float* s_down, uint32_t* amax_out, cudaStream_t s) {
+    // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
+    const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
+    if (c1z)
+        return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, hilo, a_sq, s_down,
+                                            amax_out, s);
+    return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, hilo, a_sq, s_down,
+                                         amax_out, s);
 }
 
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
@@ -574,13 +668,28 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     const int Ci = int(C);
     const char* env = getenv("I4_BS_GENERIC");            // experiment switch: force the generic phase 2
     const bool generic = env && env[0] == '1';
-#define I4_GS(GG) launch_grad_split_g<GG>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s)
-    if (!generic && C % 1024 == 0) return I4_GS(4);
-    if (!generic && C % 768 == 0) return I4_GS(3);
-    if (!generic && C % 512 == 0) return I4_GS(2);
+    const char* genv = getenv("I4_BS_G");                 // experiment switch: force the unit size
+    const int gforce = genv ? atoi(genv) : 0;
+#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s)
+    // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
+    // measured equal or slower), else 3, 4, 1
+    if (!generic && (gforce == 0 || gforce == 2) && C % 512 == 0) return I4_GS(2);
+    if (!generic && (gforce == 0 || gforce == 3) && C % 768 == 0) return I4_GS(3);
+    if (!generic && (gforce == 0 || gforce == 4) && C % 1024 == 0) return I4_GS(4);
     if (!generic && C % 256 == 0) return I4_GS(1);
 #undef I4_GS
-    return launch_grad_split_g<0>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s);
+    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s);
+}
+
+// debug export for the timing experiment: copies the stamps of the last
+// I4_BS_EXP=8 launch ([5][n] u64, n <= kGradSplitMaxBlocks) to host memory
+int grad_split_stamps(unsigned long long* host, int n) {
+    if (n > kGradSplitMaxBlocks) n = kGradSplitMaxBlocks;
+    for (int r = 0; r < 5; ++r)
+        if (cudaMemcpyFromSymbol(host + size_t(r) * n, g_gs_stamp, sizeof(unsigned long long) * n,
+                                 sizeof(unsigned long long) * kGradSplitMaxBlocks * r) != cudaSuccess)
+            return -1;
+    return n;
 }
 
 }  // namespace i4

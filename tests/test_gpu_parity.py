@@ -342,3 +342,23 @@ def test_bitsplit_unit_paths(C, clamp):
     assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64))
     assert np.array_equal(hilo[N:2 * N], bs["lo"]) and not hilo[2 * N].any()
     assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
+
+
+def test_bitsplit_repeated_calls_reuse_counters():
+    """grad_split's amax / arrival / pool counters live in plan->scratch (zero on
+    first use) and every launch returns them to zero: back-to-back calls on the
+    same plan with different grad_Y give the oracle's planes every time."""
+    N, C = 300, 1024
+    mod = p()
+    plan = mod._PlanBuffers(N, C, "cuda")
+    xsq = torch.ones(N, dtype=torch.int32, device="cuda")
+    for it, scale in enumerate((1.0, 1e-3, 40.0)):
+        g = synth.grad_output(N, C, seed=it, dense=True) * scale
+        g = (synth.bf16_bits(g).view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+        bs = o_bs.bit_split(g, synth.PHILOX_SEED, it, 0)
+        mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, it, 0, o_lss.MODE_BERNOULLI, plan.plan)
+        torch.cuda.synchronize()
+        hilo = plan.hilo.cpu().numpy().astype(np.int64)
+        assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64)), it
+        assert np.array_equal(hilo[N:2 * N], bs["lo"]), it
+        assert not plan.scratch.cpu().numpy()[-8:].any(), "counters not returned to zero"
