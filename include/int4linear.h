@@ -106,7 +106,9 @@ typedef struct {
  *   a_sq     int32 [2N]        sum_c code^2 per half-row (unscaled codes hi, lo)
  *   amax_bits uint32 [1]       out: bf16 bit pattern of max |grad_Y|
  *   s_down   float [1]         out: s_down = amax / 119 (s_up = 16 s_down), reading Z-9
- *   scratch  uint32 [2048]     scratch (per-CTA partial maxima of the fused amax pass)
+ *   scratch  uint32 [2048]     scratch of the fused amax pass: ZERO-INITIALISE before the
+ *                              first call; every call leaves it zero again (its last words
+ *                              hold the amax word and the CTA arrival / departure counters)
  *   items_w  int32 [2N + 128]  kept items of the grad_W mask, ascending ids h*N + t,
  *                              padded with the sentinel 2N up to a multiple of 128
  *   wexp_w   int8  [2N + 128]  log2 of each kept item's weight (~ m_i / p_i)
