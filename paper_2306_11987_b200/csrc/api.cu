@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -203,7 +204,7 @@ constexpr int64_t kMaxBwdTokens = 65536;
 // K-major: rows = M (or Nn), inner = K.  MN-major: rows = K, inner = M (or Nn).
 struct Operand { const int8_t* p; int64_t rows, inner, pitch; bool gather = false; };
 
-i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s) {
+i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s, int sms = 0) {
     CUtensorMap ta, tb, tc;
     const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
     bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), A.gather ? 1u : 128u) &&
@@ -215,8 +216,68 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
     const i4::GemmMaps maps{&ta, &tb, &tc};
-    I4_LAUNCH(i4::launch_gemm(maps, args, device_info().sms, s), kNames[args.epi], s);
+    I4_LAUNCH(i4::launch_gemm(maps, args, sms > 0 ? sms : device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
+}
+
+// Side stream + fork / join events of this host thread (per device), used to
+// run the grad_X and grad_W GEMMs concurrently on disjoint SM sets.  Event
+// record / wait are stream-ordered and capturable (a captured step graph gets
+// two parallel branches).
+struct SideStream { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
+thread_local SideStream t_side;
+
+i4_status side_stream(SideStream*& out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(I4_ERR_CUDA, "cudaGetDevice failed");
+    if (t_side.dev != dev) {
+        if (t_side.s) { cudaStreamDestroy(t_side.s); cudaEventDestroy(t_side.fork); cudaEventDestroy(t_side.join); }
+        t_side = SideStream{};
+        if (cudaStreamCreateWithFlags(&t_side.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t_side.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t_side.join, cudaEventDisableTiming) != cudaSuccess)
+            return fail(I4_ERR_CUDA, "side stream / event creation failed");
+        t_side.dev = dev;
+    }
+    out = &t_side;
+    return I4_OK;
+}
+
+// Work model of one persistent GEMM on P CTA pairs, in k-block units (the
+// kernel's own split-K choice: choose_splits in gemm.cu, hand-over cost H).
+int64_t gemm_cost_kb(int64_t tiles, int64_t nk, int64_t pairs, int max_splits) {
+    if (tiles <= 0 || nk <= 0) return 0;
+    constexpr int64_t H = 24;
+    int64_t best = ((tiles + pairs - 1) / pairs) * nk;
+    if (tiles <= i4::kSplitMaxTiles)
+        for (int sp = 2; sp <= max_splits; ++sp) {
+            if (nk < 2 * sp) break;
+            best = std::min(best, ((sp * tiles + pairs - 1) / pairs) * ((nk + sp - 1) / sp) + H);
+        }
+    return best;
+}
+
+// SM split for running the grad_X GEMM (tiles_x tiles of nk_x k-blocks, no
+// split-K) beside the grad_W GEMM (tiles_w x nk_w, split-K up to kSplitMaxK):
+// returns the pairs given to grad_X, or 0 when running them one after the other
+// is modelled as faster.  Each launch also costs a fixed prologue / last-tile
+// epilogue (kFixedKb, measured 5-8 us ~ 16 k-blocks) that concurrency overlaps.
+int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_w, int64_t pairs) {
+    const char* env = getenv("I4_BWD_CONCURRENT");           // experiment switch: 0 off, 1 forced on
+    if (env && env[0] == '0') return 0;
+    constexpr int64_t kFixedKb = 16;
+    const int64_t seq = gemm_cost_kb(tiles_x, nk_x, pairs, 1) + gemm_cost_kb(tiles_w, nk_w, pairs, i4::kSplitMaxK) +
+                        2 * kFixedKb;
+    int64_t best = -1, best_px = 0;
+    for (int64_t px = 1; px < pairs; ++px) {
+        const int64_t c = std::max(gemm_cost_kb(tiles_x, nk_x, px, 1), gemm_cost_kb(tiles_w, nk_w, pairs - px, i4::kSplitMaxK)) +
+                          kFixedKb;
+        if (best < 0 || c < best) { best = c; best_px = px; }
+    }
+    if (env && env[0] == '1') return int(best_px);
+    // only on a clear modelled win (BERT-large QKV: modelled 136 vs 144 k-blocks,
+    // measured 159 -> 206 us concurrent; BERT-base FFN1: 64 vs 88, 97 -> 88 us)
+    return best >= 0 && 100 * best < 85 * seq ? int(best_px) : 0;
 }
 
 }  // namespace
@@ -228,6 +289,9 @@ const char* int4_last_error(void) { return g_last_error.c_str(); }
 // timing-experiment hook (tools/gs_stamps.py), not part of the documented ABI
 __attribute__((visibility("default"))) int32_t int4_debug_grad_split_stamps(unsigned long long* host, int32_t n) {
     return i4::grad_split_stamps(host, n);
+}
+__attribute__((visibility("default"))) int32_t int4_debug_sampler_stamps(unsigned long long* host, int32_t enable) {
+    return i4::sampler_stamps(host, enable);
 }
 
 int32_t int4_set_pdl(int32_t enable) {
@@ -440,6 +504,19 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         ca.x_touched = plan->x_touched; ca.dx = dX; ca.dx_bf16 = dx_dtype == I4_OUT_BF16;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
+    // The two GEMMs are independent: when the work model says so (each alone
+    // under-fills the GPU, e.g. grad_X with fewer tiles than CTA pairs and a short
+    // grad_W), grad_W runs on a side stream on the SMs grad_X leaves free.
+    // Sizes are modelled with the budget N as the kept-item count (E[K] <= N).
+    const int64_t pairs = device_info().sms / i4::kGemmCG;
+    const int px = concurrent_split(((N + 255) / 256) * ((D + 255) / 256), (C + 127) / 128,
+                                    ((C + 255) / 256) * ((D + 255) / 256), (N + 127) / 128, pairs);
+    SideStream* side = nullptr;
+    if (px > 0) {
+        I4_RETURN_IF(side_stream(side));
+        if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
+            return fail(I4_ERR_CUDA, "int4_linear_bwd: fork to the side stream failed");
+    }
     // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
     {
         i4::GemmArgs g{};
@@ -459,7 +536,8 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.partial = w.part_x; g.flags = w.flags_x;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
         if (want_lsq) { g.delta = cache->x_delta; g.lsq_part = w.lsq_x; }
-        I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s));
+        I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s,
+                          px > 0 ? 2 * px : 0));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
     {
@@ -475,7 +553,12 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.partial = w.part_w; g.flags = w.flags_w;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;   // few (C/256 x D/256) tiles, long sampled K
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
-        I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, s));
+        I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
+                          px > 0 ? device_info().sms - 2 * px : 0));
+    }
+    if (px > 0) {
+        if (cudaEventRecord(side->join, side->s) != cudaSuccess || cudaStreamWaitEvent(s, side->join, 0) != cudaSuccess)
+            return fail(I4_ERR_CUDA, "int4_linear_bwd: join from the side stream failed");
     }
     if (want_lsq) {
         // A.3: g(s) = 1 / sqrt(Q_P N_elem), Q_P = 7 (reading Z-29 for N_elem)

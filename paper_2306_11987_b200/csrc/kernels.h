@@ -31,7 +31,8 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
                                   int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s);
 constexpr int kGradSplitMaxBlocks = 2048;   // block-max scratch words the plan provides
-int grad_split_stamps(unsigned long long* host, int n);   // timing experiment (I4_BS_EXP=8)
+int grad_split_stamps(unsigned long long* host, int n);
+int sampler_stamps(unsigned long long* host, int enable);   // timing experiment   // timing experiment (I4_BS_EXP=8)
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
                               uint32_t* amax_out, cudaStream_t s);

@@ -115,11 +115,35 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
     parity ^= 1;
 }
 
+// timing experiment: globaltimer stamps of CTA (rank 0, mask 0), thread 0:
+// [0] start [1] scores summed [2..] after each A.2 round, then Bernoulli done,
+// compaction done, end; slot 31 = number of stamps
+__device__ int g_smp_stamp_on = 0;
+__device__ unsigned long long g_smp_stamp[32];
+__device__ __forceinline__ void smp_stamp(int& n, bool on) {
+    if (on) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        if (n < 31) g_smp_stamp[n] = t;
+        ++n;
+        g_smp_stamp[31] = (unsigned long long)n;
+    }
+}
+
+int sampler_stamps(unsigned long long* host, int enable) {
+    if (cudaMemcpyToSymbol(g_smp_stamp_on, &enable, sizeof(int)) != cudaSuccess) return -1;
+    if (host && cudaMemcpyFromSymbol(host, g_smp_stamp, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
+    return 0;
+}
+
 template <int CL>
 __global__ void __launch_bounds__(kSamplerThreads, 1)
 lss_sampler_kernel(SamplerArgs a) {
     pdl_trigger();
     pdl_wait();                                   // a_sq / s_down of grad_split
+    const bool st_on = g_smp_stamp_on && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
+    int st_n = 0;
+    smp_stamp(st_n, st_on);
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SamplerSmem& sm = *reinterpret_cast<SamplerSmem*>(smem_raw);
     const Group<CL> cl;
@@ -165,6 +189,7 @@ lss_sampler_kernel(SamplerArgs a) {
     }
     uint64_t Wall; uint32_t Z;
     cluster_sum(cl, sm, parity, sum_pos, cnt_pos, Wall, Z);
+    smp_stamp(st_n, st_on);
 
     // ---- A.2 water-filling ----------------------------------------------------
     const uint64_t B = uint64_t(N);
@@ -183,6 +208,7 @@ lss_sampler_kernel(SamplerArgs a) {
             }
             uint64_t Wn; uint32_t Sc;
             cluster_sum(cl, sm, parity, wun, sc, Wn, Sc);
+            smp_stamp(st_n, st_on);
             if (Sc == s_cnt) break;
             s_cnt = Sc;
             R = B - Sc;
@@ -227,6 +253,7 @@ lss_sampler_kernel(SamplerArgs a) {
         if (mask_id == 1 && out >= 0 && a.x_touched) a.x_touched[t] = 1;
     }
 
+    smp_stamp(st_n, st_on);
     // ---- compaction: block exclusive scan + cluster prefix --------------------
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t incl = my_keep;
@@ -276,7 +303,9 @@ lss_sampler_kernel(SamplerArgs a) {
         }
         if (threadIdx.x == 0) *a.count[mask_id] = int32_t(total);
     }
-    cl.sync();                                 // keep DSMEM alive until all remote writes landed
+    smp_stamp(st_n, st_on);
+    cl.sync();
+    smp_stamp(st_n, st_on);                                 // keep DSMEM alive until all remote writes landed
 }
 
 template <int CL>
