@@ -50,30 +50,15 @@ struct HqJob {
 
 constexpr int kHqMaxThreads = 256;
 
-template <int K>
-__global__ void __launch_bounds__(kHqMaxThreads)
-hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
-    const bool second = int(blockIdx.x) >= j0.blocks;
-    const HqJob& J = second ? j1 : j0;
-    const int bid = second ? int(blockIdx.x) - j0.blocks : int(blockIdx.x);
-    const int tpr = cols >> 5;                       // threads (32-column blocks) per row
-    const int r_local = int(threadIdx.x) / tpr;
-    const int blk = int(threadIdx.x) - r_local * tpr;
-    const int64_t row = int64_t(bid) * rows_per_cta + r_local;
-    const bool active = r_local < rows_per_cta && row < J.rows;
-    pdl_trigger();
-    pdl_wait();                                        // X / W may be written by the previous kernel
-    __shared__ int sq_row[kHqMaxThreads];
-    if (threadIdx.x < rows_per_cta) sq_row[threadIdx.x] = 0;
-
+// One 32-column block of one row: FWHT (registers, + xor-shuffle stages for
+// k = 6, 7), LSQ, code / mask / delta stores; returns the block's sum of squared codes.
+template <int K, bool DELTA>
+__device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, int tpr, int cols, bool active,
+                                        const uint4 (&raw)[4]) {
     // column pairs (j, j + 16) in fp32x2 registers: the in-register FWHT stages
     // (strides 1 .. 8) and the LSQ scaling run as packed FADD2 / FMUL2
     uint64_t p[16];
     {
-        const uint16_t* src = J.x + (active ? row * cols + blk * 32 : 0);
-        uint4 raw[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) raw[q] = active ? ld_nc_v4(src + 8 * q) : make_uint4(0, 0, 0, 0);
         float v[32];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -101,46 +86,101 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
             }
         }
     }
+    if (!active) return 0;
+    // LSQ: v = fl32(t r); code = clamp(rint(v), -7, 7); mask = |v| <= 7.
+    // rint on the clamped value by the magic-number add: fl32(c + 1.5 2^23) is
+    // exact round-half-even for |c| <= 7 (ulp 1 there), and the low byte of its
+    // bits is the int8 code (0x4B400000 + q) -- one FADD instead of an F2I.
+    const uint64_t r2 = f2_pack(J.r, J.r);
+    uint32_t qb[32];                                // code in byte 0
+    uint32_t mask = 0;
+    int sq = 0;
+    float dl[DELTA ? 32 : 1];                       // A.3 delta, if requested
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        float s0, s1;
+        f2_unpack(f2_mul(p[j], r2), s0, s1);
+        const float c0 = fminf(fmaxf(s0, -7.0f), 7.0f), c1 = fminf(fmaxf(s1, -7.0f), 7.0f);
+        const float m0 = __fadd_rn(c0, 12582912.0f), m1 = __fadd_rn(c1, 12582912.0f);
+        qb[j] = __float_as_uint(m0);
+        qb[j + 16] = __float_as_uint(m1);
+        const bool in0 = fabsf(s0) <= 7.0f, in1 = fabsf(s1) <= 7.0f;
+        mask |= (uint32_t(in0) << j) | (uint32_t(in1) << (j + 16));
+        if constexpr (DELTA) {
+            const float q0 = __fsub_rn(m0, 12582912.0f), q1 = __fsub_rn(m1, 12582912.0f);   // exact
+            dl[j] = in0 ? __fsub_rn(q0, s0) : q0;                                    // exact (|.| <= 1/2)
+            dl[j + 16] = in1 ? __fsub_rn(q1, s1) : q1;
+        }
+    }
+    if (DELTA && J.delta != nullptr) {
+        float4* dd = reinterpret_cast<float4*>(J.delta + row * cols + blk * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dd[i] = make_float4(dl[4 * i], dl[4 * i + 1], dl[4 * i + 2], dl[4 * i + 3]);
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w[i] = __byte_perm(__byte_perm(qb[4 * i], qb[4 * i + 1], 0x0040),
+                           __byte_perm(qb[4 * i + 2], qb[4 * i + 3], 0x0040), 0x5410);
+        sq = __dp4a(int(w[i]), int(w[i]), sq);     // sum of squared codes, 4 per instruction
+    }
+    int8_t* dst = J.codes + row * cols + blk * 32;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    if (J.bits != nullptr) J.bits[row * tpr + blk] = mask;
+    return sq;
+}
+
+// A CTA covers PASSES x R rows: the thread of (row slot, block) handles row
+// slot + pass R for every pass, with the loads of all passes issued before the
+// first block is transformed (measured on B200: 2 and 4 passes are 20-45 %
+// slower than 1 -- the kernel is instruction-issue bound, not latency bound).
+#ifndef I4_HQ_PASSES
+#define I4_HQ_PASSES 1
+#endif
+constexpr int kHqPasses = I4_HQ_PASSES;
+
+template <int K, bool DELTA>
+__global__ void __launch_bounds__(kHqMaxThreads)
+hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
+    const bool second = int(blockIdx.x) >= j0.blocks;
+    const HqJob& J = second ? j1 : j0;
+    const int bid = second ? int(blockIdx.x) - j0.blocks : int(blockIdx.x);
+    const int tpr = cols >> 5;                       // threads (32-column blocks) per row
+    const int r_local = int(threadIdx.x) / tpr;
+    const int blk = int(threadIdx.x) - r_local * tpr;
+    const int64_t row0 = int64_t(bid) * rows_per_cta * kHqPasses + r_local;
+    pdl_trigger();
+    pdl_wait();                                        // X / W may be written by the previous kernel
+    __shared__ int sq_row[kHqPasses][kHqMaxThreads];
+    if (threadIdx.x < rows_per_cta)
+#pragma unroll
+        for (int ps = 0; ps < kHqPasses; ++ps) sq_row[ps][threadIdx.x] = 0;
+    uint4 raw[kHqPasses][4];
+#pragma unroll
+    for (int ps = 0; ps < kHqPasses; ++ps) {
+        const int64_t row = row0 + int64_t(ps) * rows_per_cta;
+        const bool active = r_local < rows_per_cta && row < J.rows;
+        const uint16_t* src = J.x + (active ? row * cols + blk * 32 : 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) raw[ps][q] = active ? ld_nc_v4(src + 8 * q) : make_uint4(0, 0, 0, 0);
+    }
     __syncthreads();                                   // sq_row initialised
-    if (active) {
-        // LSQ: v = fl32(t r); code = clamp(rint(v), -7, 7); mask = |v| <= 7
-        const uint64_t r2 = f2_pack(J.r, J.r);
-        int q[32];
-        uint32_t mask = 0;
-        int sq = 0;
-        float dl[32];                                   // A.3 delta, if requested
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            float s0, s1;
-            f2_unpack(f2_mul(p[j], r2), s0, s1);
-            q[j] = __float2int_rn(fminf(fmaxf(s0, -7.0f), 7.0f));
-            q[j + 16] = __float2int_rn(fminf(fmaxf(s1, -7.0f), 7.0f));
-            const bool in0 = fabsf(s0) <= 7.0f, in1 = fabsf(s1) <= 7.0f;
-            mask |= (uint32_t(in0) << j) | (uint32_t(in1) << (j + 16));
-            dl[j] = in0 ? __fsub_rn(float(q[j]), s0) : float(q[j]);          // exact (|.| <= 1/2)
-            dl[j + 16] = in1 ? __fsub_rn(float(q[j + 16]), s1) : float(q[j + 16]);
-        }
-        if (J.delta != nullptr) {
-            float4* dd = reinterpret_cast<float4*>(J.delta + row * cols + blk * 32);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) dd[i] = make_float4(dl[4 * i], dl[4 * i + 1], dl[4 * i + 2], dl[4 * i + 3]);
-        }
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            w[i] = __byte_perm(__byte_perm(uint32_t(q[4 * i]), uint32_t(q[4 * i + 1]), 0x0040),
-                               __byte_perm(uint32_t(q[4 * i + 2]), uint32_t(q[4 * i + 3]), 0x0040), 0x5410);
-            sq = __dp4a(int(w[i]), int(w[i]), sq);     // sum of squared codes, 4 per instruction
-        }
-        int8_t* dst = J.codes + row * cols + blk * 32;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
-        if (J.bits != nullptr) J.bits[row * tpr + blk] = mask;
-        if (J.sqnorm != nullptr) atomicAdd(&sq_row[r_local], sq);
+    for (int ps = 0; ps < kHqPasses; ++ps) {
+        const int64_t row = row0 + int64_t(ps) * rows_per_cta;
+        const bool active = r_local < rows_per_cta && row < J.rows;
+        const int sq = hq_block<K, DELTA>(J, row, blk, tpr, cols, active, raw[ps]);
+        if (active && J.sqnorm != nullptr) atomicAdd(&sq_row[ps][r_local], sq);
     }
     if (J.sqnorm != nullptr) {
         __syncthreads();
-        if (active && blk == 0) J.sqnorm[row] = sq_row[r_local];
+        if (r_local < rows_per_cta && blk == 0)
+#pragma unroll
+            for (int ps = 0; ps < kHqPasses; ++ps) {
+                const int64_t row = row0 + int64_t(ps) * rows_per_cta;
+                if (row < J.rows) J.sqnorm[row] = sq_row[ps][r_local];
+            }
     }
 }
 
@@ -154,23 +194,26 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     const int R = hq_rows_per_cta(a.cols);
     HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0};
     HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0};
-    j0.blocks = int((a.rows0 + R - 1) / R);
-    j1.blocks = int((a.rows1 + R - 1) / R);
+    j0.blocks = int((a.rows0 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
+    j1.blocks = int((a.rows1 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
     const int grid = j0.blocks + j1.blocks;
     if (grid == 0) return cudaSuccess;
     const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
     void (*kern)(HqJob, HqJob, int, int) = nullptr;
+    const bool delta = a.delta0 != nullptr || a.delta1 != nullptr;
+#define I4_HQ_K(KK) kern = delta ? hadamard_quant_kernel<KK, true> : hadamard_quant_kernel<KK, false>; break;
     switch (a.k) {
-        case 0: kern = hadamard_quant_kernel<0>; break;
-        case 1: kern = hadamard_quant_kernel<1>; break;
-        case 2: kern = hadamard_quant_kernel<2>; break;
-        case 3: kern = hadamard_quant_kernel<3>; break;
-        case 4: kern = hadamard_quant_kernel<4>; break;
-        case 5: kern = hadamard_quant_kernel<5>; break;
-        case 6: kern = hadamard_quant_kernel<6>; break;
-        case 7: kern = hadamard_quant_kernel<7>; break;
+        case 0: I4_HQ_K(0)
+        case 1: I4_HQ_K(1)
+        case 2: I4_HQ_K(2)
+        case 3: I4_HQ_K(3)
+        case 4: I4_HQ_K(4)
+        case 5: I4_HQ_K(5)
+        case 6: I4_HQ_K(6)
+        case 7: I4_HQ_K(7)
         default: return cudaErrorInvalidValue;
     }
+#undef I4_HQ_K
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(unsigned(threads));
