@@ -77,11 +77,16 @@ void trace_record(cudaEvent_t e, cudaStream_t s) {
     if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);  // graph node
     else cudaEventRecord(e, s);
 }
+// launches inside a fork / join region are traced as one entry (the region's
+// events sit on the caller's stream, before the fork and after the join)
+thread_local bool g_trace_group = false;
+struct TraceGroupReset { ~TraceGroupReset() { g_trace_group = false; } };   // error paths too
 void trace_pre(cudaStream_t s) {
+    if (g_trace_group) return;
     if (g_trace.active && g_trace.n == g_trace.first && g_trace.cap > 0) trace_record(g_trace.ev[0], s);
 }
 void trace_post(const char* name, cudaStream_t s) {
-    if (!g_trace.active) return;
+    if (!g_trace.active || g_trace_group) return;
     const int w = g_trace.n - g_trace.first;                 // position inside the window
     if (w >= 0 && w + 1 < g_trace.cap) trace_record(g_trace.ev[w + 1], s);
     if (g_trace.n < kMaxTrace) g_trace.names[g_trace.n] = name;
@@ -270,7 +275,10 @@ int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_
                         2 * kFixedKb;
     int64_t best = -1, best_px = 0;
     for (int64_t px = 1; px < pairs; ++px) {
-        const int64_t c = std::max(gemm_cost_kb(tiles_x, nk_x, px, 1), gemm_cost_kb(tiles_w, nk_w, pairs - px, i4::kSplitMaxK)) +
+        // concurrent grad_W runs without split-K: its partial-sum chains stalled the
+        // pipeline when it shared the GPU (BERT-large QKV, 4-way split on 42 pairs:
+        // grad_W 28 -> 103 us)
+        const int64_t c = std::max(gemm_cost_kb(tiles_x, nk_x, px, 1), gemm_cost_kb(tiles_w, nk_w, pairs - px, 1)) +
                           kFixedKb;
         if (best < 0 || c < best) { best = c; best_px = px; }
     }
@@ -512,7 +520,10 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     const int px = concurrent_split(((N + 255) / 256) * ((D + 255) / 256), (C + 127) / 128,
                                     ((C + 255) / 256) * ((D + 255) / 256), (N + 127) / 128, pairs);
     SideStream* side = nullptr;
+    TraceGroupReset trace_group_reset;
     if (px > 0) {
+        trace_pre(s);                            // the concurrent pair is one trace entry
+        g_trace_group = true;
         I4_RETURN_IF(side_stream(side));
         if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
             return fail(I4_ERR_CUDA, "int4_linear_bwd: fork to the side stream failed");
@@ -551,14 +562,17 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.mask = cache->w_mask;
         g.a_mn = 1; g.b_mn = 1;                  // A_W [K items, C], B_W [K, D]: both MN-major
         g.partial = w.part_w; g.flags = w.flags_w;
-        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = i4::kSplitMaxK;   // few (C/256 x D/256) tiles, long sampled K
+        g.max_tiles_split = i4::kSplitMaxTiles;  // few (C/256 x D/256) tiles, long sampled K
+        g.max_splits = px > 0 ? 1 : i4::kSplitMaxK;   // no split-K beside a concurrent grad_X
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
                           px > 0 ? device_info().sms - 2 * px : 0));
     }
     if (px > 0) {
+        g_trace_group = false;
         if (cudaEventRecord(side->join, side->s) != cudaSuccess || cudaStreamWaitEvent(s, side->join, 0) != cudaSuccess)
             return fail(I4_ERR_CUDA, "int4_linear_bwd: join from the side stream failed");
+        trace_post("gemm_i8_dgrad||gemm_i8_wgrad", s);
     }
     if (want_lsq) {
         // A.3: g(s) = 1 / sqrt(Q_P N_elem), Q_P = 7 (reading Z-29 for N_elem)
