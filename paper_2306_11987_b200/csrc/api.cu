@@ -268,8 +268,9 @@ int64_t gemm_cost_kb(int64_t tiles, int64_t nk, int64_t pairs, int max_splits) {
 // is modelled as faster.  Each launch also costs a fixed prologue / last-tile
 // epilogue (kFixedKb, measured 5-8 us ~ 16 k-blocks) that concurrency overlaps.
 int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_w, int64_t pairs) {
-    const char* env = getenv("I4_BWD_CONCURRENT");           // experiment switch: 0 off, 1 forced on
+    const char* env = getenv("I4_BWD_CONCURRENT");           // experiment switch: 0 off, 1 forced on, P: P pairs
     if (env && env[0] == '0') return 0;
+    if (env && atoi(env) > 1) return atoi(env);
     constexpr int64_t kFixedKb = 16;
     const int64_t seq = gemm_cost_kb(tiles_x, nk_x, pairs, 1) + gemm_cost_kb(tiles_w, nk_w, pairs, i4::kSplitMaxK) +
                         2 * kFixedKb;
@@ -564,6 +565,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.partial = w.part_w; g.flags = w.flags_w;
         g.max_tiles_split = i4::kSplitMaxTiles;  // few (C/256 x D/256) tiles, long sampled K
         g.max_splits = px > 0 ? 1 : i4::kSplitMaxK;   // no split-K beside a concurrent grad_X
+        if (px > 0 && getenv("I4_BWD_WSPLIT")) g.max_splits = atoi(getenv("I4_BWD_WSPLIT"));   // experiment
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
                           px > 0 ? device_info().sms - 2 * px : 0));
