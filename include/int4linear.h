@@ -109,12 +109,13 @@ typedef struct {
  *   scratch  uint32 [2048]     scratch of the fused amax pass: ZERO-INITIALISE before the
  *                              first call; every call leaves it zero again (its last words
  *                              hold the amax word and the CTA arrival / departure counters)
- *   items_w  int32 [2N + 128]  kept items of the grad_W mask, ascending ids h*N + t,
- *                              padded with the sentinel 2N up to a multiple of 128
+ *   items_w  int32 [2N + 128]  kept items of the grad_W mask (ids h*N + t) in token-major
+ *                              order (slot 2t + h, like items_x), padded with the
+ *                              sentinel 2N up to a multiple of 128
  *   wexp_w   int8  [2N + 128]  log2 of each kept item's weight (~ m_i / p_i)
  *   count_w  int32 [1]         number of kept items (device)
- *   items_x, wexp_x, count_x   the same for the grad_X mask, in token-major order
- *                              (slot 2t + h: a token's two items are adjacent)
+ *   items_x, wexp_x, count_x   the same for the grad_X mask (a token's two items are
+ *                              adjacent rows of the grad_X GEMM)
  *   x_touched uint8 [N]        1 if token t has a kept grad_X item
  *   grad_s   float [2]         nullable out (int4_linear_bwd): the LSQ step-size gradients
  *                              {grad s_X, grad s_W} (A.3; readings

@@ -198,11 +198,13 @@ def _sample_item_order(w, budget, u, mode, e_max):
 
 
 def sample_weight_mask(a_sq, b_sq, seed, call_id, token_offset, mode=MODE_BERNOULLI):
-    """LSS mask of the weight gradient, purpose-2 Philox stream."""
+    """LSS mask of the weight gradient (PAPER.md:320-334), purpose-2 Philox stream;
+    list in token-major order (t, h) like the grad_X list (reading Z-12: the
+    estimator is a sum over the kept items, independent of their order)."""
     N = np.asarray(a_sq).shape[1]
     w = weight_scores(a_sq, b_sq)
     u = mask_uniforms(seed, call_id, token_offset, N, PURPOSE_MASK_W)
-    out = sample(w, N, u, mode, E_MAX_W)
+    out = sample(w, N, u, mode, E_MAX_W, token_major=True)
     out["w"] = w
     return out
 

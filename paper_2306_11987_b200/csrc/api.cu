@@ -209,18 +209,24 @@ constexpr int64_t kMaxBwdTokens = 65536;
 // K-major: rows = M (or Nn), inner = K.  MN-major: rows = K, inner = M (or Nn).
 struct Operand { const int8_t* p; int64_t rows, inner, pitch; bool gather = false; };
 
-i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s, int sms = 0) {
-    CUtensorMap ta, tb, tc;
+// A_alt (optional): a second A the kernel may read instead, chosen on the device
+// (GemmArgs::alt_*; the grad_W GEMM reads the grad_X GEMM's A when the lists match)
+i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s, int sms = 0,
+               const Operand* A_alt = nullptr) {
+    CUtensorMap ta, tb, tc, ta2;
     const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
     bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), A.gather ? 1u : 128u) &&
               make_tmap_i8(&tb, B.p, uint64_t(B.inner), uint64_t(B.rows), uint64_t(B.pitch),
                            args.b_mn ? 128u : uint32_t(bn / i4::kGemmCG));
+    if (A_alt) ok = ok && make_tmap_i8(&ta2, A_alt->p, uint64_t(A_alt->inner), uint64_t(A_alt->rows),
+                                       uint64_t(A_alt->pitch), 128u);
+    else ta2 = ta;
     if (args.epi == i4::EPI_DGRAD) tc = ta;                 // grad_X is written with red.add, no map
     else ok = ok && make_tmap_out(&tc, args.out, args.out_bf16 != 0, args.epi == i4::EPI_INT32,
                                   uint64_t(args.Nn), uint64_t(args.M));
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
-    const i4::GemmMaps maps{&ta, &tb, &tc};
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2};
     I4_LAUNCH(i4::launch_gemm(maps, args, sms > 0 ? sms : device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
@@ -389,7 +395,8 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
 
 static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed,
                             uint32_t call_id, int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan,
-                            cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words) {
+                            cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words,
+                            int32_t* det_flags = nullptr) {
     I4_RETURN_IF(check_device());
     if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
         !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x || !plan->x_touched)
@@ -417,6 +424,7 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
     a.items[0] = plan->items_w; a.wexp[0] = plan->wexp_w; a.count[0] = plan->count_w;
     a.items[1] = plan->items_x; a.wexp[1] = plan->wexp_x; a.count[1] = plan->count_x;
     a.zero_words = zero_words; a.n_zero_words = n_zero_words;
+    a.det_flags = det_flags;
     a.x_touched = plan->x_touched;
     I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
     return I4_OK;
@@ -438,6 +446,7 @@ struct BwdWs {
     int8_t* a_x; int8_t* a_w; int8_t* b_w;
     int32_t* part_x; int32_t* part_w; uint32_t* flags_x; uint32_t* flags_w;
     double* lsq_x; double* lsq_w;        // A.3 fp64 partials (zeroed with the flags by the sampler)
+    int32_t* det;                        // [2] deterministic-mask flags (written by the sampler)
     size_t total;
 };
 
@@ -453,6 +462,7 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
     const size_t o_pw = take(i4::gemm_split_partial_bytes());
     // split-K flags and the A.3 partials are one contiguous region: the sampler zeroes it
     const size_t o_f = take(2 * i4::gemm_split_flag_words() * sizeof(uint32_t) + 2 * i4::kLsqPartials * sizeof(double));
+    const size_t o_det = take(2 * sizeof(int32_t));
     w.total = off;
     if (ws) {
         uint8_t* b = static_cast<uint8_t*>(ws);
@@ -465,6 +475,7 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
         w.flags_w = w.flags_x + i4::gemm_split_flag_words();
         w.lsq_x = reinterpret_cast<double*>(w.flags_w + i4::gemm_split_flag_words());
         w.lsq_w = w.lsq_x + i4::kLsqPartials;
+        w.det = reinterpret_cast<int32_t*>(b + o_det);
     }
     return w;
 }
@@ -498,7 +509,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         const int32_t words = int32_t(2 * i4::gemm_split_flag_words() +
                                       (want_lsq ? 2 * i4::kLsqPartials * sizeof(double) / sizeof(uint32_t) : 0));
         I4_RETURN_IF(bitsplit_lss_impl(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, s,
-                                       w0.flags_x, words));
+                                       w0.flags_x, words, w0.det));
     }
 
     const int64_t kcap = round_up(2 * N, 128);
@@ -511,6 +522,7 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         ca.items_w = plan->items_w; ca.wexp_w = plan->wexp_w; ca.count_w = plan->count_w;
         ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
         ca.x_touched = plan->x_touched; ca.dx = dX; ca.dx_bf16 = dx_dtype == I4_OUT_BF16;
+        ca.det_flags = w.det;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
     // The two GEMMs are independent: when the work model says so (each alone
@@ -567,8 +579,10 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
         g.max_splits = px > 0 ? 1 : i4::kSplitMaxK;   // no split-K beside a concurrent grad_X
         if (px > 0 && getenv("I4_BWD_WSPLIT")) g.max_splits = atoi(getenv("I4_BWD_WSPLIT"));   // experiment
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
+        g.alt_det_flags = w.det; g.alt_count_w = plan->count_w; g.alt_count_x = plan->count_x;
+        const Operand a_x_view{w.a_x, 2 * N + 128, C, C};   // = A_W when the two item lists are equal
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
-                          px > 0 ? device_info().sms - 2 * px : 0));
+                          px > 0 ? device_info().sms - 2 * px : 0, &a_x_view));
     }
     if (px > 0) {
         g_trace_group = false;

@@ -14,7 +14,8 @@ constexpr int kGroup = 8;                 // 16-byte loads in flight per lane
 
 // One launch builds all three compacted operands; one warp per output row:
 //   A_X[j, :] = plane[items_x[j], :]              (C bytes; grad_X GEMM A, K-major)
-//   A_W[j, :] = plane[items_w[j], :]              (C bytes; grad_W GEMM A, MN-major)
+//   A_W[j, :] = plane[items_w[j], :]              (C bytes; grad_W GEMM A, MN-major;
+//                                                  skipped when the lists are equal)
 //   B_W[j, :] = 2^wexp_w[j] X_hat[t(items_w[j]), :]   (D bytes, |.| <= 112; grad_W GEMM B)
 // The plane rows hold 16 hi or lo, so acc[c, d] = sum_j A_W[j, c] B_W[j, d] is the
 // weighted bit-split product with s_up = 16 s_down folded in (reading Z-17).
@@ -58,13 +59,17 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t n_straddle = (cnt_x + 31) / 32;            // candidate positions 31, 63, ...
-    const int64_t total = pad_x + 2 * pad_w + a.N + n_straddle;
+    // equal item lists: the grad_W GEMM reads A_X (its A map is chosen on the device
+    // by the same test), so the A_W copy is skipped
+    const int64_t pad_aw = lists_equal(a.det_flags, a.count_w, a.count_x) ? 0 : pad_w;
+    const int64_t seg_bw = pad_x + pad_aw;                   // first B_W row job
+    const int64_t total = seg_bw + pad_w + a.N + n_straddle;
     const int two_n = 2 * a.N;
     for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
-        if (j >= pad_x + 2 * pad_w) {
+        if (j >= seg_bw + pad_w) {
             // grad_X rows the GEMM epilogue does not store: tokens without a kept
             // item, and tokens whose two items straddle a 32-row group (both red.add)
-            const int64_t r = j - pad_x - 2 * pad_w;
+            const int64_t r = j - seg_bw - pad_w;
             if (r < a.N) {
                 if (__ldg(a.x_touched + r) == 0) zero_row(a.dx, r, a.D, a.dx_bf16, lane);
             } else {
@@ -79,13 +84,13 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
             const int32_t item = __ldg(a.items_x + j);
             const bool pad = item >= two_n;
             copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1);
-        } else if (j < pad_x + pad_w) {
+        } else if (j < seg_bw) {
             const int64_t r = j - pad_x;
             const int32_t item = __ldg(a.items_w + r);
             const bool pad = item >= two_n;
             copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_w + r * a.C, a.C, lane, pad, 1);
         } else {
-            const int64_t r = j - pad_x - pad_w;
+            const int64_t r = j - seg_bw;
             const int32_t item = __ldg(a.items_w + r);
             const bool pad = item >= two_n;
             const int t = pad ? 0 : (item >= a.N ? item - a.N : item);

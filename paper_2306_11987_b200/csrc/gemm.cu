@@ -153,7 +153,7 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(EpiShape<BN, EPI, kh_ch(KH)>::THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2, const GemmArgs g) {
     constexpr int CH = kh_ch(KH);
     using Epi = EpiShape<BN, EPI, CH>;
     constexpr int kEpiWarps = Epi::WARPS;
@@ -179,6 +179,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
+        if (EPI == EPI_WGRAD) tma_prefetch_desc(&tmA2);
         tma_prefetch_desc(&tmB);
         if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -214,6 +215,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // lane 0 issues the TMA; with a gathered A the 32 lanes first fetch the
         // 128 row indices of the stage (4 per lane) and hand them out by shuffles.
         const bool gather = g.a_gather != nullptr;
+        // grad_W: the A operand may be the grad_X GEMM's (identical item lists)
+        const CUtensorMap* pA = &tmA;
+        if (EPI == EPI_WGRAD && lists_equal(g.alt_det_flags, g.alt_count_w, g.alt_count_x)) pA = &tmA2;
         const int gcount = gather ? __ldg(g.gather_count) : 0;
         auto load_idx4 = [&](int r) {
             int4 v;
@@ -245,13 +249,13 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
                 const uint32_t fb = CG == 2 ? mapa_shared(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
                 if (gather)                            // every lane issues the gather of its own 4 rows
-                    tma_gather4<CG>(a_dst + lane * 4 * 128, &tmA, fb, A_MN ? m0 : kb * kBK,
+                    tma_gather4<CG>(a_dst + lane * 4 * 128, pA, fb, A_MN ? m0 : kb * kBK,
                                     gidx.x, gidx.y, gidx.z, gidx.w);
                 if (lane == 0) {
                     if constexpr (CG == 2) {
                         if (!gather) {
-                            if (A_MN) tma_load_2d_2sm(a_dst, &tmA, fb, m0, kb * kBK);
-                            else      tma_load_2d_2sm(a_dst, &tmA, fb, kb * kBK, m0);
+                            if (A_MN) tma_load_2d_2sm(a_dst, pA, fb, m0, kb * kBK);
+                            else      tma_load_2d_2sm(a_dst, pA, fb, kb * kBK, m0);
                         }
                         if (B_MN) {
 #pragma unroll
@@ -262,8 +266,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                     } else {
                         if (!gather) {
-                            if (A_MN) tma_load_2d(a_dst, &tmA, &full[stage], m0, kb * kBK);
-                            else      tma_load_2d(a_dst, &tmA, &full[stage], kb * kBK, m0);
+                            if (A_MN) tma_load_2d(a_dst, pA, &full[stage], m0, kb * kBK);
+                            else      tma_load_2d(a_dst, pA, &full[stage], kb * kBK, m0);
                         }
                         if (B_MN) {
 #pragma unroll
@@ -636,7 +640,8 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cu
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
     return cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(m.a),
-                              *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c), g);
+                              *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c),
+                              *reinterpret_cast<const CUtensorMap*>(m.a2 ? m.a2 : m.a), g);
 }
 
 template <int EPI, int KH, bool A_MN, bool B_MN>

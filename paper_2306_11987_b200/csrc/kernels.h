@@ -51,6 +51,7 @@ struct SamplerArgs {
     uint8_t* x_touched;       // [N]: 1 if the token has a kept grad_X item (optional)
     uint32_t* zero_words;     // optional: words zeroed by the launch (split-K flags of the GEMMs)
     int32_t n_zero_words;
+    int32_t* det_flags;       // optional [2]: 1 if mask m kept a deterministic set (all positives / all items)
 };
 int sampler_max_tokens();
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
@@ -68,7 +69,12 @@ struct CompactArgs {
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]
+    const int32_t* det_flags; // optional [2] (sampler): both set + equal counts -> lists equal, A_W = A_X
 };
+// the grad_W list equals the grad_X list: both masks deterministic, equal counts
+__device__ __forceinline__ bool lists_equal(const int32_t* det_flags, const int32_t* count_w, const int32_t* count_x) {
+    return det_flags != nullptr && __ldg(det_flags) != 0 && __ldg(det_flags + 1) != 0 && __ldg(count_w) == __ldg(count_x);
+}
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
@@ -104,13 +110,15 @@ struct GemmArgs {
     // LSQ step-size gradient (A.3), optional: sum(acc o delta) per CTA epilogue warp
     const float* delta;       // dgrad: delta_X [N, Nn] (row = token); wgrad: delta_W [M, Nn]
     double* lsq_part;         // [gridDim.x * 8] fp64 partials (entries of absent CTAs pre-zeroed)
+    // wgrad: read A through the alternate map (the grad_X GEMM's A) when lists_equal(...)
+    const int32_t* alt_det_flags; const int32_t* alt_count_w; const int32_t* alt_count_x;
 };
 constexpr int kSplitMaxTiles = 96;        // workspace tiles reserved for split-K
 constexpr int kSplitMaxK = 4;
 size_t gemm_split_partial_bytes();        // bytes of one GEMM's split-K partial workspace
 size_t gemm_split_flag_words();
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
-struct GemmMaps { const void* a; const void* b; const void* c; };   // CUtensorMap* (host)
+struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; };   // CUtensorMap* (host)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
 int gemm_block_n(int Nn, bool b_mn);
 

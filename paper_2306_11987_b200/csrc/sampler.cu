@@ -14,7 +14,7 @@
 //            T2 = floor(R w 2^32 / W), T1 = 2 T2 - 2^(32-e); Philox word u of item
 //            (h, t): keep iff u < T2, weight 2^e if u < T1 else 2^(e+1); floor
 //            weight 2^E_MAX (4 for grad_W whose weights fold into int8, 24 for grad_X).
-//   compaction  ascending item ids h*N + t via block scan + cluster prefix, list
+//   compaction  token-major item ids (slot 2t + h) via block scan + cluster prefix, list
 //            padded to a multiple of 128 with the sentinel 2N; count stays on device.
 //
 // The item scores live in shared memory (16384 items per CTA -> N <= 65536,
@@ -159,10 +159,12 @@ lss_sampler_kernel(SamplerArgs a) {
     const int t_hi = min(nloc, t_lo + ipt);
     const int e_max = mask_id == 0 ? kEMaxW : kEMaxX;
     const uint32_t purpose = mask_id == 0 ? kPurposeMaskW : kPurposeMaskX;
-    // slot -> item id: the grad_W list is in item order h*N + t; the grad_X list is
-    // token-major (slot 2t + h) so that a token's two items are adjacent rows of
-    // the grad_X GEMM and combine in its epilogue without atomics
-    auto item_of = [&](int slot) { return mask_id == 0 ? slot : (slot & 1) * N + (slot >> 1); };
+    // slot -> item id: both lists are token-major (slot 2t + h): a token's two items
+    // are adjacent rows of the grad_X GEMM (they combine in its epilogue without
+    // atomics), and when both masks keep the same set (deterministic masks with
+    // equal counts) the two lists are identical, so the grad_W GEMM reads the
+    // grad_X GEMM's compacted A and compact skips its own copy
+    auto item_of = [&](int slot) { return (slot & 1) * N + (slot >> 1); };
     int parity = 0;
     if (blockIdx.y == 0 && rank == 0)
         for (int i = threadIdx.x; i < a.n_zero_words; i += kSamplerThreads) a.zero_words[i] = 0u;
@@ -195,6 +197,10 @@ lss_sampler_kernel(SamplerArgs a) {
     const uint64_t B = uint64_t(N);
     const bool bernoulli = a.mode == 0;
     const bool binding = bernoulli && uint64_t(Z) > B;
+    // deterministic set (every positive item with weight 1, or all items): the
+    // grad_W set is then a subset of the grad_X set (w_W > 0 implies w_X > 0), so
+    // equal counts mean equal lists
+    if (a.det_flags && rank == 0 && threadIdx.x == 0) a.det_flags[mask_id] = binding ? 0 : 1;
     uint64_t R = B, W = Wall;
     if (binding) {
         uint32_t s_cnt = 0;
