@@ -334,17 +334,24 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         constexpr bool kMask = EPI == EPI_DGRAD || EPI == EPI_WGRAD;
         constexpr int NW = kMask ? Epi::COLS / 32 : 1;
         const int two_n = 2 * g.n_tokens;
-        struct RowInfo { int item, inext, iprev, e; };
+        // Loaded two tiles ahead and left raw until the tile is processed (a consumer
+        // right after the load -- e.g. the int8 sign extension of the weight
+        // exponent -- made every tile wait for the load, ncu: long-scoreboard on
+        // the epilogue warps): the item of this lane's row, the items of the rows
+        // just outside the warp's 32 (lanes 31 / 0 only; inner neighbours come by
+        // shuffle at use time) and the 32-bit word holding the weight exponent.
+        struct RowInfo { int item, edge, eword, rw; };
         auto load_ri = [&](int u) {
-            RowInfo x{two_n, two_n, two_n, 0};
+            RowInfo x{two_n, two_n, 0, 0};
             if (EPI == EPI_DGRAD && u < units) {
                 const int tl = u % T;
                 const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+                x.rw = rw;
                 if (rw < M) {
                     x.item = __ldg(g.items + rw);
-                    x.e = int(__ldg(g.wexp + rw));
-                    if (rw + 1 < M) x.inext = __ldg(g.items + rw + 1);
-                    if (rw > 0) x.iprev = __ldg(g.items + rw - 1);
+                    x.eword = int(__ldg(reinterpret_cast<const uint32_t*>(g.wexp + (rw & ~3))));
+                    if (lane == 31 && rw + 1 < M) x.edge = __ldg(g.items + rw + 1);
+                    if (lane == 0 && rw > 0) x.edge = __ldg(g.items + rw - 1);
                 }
             }
             return x;
@@ -408,11 +415,19 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 valid = valid && item < two_n;
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
-                const int e = valid ? ri_cur.e : 0;
+                const int e = valid ? int(int8_t(uint32_t(ri_cur.eword) >> (8 * (ri_cur.rw & 3)))) : 0;
+                // neighbours: rows rw + 1 / rw - 1 (lanes 31 / 0 loaded them; others shuffle);
+                // rows at or past M read as the sentinel
+                int nx = __shfl_down_sync(0xFFFFFFFFu, ri_cur.item, 1);
+                int pv = __shfl_up_sync(0xFFFFFFFFu, ri_cur.item, 1);
+                if (lane == 31) nx = ri_cur.edge;
+                if (lane == 0) pv = ri_cur.edge;
+                if (row + 1 >= M) nx = two_n;
+                if (row == 0) pv = two_n;
                 row_e = e;
                 rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
-                const int inext = valid ? ri_cur.inext : two_n;
-                const int iprev = valid ? ri_cur.iprev : two_n;
+                const int inext = valid ? nx : two_n;
+                const int iprev = valid ? pv : two_n;
                 const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;
                 const bool second = iprev < two_n && (iprev >= g.n_tokens ? iprev - g.n_tokens : iprev) == out_row;
                 if ((first && lane == 31) || (second && lane == 0)) dmode = 3;
