@@ -221,8 +221,9 @@ I4_API size_t hq_select_k_workspace_size(void);
  *   k_mask uint32 [B, P, M/32], q_sqnorm int32 [B, N];
  * B, N, P, M, k are filled by int4_bmm_fwd.  Shape rules as for the linear
  * operator (M, P multiples of 64; N <= 65536 for the backward).
- * This version runs the per-batch operator for b = 0 .. B-1 on `stream` (every
- * step in the library's kernels; the batch loop is host orchestration). */
+ * This version runs the per-batch operator for b = 0 .. B-1 (every step in the
+ * library's kernels; the batch loop is host orchestration): batch b on stream
+ * b % S, S = min(B, 4), library-owned streams forked from / joined into `stream`. */
 typedef struct {
     int8_t* qq;
     int8_t* kq;
@@ -240,11 +241,17 @@ I4_API i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N
 
 /* Per-batch LSS-MM backward: dQ [B, N, M] (fp32 or bf16), dK [B, P, M] fp32.  Batch b
  * uses token_offset = b N (its Philox streams are distinct, reading Z-31), its own
- * amax and budget N.  plan: an i4_lss_plan sized for ONE batch (N tokens, C = P),
- * reused batch after batch; ws: int4_bwd_workspace_size(N, M, P) bytes. */
+ * amax and budget N.  plans: n_plans i4_lss_plan structs, each sized for ONE batch
+ * (N tokens, C = P; scratch zeroed before first use); ws: n_plans x
+ * int4_bwd_workspace_size(N, M, P) bytes.  Batch b runs as chain j = b % S,
+ * S = min(B, n_plans, 4), with plans[j], workspace slice j and, for j > 0, a
+ * library-owned stream forked from and joined back into `stream` (event
+ * record / wait only: capturable, no host synchronisation).  Results do not
+ * depend on S. */
 I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k,
-                              uint64_t seed, uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plan, void* dQ,
-                              i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes, void* stream);
+                              uint64_t seed, uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plans,
+                              int32_t n_plans, void* dQ, i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes,
+                              void* stream);
 
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);

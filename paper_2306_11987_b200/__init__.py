@@ -79,8 +79,8 @@ def _load():
         "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
         "hq_select_k": [vp, i64, vp, i64, i64, f32, f32, i32, i32, vp, vp, vp, ctypes.c_size_t, vp],
         "int4_bmm_fwd": [vp, vp, i64, i64, i64, i64, i32, vp, vp, vp, i32, ctypes.POINTER(I4BmmCache), vp],
-        "int4_bmm_bwd": [vp, ctypes.POINTER(I4BmmCache), vp, vp, u64, u32, i32, ctypes.POINTER(I4LssPlan), vp, i32,
-                         vp, vp, ctypes.c_size_t, vp],
+        "int4_bmm_bwd": [vp, ctypes.POINTER(I4BmmCache), vp, vp, u64, u32, i32, ctypes.POINTER(I4LssPlan), i32, vp,
+                         i32, vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -336,15 +336,16 @@ def int4_bmm_fwd(Q, K, k, s_q, s_k, T, cache, stream=None):
                             ctypes.byref(cache), _stream(stream)))
 
 
-def int4_bmm_bwd(dT, cache, s_q, s_k, seed, call_id, mode, plan, dQ, dK, ws, stream=None):
-    """A.1 BMM backward: per-batch LSS-MM with token offsets b N (reading Z-31)."""
+def int4_bmm_bwd(dT, cache, s_q, s_k, seed, call_id, mode, plans, dQ, dK, ws, stream=None):
+    """A.1 BMM backward: per-batch LSS-MM with token offsets b N (reading Z-31).
+    plans: a ctypes array of I4LssPlan (one per concurrent batch chain)."""
     import numpy as np
     import torch
     sq = np.ascontiguousarray(s_q, dtype=np.float32)
     sk = np.ascontiguousarray(s_k, dtype=np.float32)
     dq_dtype = OUT_BF16 if dQ.dtype == torch.bfloat16 else OUT_F32
     _check(lib.int4_bmm_bwd(_ptr(dT), ctypes.byref(cache), sq.ctypes.data, sk.ctypes.data, int(seed), int(call_id),
-                            int(mode), ctypes.byref(plan), _ptr(dQ), dq_dtype, _ptr(dK), _ptr(ws),
+                            int(mode), plans, len(plans), _ptr(dQ), dq_dtype, _ptr(dK), _ptr(ws),
                             ws.numel() * ws.element_size(), _stream(stream)))
 
 
@@ -363,13 +364,16 @@ class Int4BMM:
         self.q_sqnorm = torch.empty(B, N, dtype=i32, device=dev)
         self.cache = I4BmmCache(qq=self.qq.data_ptr(), kq=self.kq.data_ptr(), q_mask=self.q_mask.data_ptr(),
                                 k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr())
-        self._plan_bufs = _PlanBuffers(N, P, dev)            # one batch's plan, reused batch after batch
-        self.plan = self._plan_bufs.plan
-        self.ws = torch.empty(int4_bwd_workspace_size(N, M, P), dtype=torch.uint8, device=dev)
+        # one plan + workspace slice per concurrent batch chain (batch b -> chain b % S)
+        S = min(B, 4)
+        self._plan_bufs = [_PlanBuffers(N, P, dev) for _ in range(S)]
+        self.plans = (I4LssPlan * S)(*[pb.plan for pb in self._plan_bufs])
+        self.plan = self.plans[0]
+        self.ws = torch.empty(S * int4_bwd_workspace_size(N, M, P), dtype=torch.uint8, device=dev)
 
     def forward(self, Q, K, s_q, s_k, T, stream=None):
         self.s_q, self.s_k = s_q, s_k
         int4_bmm_fwd(Q, K, self.k, s_q, s_k, T, self.cache, stream)
 
     def backward(self, dT, dQ, dK, seed, call_id=0, mode=LSS_BERNOULLI, stream=None):
-        int4_bmm_bwd(dT, self.cache, self.s_q, self.s_k, seed, call_id, mode, self.plan, dQ, dK, self.ws, stream)
+        int4_bmm_bwd(dT, self.cache, self.s_q, self.s_k, seed, call_id, mode, self.plans, dQ, dK, self.ws, stream)

@@ -237,19 +237,26 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
 // two parallel branches).
 struct SideStream { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
 thread_local SideStream t_side;
+constexpr int kBmmStreams = 4;                       // batch chains of int4_bmm_fwd run on this many streams
+thread_local SideStream t_bmm[kBmmStreams - 1];
 
-i4_status side_stream(SideStream*& out) {
+i4_status make_side(SideStream& st) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(I4_ERR_CUDA, "cudaGetDevice failed");
-    if (t_side.dev != dev) {
-        if (t_side.s) { cudaStreamDestroy(t_side.s); cudaEventDestroy(t_side.fork); cudaEventDestroy(t_side.join); }
-        t_side = SideStream{};
-        if (cudaStreamCreateWithFlags(&t_side.s, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&t_side.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&t_side.join, cudaEventDisableTiming) != cudaSuccess)
+    if (st.dev != dev) {
+        if (st.s) { cudaStreamDestroy(st.s); cudaEventDestroy(st.fork); cudaEventDestroy(st.join); }
+        st = SideStream{};
+        if (cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.join, cudaEventDisableTiming) != cudaSuccess)
             return fail(I4_ERR_CUDA, "side stream / event creation failed");
-        t_side.dev = dev;
+        st.dev = dev;
     }
+    return I4_OK;
+}
+
+i4_status side_stream(SideStream*& out) {
+    I4_RETURN_IF(make_side(t_side));
     out = &t_side;
     return I4_OK;
 }
@@ -486,9 +493,24 @@ extern "C" {
 
 size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) { return carve_bwd_ws(nullptr, N, D, C).total; }
 
+static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
+                                 int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
+                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream,
+                                 bool allow_concurrent);
+
 i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                           int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
                           i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream) {
+    return linear_bwd_impl(dY, cache, seed, call_id, token_offset, mode, plan, dX, dx_dtype, dW, ws, ws_bytes, stream,
+                           true);
+}
+
+}  // extern "C"
+
+static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
+                                 int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
+                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream,
+                                 bool allow_concurrent) {
     I4_RETURN_IF(check_device());
     if (!cache || !dX || !dW || !ws) return fail(I4_ERR_ARG, "int4_linear_bwd: NULL pointer");
     if (dx_dtype != I4_OUT_F32 && dx_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "int4_linear_bwd: bad dx_dtype");
@@ -530,7 +552,8 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     // grad_W), grad_W runs on a side stream on the SMs grad_X leaves free.
     // Sizes are modelled with the budget N as the kept-item count (E[K] <= N).
     const int64_t pairs = device_info().sms / i4::kGemmCG;
-    const int px = concurrent_split(((N + 255) / 256) * ((D + 255) / 256), (C + 127) / 128,
+    const int px = !allow_concurrent ? 0 :
+                   concurrent_split(((N + 255) / 256) * ((D + 255) / 256), (C + 127) / 128,
                                     ((C + 255) / 256) * ((D + 255) / 256), (N + 127) / 128, pairs);
     SideStream* side = nullptr;
     TraceGroupReset trace_group_reset;
@@ -601,6 +624,8 @@ i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t se
     return I4_OK;
 }
 
+extern "C" {
+
 namespace {
 i4_fwd_cache bmm_view(const i4_bmm_cache* c, int64_t b, float s_q, float s_k) {
     i4_fwd_cache v{};
@@ -626,28 +651,74 @@ i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64
         return fail(I4_ERR_SHAPE, "int4_bmm_fwd: need N > 0 and M, P positive multiples of 64");
     cache->B = B; cache->N = N; cache->P = P; cache->M = M; cache->k = k;
     const size_t ob = t_dtype == I4_OUT_BF16 ? 2 : 4;
+    // the batches are independent (each writes its own cache slices and T slice):
+    // batch b runs on stream b % S (S = min(B, kBmmStreams); the caller's stream
+    // and side streams joined back into it), so the small per-batch kernels overlap
+    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    const char* env = getenv("I4_BMM_STREAMS");          // experiment switch
+    const int S = int(std::min<int64_t>(B, env ? std::max(1, std::min(atoi(env), kBmmStreams)) : kBmmStreams));
+    cudaEvent_t fork_ev = nullptr;
+    for (int j = 1; j < S; ++j) {
+        I4_RETURN_IF(make_side(t_bmm[j - 1]));
+        if (j == 1) fork_ev = t_bmm[0].fork;
+    }
+    if (S > 1) {
+        if (cudaEventRecord(fork_ev, s0) != cudaSuccess) return fail(I4_ERR_CUDA, "int4_bmm_fwd: fork failed");
+        for (int j = 1; j < S; ++j)
+            if (cudaStreamWaitEvent(t_bmm[j - 1].s, fork_ev, 0) != cudaSuccess)
+                return fail(I4_ERR_CUDA, "int4_bmm_fwd: fork failed");
+    }
     for (int64_t b = 0; b < B; ++b) {
         i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
+        cudaStream_t sb = (b % S) == 0 ? s0 : t_bmm[b % S - 1].s;
         I4_RETURN_IF(int4_linear_fwd(static_cast<const uint16_t*>(Q) + b * N * M, static_cast<const uint16_t*>(K) + b * P * M,
                                      N, M, P, k, s_q[b], s_k[b], static_cast<uint8_t*>(T) + size_t(b * N * P) * ob, t_dtype,
-                                     &v, stream));
+                                     &v, sb));
     }
+    for (int j = 1; j < S; ++j)
+        if (cudaEventRecord(t_bmm[j - 1].join, t_bmm[j - 1].s) != cudaSuccess ||
+            cudaStreamWaitEvent(s0, t_bmm[j - 1].join, 0) != cudaSuccess)
+            return fail(I4_ERR_CUDA, "int4_bmm_fwd: join failed");
     return I4_OK;
 }
 
 i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k, uint64_t seed,
-                       uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plan, void* dQ, i4_out_dtype dq_dtype,
-                       float* dK, void* ws, size_t ws_bytes, void* stream) {
-    if (!dT || !cache || !s_q || !s_k || !dQ || !dK) return fail(I4_ERR_ARG, "int4_bmm_bwd: NULL pointer");
+                       uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plans, int32_t n_plans, void* dQ,
+                       i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes, void* stream) {
+    if (!dT || !cache || !s_q || !s_k || !dQ || !dK || !plans) return fail(I4_ERR_ARG, "int4_bmm_bwd: NULL pointer");
     if (cache->B <= 0) return fail(I4_ERR_ARG, "int4_bmm_bwd: cache not filled by int4_bmm_fwd");
+    if (n_plans < 1) return fail(I4_ERR_ARG, "int4_bmm_bwd: n_plans must be >= 1");
     const int64_t B = cache->B, N = cache->N, P = cache->P, M = cache->M;
     const size_t oq = dq_dtype == I4_OUT_BF16 ? 2 : 4;
-    for (int64_t b = 0; b < B; ++b) {
-        const i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
-        I4_RETURN_IF(int4_linear_bwd(static_cast<const uint16_t*>(dT) + b * N * P, &v, seed, call_id, b * N, mode, plan,
-                                     static_cast<uint8_t*>(dQ) + size_t(b * N * M) * oq, dq_dtype, dK + b * P * M, ws,
-                                     ws_bytes, stream));
+    // chain j = b % S owns plan j and workspace slice j and runs on stream j (the
+    // caller's stream for j = 0, library side streams joined back otherwise), so
+    // the per-batch kernel chains overlap; S = min(B, n_plans, kBmmStreams)
+    const size_t per_ws = int4_bwd_workspace_size(N, M, P);
+    const char* env = getenv("I4_BMM_STREAMS");          // experiment switch
+    int S = int(std::min<int64_t>(B, std::min<int64_t>(n_plans, kBmmStreams)));
+    if (env) S = std::max(1, std::min(S, atoi(env)));
+    if (ws_bytes < size_t(S) * per_ws)
+        return fail(I4_ERR_WORKSPACE, "int4_bmm_bwd: ws_bytes %zu < %d x %zu", ws_bytes, S, per_ws);
+    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    for (int j = 1; j < S; ++j) I4_RETURN_IF(make_side(t_bmm[j - 1]));
+    if (S > 1) {
+        if (cudaEventRecord(t_bmm[0].fork, s0) != cudaSuccess) return fail(I4_ERR_CUDA, "int4_bmm_bwd: fork failed");
+        for (int j = 1; j < S; ++j)
+            if (cudaStreamWaitEvent(t_bmm[j - 1].s, t_bmm[0].fork, 0) != cudaSuccess)
+                return fail(I4_ERR_CUDA, "int4_bmm_bwd: fork failed");
     }
+    for (int64_t b = 0; b < B; ++b) {
+        const int j = int(b % S);
+        const i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
+        I4_RETURN_IF(linear_bwd_impl(static_cast<const uint16_t*>(dT) + b * N * P, &v, seed, call_id, b * N, mode,
+                                     plans + j, static_cast<uint8_t*>(dQ) + size_t(b * N * M) * oq, dq_dtype,
+                                     dK + b * P * M, static_cast<uint8_t*>(ws) + size_t(j) * per_ws, per_ws,
+                                     j == 0 ? s0 : t_bmm[j - 1].s, S == 1));
+    }
+    for (int j = 1; j < S; ++j)
+        if (cudaEventRecord(t_bmm[j - 1].join, t_bmm[j - 1].s) != cudaSuccess ||
+            cudaStreamWaitEvent(s0, t_bmm[j - 1].join, 0) != cudaSuccess)
+            return fail(I4_ERR_CUDA, "int4_bmm_bwd: join failed");
     return I4_OK;
 }
 

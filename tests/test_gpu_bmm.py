@@ -23,7 +23,7 @@ def p():
 
 
 @pytest.mark.parametrize("mode", [o_lss.MODE_BERNOULLI, o_lss.MODE_NONE])
-@pytest.mark.parametrize("B,N,P,M,k", [(3, 128, 128, 64, 4), (2, 200, 192, 128, 5)])
+@pytest.mark.parametrize("B,N,P,M,k", [(3, 128, 128, 64, 4), (2, 200, 192, 128, 5), (6, 64, 128, 64, 3)])
 def test_bmm_parity(B, N, P, M, k, mode):
     q = np.stack([synth.activations(N, M, seed=10 + b) for b in range(B)])
     kk = np.stack([synth.activations(P, M, seed=20 + b) for b in range(B)])
@@ -63,3 +63,28 @@ def test_bmm_bad_shape():
     with pytest.raises(p().I4Error):
         op.forward(to_bf16_cuda(synth.activations(64, 64)[None]), to_bf16_cuda(synth.activations(96, 64)[None]),
                    np.ones(1, np.float32), np.ones(1, np.float32), T)
+
+
+def test_bmm_chains_bitwise_independent_of_stream_count(monkeypatch):
+    """Batches run as up to 4 concurrent chains (own plan, workspace slice, stream):
+    the results are byte-identical to one chain on the caller's stream."""
+    B, N, P, M, k = 7, 128, 128, 64, 4
+    q = np.stack([synth.activations(N, M, seed=50 + b) for b in range(B)])
+    kk = np.stack([synth.activations(P, M, seed=60 + b) for b in range(B)])
+    dt = np.stack([synth.grad_output(N, P, seed=70 + b, dense=(b % 3 == 0)) for b in range(B)])
+    s_q = np.array([synth.cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
+    s_k = np.array([synth.cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
+    outs = []
+    for streams in ("1", "4"):
+        monkeypatch.setenv("I4_BMM_STREAMS", streams)
+        op = p().Int4BMM(B, N, P, M, k)
+        T = torch.empty(B, N, P, dtype=torch.float32, device="cuda")
+        dQ = torch.empty(B, N, M, dtype=torch.bfloat16, device="cuda")
+        dK = torch.empty(B, P, M, dtype=torch.float32, device="cuda")
+        op.forward(to_bf16_cuda(q), to_bf16_cuda(kk), s_q, s_k, T)
+        op.backward(to_bf16_cuda(dt), dQ, dK, synth.PHILOX_SEED, call_id=2)
+        torch.cuda.synchronize()
+        outs.append([t.view(torch.uint8).cpu().numpy() if t.dtype == torch.bfloat16 else t.cpu().numpy().view(np.uint32)
+                     for t in (T, dQ, dK)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
