@@ -223,7 +223,7 @@ I4_API size_t hq_select_k_workspace_size(void);
  * operator (M, P multiples of 64; N <= 65536 for the backward).
  * This version runs the per-batch operator for b = 0 .. B-1 (every step in the
  * library's kernels; the batch loop is host orchestration): batch b on stream
- * b % S, S = min(B, 4), library-owned streams forked from / joined into `stream`. */
+ * b % S, S = min(B, 16), library-owned streams forked from / joined into `stream`. */
 typedef struct {
     int8_t* qq;
     int8_t* kq;
@@ -244,7 +244,7 @@ I4_API i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N
  * amax and budget N.  plans: n_plans i4_lss_plan structs, each sized for ONE batch
  * (N tokens, C = P; scratch zeroed before first use); ws: n_plans x
  * int4_bwd_workspace_size(N, M, P) bytes.  Batch b runs as chain j = b % S,
- * S = min(B, n_plans, 4), with plans[j], workspace slice j and, for j > 0, a
+ * S = min(B, n_plans, 16), with plans[j], workspace slice j and, for j > 0, a
  * library-owned stream forked from and joined back into `stream` (event
  * record / wait only: capturable, no host synchronisation).  Results do not
  * depend on S. */

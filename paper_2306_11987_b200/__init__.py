@@ -365,7 +365,7 @@ class Int4BMM:
         self.cache = I4BmmCache(qq=self.qq.data_ptr(), kq=self.kq.data_ptr(), q_mask=self.q_mask.data_ptr(),
                                 k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr())
         # one plan + workspace slice per concurrent batch chain (batch b -> chain b % S)
-        S = min(B, 4)
+        S = min(B, int(os.environ.get("I4_BMM_CHAINS", "16")))
         self._plan_bufs = [_PlanBuffers(N, P, dev) for _ in range(S)]
         self.plans = (I4LssPlan * S)(*[pb.plan for pb in self._plan_bufs])
         self.plan = self.plans[0]

@@ -237,7 +237,10 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
 // two parallel branches).
 struct SideStream { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
 thread_local SideStream t_side;
-constexpr int kBmmStreams = 4;                       // batch chains of int4_bmm_fwd run on this many streams
+#ifndef I4_BMM_MAX_STREAMS
+#define I4_BMM_MAX_STREAMS 16
+#endif
+constexpr int kBmmStreams = I4_BMM_MAX_STREAMS;                       // batch chains of int4_bmm_fwd run on this many streams
 thread_local SideStream t_bmm[kBmmStreams - 1];
 
 i4_status make_side(SideStream& st) {

@@ -66,7 +66,7 @@ def test_bmm_bad_shape():
 
 
 def test_bmm_chains_bitwise_independent_of_stream_count(monkeypatch):
-    """Batches run as up to 4 concurrent chains (own plan, workspace slice, stream):
+    """Batches run as up to 16 concurrent chains (own plan, workspace slice, stream):
     the results are byte-identical to one chain on the caller's stream."""
     B, N, P, M, k = 7, 128, 128, 64, 4
     q = np.stack([synth.activations(N, M, seed=50 + b) for b in range(B)])
@@ -75,7 +75,7 @@ def test_bmm_chains_bitwise_independent_of_stream_count(monkeypatch):
     s_q = np.array([synth.cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
     s_k = np.array([synth.cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
     outs = []
-    for streams in ("1", "4"):
+    for streams in ("1", "16"):
         monkeypatch.setenv("I4_BMM_STREAMS", streams)
         op = p().Int4BMM(B, N, P, M, k)
         T = torch.empty(B, N, P, dtype=torch.float32, device="cuda")

@@ -75,7 +75,7 @@ def main():
                       "ms_per_step": t_ours, "fwd_ms": t_fwd, "value": work / (t_ours * 1e-3) / 1e12, "unit": "TOPS",
                       "bf16_cublas_ms_per_step": t_blas, "speedup_vs_bf16_cublas": t_blas / t_ours,
                       "launches_per_step": 7 * B, "note": "per-batch loop over the linear-operator kernels "
-                      "(host orchestration, graph-captured; forward batches spread over 4 streams); "
+                      "(host orchestration, graph-captured; batch chains on up to 16 streams); "
                       "not yet batched inside the kernels"}))
 
 
