@@ -37,10 +37,10 @@ constexpr int kEMaxX = 24;
 
 int sampler_max_tokens() { return kClusterCTAs * kItemsPerCTA / 2; }
 
+// fixed part of the shared memory; the per-item arrays follow it, sized for the
+// CTA's share of the items (launch-time: a small N gets a small footprint):
+//   uint64_t w[per] (scores), uint8_t clamped[per] (A.2 set S), int8_t wexp[per]
 struct SamplerSmem {
-    uint64_t w[kItemsPerCTA];        // scores
-    uint8_t clamped[kItemsPerCTA];   // A.2 set S
-    int8_t wexp[kItemsPerCTA];       // -1: dropped, else log2 weight
     uint64_t red_w[2][kClusterCTAs];
     uint32_t red_c[2][kClusterCTAs];
     uint64_t warp_w[kSamplerThreads / 32];
@@ -152,6 +152,10 @@ lss_sampler_kernel(SamplerArgs a) {
     const int N = a.N;
     const int n_items = 2 * N;
     const int per = (n_items + CL - 1) / CL;
+    const int per16 = (per + 15) & ~15;
+    uint64_t* sw = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SamplerSmem));
+    uint8_t* scl = reinterpret_cast<uint8_t*>(sw + per16);
+    int8_t* swe = reinterpret_cast<int8_t*>(scl + per16);
     const int base = rank * per;
     const int nloc = max(0, min(per, n_items - base));
     const int ipt = (per + kSamplerThreads - 1) / kSamplerThreads;   // items per thread
@@ -184,8 +188,8 @@ lss_sampler_kernel(SamplerArgs a) {
             const double root = __dsqrt_rn(prod);
             w = uint64_t(root * (h == 0 ? 1048576.0 : 65536.0));   // floor(root 2^(16+4[up]))
         }
-        sm.w[j] = w;
-        sm.clamped[j] = 0;
+        sw[j] = w;
+        scl[j] = 0;
         sum_pos += w;
         cnt_pos += (w > 0);
     }
@@ -207,10 +211,10 @@ lss_sampler_kernel(SamplerArgs a) {
         for (int round = 0; round <= n_items + 1; ++round) {
             uint64_t wun = 0; uint32_t sc = 0;
             for (int j = t_lo; j < t_hi; ++j) {
-                const uint64_t w = sm.w[j];
+                const uint64_t w = sw[j];
                 if (w == 0) continue;
-                if (!sm.clamped[j] && R * w >= W) sm.clamped[j] = 1;
-                if (sm.clamped[j]) sc += 1; else wun += w;
+                if (!scl[j] && R * w >= W) scl[j] = 1;
+                if (scl[j]) sc += 1; else wun += w;
             }
             uint64_t Wn; uint32_t Sc;
             cluster_sum(cl, sm, parity, wun, sc, Wn, Sc);
@@ -228,12 +232,12 @@ lss_sampler_kernel(SamplerArgs a) {
         const int i = item_of(base + j);
         const int h = i >= N ? 1 : 0;
         const int t = i - h * N;
-        const uint64_t w = sm.w[j];
+        const uint64_t w = sw[j];
         int8_t out = -1;
         if (a.mode == 2) {                 // I4_LSS_NONE: every item, weight 1
             out = 0;
         } else if (w > 0) {
-            if (!binding || sm.clamped[j]) {
+            if (!binding || scl[j]) {
                 out = 0;                   // p = 1 (Z-16 / clamped by A.2)
             } else {
                 const uint64_t num = R * w;                       // R w < W
@@ -254,7 +258,7 @@ lss_sampler_kernel(SamplerArgs a) {
                 if (u < T2) out = int8_t(u < T1 ? e : e + 1);
             }
         }
-        sm.wexp[j] = out;
+        swe[j] = out;
         my_keep += (out >= 0);
         if (mask_id == 1 && out >= 0 && a.x_touched) a.x_touched[t] = 1;
     }
@@ -294,7 +298,7 @@ lss_sampler_kernel(SamplerArgs a) {
     int32_t* items = a.items[mask_id];
     int8_t* wexp = a.wexp[mask_id];
     for (int j = t_lo; j < t_hi; ++j) {
-        const int8_t e = sm.wexp[j];
+        const int8_t e = swe[j];
         if (e >= 0) {
             items[pos] = item_of(base + j);
             wexp[pos] = e;
@@ -316,10 +320,17 @@ lss_sampler_kernel(SamplerArgs a) {
 
 template <int CL>
 static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
-    const size_t smem = sizeof(SamplerSmem);
+    const int per = (2 * a.N + CL - 1) / CL;
+    const int per16 = (per + 15) & ~15;
+    const size_t smem = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
+    const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1 + 1);
     auto kern = lss_sampler_kernel<CL>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
+    static bool attr_set = false;                 // once per instantiation: the largest footprint
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask
     cfg.blockDim = dim3(kSamplerThreads);
