@@ -235,7 +235,10 @@ def dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, k
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+        tt = json.load(open(tpath)).get(args.config, {})
+        traffic = tt.get(dom)
+        if dom == GROUP and "gemm_i8_dgrad" in tt and "gemm_i8_wgrad" in tt:   # the pair: both kernels' bytes
+            traffic = tt["gemm_i8_dgrad"] + tt["gemm_i8_wgrad"]
     if kind == "ops":
         achieved = amount / avg_s / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",

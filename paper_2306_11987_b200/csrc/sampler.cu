@@ -174,24 +174,41 @@ lss_sampler_kernel(SamplerArgs a) {
         for (int i = threadIdx.x; i < a.n_zero_words; i += kSamplerThreads) a.zero_words[i] = 0u;
 
     // ---- scores -------------------------------------------------------------
+    // the inputs of 8 items are loaded before any is used (one round of load
+    // latency per 8 items, not per item: 12 items per thread at ViT sizes)
     uint64_t sum_pos = 0; uint32_t cnt_pos = 0;
-    for (int j = t_lo; j < t_hi; ++j) {
-        const int i = item_of(base + j);
-        const int h = i >= N ? 1 : 0;
-        const int t = i - h * N;
-        if (mask_id == 1 && h == 0 && a.x_touched) a.x_touched[t] = 0;   // set below for kept items
-        uint64_t w = 0;
-        if (a.mode != 2) {                                           // I4_LSS_NONE needs no scores
-            const double av = double(__ldg(a.a_sq + i));
-            double prod = av;
-            if (mask_id == 0) prod = av * double(__ldg(a.x_sqnorm + t));    // exact: < 2^53
-            const double root = __dsqrt_rn(prod);
-            w = uint64_t(root * (h == 0 ? 1048576.0 : 65536.0));   // floor(root 2^(16+4[up]))
+    for (int j0 = t_lo; j0 < t_hi; j0 += 8) {
+        int32_t av[8], bv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            av[q] = 0; bv[q] = 1;
+            const int j = j0 + q;
+            if (j < t_hi && a.mode != 2) {
+                const int i = item_of(base + j);
+                const int t = i >= N ? i - N : i;
+                av[q] = __ldg(a.a_sq + i);
+                if (mask_id == 0) bv[q] = __ldg(a.x_sqnorm + t);
+            }
         }
-        sw[j] = w;
-        scl[j] = 0;
-        sum_pos += w;
-        cnt_pos += (w > 0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int j = j0 + q;
+            if (j >= t_hi) break;
+            const int i = item_of(base + j);
+            const int h = i >= N ? 1 : 0;
+            const int t = i - h * N;
+            if (mask_id == 1 && h == 0 && a.x_touched) a.x_touched[t] = 0;   // set below for kept items
+            uint64_t w = 0;
+            if (a.mode != 2) {                                       // I4_LSS_NONE needs no scores
+                const double prod = double(av[q]) * double(bv[q]);   // exact: < 2^53
+                const double root = __dsqrt_rn(prod);
+                w = uint64_t(root * (h == 0 ? 1048576.0 : 65536.0));   // floor(root 2^(16+4[up]))
+            }
+            sw[j] = w;
+            scl[j] = 0;
+            sum_pos += w;
+            cnt_pos += (w > 0);
+        }
     }
     uint64_t Wall; uint32_t Z;
     cluster_sum(cl, sm, parity, sum_pos, cnt_pos, Wall, Z);
