@@ -100,9 +100,11 @@ typedef struct {
 
 /* Bit-split + sampling plan (Procedure LSS-MM steps 1-4).  Device buffers,
  * caller-allocated, written by bitsplit_lss:
- *   hilo     int8  [2N+1, C]   the bit-split plane: row t = 16 grad_up[t] (the high 4 bits,
- *                              scaled so that s_up = 16 s_down is folded in; |.| <= 112),
- *                              row N + t = grad_down[t] (low 4 bits), row 2N = zeros
+ *   q8       int8  [N+1, C]    the 8-bit stochastically rounded codes q = 16 hi + lo of
+ *                              grad_Y / s_down (|q| <= 119, reading Z-9); the bit split
+ *                              (Eq. 5) is q's high half hi = floor((q + 8) / 16) and low
+ *                              half lo = q - 16 hi (Z-11), split on the fly where a
+ *                              half-row is needed; row N = zeros
  *   a_sq     int32 [2N]        sum_c code^2 per half-row (unscaled codes hi, lo)
  *   amax_bits uint32 [1]       out: bf16 bit pattern of max |grad_Y|
  *   s_down   float [1]         out: s_down = amax / 119 (s_up = 16 s_down), reading Z-9
@@ -123,7 +125,7 @@ typedef struct {
  *   n_elem_x, n_elem_w         host: N_X, N_W of g(s) = 1/sqrt(Q_P N) (0 = this call's
  *                              N*D and C*D; a token-sharded caller passes the global counts) */
 typedef struct {
-    int8_t* hilo;
+    int8_t* q8;
     int32_t* a_sq;
     uint32_t* amax_bits;
     float* s_down;

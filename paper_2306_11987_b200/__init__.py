@@ -48,7 +48,7 @@ class I4FwdCache(ctypes.Structure):
 
 
 class I4LssPlan(ctypes.Structure):
-    _fields_ = [("hilo", ctypes.c_void_p), ("a_sq", ctypes.c_void_p), ("amax_bits", ctypes.c_void_p),
+    _fields_ = [("q8", ctypes.c_void_p), ("a_sq", ctypes.c_void_p), ("amax_bits", ctypes.c_void_p),
                 ("s_down", ctypes.c_void_p), ("scratch", ctypes.c_void_p), ("items_w", ctypes.c_void_p),
                 ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
@@ -246,7 +246,7 @@ class _PlanBuffers:
         import torch
         i8, i32 = torch.int8, torch.int32
         n2 = 2 * N + 128
-        self.hilo = torch.empty(2 * N + 1, C, dtype=i8, device=dev)   # row 2N: zero pad
+        self.q8 = torch.empty(N + 1, C, dtype=i8, device=dev)   # 8-bit SR codes q = 16 hi + lo; row N: zeros
         self.a_sq = torch.empty(2 * N, dtype=i32, device=dev)
         self.scalars = torch.zeros(8, dtype=i32, device=dev)      # amax_bits, s_down, count_w, count_x
         self.scratch = torch.zeros(2048, dtype=i32, device=dev)  # fused-amax block maxima
@@ -256,14 +256,14 @@ class _PlanBuffers:
         self.wexp_x = torch.empty(n2, dtype=i8, device=dev)
         self.x_touched = torch.empty(N, dtype=torch.uint8, device=dev)
         sp = self.scalars.data_ptr()
-        self.plan = I4LssPlan(hilo=self.hilo.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
+        self.plan = I4LssPlan(q8=self.q8.data_ptr(), a_sq=self.a_sq.data_ptr(), amax_bits=sp, s_down=sp + 4,
                               scratch=self.scratch.data_ptr(),
                               items_w=self.items_w.data_ptr(), wexp_w=self.wexp_w.data_ptr(), count_w=sp + 8,
                               items_x=self.items_x.data_ptr(), wexp_x=self.wexp_x.data_ptr(), count_x=sp + 12,
                               x_touched=self.x_touched.data_ptr())
 
     def views(self):
-        return {k: getattr(self, k) for k in ("hilo", "a_sq", "scalars", "scratch", "items_w", "wexp_w",
+        return {k: getattr(self, k) for k in ("q8", "a_sq", "scalars", "scratch", "items_w", "wexp_w",
                                               "items_x", "wexp_x", "x_touched")}
 
 

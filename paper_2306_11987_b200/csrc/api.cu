@@ -408,7 +408,7 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
                             cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words,
                             int32_t* det_flags = nullptr) {
     I4_RETURN_IF(check_device());
-    if (!dY || !plan || !plan->hilo || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
+    if (!dY || !plan || !plan->q8 || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
         !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x || !plan->x_touched)
         return fail(I4_ERR_ARG, "bitsplit_lss: NULL pointer");
     if (mode != I4_LSS_BERNOULLI && mode != I4_LSS_KEEP_POSITIVE && mode != I4_LSS_NONE)
@@ -419,9 +419,9 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
         return fail(I4_ERR_SHAPE, "bitsplit_lss: N = %lld exceeds %lld tokens per call (reading Z-21)", (long long)N,
                     (long long)kMaxBwdTokens);
     if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
-    if (!aligned16(dY) || !aligned16(plan->hilo)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
+    if (!aligned16(dY) || !aligned16(plan->q8)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
     I4_LAUNCH(i4::launch_grad_split(static_cast<const uint16_t*>(dY), N, C, plan->scratch, seed, call_id, token_offset,
-                                    plan->hilo, plan->a_sq, plan->s_down, plan->amax_bits, s), "grad_split", s);
+                                    plan->q8, plan->a_sq, plan->s_down, plan->amax_bits, s), "grad_split", s);
     i4::SamplerArgs a{};
     a.a_sq = plan->a_sq;
     a.x_sqnorm = x_sqnorm;
@@ -541,7 +541,7 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
     const BwdWs w = carve_bwd_ws(ws, N, D, C);
     {
         i4::CompactArgs ca{};
-        ca.plane = plan->hilo; ca.xq = cache->xq;
+        ca.q8 = plan->q8; ca.xq = cache->xq;
         ca.N = int32_t(N); ca.C = int32_t(C); ca.D = int32_t(D);
         ca.items_x = plan->items_x; ca.count_x = plan->count_x;
         ca.items_w = plan->items_w; ca.wexp_w = plan->wexp_w; ca.count_w = plan->count_w;

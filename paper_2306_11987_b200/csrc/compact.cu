@@ -13,11 +13,12 @@ namespace i4 {
 constexpr int kGroup = 8;                 // 16-byte loads in flight per lane
 
 // One launch builds all three compacted operands; one warp per output row:
-//   A_X[j, :] = plane[items_x[j], :]              (C bytes; grad_X GEMM A, K-major)
-//   A_W[j, :] = plane[items_w[j], :]              (C bytes; grad_W GEMM A, MN-major;
+//   A_X[j, :] = half h of Q[t, :] for item (h, t)  (C bytes; grad_X GEMM A, K-major):
+//               16 hi (h = 0) or lo (h = 1), split from the 8-bit codes on the fly
+//   A_W[j, :] = the same for items_w[j]           (C bytes; grad_W GEMM A, MN-major;
 //                                                  skipped when the lists are equal)
 //   B_W[j, :] = 2^wexp_w[j] X_hat[t(items_w[j]), :]   (D bytes, |.| <= 112; grad_W GEMM B)
-// The plane rows hold 16 hi or lo, so acc[c, d] = sum_j A_W[j, c] B_W[j, d] is the
+// The A rows hold 16 hi or lo, so acc[c, d] = sum_j A_W[j, c] B_W[j, d] is the
 // weighted bit-split product with s_up = 16 s_down folded in (reading Z-17).
 // Rows past a list's count, up to its multiple of 128, are zero (the MMA pad).
 __device__ __forceinline__ uint4 scale_i8x16(uint4 u, int mul) {
@@ -27,8 +28,16 @@ __device__ __forceinline__ uint4 scale_i8x16(uint4 u, int mul) {
     return u;
 }
 
+// bit split of 4 packed 8-bit codes q (reading Z-11): t = (q + 128) + 8 per byte
+// (no carries: q + 136 <= 255); 16 hi = (t & 0xF0) ^ 0x80, lo = ((t & 0x0F) + 0x78) ^ 0x80
+__device__ __forceinline__ uint32_t split_word(uint32_t q, int half) {
+    const uint32_t t = (q ^ 0x80808080u) + 0x08080808u;
+    return half == 0 ? ((t & 0xF0F0F0F0u) ^ 0x80808080u) : (((t & 0x0F0F0F0Fu) + 0x78787878u) ^ 0x80808080u);
+}
+
+// half: -1 copy (optionally scaled by mul), 0 / 1: the high (16 hi) / low half of the codes
 __device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t* __restrict__ dst, int n, int lane,
-                                         bool zero, int mul) {
+                                         bool zero, int mul, int half = -1) {
     for (int c0 = 0; c0 < n; c0 += 512 * kGroup) {
         uint4 u[kGroup];
 #pragma unroll
@@ -39,7 +48,13 @@ __device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t*
 #pragma unroll
         for (int gq = 0; gq < kGroup; ++gq) {
             const int c = c0 + 512 * gq + lane * 16;
-            if (c < n) *reinterpret_cast<uint4*>(dst + c) = mul == 1 ? u[gq] : scale_i8x16(u[gq], mul);
+            if (c >= n) continue;
+            uint4 v = u[gq];
+            if (half >= 0)
+                v = make_uint4(split_word(v.x, half), split_word(v.y, half), split_word(v.z, half), split_word(v.w, half));
+            else if (mul != 1)
+                v = scale_i8x16(v, mul);
+            *reinterpret_cast<uint4*>(dst + c) = v;
         }
     }
 }
@@ -83,12 +98,14 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
         } else if (j < pad_x) {
             const int32_t item = __ldg(a.items_x + j);
             const bool pad = item >= two_n;
-            copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1);
+            const int h = item >= a.N ? 1 : 0;
+            copy_row(a.q8 + int64_t(pad ? 0 : item - h * a.N) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1, h);
         } else if (j < seg_bw) {
             const int64_t r = j - pad_x;
             const int32_t item = __ldg(a.items_w + r);
             const bool pad = item >= two_n;
-            copy_row(a.plane + int64_t(pad ? 0 : item) * a.C, a.a_w + r * a.C, a.C, lane, pad, 1);
+            const int h = item >= a.N ? 1 : 0;
+            copy_row(a.q8 + int64_t(pad ? 0 : item - h * a.N) * a.C, a.a_w + r * a.C, a.C, lane, pad, 1, h);
         } else {
             const int64_t r = j - seg_bw;
             const int32_t item = __ldg(a.items_w + r);

@@ -34,7 +34,7 @@ constexpr int kGradSplitMaxBlocks = 2048;   // block-max scratch words the plan 
 int grad_split_stamps(unsigned long long* host, int n);
 int sampler_stamps(unsigned long long* host, int enable);   // timing experiment   // timing experiment (I4_BS_EXP=8)
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
-                              uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
+                              uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
                               uint32_t* amax_out, cudaStream_t s);
 
 // sampler.cu ------------------------------------------------------------------
@@ -58,7 +58,7 @@ cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
 
 // compact.cu ------------------------------------------------------------------
 struct CompactArgs {
-    const int8_t* plane;      // [2N+1, C] bit-split plane (16 hi / lo / zero row)
+    const int8_t* q8;         // [N+1, C] 8-bit SR codes q = 16 hi + lo (row N: zeros)
     const int8_t* xq;         // [N, D] X_hat
     int32_t N, C, D;
     const int32_t* items_x; const int32_t* count_x;

@@ -4,8 +4,8 @@
 //                    thread per 32-column block, Hadamard order k compile-time,
 //                    butterflies and scaling on fp32 pairs (FADD2 / FMUL2)
 //   grad_split     : B1 + B2 -- per-tensor max |grad_Y| (reading
-//                    Z-9), then Philox SR to the 8-bit code, split into high /
-//                    low 4-bit planes, per-row integer norms (PAPER.md:234-239,
+//                    Z-9), then Philox SR to the 8-bit code q (stored), its high /
+//                    low 4-bit halves' per-row integer norms (PAPER.md:234-239,
 //                    :680); one cooperative launch with one grid barrier
 #include <cstdlib>
 
@@ -246,9 +246,10 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 //            high word = floor(a) (+1 when frac's threshold wraps), low word =
 //            T = ceil(frac(a) 2^32) mod 2^32; q = sign(v) (hi(A) + [u < lo(A)])
 //            with u the element's Philox word: P(round up) = frac(a) exactly
-//            (reading Z-10); hi = floor((q+8)/16), lo = q - 16 hi (Z-11); the
-//            plane stores 16 hi (s_up = 16 s_down folded in) and lo;
-//            per-row sum hi^2, sum lo^2 (the leverage scores' INT data).
+//            (reading Z-10); the code plane stores q itself; hi = floor((q+8)/16),
+//            lo = q - 16 hi (Z-11) are formed in registers for the per-row
+//            sum hi^2, sum lo^2 (the leverage scores' INT data) and
+//            split again on the fly where a half-row is an operand (compact).
 //            grad_Y is re-read right after phase 1, mostly from L2.
 // ---------------------------------------------------------------------------
 constexpr int kSplitThreads = 256;
@@ -330,7 +331,7 @@ __device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const P
 //   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
 template <bool CLAMP>
 __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float R32,
-                                             uint2& ph, uint2& pl, int& shi, int& slo) {
+                                             uint2& pq, int& shi, int& slo) {
     const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t mag[8];
@@ -352,7 +353,13 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0,
         const uint32_t lo = ((t & 0x0F0F0F0Fu) + 0x78787878u) ^ 0x80808080u;
         shi = __dp4a(int(hi16), int(hi16), shi);
         slo = __dp4a(int(lo), int(lo), slo);
-        if (h == 0) { ph.x = hi16; pl.x = lo; } else { ph.y = hi16; pl.y = lo; }
+        // q = sign * magnitude per byte: two's complement of the nonzero negative
+        // bytes only (a "-0" byte would carry into its neighbour): mag <= 119, so
+        // mag + 0x7F sets bit 7 exactly for nonzero magnitudes, without carries
+        const uint32_t nz = (((M + 0x7F7F7F7Fu) & 0x80808080u) >> 7) * 0xFFu;
+        const uint32_t Sn = S & nz;
+        const uint32_t q = (M ^ Sn) + (Sn & 0x01010101u);
+        if (h == 0) pq.x = q; else pq.y = q;
     }
 }
 
@@ -401,8 +408,8 @@ __device__ __forceinline__ void load_unit(const uint4* src, int64_t un, uint4 (&
 // split, plane stores, norms into shi / slo.
 template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG>
 __device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, const float R32, const PhiloxKeys& keys,
-                                           uint32_t call_id, uint64_t tbase, int8_t* __restrict__ hilo,
-                                           int8_t* __restrict__ lo_plane, int& shi, int& slo) {
+                                           uint32_t call_id, uint64_t tbase, int8_t* __restrict__ q8,
+                                           int& shi, int& slo) {
     const int lane = lane_id();
 #pragma unroll
     for (int gi = 0; gi < G; ++gi) {
@@ -415,10 +422,9 @@ __device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, co
         } else {
             sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
         }
-        uint2 ph, pl;
-        split_chunk8<CLAMP>(cur[gi], p0, p1, R32, ph, pl, shi, slo);
-        *reinterpret_cast<uint2*>(hilo + flat) = ph;
-        *reinterpret_cast<uint2*>(lo_plane + flat) = pl;
+        uint2 pq;
+        split_chunk8<CLAMP>(cur[gi], p0, p1, R32, pq, shi, slo);
+        *reinterpret_cast<uint2*>(q8 + flat) = pq;
     }
 }
 
@@ -438,12 +444,11 @@ __device__ __forceinline__ void flush_norms(int& shi, int& slo, int32_t* __restr
 template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG = false>
 __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int64_t N, int C, const float R32,
                                             const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset,
-                                            int8_t* __restrict__ hilo, int32_t* __restrict__ a_sq, int64_t u0,
+                                            int8_t* __restrict__ q8, int32_t* __restrict__ a_sq, int64_t u0,
                                             int64_t u1, uint4 (&buf)[G]) {
     const int upr = C / (256 * G);                                    // units per row
     const uint4* src = reinterpret_cast<const uint4*>(g) + lane_id();
     const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);       // Z-20: L = (t0 + t) C + c
-    int8_t* lo_plane = hilo + N * int64_t(C);
     int shi = 0, slo = 0;
     // range [u0, u1): its first unit's loads were issued before the phase-1 wait
     if (u0 < u1) {
@@ -454,7 +459,7 @@ __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int6
 #pragma unroll
             for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
             if (un + 1 < u1) load_unit<G>(src, un + 1, buf);        // next unit's loads in flight
-            split_unit<G, CLAMP, C1Z, FAKE_RNG>(cur, un, R32, keys, call_id, tbase, hilo, lo_plane, shi, slo);
+            split_unit<G, CLAMP, C1Z, FAKE_RNG>(cur, un, R32, keys, call_id, tbase, q8, shi, slo);
             if (++seg == upr || un + 1 == u1) {                       // row done (or range end): flush
                 flush_norms(shi, slo, a_sq, N, row);
                 seg = 0; ++row;
@@ -475,7 +480,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <int G, bool C1Z>
 __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ scratch,
-                  const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ hilo,
+                  const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
                   int exp_flags) {
     const int lane = lane_id();
@@ -550,26 +555,26 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     }
 
     // ---- phase 2: SR + bit split ------------------------------------------
-    if (blockIdx.x == gridDim.x - 1)                      // plane row 2N: the all-zero gather pad
+    if (blockIdx.x == gridDim.x - 1)                      // code row N: the all-zero pad row
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
-            *reinterpret_cast<uint4*>(hilo + 2 * N * C + c) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(q8 + N * C + c) = make_uint4(0, 0, 0, 0);
     if constexpr (G > 0) {
         if (exp_flags & 3) {                              // timing experiments: phase 1 only / no Philox
             if (exp_flags & 2)
                 split_units<G, false, C1Z, true>(g, N, C, __fmul_rn(r8, 4294967296.0f), keys, call_id, token_offset,
-                                                 hilo, a_sq, pu0, pu1, pbuf);
+                                                 q8, a_sq, pu0, pu1, pbuf);
             depart(scratch);
             return;
         }
         if (zero) {                                       // all-zero grad_Y: codes 0, norms 0 (zeroed above)
-            split_units<G, false, C1Z>(g, N, C, 0.0f, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+            split_units<G, false, C1Z>(g, N, C, 0.0f, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         } else {
             const float R32 = __fmul_rn(r8, 4294967296.0f);
             // only elements with |g| = amax can land above 119 (fl32(amax r8) may round up by an ulp)
             if (__fmul_rn(amax, r8) > 119.0f)
-                split_units<G, true, C1Z>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+                split_units<G, true, C1Z>(g, N, C, R32, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
             else
-                split_units<G, false, C1Z>(g, N, C, R32, keys, call_id, token_offset, hilo, a_sq, pu0, pu1, pbuf);
+                split_units<G, false, C1Z>(g, N, C, R32, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         }
         if (stamp && lane == 0) atomicMax(&g_gs_stamp[4][blockIdx.x], gtimer());
         depart(scratch);
@@ -581,8 +586,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     const int nch = (C + 255) >> 8;
     for (int64_t row = warp0; row < N; row += wstride) {
         const uint16_t* gr = g + row * C;
-        int8_t* hr = hilo + row * C;
-        int8_t* lr = hilo + (N + row) * C;
+        int8_t* qr = q8 + row * C;
         const uint64_t tglob = uint64_t(token_offset + row);
         int shi = 0, slo = 0;
         for (int g0 = 0; g0 < nch; g0 += kBsGroup) {
@@ -612,11 +616,11 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                     const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
                     qv[i] = sv < 0.0f ? -mag : mag;
                 }
-                // bit split on 4 packed codes at a time: t = (q + 128) + 8 per byte (no
-                // carries: q + 136 <= 255); hi = floor((q + 8) / 16) = (t >> 4) - 8, so the
-                // high plane byte 16 hi = (t & 0xF0) - 128 = (t & 0xF0) ^ 0x80; the low
-                // nibble t & 15 = lo + 8, i.e. lo in 4-bit two's complement after ^ 8,
-                // sign-extended to a byte by adding 0xF0 when its bit 3 is set
+                // bit split (for the norms) on 4 packed codes at a time: t = (q + 128) + 8 per
+                // byte (no carries: q + 136 <= 255); hi = floor((q + 8) / 16) = (t >> 4) - 8,
+                // so 16 hi = (t & 0xF0) - 128 = (t & 0xF0) ^ 0x80; the low nibble t & 15 =
+                // lo + 8, i.e. lo in 4-bit two's complement after ^ 8, sign-extended to a
+                // byte by adding 0xF0 when its bit 3 is set
                 const uint2 qp = pack8_i8(qv);
                 uint32_t ph[2], pl[2];
 #pragma unroll
@@ -629,8 +633,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 // sums of squares: the high plane holds 16 hi, so its dp4a sum is 256 sum hi^2
                 shi = __dp4a(int(ph[0]), int(ph[0]), __dp4a(int(ph[1]), int(ph[1]), shi));
                 slo = __dp4a(int(pl[0]), int(pl[0]), __dp4a(int(pl[1]), int(pl[1]), slo));
-                *reinterpret_cast<uint2*>(hr + col) = make_uint2(ph[0], ph[1]);
-                *reinterpret_cast<uint2*>(lr + col) = make_uint2(pl[0], pl[1]);
+                *reinterpret_cast<uint2*>(qr + col) = qp;          // the 8-bit code plane Q
             }
         }
 #pragma unroll
@@ -663,7 +666,7 @@ int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
 
 template <int G, bool C1Z>
 static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
-                                       uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq,
+                                       uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
                                        float* s_down, uint32_t* amax_out, cudaStream_t s) {
     static const int exp_flags = getenv("I4_BS_EXP") ? atoi(getenv("I4_BS_EXP")) : 0;   // timing experiments only
     int blocks = grad_split_max_blocks<G, C1Z>();
@@ -680,31 +683,31 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
     cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id,
-                                       token_offset, hilo, a_sq, s_down, amax_out, exp_flags);
+                                       token_offset, q8, a_sq, s_down, amax_out, exp_flags);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id, token_offset,
-                               hilo, a_sq, s_down, amax_out, exp_flags);
+                               q8, a_sq, s_down, amax_out, exp_flags);
     }
     return e;
 }
 
 template <int G>
 static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint32_t* block_max,
-                                       const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* hilo,
+                                       const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* q8,
                                        int32_t* a_sq, float* s_down, uint32_t* amax_out, cudaStream_t s) {
     // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
     const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
     if (c1z)
-        return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, hilo, a_sq, s_down,
+        return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
                                             amax_out, s);
-    return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, hilo, a_sq, s_down,
+    return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
                                          amax_out, s);
 }
 
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
-                              uint32_t call_id, int64_t token_offset, int8_t* hilo, int32_t* a_sq, float* s_down,
+                              uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
                               uint32_t* amax_out, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
     const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
@@ -713,7 +716,7 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     const bool generic = env && env[0] == '1';
     const char* genv = getenv("I4_BS_G");                 // experiment switch: force the unit size
     const int gforce = genv ? atoi(genv) : 0;
-#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s)
+#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, s)
     // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
     // measured equal or slower), else 3, 4, 1
     if (!generic && (gforce == 0 || gforce == 2) && C % 512 == 0) return I4_GS(2);
@@ -721,7 +724,7 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
     if (!generic && (gforce == 0 || gforce == 4) && C % 1024 == 0) return I4_GS(4);
     if (!generic && C % 256 == 0) return I4_GS(1);
 #undef I4_GS
-    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, hilo, a_sq, s_down, amax_out, s);
+    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, s);
 }
 
 // debug export for the timing experiment: copies the stamps of the last

@@ -164,9 +164,9 @@ def _check_backward(layer, g, s_x, s_w, k, dX, dW, mode, call_id=3, token_offset
     N, C = g.shape
     # (i) bit split: bit-exact planes and norms
     bs = o_bs.bit_split(g, synth.PHILOX_SEED, call_id, token_offset)
-    hilo = layer.hilo.cpu().numpy().astype(np.int64)
-    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64))       # plane stores 16 hi
-    assert np.array_equal(hilo[N:2 * N], bs["lo"]) and not hilo[2 * N].any()
+    q8 = layer.q8.cpu().numpy().astype(np.int64)
+    assert np.array_equal(q8[:N], bs["q"]) and not q8[N].any()             # 8-bit codes; pad row
+    assert np.array_equal(16 * bs["hi"].astype(np.int64) + bs["lo"], bs["q"])
     assert np.array_equal(layer.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
     assert layer.s_down().cpu().numpy()[0] == bs["s_down"]
     assert np.array_equal(fwd["x_sq"], (fwd["xq"].astype(np.int64) ** 2).sum(1))
@@ -247,10 +247,9 @@ def test_shard_invariance_of_random_streams():
     g_half[0, 0] = g[0, 0]
     _, _, _, _, full, _, _, _ = _bwd_case(N, D, C, k, g=g)
     _, _, _, _, half, _, _, _ = _bwd_case(N // 2, D, C, k, g=g_half, token_offset=N // 2)
-    hf = full.hilo.cpu().numpy()
-    hh = half.hilo.cpu().numpy()
+    hf = full.q8.cpu().numpy()
+    hh = half.q8.cpu().numpy()
     assert np.array_equal(hf[N // 2 + 1:N], hh[1:N // 2])
-    assert np.array_equal(hf[N + N // 2 + 1:2 * N], hh[N // 2 + 1:N])
 
 
 def test_api_errors_are_loud():
@@ -286,8 +285,7 @@ def test_full_size_sampled_parity(cfg):
     assert rel_frob(Y.cpu().numpy()[rows], y_ref) < FROB_TOL
     # backward: full sampler parity, outputs on sampled tokens / channels
     bs = o_bs.bit_split(g, synth.PHILOX_SEED, 3, 0)
-    hilo = layer.hilo.cpu().numpy().astype(np.int64)
-    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64)) and np.array_equal(hilo[N:2 * N], bs["lo"])
+    assert np.array_equal(layer.q8.cpu().numpy().astype(np.int64)[:N], bs["q"])
     x_sq = layer.x_sqnorm.cpu().numpy().astype(np.int64)
     mw = o_lss.sample_weight_mask(bs["a_sq"], x_sq, synth.PHILOX_SEED, 3, 0)
     mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 3, 0)
@@ -338,9 +336,8 @@ def test_bitsplit_unit_paths(C, clamp):
     xsq = torch.ones(N, dtype=torch.int32, device="cuda")
     mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, 9, 123, o_lss.MODE_BERNOULLI, plan.plan)
     torch.cuda.synchronize()
-    hilo = plan.hilo.cpu().numpy().astype(np.int64)
-    assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64))
-    assert np.array_equal(hilo[N:2 * N], bs["lo"]) and not hilo[2 * N].any()
+    q8 = plan.q8.cpu().numpy().astype(np.int64)
+    assert np.array_equal(q8[:N], bs["q"]) and not q8[N].any()
     assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
 
 
@@ -358,7 +355,5 @@ def test_bitsplit_repeated_calls_reuse_counters():
         bs = o_bs.bit_split(g, synth.PHILOX_SEED, it, 0)
         mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, it, 0, o_lss.MODE_BERNOULLI, plan.plan)
         torch.cuda.synchronize()
-        hilo = plan.hilo.cpu().numpy().astype(np.int64)
-        assert np.array_equal(hilo[:N], 16 * bs["hi"].astype(np.int64)), it
-        assert np.array_equal(hilo[N:2 * N], bs["lo"]), it
+        assert np.array_equal(plan.q8.cpu().numpy().astype(np.int64)[:N], bs["q"]), it
         assert not plan.scratch.cpu().numpy()[-8:].any(), "counters not returned to zero"
