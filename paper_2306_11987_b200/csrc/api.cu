@@ -212,8 +212,8 @@ struct Operand { const int8_t* p; int64_t rows, inner, pitch; bool gather = fals
 // A_alt (optional): a second A the kernel may read instead, chosen on the device
 // (GemmArgs::alt_*; the grad_W GEMM reads the grad_X GEMM's A when the lists match)
 i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s, int sms = 0,
-               const Operand* A_alt = nullptr) {
-    CUtensorMap ta, tb, tc, ta2;
+               const Operand* A_alt = nullptr, const Operand* A_dense = nullptr, const Operand* B_dense = nullptr) {
+    CUtensorMap ta, tb, tc, ta2, ta3, tb2;
     const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
     bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), A.gather ? 1u : 128u) &&
               make_tmap_i8(&tb, B.p, uint64_t(B.inner), uint64_t(B.rows), uint64_t(B.pitch),
@@ -221,12 +221,19 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
     if (A_alt) ok = ok && make_tmap_i8(&ta2, A_alt->p, uint64_t(A_alt->inner), uint64_t(A_alt->rows),
                                        uint64_t(A_alt->pitch), 128u);
     else ta2 = ta;
+    // dense-mode operands (device-selected): A_dense MN-major like A, B_dense MN-major like B
+    if (A_dense) ok = ok && make_tmap_i8(&ta3, A_dense->p, uint64_t(A_dense->inner), uint64_t(A_dense->rows),
+                                         uint64_t(A_dense->pitch), 128u);
+    else ta3 = ta;
+    if (B_dense) ok = ok && make_tmap_i8(&tb2, B_dense->p, uint64_t(B_dense->inner), uint64_t(B_dense->rows),
+                                         uint64_t(B_dense->pitch), 128u);
+    else tb2 = tb;
     if (args.epi == i4::EPI_DGRAD) tc = ta;                 // grad_X is written with red.add, no map
     else ok = ok && make_tmap_out(&tc, args.out, args.out_bf16 != 0, args.epi == i4::EPI_INT32,
                                   uint64_t(args.Nn), uint64_t(args.M));
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
-    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2};
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2};
     I4_LAUNCH(i4::launch_gemm(maps, args, sms > 0 ? sms : device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
@@ -586,8 +593,10 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         g.partial = w.part_x; g.flags = w.flags_x;
         g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
         if (want_lsq) { g.delta = cache->x_delta; g.lsq_part = w.lsq_x; }
+        g.dense_flag = w.det + 1;                // grad_X mask deterministic: rows = tokens of Q
+        const Operand q_rows{plan->q8, N + 1, C, C};
         I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s,
-                          px > 0 ? 2 * px : 0));
+                          px > 0 ? 2 * px : 0, &q_rows));
     }
     // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
     {
@@ -606,9 +615,13 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         if (px > 0 && getenv("I4_BWD_WSPLIT")) g.max_splits = atoi(getenv("I4_BWD_WSPLIT"));   // experiment
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
         g.alt_det_flags = w.det; g.alt_count_w = plan->count_w; g.alt_count_x = plan->count_x;
+        g.dense_flag = w.det;                    // grad_W mask deterministic: K = tokens, A = Q, B = X_hat
+        g.n_tokens = int32_t(N);
         const Operand a_x_view{w.a_x, 2 * N + 128, C, C};   // = A_W when the two item lists are equal
+        const Operand q_k{plan->q8, N + 1, C, C};            // Q as the MN-major A (rows = K = tokens)
+        const Operand xq_k{cache->xq, N, D, D};             // X_hat as the MN-major B
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
-                          px > 0 ? device_info().sms - 2 * px : 0, &a_x_view));
+                          px > 0 ? device_info().sms - 2 * px : 0, &a_x_view, &q_k, &xq_k));
     }
     if (px > 0) {
         g_trace_group = false;

@@ -69,22 +69,29 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     pdl_trigger();
     pdl_wait();                                               // counts / lists of the sampler
     const int64_t cnt_x = __ldg(a.count_x);
-    const int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
+    int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
     const int64_t pad_w = (int64_t(__ldg(a.count_w)) + 127) & ~int64_t(127);
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int64_t n_straddle = (cnt_x + 31) / 32;            // candidate positions 31, 63, ...
-    // equal item lists: the grad_W GEMM reads A_X (its A map is chosen on the device
-    // by the same test), so the A_W copy is skipped
-    const int64_t pad_aw = lists_equal(a.det_flags, a.count_w, a.count_x) ? 0 : pad_w;
+    // deterministic masks (the sampler's flags; the GEMMs pick their operands by the
+    // same tests): grad_X dense -> no A_X rows and no zero rows (its GEMM writes every
+    // token row from Q); grad_W dense -> no A_W / B_W rows (Q and X_hat are read);
+    // equal item lists -> the grad_W GEMM reads A_X, no A_W copy
+    const bool dense_x = a.det_flags != nullptr && __ldg(a.det_flags + 1) != 0;
+    const bool dense_w = a.det_flags != nullptr && __ldg(a.det_flags) != 0;
+    const int64_t n_straddle = dense_x ? 0 : (cnt_x + 31) / 32;   // candidate positions 31, 63, ...
+    if (dense_x) pad_x = 0;
+    const int64_t pad_aw = (dense_w || lists_equal(a.det_flags, a.count_w, a.count_x)) ? 0 : pad_w;
+    const int64_t pad_bw = dense_w ? 0 : pad_w;
     const int64_t seg_bw = pad_x + pad_aw;                   // first B_W row job
-    const int64_t total = seg_bw + pad_w + a.N + n_straddle;
+    const int64_t n_zero = dense_x ? 0 : a.N;
+    const int64_t total = seg_bw + pad_bw + n_zero + n_straddle;
     const int two_n = 2 * a.N;
     for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
-        if (j >= seg_bw + pad_w) {
+        if (j >= seg_bw + pad_bw) {
             // grad_X rows the GEMM epilogue does not store: tokens without a kept
             // item, and tokens whose two items straddle a 32-row group (both red.add)
-            const int64_t r = j - seg_bw - pad_w;
+            const int64_t r = j - seg_bw - pad_bw;
             if (r < a.N) {
                 if (__ldg(a.x_touched + r) == 0) zero_row(a.dx, r, a.D, a.dx_bf16, lane);
             } else {

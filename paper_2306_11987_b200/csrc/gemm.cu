@@ -153,7 +153,8 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(EpiShape<BN, EPI, kh_ch(KH)>::THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2, const GemmArgs g) {
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+               const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
     constexpr int CH = kh_ch(KH);
     using Epi = EpiShape<BN, EPI, CH>;
     constexpr int kEpiWarps = Epi::WARPS;
@@ -179,7 +180,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
-        if (EPI == EPI_WGRAD) tma_prefetch_desc(&tmA2);
+        if (EPI == EPI_WGRAD || EPI == EPI_DGRAD) tma_prefetch_desc(&tmA2);
+        if (EPI == EPI_WGRAD) { tma_prefetch_desc(&tmA3); tma_prefetch_desc(&tmB2); }
         tma_prefetch_desc(&tmB);
         if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -195,8 +197,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     pdl_wait();                                  // operands / metadata of the previous kernels
 
     // problem size (possibly data-dependent, so read after the PDL wait) and work units
-    const int M = g.m_dev ? __ldg(g.m_dev) : g.M;
-    const int K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
+    // dense mode (the mask kept every nonzero item with weight 1, reading Z-12): the
+    // operands are the 8-bit code plane Q and X_hat themselves, one row per token
+    const bool dense = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr && __ldg(g.dense_flag) != 0;
+    const int M = (EPI == EPI_DGRAD && dense) ? g.n_tokens : (g.m_dev ? __ldg(g.m_dev) : g.M);
+    const int K = (EPI == EPI_WGRAD && dense) ? ((g.n_tokens + kBK - 1) / kBK) * kBK
+                                                : (g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K);
     const int m_tiles = (M + BMP - 1) / BMP;
     const int n_tiles = (g.Nn + BN - 1) / BN;
     const int T = m_tiles * n_tiles;
@@ -217,7 +223,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const bool gather = g.a_gather != nullptr;
         // grad_W: the A operand may be the grad_X GEMM's (identical item lists)
         const CUtensorMap* pA = &tmA;
-        if (EPI == EPI_WGRAD && lists_equal(g.alt_det_flags, g.alt_count_w, g.alt_count_x)) pA = &tmA2;
+        const CUtensorMap* pB = &tmB;
+        if (EPI == EPI_DGRAD && dense) pA = &tmA2;                     // Q, K-major
+        if (EPI == EPI_WGRAD) {
+            if (dense) { pA = &tmA3; pB = &tmB2; }                    // Q and X_hat, MN-major
+            else if (lists_equal(g.alt_det_flags, g.alt_count_w, g.alt_count_x)) pA = &tmA2;
+        }
         const int gcount = gather ? __ldg(g.gather_count) : 0;
         auto load_idx4 = [&](int r) {
             int4 v;
@@ -260,9 +271,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if (B_MN) {
 #pragma unroll
                             for (int j = 0; j < BNC / 128; ++j)
-                                tma_load_2d_2sm(b_dst + j * 128 * kBK, &tmB, fb, nb + 128 * j, kb * kBK);
+                                tma_load_2d_2sm(b_dst + j * 128 * kBK, pB, fb, nb + 128 * j, kb * kBK);
                         } else {
-                            tma_load_2d_2sm(b_dst, &tmB, fb, kb * kBK, nb);
+                            tma_load_2d_2sm(b_dst, pB, fb, kb * kBK, nb);
                         }
                     } else {
                         if (!gather) {
@@ -272,9 +283,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if (B_MN) {
 #pragma unroll
                             for (int j = 0; j < BNC / 128; ++j)
-                                tma_load_2d(b_dst + j * 128 * kBK, &tmB, &full[stage], nb + 128 * j, kb * kBK);
+                                tma_load_2d(b_dst + j * 128 * kBK, pB, &full[stage], nb + 128 * j, kb * kBK);
                         } else {
-                            tma_load_2d(b_dst, &tmB, &full[stage], kb * kBK, nb);
+                            tma_load_2d(b_dst, pB, &full[stage], kb * kBK, nb);
                         }
                     }
                 }
@@ -347,7 +358,9 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int tl = u % T;
                 const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
                 x.rw = rw;
-                if (rw < M) {
+                if (rw < M && dense) {
+                    x.item = rw;                       // token rw, weight 1, never paired
+                } else if (rw < M) {
                     x.item = __ldg(g.items + rw);
                     x.eword = int(__ldg(reinterpret_cast<const uint32_t*>(g.wexp + (rw & ~3))));
                     if (lane == 31 && rw + 1 < M) x.edge = __ldg(g.items + rw + 1);
@@ -422,8 +435,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 int pv = __shfl_up_sync(0xFFFFFFFFu, ri_cur.item, 1);
                 if (lane == 31) nx = ri_cur.edge;
                 if (lane == 0) pv = ri_cur.edge;
-                if (row + 1 >= M) nx = two_n;
-                if (row == 0) pv = two_n;
+                if (row + 1 >= M || dense) nx = two_n;
+                if (row == 0 || dense) pv = two_n;
                 row_e = e;
                 rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
                 const int inext = valid ? nx : two_n;
@@ -656,7 +669,9 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cu
     cfg.numAttrs = add_pdl_attr(attr, 1);
     return cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(m.a),
                               *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c),
-                              *reinterpret_cast<const CUtensorMap*>(m.a2 ? m.a2 : m.a), g);
+                              *reinterpret_cast<const CUtensorMap*>(m.a2 ? m.a2 : m.a),
+                              *reinterpret_cast<const CUtensorMap*>(m.a3 ? m.a3 : m.a),
+                              *reinterpret_cast<const CUtensorMap*>(m.b2 ? m.b2 : m.b), g);
 }
 
 template <int EPI, int KH, bool A_MN, bool B_MN>

@@ -69,7 +69,8 @@ struct CompactArgs {
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]
-    const int32_t* det_flags; // optional [2] (sampler): both set + equal counts -> lists equal, A_W = A_X
+    const int32_t* det_flags; // optional [2] (sampler): both set + equal counts -> lists equal, A_W = A_X;
+                              // [1] set: grad_X GEMM dense (no A_X, no zero rows); [0] set: grad_W dense
 };
 // the grad_W list equals the grad_X list: both masks deterministic, equal counts
 __device__ __forceinline__ bool lists_equal(const int32_t* det_flags, const int32_t* count_w, const int32_t* count_x) {
@@ -112,13 +113,17 @@ struct GemmArgs {
     double* lsq_part;         // [gridDim.x * 8] fp64 partials (entries of absent CTAs pre-zeroed)
     // wgrad: read A through the alternate map (the grad_X GEMM's A) when lists_equal(...)
     const int32_t* alt_det_flags; const int32_t* alt_count_w; const int32_t* alt_count_x;
+    // dgrad / wgrad: if *dense_flag != 0 the mask is deterministic (every nonzero item kept
+    // with weight 1): dgrad reads A = Q (map a2, M = n_tokens rows = tokens), wgrad reads
+    // A = Q and B = X_hat (maps a3, b2, K = n_tokens)
+    const int32_t* dense_flag;
 };
 constexpr int kSplitMaxTiles = 96;        // workspace tiles reserved for split-K
 constexpr int kSplitMaxK = 4;
 size_t gemm_split_partial_bytes();        // bytes of one GEMM's split-K partial workspace
 size_t gemm_split_flag_words();
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
-struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; };   // CUtensorMap* (host)
+struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; const void* a3; const void* b2; };   // CUtensorMap* (host)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
 int gemm_block_n(int Nn, bool b_mn);
 
