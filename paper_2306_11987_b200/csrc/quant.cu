@@ -353,12 +353,9 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0,
         const uint32_t lo = ((t & 0x0F0F0F0Fu) + 0x78787878u) ^ 0x80808080u;
         shi = __dp4a(int(hi16), int(hi16), shi);
         slo = __dp4a(int(lo), int(lo), slo);
-        // q = sign * magnitude per byte: two's complement of the nonzero negative
-        // bytes only (a "-0" byte would carry into its neighbour): mag <= 119, so
-        // mag + 0x7F sets bit 7 exactly for nonzero magnitudes, without carries
-        const uint32_t nz = (((M + 0x7F7F7F7Fu) & 0x80808080u) >> 7) * 0xFFu;
-        const uint32_t Sn = S & nz;
-        const uint32_t q = (M ^ Sn) + (Sn & 0x01010101u);
+        // q = 16 hi + lo per byte (fits int8), added without cross-byte carries:
+        // low 7 bits summed, bit 7 = xor of the operands' bit 7 and the low carry
+        const uint32_t q = ((hi16 & 0x7F7F7F7Fu) + (lo & 0x7F7F7F7Fu)) ^ ((hi16 ^ lo) & 0x80808080u);
         if (h == 0) pq.x = q; else pq.y = q;
     }
 }
