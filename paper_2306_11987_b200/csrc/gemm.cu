@@ -93,7 +93,10 @@ __device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
 // CTAs cannot deadlock.
 // The partial-sum hand-over costs about kSplitHandoverKb k-blocks of MMA time
 // (measured: a 2-way split of a 32-k-block grad_W took longer than none).
-constexpr int kSplitHandoverKb = 24;
+#ifndef I4_SPLIT_HANDOVER_KB
+#define I4_SPLIT_HANDOVER_KB 24
+#endif
+constexpr int kSplitHandoverKb = I4_SPLIT_HANDOVER_KB;
 __device__ __forceinline__ int choose_splits(int tiles, int pairs, int nk, int max_splits) {
     int best = 1, best_cost = ((tiles + pairs - 1) / pairs) * nk;
     for (int s = 2; s <= max_splits; ++s) {
