@@ -522,10 +522,12 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if (EPI == EPI_DGRAD) {
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
+                    if (!dense) {                           // token rows (dense) have no partner item
 #pragma unroll
-                    for (int i = 0; i < CW; ++i) {         // warp-wide: every lane takes part
-                        const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
-                        if (dmode == 1) v[i] = __fadd_rn(v[i], o);
+                        for (int i = 0; i < CW; ++i) {     // warp-wide: every lane takes part
+                            const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
+                            if (dmode == 1) v[i] = __fadd_rn(v[i], o);
+                        }
                     }
                     if (g.out_bf16) {                       // perf mode: bf16 grad_X (reading Z-24)
                         uint32_t pk[CW / 2];
