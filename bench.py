@@ -170,7 +170,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv:
@@ -182,6 +182,10 @@ class ClockSampler:
         self._stop.set()
         if self.nv:
             self.t.join()
+            try:                                  # one more sample at the end of the timed region
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
