@@ -193,31 +193,35 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- our arm
-def algorithmic_work(name, N, D, C, kx, kw):
+def algorithmic_work(name, N, D, C, kx, kw, dense=(False, False)):
     """(kind, amount) per launch: kind 'ops' (tensor) or 'bytes' (HBM); the
-    per-unit figures are stated in DESIGN.md "Rooflines"."""
+    per-unit figures are stated in DESIGN.md "Rooflines".  dense = (grad_W mask,
+    grad_X mask) deterministic: that GEMM ran over the N token rows of Q (reading
+    Z-32) and compact moved none of its operands."""
+    dw, dx = dense
+    rx = N if dx else kx                      # rows of the grad_X GEMM
+    rw = N if dw else kw                      # K of the grad_W GEMM
     if name == "gemm_i8_fwd":
         return "ops", 2.0 * N * C * D
     if name == "gemm_i8_dgrad":
-        return "ops", 2.0 * kx * C * D
+        return "ops", 2.0 * rx * C * D
     if name == "gemm_i8_wgrad":
-        return "ops", 2.0 * kw * C * D
+        return "ops", 2.0 * rw * C * D
     if name == GROUP:                         # grad_X and grad_W GEMMs run concurrently: one unit
-        return "ops", 2.0 * (kx + kw) * C * D
+        return "ops", 2.0 * (rx + rw) * C * D
     if name == "hadamard_quant":              # X and W: read bf16, write int8 codes + 1-bit mask (+ int32 norm)
         return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
-    if name == "grad_split":                  # amax + SR + bit split: read bf16 grad_Y once (the amax
-        return "bytes", N * C * (2 + 2) + 8 * N  # pass's re-read is an implementation cost), write hi + lo planes
-    if name == "compact":                     # A_X, A_W (plane rows) and B_W rows: read + write
-        return "bytes", 2.0 * (kx * C + kw * (C + D))
+    if name == "grad_split":                  # amax + SR: read bf16 grad_Y once (the amax pass's re-read is an
+        return "bytes", N * C * (2 + 1) + 8 * N  # implementation cost), write the 8-bit code plane Q + norms
+    if name == "compact":                     # half-rows of the sampled masks' items (+ B_W rows): read + write
+        return "bytes", 2.0 * ((0 if dx else kx * C) + (0 if dw else kw * (C + D)))
     if name == "lss_sampler":
         return "latency", 0.0
-    if name == "memsets":
-        return "bytes", 4.0 * N * D + 4
     return "bytes", 0.0
 
 
-def dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels):
+def dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels,
+                      dense=(False, False)):
     """roofline entry of the dominant kernel: CUDA events around its node in the step graph."""
     import torch
 
@@ -235,7 +239,7 @@ def dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, k
     timed_replays(g_dom, args.warmup)
     timed_replays(g_dom, args.steps, on_step=lambda: dom_ms.append(dom_ev[0].elapsed_time(dom_ev[1])))
     avg_s = statistics.mean(dom_ms) * 1e-3
-    kind, amount = algorithmic_work(dom, N, D, C, kx, kw)
+    kind, amount = algorithmic_work(dom, N, D, C, kx, kw, dense)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -393,6 +397,7 @@ def run_ours(args):
 
     # ---- kernel breakdown: CUPTI kernel records (torch.profiler) over extra replays
     kx, kw = [int(v) for v in layer.counts().cpu().numpy()]
+    dense = tuple(bool(v) for v in layer.dense_flags().cpu().numpy())   # (grad_W, grad_X) masks, Z-32
     # per-kernel numbers come from a PDL-off capture of the same step: with PDL a
     # kernel launches early and its duration would include the wait on its predecessor
     prev_pdl = i4.int4_set_pdl(False)
@@ -402,7 +407,7 @@ def run_ours(args):
     cupti = cupti_kernel_times(graph_serial, flush, min(args.steps, 20))
     kernels = {}
     for nm, avg_us in cupti.items():
-        kind, amount = algorithmic_work(nm, N, D, C, kx, kw)
+        kind, amount = algorithmic_work(nm, N, D, C, kx, kw, dense)
         ent = {"avg_us": avg_us, "share": avg_us * 1e-3 / ms if ms else 0.0}
         if kind == "ops" and avg_us > 0:
             ent.update(achieved_tops=amount / (avg_us * 1e-6) / 1e12, frac_int8_peak=amount / (avg_us * 1e-6) / 1e12 / int8_peak)
@@ -418,9 +423,10 @@ def run_ours(args):
               default=None)   # None when CUPTI is unavailable (e.g. the run is under ncu)
     roof = None
     if dom is not None:
-        roof = dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels)
+        roof = dominant_roofline(dom, names, step_body, timed_replays, args, N, D, C, kx, kw, int8_peak, peaks, kernels,
+                                 dense)
     i4.int4_set_pdl(prev_pdl)
-    gemm_ops = 2.0 * C * D * (N + kx + kw)
+    gemm_ops = 2.0 * C * D * (N + (N if dense[1] else kx) + (N if dense[0] else kw))
     bwd_gemms = (GROUP,) if (GROUP in kernels and GROUP in names) else ("gemm_i8_dgrad", "gemm_i8_wgrad")
     gemm_us = sum(kernels[nm]["avg_us"] for nm in ("gemm_i8_fwd",) + bwd_gemms if nm in kernels)
 
@@ -464,6 +470,8 @@ def run_ours(args):
                 "speedup_vs_bf16_cublas": bf16 / ms, "bf16_cublas_ms_per_step": bf16,
                 "gemm_int8_peak_frac": gemm_ops / (gemm_us * 1e-6) / 1e12 / int8_peak if gemm_us else None,
                 "kept_items": {"grad_W": kw, "grad_X": kx, "budget": N},
+                "dense_masks": {"grad_W": dense[0], "grad_X": dense[1],
+                                "note": "deterministic mask: its GEMM ran on the code plane Q (DESIGN.md Z-32)"},
                 "roofline": roof, "kernels": kernels, "kernels_timing": "CUPTI kernel records (torch.profiler) over extra flushed replays",
                 "gpu_launches": n_launch_ours(names) * args.steps,
                 "clocks": clocks.summary(), "e2e": e2e}
@@ -489,9 +497,7 @@ def short_kernel_name(full):
     for key, short in KERNEL_NAMES:
         if key in full:
             return short
-    if "memset" in full.lower():
-        return "memsets"                 # cudaMemsetAsync: zeroed grad_X + the 4-byte amax word
-    return None
+    return None                          # not ours (e.g. the L2-flush memset between timed steps)
 
 
 def cupti_kernel_times(graph, flush, n):

@@ -92,6 +92,8 @@ def _load():
     L.lsq_cold_start_workspace_size.restype = ctypes.c_size_t
     L.hq_select_k_workspace_size.argtypes = []
     L.hq_select_k_workspace_size.restype = ctypes.c_size_t
+    L.int4_bwd_ws_det_offset.argtypes = [i64, i64, i64]
+    L.int4_bwd_ws_det_offset.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
     L.int4_set_pdl.argtypes = [i32]
@@ -315,6 +317,13 @@ class Int4Linear:
 
     def counts(self):
         return self.scalars[2:4]
+
+    def dense_flags(self):
+        """[grad_W mask deterministic, grad_X mask deterministic] of the last backward
+        (reading Z-32: the GEMMs then ran on Q / X_hat), an int32 device tensor."""
+        import torch
+        off = lib.int4_bwd_ws_det_offset(self.N, self.D, self.C)
+        return self.ws[off:off + 8].view(torch.int32)
 
     def grad_s(self):
         """{grad s_X, grad s_W} of the last backward (A.3), a float32 device tensor."""

@@ -503,6 +503,15 @@ extern "C" {
 
 size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) { return carve_bwd_ws(nullptr, N, D, C).total; }
 
+// introspection (bench / tests): byte offset in the backward workspace of the two
+// int32 flags the sampler writes -- [0] grad_W mask deterministic, [1] grad_X mask
+// deterministic (reading Z-32: the GEMMs then read Q / X_hat and compact moves nothing)
+__attribute__((visibility("default"))) size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C) {
+    uint8_t* const base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);
+    const BwdWs w = carve_bwd_ws(base, N, D, C);
+    return size_t(reinterpret_cast<uint8_t*>(w.det) - base);
+}
+
 static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                                  int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
                                  i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream,

@@ -357,3 +357,16 @@ def test_bitsplit_repeated_calls_reuse_counters():
         torch.cuda.synchronize()
         assert np.array_equal(plan.q8.cpu().numpy().astype(np.int64)[:N], bs["q"]), it
         assert not plan.scratch.cpu().numpy()[-8:].any(), "counters not returned to zero"
+
+
+@pytest.mark.parametrize("mode,dense_g,expect", [(o_lss.MODE_KEEP_POSITIVE, True, (1, 1)), (o_lss.MODE_NONE, True, (1, 1)),
+                                                 (o_lss.MODE_BERNOULLI, True, (0, 0))])
+def test_dense_path_selection_and_parity(mode, dense_g, expect):
+    """Reading Z-32: a deterministic mask (every positive item kept with weight 1)
+    makes its GEMM run on the code plane Q (and X_hat); a sampled (binding) mask
+    keeps the compacted path.  The device-side choice is visible in the flags and
+    both paths give the oracle's gradients."""
+    N, D, C, k = 640, 256, 384, 5                          # dense grad_Y: 2N positive items > budget N
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=dense_g, mode=mode)
+    assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == expect
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, mode)
