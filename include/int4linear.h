@@ -258,6 +258,13 @@ I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const f
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
 
+/* Introspection: byte offset, inside int4_linear_bwd's workspace, of two int32
+ * flags the last backward left there: [0] the grad_W mask, [1] the grad_X mask was
+ * deterministic (every item with a positive score kept with weight 1; DESIGN.md
+ * reading Z-32), so that GEMM ran on the 8-bit code plane q8 (and X_hat) with no
+ * compaction.  Informational only: results do not depend on which form ran. */
+I4_API size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C);
+
 /* Exact INT8 x INT8 -> INT32 product acc[m, n] = sum_k A(m, k) B(n, k) on the
  * tcgen05 path used by every GEMM of the operator ("Multiply the
  * two INT4 matrices").  A is [M, K] (a_mn_major = 0) or [K, M] (a_mn_major = 1);

@@ -506,7 +506,7 @@ size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C) { return carve_b
 // introspection (bench / tests): byte offset in the backward workspace of the two
 // int32 flags the sampler writes -- [0] grad_W mask deterministic, [1] grad_X mask
 // deterministic (reading Z-32: the GEMMs then read Q / X_hat and compact moves nothing)
-__attribute__((visibility("default"))) size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C) {
+size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C) {
     uint8_t* const base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);
     const BwdWs w = carve_bwd_ws(base, N, D, C);
     return size_t(reinterpret_cast<uint8_t*>(w.det) - base);
