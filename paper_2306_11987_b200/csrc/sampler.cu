@@ -30,7 +30,11 @@ namespace cg = cooperative_groups;
 namespace i4 {
 
 constexpr int kClusterCTAs = 8;
-constexpr int kSamplerThreads = 1024;
+// threads per CTA: 512 when a CTA holds at most 4096 items (the A.2 rounds and
+// the scan are barrier-bound, fewer warps sync faster: cfg2 sampler 8.5 -> 6.9 us,
+// BERT-large FFN-up 24.6 -> 21.4 us), 1024 above (ViT: 12.6 K items per CTA)
+constexpr int kSamplerThreads = 1024;                 // the maximum
+constexpr int kSmallItemsPerCTA = 4096;
 constexpr int kItemsPerCTA = 16384;
 constexpr int kEMaxW = 4;
 constexpr int kEMaxX = 24;
@@ -45,7 +49,7 @@ struct SamplerSmem {
     uint32_t red_c[2][kClusterCTAs];
     uint64_t warp_w[kSamplerThreads / 32];
     uint32_t warp_c[kSamplerThreads / 32];
-    uint32_t scan[kSamplerThreads / 32];
+    uint32_t scan[32];
     uint32_t cta_tot[kClusterCTAs];
 };
 
@@ -100,7 +104,7 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
     __syncthreads();
     if (threadIdx.x == 0) {
         uint64_t bw = 0; uint32_t bc = 0;
-        for (int i = 0; i < kSamplerThreads / 32; ++i) { bw += sm.warp_w[i]; bc += sm.warp_c[i]; }
+        for (int i = 0; i < int(blockDim.x) / 32; ++i) { bw += sm.warp_w[i]; bc += sm.warp_c[i]; }
         const unsigned me = cl.rank();
         for (int r = 0; r < CL; ++r) {
             uint64_t* rw = cl.map(&sm.red_w[parity][me], r);
@@ -136,8 +140,8 @@ int sampler_stamps(unsigned long long* host, int enable) {
     return 0;
 }
 
-template <int CL>
-__global__ void __launch_bounds__(kSamplerThreads, 1)
+template <int CL, int NT>
+__global__ void __launch_bounds__(NT, 1)
 lss_sampler_kernel(SamplerArgs a) {
     pdl_trigger();
     pdl_wait();                                   // a_sq / s_down of grad_split
@@ -158,7 +162,7 @@ lss_sampler_kernel(SamplerArgs a) {
     int8_t* swe = reinterpret_cast<int8_t*>(scl + per16);
     const int base = rank * per;
     const int nloc = max(0, min(per, n_items - base));
-    const int ipt = (per + kSamplerThreads - 1) / kSamplerThreads;   // items per thread
+    const int ipt = (per + NT - 1) / NT;                 // items per thread
     const int t_lo = min(nloc, int(threadIdx.x) * ipt);
     const int t_hi = min(nloc, t_lo + ipt);
     const int e_max = mask_id == 0 ? kEMaxW : kEMaxX;
@@ -171,7 +175,7 @@ lss_sampler_kernel(SamplerArgs a) {
     auto item_of = [&](int slot) { return (slot & 1) * N + (slot >> 1); };
     int parity = 0;
     if (blockIdx.y == 0 && rank == 0)
-        for (int i = threadIdx.x; i < a.n_zero_words; i += kSamplerThreads) a.zero_words[i] = 0u;
+        for (int i = threadIdx.x; i < a.n_zero_words; i += NT) a.zero_words[i] = 0u;
 
     // ---- scores -------------------------------------------------------------
     // the inputs of 8 items are loaded before any is used (one round of load
@@ -292,14 +296,14 @@ lss_sampler_kernel(SamplerArgs a) {
     if (lane == 31) sm.scan[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        uint32_t v = sm.scan[lane];
+        uint32_t v = lane < NT / 32 ? sm.scan[lane] : 0u;
         uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, x, o);
             if (lane >= o) x += n;
         }
-        sm.scan[lane] = x - v;                 // exclusive warp offsets
+        if (lane < NT / 32) sm.scan[lane] = x - v;          // exclusive warp offsets
         if (lane == 31) {
             for (int r = 0; r < CL; ++r)
                 *cl.map(&sm.cta_tot[rank], r) = x;
@@ -324,7 +328,7 @@ lss_sampler_kernel(SamplerArgs a) {
     }
     if (rank == 0) {
         const uint32_t padded = (total + 127u) & ~127u;
-        for (uint32_t p = total + threadIdx.x; p < padded; p += kSamplerThreads) {
+        for (uint32_t p = total + threadIdx.x; p < padded; p += NT) {
             items[p] = n_items;                // sentinel: an all-zero row
             wexp[p] = 0;
         }
@@ -335,13 +339,13 @@ lss_sampler_kernel(SamplerArgs a) {
     smp_stamp(st_n, st_on);                                 // keep DSMEM alive until all remote writes landed
 }
 
-template <int CL>
+template <int CL, int NT>
 static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
     const int per = (2 * a.N + CL - 1) / CL;
     const int per16 = (per + 15) & ~15;
     const size_t smem = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
     const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1 + 1);
-    auto kern = lss_sampler_kernel<CL>;
+    auto kern = lss_sampler_kernel<CL, NT>;
     static bool attr_set = false;                 // once per instantiation: the largest footprint
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
@@ -350,7 +354,7 @@ static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask
-    cfg.blockDim = dim3(kSamplerThreads);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -367,8 +371,9 @@ cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
     // an 8-CTA cluster per mask: the A.2 rounds are dominated by the per-item
     // work, which the cluster spreads over 8 SMs (a single CTA measured 6x slower
     // on binding budgets); tiny problems use one CTA
-    if (2 * int64_t(a.N) <= 2048) return launch_cl<1>(a, s);
-    return launch_cl<kClusterCTAs>(a, s);
+    if (2 * int64_t(a.N) <= 2048) return launch_cl<1, 1024>(a, s);
+    if (2 * int64_t(a.N) <= int64_t(kClusterCTAs) * kSmallItemsPerCTA) return launch_cl<kClusterCTAs, 512>(a, s);
+    return launch_cl<kClusterCTAs, 1024>(a, s);
 }
 
 }  // namespace i4
