@@ -96,22 +96,32 @@ __device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, in
     uint32_t mask = 0;
     int sq = 0;
     float dl[DELTA ? 32 : 1];                       // A.3 delta, if requested
+    // clamp mask from sign bits: o = 7 - |v| is exact near |v| = 7 (Sterbenz) and
+    // never rounds across 0, so its sign bit is [|v| > 7]; a funnel shift moves it
+    // into the mask word (one ALU op per element; elements taken 15 .. 0 so that
+    // element j lands in bit j, the high 16 in a second word)
+    uint32_t out_lo = 0, out_hi = 0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 15; j >= 0; --j) {
         float s0, s1;
         f2_unpack(f2_mul(p[j], r2), s0, s1);
         const float c0 = fminf(fmaxf(s0, -7.0f), 7.0f), c1 = fminf(fmaxf(s1, -7.0f), 7.0f);
         const float m0 = __fadd_rn(c0, 12582912.0f), m1 = __fadd_rn(c1, 12582912.0f);
         qb[j] = __float_as_uint(m0);
         qb[j + 16] = __float_as_uint(m1);
-        const bool in0 = fabsf(s0) <= 7.0f, in1 = fabsf(s1) <= 7.0f;
-        mask |= (uint32_t(in0) << j) | (uint32_t(in1) << (j + 16));
+        const float o0 = __fsub_rn(7.0f, fabsf(s0)), o1 = __fsub_rn(7.0f, fabsf(s1));
+        out_lo = __funnelshift_l(__float_as_uint(o0), out_lo, 1);   // (out_lo << 1) | sign(o0)
+        out_hi = __funnelshift_l(__float_as_uint(o1), out_hi, 1);
+        const bool in0 = !(__float_as_uint(o0) >> 31), in1 = !(__float_as_uint(o1) >> 31);
         if constexpr (DELTA) {
             const float q0 = __fsub_rn(m0, 12582912.0f), q1 = __fsub_rn(m1, 12582912.0f);   // exact
             dl[j] = in0 ? __fsub_rn(q0, s0) : q0;                                    // exact (|.| <= 1/2)
             dl[j + 16] = in1 ? __fsub_rn(q1, s1) : q1;
+        } else {
+            (void)in0; (void)in1;
         }
     }
+    mask = ~(out_lo | (out_hi << 16));
     if (DELTA && J.delta != nullptr) {
         float4* dd = reinterpret_cast<float4*>(J.delta + row * cols + blk * 32);
 #pragma unroll
