@@ -683,7 +683,9 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
     if (blocks > kAmaxWord) blocks = kAmaxWord;
-    const bool p1_stream = N * int64_t(C) * 3 > (int64_t(126) << 20);   // grad_Y + Q beyond the 126 MB L2
+    static const int p1_env = getenv("I4_BS_P1_STREAM") ? atoi(getenv("I4_BS_P1_STREAM")) : -1;   // experiment
+    const bool p1_stream = p1_env >= 0 ? p1_env != 0
+                                       : N * int64_t(C) * 3 > (int64_t(126) << 20);   // grad_Y + Q beyond the 126 MB L2
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(blocks));
     cfg.blockDim = dim3(kSplitThreads);
