@@ -508,8 +508,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
 #pragma unroll
             for (int j = 0; j < kAmaxUnroll; ++j) {
                 const int64_t i = i0 + j * stride;
-                // grad_Y larger than L2 (with the code plane): stream it past L1
-                // (ViT FFN-up 229 -> 218 us); smaller: the cached load (BERT shapes)
+                // streamed past L1 (default) or the cached load (experiment switch)
                 if (p1_stream) u[j] = i < n8 ? ld_nc_v4(g4 + i) : make_uint4(0, 0, 0, 0);
                 else u[j] = i < n8 ? __ldg(g4 + i) : make_uint4(0, 0, 0, 0);
             }
@@ -684,8 +683,9 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     if (want < blocks) blocks = int(want);
     if (blocks > kAmaxWord) blocks = kAmaxWord;
     static const int p1_env = getenv("I4_BS_P1_STREAM") ? atoi(getenv("I4_BS_P1_STREAM")) : -1;   // experiment
-    const bool p1_stream = p1_env >= 0 ? p1_env != 0
-                                       : N * int64_t(C) * 3 > (int64_t(126) << 20);   // grad_Y + Q beyond the 126 MB L2
+    // amax pass past L1 (the phase-2 re-reads come from L2 on other SMs): measured
+    // equal or faster on every config with a flushed L2 (ViT FFN-up 229 -> 218 us)
+    const bool p1_stream = p1_env >= 0 ? p1_env != 0 : true;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(blocks));
     cfg.blockDim = dim3(kSplitThreads);
