@@ -28,7 +28,8 @@
 //            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; dW
 //            -> swizzled shared-memory staging -> TMA bulk tensor store
 //            EPI_DGRAD  row = kept item (h, t): v = acc * s_w s_down 2^wexp 2^{-k/2} (the
-//                       plane row holds 16 hi or lo, so s_up = 16 s_down is folded in);
+//                       A row holds 16 hi or lo -- or q = 16 hi + lo in the dense form --
+//                       so s_up = 16 s_down is folded in);
 //                       v = I_X[t] o v; v = v H; rows are token-major, so a token's
 //                       two items are adjacent lanes: summed by a shuffle and stored
 //                       once (pairs straddling a 32-row group: red.add.v4 of 2
@@ -441,7 +442,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if (row + 1 >= M || dense) nx = two_n;
                 if (row == 0 || dense) pv = two_n;
                 row_e = e;
-                rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the plane codes
+                rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the A codes
                 const int inext = valid ? nx : two_n;
                 const int iprev = valid ? pv : two_n;
                 const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;

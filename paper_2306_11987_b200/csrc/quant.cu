@@ -412,7 +412,7 @@ __device__ __forceinline__ void load_unit(const uint4* src, int64_t un, uint4 (&
 }
 
 // One unit: SR words (Philox, or a fake stream for the timing experiment),
-// split, plane stores, norms into shi / slo.
+// codes stored to the Q plane, half-row norms into shi / slo.
 template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG>
 __device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, const float R32, const PhiloxKeys& keys,
                                            uint32_t call_id, uint64_t tbase, int8_t* __restrict__ q8,
@@ -639,7 +639,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                     const uint32_t x = (t & 0x0F0F0F0Fu) ^ 0x08080808u;
                     pl[h] = (x & 0x08080808u) * 0x1Eu + x;
                 }
-                // sums of squares: the high plane holds 16 hi, so its dp4a sum is 256 sum hi^2
+                // sums of squares: ph holds 16 hi, so its dp4a sum is 256 sum hi^2
                 shi = __dp4a(int(ph[0]), int(ph[0]), __dp4a(int(ph[1]), int(ph[1]), shi));
                 slo = __dp4a(int(pl[0]), int(pl[0]), __dp4a(int(pl[1]), int(pl[1]), slo));
                 *reinterpret_cast<uint2*>(qr + col) = qp;          // the 8-bit code plane Q
