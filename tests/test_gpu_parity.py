@@ -370,3 +370,13 @@ def test_dense_path_selection_and_parity(mode, dense_g, expect):
     x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=dense_g, mode=mode)
     assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == expect
     _check_backward(layer, g, s_x, s_w, k, dX, dW, mode)
+
+
+@pytest.mark.parametrize("N,D,C,k", [(333, 256, 192, 5), (1000, 512, 768, 4)])
+def test_dense_path_ragged_tokens(N, D, C, k):
+    """The dense form (Z-32) with N not a multiple of the 128-row tile: the tail
+    rows of Q / X_hat beyond N read as zeros (TMA bounds), and every token row of
+    grad_X is written by the GEMM."""
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=True, mode=o_lss.MODE_KEEP_POSITIVE)
+    assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == (1, 1)
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, o_lss.MODE_KEEP_POSITIVE)
