@@ -20,6 +20,8 @@
 // The item scores live in shared memory (16384 items per CTA -> N <= 65536,
 // the same bound the grad_W INT32 accumulator imposes).  The kernel is
 // latency-bound (it moves < 2 MB); it is not an HBM-roofline kernel.
+#include <cstdlib>
+
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -45,12 +47,12 @@ int sampler_max_tokens() { return kClusterCTAs * kItemsPerCTA / 2; }
 // CTA's share of the items (launch-time: a small N gets a small footprint):
 //   uint64_t w[per] (scores), uint8_t clamped[per] (A.2 set S), int8_t wexp[per]
 struct SamplerSmem {
-    uint64_t red_w[2][kClusterCTAs];
-    uint32_t red_c[2][kClusterCTAs];
+    uint64_t red_w[2][16];                // per-CTA partials (clusters of up to 16)
+    uint32_t red_c[2][16];
     uint64_t warp_w[kSamplerThreads / 32];
     uint32_t warp_c[kSamplerThreads / 32];
     uint32_t scan[32];
-    uint32_t cta_tot[kClusterCTAs];
+    uint32_t cta_tot[16];
 };
 
 
@@ -67,17 +69,16 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 
 // CTA group of one mask: a single CTA (2N <= 16384 items) or an 8-CTA cluster
 // sharing partial sums through distributed shared memory.
-template <int CL> struct Group;
-template <> struct Group<1> {
-    __device__ unsigned rank() const { return 0; }
-    __device__ void sync() const { __syncthreads(); }
-    template <class T> __device__ T* map(T* p, int) const { return p; }
-};
-template <> struct Group<kClusterCTAs> {
+template <int CL> struct Group {                  // CL > 1: a thread-block cluster
     cg::cluster_group g = cg::this_cluster();
     __device__ unsigned rank() const { return g.block_rank(); }
     __device__ void sync() const { g.sync(); }
     template <class T> __device__ T* map(T* p, int r) const { return g.map_shared_rank(p, r); }
+};
+template <> struct Group<1> {
+    __device__ unsigned rank() const { return 0; }
+    __device__ void sync() const { __syncthreads(); }
+    template <class T> __device__ T* map(T* p, int) const { return p; }
 };
 
 // Exact floor(num 2^32 / W) for 0 < num < W < 2^64 without a 128-bit division:
@@ -350,6 +351,10 @@ static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
         if (e != cudaSuccess) return e;
+        if (CL > 8) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -373,6 +378,13 @@ cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
     // on binding budgets); tiny problems use one CTA
     if (2 * int64_t(a.N) <= 2048) return launch_cl<1, 1024>(a, s);
     if (2 * int64_t(a.N) <= int64_t(kClusterCTAs) * kSmallItemsPerCTA) return launch_cl<kClusterCTAs, 512>(a, s);
+    static const int big = getenv("I4_SMP_CL16") ? atoi(getenv("I4_SMP_CL16")) : 1;   // experiment switch
+    if (big && 2 * int64_t(a.N) > int64_t(kClusterCTAs) * 2 * kSmallItemsPerCTA) {
+        // > 8 K items per CTA: a 16-CTA (non-portable) cluster halves each CTA's share
+        const cudaError_t e = launch_cl<16, 1024>(a, s);
+        if (e == cudaSuccess) return e;
+        (void)cudaGetLastError();                  // cluster of 16 refused: fall back to 8
+    }
     return launch_cl<kClusterCTAs, 1024>(a, s);
 }
 
