@@ -380,3 +380,29 @@ def test_dense_path_ragged_tokens(N, D, C, k):
     x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=True, mode=o_lss.MODE_KEEP_POSITIVE)
     assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == (1, 1)
     _check_backward(layer, g, s_x, s_w, k, dX, dW, o_lss.MODE_KEEP_POSITIVE)
+
+
+@pytest.mark.parametrize("dense_g", [True, False])
+def test_sampler_16cta_cluster_parity(dense_g):
+    """N > 32768 tokens (> 8 K items per CTA) runs the sampler as 16-CTA clusters:
+    kept item lists, weight exponents and counts bit-exact against the oracle
+    (binding budget with dense grad_Y, non-binding with sparse)."""
+    N, C = 40000, 256
+    g = synth.grad_output(N, C, seed=7, dense=dense_g)
+    g = (synth.bf16_bits(g).view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+    xsq_np = np.random.default_rng(3).integers(1, 49 * 64, size=N).astype(np.int32)
+    mod = p()
+    plan = mod._PlanBuffers(N, C, "cuda")
+    xsq = torch.from_numpy(xsq_np).cuda()
+    mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, 5, 0, o_lss.MODE_BERNOULLI, plan.plan)
+    torch.cuda.synchronize()
+    bs = o_bs.bit_split(g, synth.PHILOX_SEED, 5, 0)
+    assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
+    mw = o_lss.sample_weight_mask(bs["a_sq"], xsq_np.astype(np.int64), synth.PHILOX_SEED, 5, 0)
+    mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 5, 0)
+    cw, cx = int(plan.scalars[2].item()), int(plan.scalars[3].item())
+    assert cw == mw["count"] and cx == mx["count"]
+    assert np.array_equal(plan.items_w.cpu().numpy()[:cw], mw["items"])
+    assert np.array_equal(plan.wexp_w.cpu().numpy()[:cw].astype(np.int64), mw["wexp"])
+    assert np.array_equal(plan.items_x.cpu().numpy()[:cx], mx["items"])
+    assert np.array_equal(plan.wexp_x.cpu().numpy()[:cx].astype(np.int64), mx["wexp"])
