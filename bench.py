@@ -76,7 +76,8 @@ def oracle_step(cfg, n_tokens, grad, mode):
     x = synth.activations(n_tokens, cfg["D"])
     w = synth.weights(cfg["C"], cfg["D"])
     g = synth.grad_output(n_tokens, cfg["C"], dense=(grad == "dense"))
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    from oracle.lsq_grad import cold_start_step
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     t0 = time.perf_counter()
     f = linear.forward(x, w, cfg["k"], s_x, s_w)
     linear.backward(g, f, synth.PHILOX_SEED, 0, 0, MODES[mode])
@@ -286,12 +287,12 @@ def run_ours(args):
     x = synth.activations(N, D, seed=synth.DATA_SEED + rank)
     w = synth.weights(C, D)
     g = synth.grad_output(N, C, seed=synth.DATA_SEED + rank, dense=(args.grad == "dense"))
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
 
     def up(a):
         return torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).to(dev)
 
     X, W, G = up(x), up(w), up(g)
+    s_x, s_w = i4.cold_start_step(X), i4.cold_start_step(W)   # A.4 rule, the library's kernel
     layer = i4.Int4Linear(N, D, C, k, device=dev)
     Y = torch.empty(N, C, dtype=torch.bfloat16, device=dev)
     dX = torch.empty(N, D, dtype=torch.bfloat16, device=dev)   # perf mode: bf16 Y and grad_X (Z-24)

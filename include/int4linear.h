@@ -14,7 +14,16 @@
  *     cuBLAS BF16 baseline).  Step sizes are fp32 host scalars.
  *   - Ownership: the caller allocates EVERY buffer (outputs, caches, plans,
  *     workspace); the library never allocates device memory and keeps no
- *     per-call state.  Buffer sizes are stated per field below.
+ *     per-call state.  Buffer sizes are stated per field below.  Library-owned
+ *     global state: per-device caches of launch parameters (SM count, occupancy,
+ *     the sampler's cluster size), the PDL switch (int4_set_pdl), and per
+ *     (host thread, device) side streams + fork / join events (created on first
+ *     use, never destroyed) that int4_linear_bwd uses to run the grad_X and
+ *     grad_W GEMMs concurrently when they under-fill the GPU, and that
+ *     int4_bmm_fwd / int4_bmm_bwd use for concurrent batch chains.  Work on
+ *     them is forked from and joined back into `stream` by event record / wait,
+ *     so stream order, graph capture and results are unaffected.
+ *   - No environment variables are read by the library.
  *   - Execution: stream-ordered and asynchronous on `stream` (a cudaStream_t
  *     passed as void*; NULL = legacy default stream).  No entry point
  *     synchronises the device or reads device memory from the host, so the
@@ -80,6 +89,15 @@ typedef enum {
  *                              v = XH / s_X (A.3, reading Z-27), exact
  *                              in fp32; needed only for the step-size gradients
  *   w_delta  float [C, D]      nullable: delta_W, the same for W
+ *   dev_status int32 [1]      nullable: device status word.  The forward ORs in
+ *                              I4_STATUS_NONFINITE when an element of X (or of W,
+ *                              when it is quantized) is Inf / NaN or its block
+ *                              transform overflows fp32 ("input error",
+ *                              which a stream-ordered call cannot return
+ *                              synchronously).  The codes of such a block are not
+ *                              meaningful.  The library only ORs bits in; the caller
+ *                              zeroes the word and reads it when it wants to (like
+ *                              a GradScaler's found-inf flag).
  * Host scalars: N, D, C, k, s_x, s_w are filled by int4_linear_fwd.  Set
  * w_valid = 1 to reuse wq / w_mask (/ w_delta) from a previous call with the
  * same W and s_w (one weight quantization per weight version); the library
@@ -96,7 +114,12 @@ typedef struct {
     int32_t w_valid;
     float* x_delta;
     float* w_delta;
+    int32_t* dev_status;
 } i4_fwd_cache;
+
+/* Bits of the device status words (i4_fwd_cache::dev_status, i4_lss_plan::dev_status). */
+#define I4_STATUS_NONFINITE 1   /* an input element was Inf / NaN                  */
+#define I4_STATUS_ZERO_GRAD 2   /* grad_Y was all zero ("degenerate"): s_down = 0    */
 
 /* Bit-split + sampling plan (Procedure LSS-MM steps 1-4).  Device buffers,
  * caller-allocated, written by bitsplit_lss:
@@ -123,7 +146,14 @@ typedef struct {
  *                              {grad s_X, grad s_W} (A.3; readings
  *                              Z-27..Z-29), computed when the cache holds x_delta and w_delta
  *   n_elem_x, n_elem_w         host: N_X, N_W of g(s) = 1/sqrt(Q_P N) (0 = this call's
- *                              N*D and C*D; a token-sharded caller passes the global counts) */
+ *                              N*D and C*D; a token-sharded caller passes the global counts)
+ *   dev_status int32 [1]       nullable: device status word, bits ORed in by the backward:
+ *                              I4_STATUS_NONFINITE when grad_Y holds an Inf / NaN (the
+ *                              tensor is then treated as all-zero: codes 0, s_down = 0, no
+ *                              item kept, grad_X = grad_W = 0 -- the caller must check the
+ *                              word, like a GradScaler's found-inf flag, and skip the step);
+ *                              I4_STATUS_ZERO_GRAD when grad_Y is all zero (a valid,
+ *                              degenerate call: zero gradients). */
 typedef struct {
     int8_t* q8;
     int32_t* a_sq;
@@ -139,6 +169,7 @@ typedef struct {
     uint8_t* x_touched;
     float* grad_s;
     int64_t n_elem_x, n_elem_w;
+    int32_t* dev_status;
 } i4_lss_plan;
 
 /* F1+F2 / F3: block-Hadamard transform + LSQ quantize of a bf16 matrix
@@ -292,11 +323,16 @@ I4_API int32_t int4_trace_end(const char** names, int32_t capacity);
 /* Programmatic dependent launch: every kernel of the library is launched so that
  * the next kernel in the stream may start launching while it drains (each kernel
  * waits for its predecessor's completion before touching its data).  On by
- * default (environment I4_PDL=0 turns it off); int4_set_pdl(0/1) switches it
- * process-wide and returns the previous setting.  Timing per kernel (bench.py's
+ * default; int4_set_pdl(0/1) switches it process-wide and returns the previous
+ * setting.  Timing per kernel (bench.py's
  * breakdown) is taken with it off, since an early-launched kernel's duration
  * includes its wait. */
 I4_API int32_t int4_set_pdl(int32_t enable);
+
+/* Introspection (tests): CTAs per mask in the thread-block cluster the LSS sampler
+ * launches for N tokens on the current device -- 1, 8, or 16 (non-portable, chosen
+ * only when the occupancy API reports that a 16-CTA cluster fits). */
+I4_API int32_t int4_sampler_cluster_ctas(int64_t N);
 
 /* Thread-local message describing the last non-OK status of this thread. */
 I4_API const char* int4_last_error(void);

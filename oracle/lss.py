@@ -152,26 +152,16 @@ def dyadic_thresholds(p, e_max):
     return e, T1, T2
 
 
-def sample(w, budget, u, mode, e_max, token_major=False):
+def sample(w, budget, u, mode, e_max):
     """Masks m_i and weights for all 2N items, compacted in ascending item order
-    (ids h*N + t), or token-major (t, h) when `token_major` (the order of the
-    grad_X list; the estimator does not depend on the order).
+    (ids h*N + t).  The estimator is a sum over the kept
+    items and does not depend on their order (a kernel may store them in any
+    order; parity compares the (item, weight) pairs as sets).
 
     w: uint64 [2, N] scores, u: uint64 [2, N] Philox words (row h).
     Returns dict(items int64 [K], wexp int64 [K], count K, p list, e, T1, T2).
     """
     w = np.asarray(w)
-    two, N = w.shape
-    out = _sample_item_order(w, budget, u, mode, e_max)
-    if token_major and out["count"]:
-        key = (out["items"] % N) * 2 + out["items"] // N
-        order = np.argsort(key, kind="stable")
-        out["items"] = out["items"][order]
-        out["wexp"] = out["wexp"][order]
-    return out
-
-
-def _sample_item_order(w, budget, u, mode, e_max):
     two, N = w.shape
     wf = [int(x) for x in w.reshape(-1)]          # item id i = h*N + t
     uf = [int(x) for x in np.asarray(u).reshape(-1)]
@@ -198,23 +188,20 @@ def _sample_item_order(w, budget, u, mode, e_max):
 
 
 def sample_weight_mask(a_sq, b_sq, seed, call_id, token_offset, mode=MODE_BERNOULLI):
-    """LSS mask of the weight gradient (PAPER.md:320-334), purpose-2 Philox stream;
-    list in token-major order (t, h) like the grad_X list (reading Z-12: the
-    estimator is a sum over the kept items, independent of their order)."""
+    """LSS mask of the weight gradient, purpose-2 Philox stream."""
     N = np.asarray(a_sq).shape[1]
     w = weight_scores(a_sq, b_sq)
     u = mask_uniforms(seed, call_id, token_offset, N, PURPOSE_MASK_W)
-    out = sample(w, N, u, mode, E_MAX_W, token_major=True)
+    out = sample(w, N, u, mode, E_MAX_W)
     out["w"] = w
     return out
 
 
 def sample_activation_mask(a_sq, seed, call_id, token_offset, mode=MODE_BERNOULLI):
-    """LSS mask of the activation gradient (PAPER.md:619-632), purpose-3 stream;
-    list in token-major order (t, h)."""
+    """LSS mask of the activation gradient, purpose-3 stream."""
     N = np.asarray(a_sq).shape[1]
     w = activation_scores(a_sq)
     u = mask_uniforms(seed, call_id, token_offset, N, PURPOSE_MASK_X)
-    out = sample(w, N, u, mode, E_MAX_X, token_major=True)
+    out = sample(w, N, u, mode, E_MAX_X)
     out["w"] = w
     return out

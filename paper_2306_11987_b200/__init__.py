@@ -20,14 +20,17 @@ __all__ = [
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
     "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step", "hq_select_k", "hq_select_k_workspace_size",
     "int4_bmm_fwd", "int4_bmm_bwd", "Int4BMM", "I4BmmCache",
-    "lsq_cold_start_workspace_size", "Int4Linear", "LaunchTrace",
+    "lsq_cold_start_workspace_size", "cold_start_step", "Int4Linear", "LaunchTrace",
+    "STATUS_NONFINITE", "STATUS_ZERO_GRAD",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libint4linear.so")
-# development knob: time a compile variant of the same library (tools/exp_bwd.py)
+# development knob of the timing tools (tools/exp_bwd.py, tools/hq_time.py): load a
+# compile variant of the same sources (tools/build_variants.sh -D knobs) instead
 LIB_PATH = os.environ.get("I4_LIB_OVERRIDE", LIB_PATH)
 
 LSS_BERNOULLI, LSS_KEEP_POSITIVE, LSS_NONE = 0, 1, 2
+STATUS_NONFINITE, STATUS_ZERO_GRAD = 1, 2
 OUT_F32, OUT_BF16 = 0, 1
 _STATUS = {0: "I4_OK", 1: "I4_ERR_SHAPE", 2: "I4_ERR_ALIGN", 3: "I4_ERR_ARG",
            4: "I4_ERR_UNSUPPORTED", 5: "I4_ERR_WORKSPACE", 6: "I4_ERR_CUDA"}
@@ -44,7 +47,8 @@ class I4FwdCache(ctypes.Structure):
                 ("x_mask", ctypes.c_void_p), ("w_mask", ctypes.c_void_p), ("x_sqnorm", ctypes.c_void_p),
                 ("N", ctypes.c_int64), ("D", ctypes.c_int64), ("C", ctypes.c_int64),
                 ("k", ctypes.c_int32), ("s_x", ctypes.c_float), ("s_w", ctypes.c_float),
-                ("w_valid", ctypes.c_int32), ("x_delta", ctypes.c_void_p), ("w_delta", ctypes.c_void_p)]
+                ("w_valid", ctypes.c_int32), ("x_delta", ctypes.c_void_p), ("w_delta", ctypes.c_void_p),
+                ("dev_status", ctypes.c_void_p)]
 
 
 class I4LssPlan(ctypes.Structure):
@@ -53,7 +57,7 @@ class I4LssPlan(ctypes.Structure):
                 ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
                 ("count_x", ctypes.c_void_p), ("x_touched", ctypes.c_void_p), ("grad_s", ctypes.c_void_p),
-                ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64)]
+                ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64), ("dev_status", ctypes.c_void_p)]
 
 
 class I4BmmCache(ctypes.Structure):
@@ -96,6 +100,8 @@ def _load():
     L.int4_bwd_ws_det_offset.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
     L.int4_bwd_workspace_size.restype = ctypes.c_size_t
+    L.int4_sampler_cluster_ctas.argtypes = [i64]
+    L.int4_sampler_cluster_ctas.restype = i32
     L.int4_set_pdl.argtypes = [i32]
     L.int4_set_pdl.restype = i32
     L.int4_last_error.argtypes = []
@@ -203,6 +209,17 @@ def lsq_cold_start_step(x, step, ws, stream=None):
                                    _stream(stream)))
 
 
+def cold_start_step(x, stream=None):
+    """A.4 cold-start step size of a bf16 device tensor, computed by the library's
+    lsq_cold_start_step kernel and returned as a host float (synchronises `stream`;
+    a setup-time convenience, not for the hot path)."""
+    import torch
+    step = torch.empty(1, dtype=torch.float32, device=x.device)
+    ws = torch.zeros(lsq_cold_start_workspace_size(), dtype=torch.uint8, device=x.device)
+    lsq_cold_start_step(x, step, ws, stream)
+    return float(step.cpu()[0])
+
+
 def int4_set_pdl(enable):
     """Switch programmatic dependent launch for all library launches; returns the previous setting."""
     return bool(lib.int4_set_pdl(1 if enable else 0))
@@ -295,6 +312,10 @@ class Int4Linear:
         self.__dict__.update(self._plan_bufs.views())
         self.plan = self._plan_bufs.plan
         self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
+        # device status word shared by the forward cache and the plan (I4_STATUS_* bits)
+        self.status_buf = torch.zeros(1, dtype=i32, device=dev)
+        self.cache.dev_status = self.status_buf.data_ptr()
+        self.plan.dev_status = self.status_buf.data_ptr()
         self.step_grads = bool(step_grads)
         if self.step_grads:
             self.x_delta = torch.empty(N, D, dtype=f32, device=dev)
@@ -310,6 +331,15 @@ class Int4Linear:
 
     def backward(self, dY, dX, dW, seed, call_id=0, token_offset=0, mode=LSS_BERNOULLI, stream=None):
         int4_linear_bwd(dY, self.cache, seed, call_id, token_offset, mode, self.plan, dX, dW, self.ws, stream)
+
+    def status(self):
+        """Device status word (int32 tensor [1]): bit 0 = I4_STATUS_NONFINITE (an Inf / NaN
+        input), bit 1 = I4_STATUS_ZERO_GRAD (all-zero grad_Y).  Bits accumulate until
+        clear_status()."""
+        return self.status_buf
+
+    def clear_status(self):
+        self.status_buf.zero_()
 
     # views of the device-side sampling state (for tests and reports)
     def s_down(self):
@@ -374,7 +404,7 @@ class Int4BMM:
         self.cache = I4BmmCache(qq=self.qq.data_ptr(), kq=self.kq.data_ptr(), q_mask=self.q_mask.data_ptr(),
                                 k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr())
         # one plan + workspace slice per concurrent batch chain (batch b -> chain b % S)
-        S = min(B, int(os.environ.get("I4_BMM_CHAINS", "16")))
+        S = min(B, 16)
         self._plan_bufs = [_PlanBuffers(N, P, dev) for _ in range(S)]
         self.plans = (I4LssPlan * S)(*[pb.plan for pb in self._plan_bufs])
         self.plan = self.plans[0]

@@ -20,17 +20,9 @@
 #include <cstdlib>
 
 namespace i4 {
-// process-wide PDL switch: on unless I4_PDL=0; int4_set_pdl() overrides it
-static std::atomic<int> g_pdl{-1};
-bool pdl_enabled() {
-    int v = g_pdl.load(std::memory_order_relaxed);
-    if (v < 0) {
-        const char* e = std::getenv("I4_PDL");
-        v = (e != nullptr && e[0] == '0') ? 0 : 1;
-        g_pdl.store(v, std::memory_order_relaxed);
-    }
-    return v != 0;
-}
+// process-wide PDL switch: on by default; int4_set_pdl() changes it
+static std::atomic<int> g_pdl{1};
+bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
 }  // namespace i4
 
 namespace {
@@ -125,11 +117,18 @@ DeviceInfo query_device() {
     return d;
 }
 
+// cached per device ordinal (a process may drive several GPUs)
 const DeviceInfo& device_info() {
-    static DeviceInfo info;
-    static std::once_flag once;
-    std::call_once(once, [] { info = query_device(); });
-    return info;
+    static DeviceInfo info[i4::kMaxDevices];
+    static std::once_flag once[i4::kMaxDevices];
+    static DeviceInfo none;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= i4::kMaxDevices) {
+        none.why = "no CUDA device (or device ordinal >= 64)";
+        return none;
+    }
+    std::call_once(once[dev], [dev] { info[dev] = query_device(); });
+    return info[dev];
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -210,7 +209,8 @@ constexpr int64_t kMaxBwdTokens = 65536;
 struct Operand { const int8_t* p; int64_t rows, inner, pitch; bool gather = false; };
 
 // A_alt (optional): a second A the kernel may read instead, chosen on the device
-// (GemmArgs::alt_*; the grad_W GEMM reads the grad_X GEMM's A when the lists match)
+// (the grad_X GEMM reads the code plane Q when its mask is deterministic, Z-32);
+// A_dense / B_dense: the grad_W GEMM's operands Q and X_hat for that case
 i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cudaStream_t s, int sms = 0,
                const Operand* A_alt = nullptr, const Operand* A_dense = nullptr, const Operand* B_dense = nullptr) {
     CUtensorMap ta, tb, tc, ta2, ta3, tb2;
@@ -291,9 +291,6 @@ int64_t gemm_cost_kb(int64_t tiles, int64_t nk, int64_t pairs, int max_splits) {
 // is modelled as faster.  Each launch also costs a fixed prologue / last-tile
 // epilogue (kFixedKb, measured 5-8 us ~ 16 k-blocks) that concurrency overlaps.
 int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_w, int64_t pairs) {
-    const char* env = getenv("I4_BWD_CONCURRENT");           // experiment switch: 0 off, 1 forced on, P: P pairs
-    if (env && env[0] == '0') return 0;
-    if (env && atoi(env) > 1) return atoi(env);
     constexpr int64_t kFixedKb = 16;
     const int64_t seq = gemm_cost_kb(tiles_x, nk_x, pairs, 1) + gemm_cost_kb(tiles_w, nk_w, pairs, i4::kSplitMaxK) +
                         2 * kFixedKb;
@@ -306,7 +303,6 @@ int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_
                           kFixedKb;
         if (best < 0 || c < best) { best = c; best_px = px; }
     }
-    if (env && env[0] == '1') return int(best_px);
     // only on a clear modelled win (BERT-large QKV: modelled 136 vs 144 k-blocks,
     // measured 159 -> 206 us concurrent; BERT-base FFN1: 64 vs 88, 97 -> 88 us)
     return best >= 0 && 100 * best < 85 * seq ? int(best_px) : 0;
@@ -325,6 +321,8 @@ __attribute__((visibility("default"))) int32_t int4_debug_grad_split_stamps(unsi
 __attribute__((visibility("default"))) int32_t int4_debug_sampler_stamps(unsigned long long* host, int32_t enable) {
     return i4::sampler_stamps(host, enable);
 }
+
+int32_t int4_sampler_cluster_ctas(int64_t N) { return i4::sampler_cluster_ctas(N); }
 
 int32_t int4_set_pdl(int32_t enable) {
     const int32_t prev = i4::pdl_enabled() ? 1 : 0;
@@ -362,7 +360,7 @@ i4_status hadamard_quant(const void* x_bf16, int64_t rows, int64_t cols, int32_t
     if (!aligned16(x_bf16) || !aligned16(codes)) return fail(I4_ERR_ALIGN, "hadamard_quant: pointers must be 16-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     I4_LAUNCH(i4::launch_hadamard_quant(static_cast<const uint16_t*>(x_bf16), rows, cols, k, step_recip(k, step),
-                                        codes, clamp_bits, row_sqnorm, s),
+                                        codes, clamp_bits, row_sqnorm, nullptr, s),
               "hadamard_quant", s);
     return I4_OK;
 }
@@ -397,6 +395,7 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
             h.delta1 = cache->w_delta;
         }
         h.cols = D; h.k = k;
+        h.status = cache->dev_status;
         I4_LAUNCH(i4::launch_hadamard_quant2(h, s), "hadamard_quant", s);
     }
     i4::GemmArgs g{};
@@ -428,7 +427,8 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
     if (token_offset < 0) return fail(I4_ERR_ARG, "bitsplit_lss: token_offset < 0");
     if (!aligned16(dY) || !aligned16(plan->q8)) return fail(I4_ERR_ALIGN, "bitsplit_lss: unaligned pointer");
     I4_LAUNCH(i4::launch_grad_split(static_cast<const uint16_t*>(dY), N, C, plan->scratch, seed, call_id, token_offset,
-                                    plan->q8, plan->a_sq, plan->s_down, plan->amax_bits, s), "grad_split", s);
+                                    plan->q8, plan->a_sq, plan->s_down, plan->amax_bits, plan->dev_status, s),
+              "grad_split", s);
     i4::SamplerArgs a{};
     a.a_sq = plan->a_sq;
     a.x_sqnorm = x_sqnorm;
@@ -621,16 +621,13 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         g.partial = w.part_w; g.flags = w.flags_w;
         g.max_tiles_split = i4::kSplitMaxTiles;  // few (C/256 x D/256) tiles, long sampled K
         g.max_splits = px > 0 ? 1 : i4::kSplitMaxK;   // no split-K beside a concurrent grad_X
-        if (px > 0 && getenv("I4_BWD_WSPLIT")) g.max_splits = atoi(getenv("I4_BWD_WSPLIT"));   // experiment
         if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
-        g.alt_det_flags = w.det; g.alt_count_w = plan->count_w; g.alt_count_x = plan->count_x;
         g.dense_flag = w.det;                    // grad_W mask deterministic: K = tokens, A = Q, B = X_hat
         g.n_tokens = int32_t(N);
-        const Operand a_x_view{w.a_x, 2 * N + 128, C, C};   // = A_W when the two item lists are equal
         const Operand q_k{plan->q8, N + 1, C, C};            // Q as the MN-major A (rows = K = tokens)
         const Operand xq_k{cache->xq, N, D, D};             // X_hat as the MN-major B
         I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
-                          px > 0 ? device_info().sms - 2 * px : 0, &a_x_view, &q_k, &xq_k));
+                          px > 0 ? device_info().sms - 2 * px : 0, nullptr, &q_k, &xq_k));
     }
     if (px > 0) {
         g_trace_group = false;
@@ -680,8 +677,7 @@ i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64
     // batch b runs on stream b % S (S = min(B, kBmmStreams); the caller's stream
     // and side streams joined back into it), so the small per-batch kernels overlap
     cudaStream_t s0 = static_cast<cudaStream_t>(stream);
-    const char* env = getenv("I4_BMM_STREAMS");          // experiment switch
-    const int S = int(std::min<int64_t>(B, env ? std::max(1, std::min(atoi(env), kBmmStreams)) : kBmmStreams));
+    const int S = int(std::min<int64_t>(B, kBmmStreams));
     cudaEvent_t fork_ev = nullptr;
     for (int j = 1; j < S; ++j) {
         I4_RETURN_IF(make_side(t_bmm[j - 1]));
@@ -719,9 +715,7 @@ i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s
     // caller's stream for j = 0, library side streams joined back otherwise), so
     // the per-batch kernel chains overlap; S = min(B, n_plans, kBmmStreams)
     const size_t per_ws = int4_bwd_workspace_size(N, M, P);
-    const char* env = getenv("I4_BMM_STREAMS");          // experiment switch
-    int S = int(std::min<int64_t>(B, std::min<int64_t>(n_plans, kBmmStreams)));
-    if (env) S = std::max(1, std::min(S, atoi(env)));
+    const int S = int(std::min<int64_t>(B, std::min<int64_t>(n_plans, kBmmStreams)));
     if (ws_bytes < size_t(S) * per_ws)
         return fail(I4_ERR_WORKSPACE, "int4_bmm_bwd: ws_bytes %zu < %d x %zu", ws_bytes, S, per_ws);
     cudaStream_t s0 = static_cast<cudaStream_t>(stream);

@@ -15,8 +15,7 @@ constexpr int kGroup = 8;                 // 16-byte loads in flight per lane
 // One launch builds all three compacted operands; one warp per output row:
 //   A_X[j, :] = half h of Q[t, :] for item (h, t)  (C bytes; grad_X GEMM A, K-major):
 //               16 hi (h = 0) or lo (h = 1), split from the 8-bit codes on the fly
-//   A_W[j, :] = the same for items_w[j]           (C bytes; grad_W GEMM A, MN-major;
-//                                                  skipped when the lists are equal)
+//   A_W[j, :] = the same for items_w[j]           (C bytes; grad_W GEMM A, MN-major)
 //   B_W[j, :] = 2^wexp_w[j] X_hat[t(items_w[j]), :]   (D bytes, |.| <= 112; grad_W GEMM B)
 // The A rows hold 16 hi or lo, so acc[c, d] = sum_j A_W[j, c] B_W[j, d] is the
 // weighted bit-split product with s_up = 16 s_down folded in (reading Z-17).
@@ -75,13 +74,12 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     // deterministic masks (the sampler's flags; the GEMMs pick their operands by the
     // same tests): grad_X dense -> no A_X rows and no zero rows (its GEMM writes every
-    // token row from Q); grad_W dense -> no A_W / B_W rows (Q and X_hat are read);
-    // equal item lists -> the grad_W GEMM reads A_X, no A_W copy
+    // token row from Q); grad_W dense -> no A_W / B_W rows (Q and X_hat are read)
     const bool dense_x = a.det_flags != nullptr && __ldg(a.det_flags + 1) != 0;
     const bool dense_w = a.det_flags != nullptr && __ldg(a.det_flags) != 0;
     const int64_t n_straddle = dense_x ? 0 : (cnt_x + 31) / 32;   // candidate positions 31, 63, ...
     if (dense_x) pad_x = 0;
-    const int64_t pad_aw = (dense_w || lists_equal(a.det_flags, a.count_w, a.count_x)) ? 0 : pad_w;
+    const int64_t pad_aw = dense_w ? 0 : pad_w;
     const int64_t pad_bw = dense_w ? 0 : pad_w;
     const int64_t seg_bw = pad_x + pad_aw;                   // first B_W row job
     const int64_t n_zero = dense_x ? 0 : a.N;

@@ -184,7 +184,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
-        if (EPI == EPI_WGRAD || EPI == EPI_DGRAD) tma_prefetch_desc(&tmA2);
+        if (EPI == EPI_DGRAD) tma_prefetch_desc(&tmA2);
         if (EPI == EPI_WGRAD) { tma_prefetch_desc(&tmA3); tma_prefetch_desc(&tmB2); }
         tma_prefetch_desc(&tmB);
         if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
@@ -225,13 +225,11 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // lane 0 issues the TMA; with a gathered A the 32 lanes first fetch the
         // 128 row indices of the stage (4 per lane) and hand them out by shuffles.
         const bool gather = g.a_gather != nullptr;
-        // grad_W: the A operand may be the grad_X GEMM's (identical item lists)
         const CUtensorMap* pA = &tmA;
         const CUtensorMap* pB = &tmB;
         if (EPI == EPI_DGRAD && dense) pA = &tmA2;                     // Q, K-major
         if (EPI == EPI_WGRAD) {
             if (dense) { pA = &tmA3; pB = &tmB2; }                    // Q and X_hat, MN-major
-            else if (lists_equal(g.alt_det_flags, g.alt_count_w, g.alt_count_x)) pA = &tmA2;
         }
         const int gcount = gather ? __ldg(g.gather_count) : 0;
         auto load_idx4 = [&](int r) {

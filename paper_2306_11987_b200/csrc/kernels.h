@@ -9,7 +9,7 @@
 namespace i4 {
 
 // Programmatic dependent launch attribute for every launch of the library
-// (disabled with the environment variable I4_PDL=0, for A/B timing).
+// (int4_set_pdl(0) turns it off, for per-kernel timing).
 bool pdl_enabled();
 inline int add_pdl_attr(cudaLaunchAttribute* attrs, int n) {
     if (pdl_enabled()) {
@@ -20,22 +20,28 @@ inline int add_pdl_attr(cudaLaunchAttribute* attrs, int n) {
     return n;
 }
 
+constexpr int kMaxDevices = 64;          // per-device caches of launch parameters
+// device status word bits (i4_fwd_cache::dev_status, i4_lss_plan::dev_status)
+constexpr int32_t kStatusNonFinite = 1;  // an input element is Inf / NaN ("input error")
+constexpr int32_t kStatusZeroGrad = 2;   // grad_Y is all zero ("degenerate")
+
 // quant.cu --------------------------------------------------------------------
 struct HqArgs {                          // two independent hadamard_quant jobs in one launch
     const uint16_t* x0; int64_t rows0; float r0; int8_t* codes0; uint32_t* bits0; int32_t* sqnorm0;
     const uint16_t* x1; int64_t rows1; float r1; int8_t* codes1; uint32_t* bits1; int32_t* sqnorm1;
     int64_t cols; int k;
     float* delta0; float* delta1;        // optional A.3 delta = <v> - I o v (fp32, exact)
+    int32_t* status;                     // optional device status word (bit 0: non-finite input)
 };
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
-                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s);
+                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, int32_t* status, cudaStream_t s);
 constexpr int kGradSplitMaxBlocks = 2048;   // block-max scratch words the plan provides
 int grad_split_stamps(unsigned long long* host, int n);
-int sampler_stamps(unsigned long long* host, int enable);   // timing experiment   // timing experiment (I4_BS_EXP=8)
+int sampler_stamps(unsigned long long* host, int enable);   // timing experiment (-DI4_STAMPS=1 builds)
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, cudaStream_t s);
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s);
 
 // sampler.cu ------------------------------------------------------------------
 struct SamplerArgs {
@@ -54,6 +60,7 @@ struct SamplerArgs {
     int32_t* det_flags;       // optional [2]: 1 if mask m kept a deterministic set (all positives / all items)
 };
 int sampler_max_tokens();
+int sampler_cluster_ctas(int64_t N);      // CTAs per mask the sampler launches for N tokens (introspection)
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s);
 
 // compact.cu ------------------------------------------------------------------
@@ -69,13 +76,9 @@ struct CompactArgs {
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]
-    const int32_t* det_flags; // optional [2] (sampler): both set + equal counts -> lists equal, A_W = A_X;
-                              // [1] set: grad_X GEMM dense (no A_X, no zero rows); [0] set: grad_W dense
+    const int32_t* det_flags; // optional [2] (sampler): [1] set: grad_X GEMM dense (no A_X, no zero
+                              // rows); [0] set: grad_W GEMM dense (no A_W / B_W)
 };
-// the grad_W list equals the grad_X list: both masks deterministic, equal counts
-__device__ __forceinline__ bool lists_equal(const int32_t* det_flags, const int32_t* count_w, const int32_t* count_x) {
-    return det_flags != nullptr && __ldg(det_flags) != 0 && __ldg(det_flags + 1) != 0 && __ldg(count_w) == __ldg(count_x);
-}
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
@@ -111,8 +114,6 @@ struct GemmArgs {
     // LSQ step-size gradient (A.3), optional: sum(acc o delta) per CTA epilogue warp
     const float* delta;       // dgrad: delta_X [N, Nn] (row = token); wgrad: delta_W [M, Nn]
     double* lsq_part;         // [gridDim.x * 8] fp64 partials (entries of absent CTAs pre-zeroed)
-    // wgrad: read A through the alternate map (the grad_X GEMM's A) when lists_equal(...)
-    const int32_t* alt_det_flags; const int32_t* alt_count_w; const int32_t* alt_count_x;
     // dgrad / wgrad: if *dense_flag != 0 the mask is deterministic (every nonzero item kept
     // with weight 1): dgrad reads A = Q (map a2, M = n_tokens rows = tokens), wgrad reads
     // A = Q and B = X_hat (maps a3, b2, K = n_tokens)

@@ -7,6 +7,7 @@
 //                    Z-9), then Philox SR to the 8-bit code q (stored), its high /
 //                    low 4-bit halves' per-row integer norms (PAPER.md:234-239,
 //                    :680); one cooperative launch with one grid barrier
+#include <atomic>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -46,6 +47,7 @@ struct HqJob {
     int32_t* sqnorm;
     float* delta;                        // optional: A.3 delta = code - I o v (fp32, exact)
     int blocks;                          // CTAs assigned to this job
+    int32_t* status;                     // optional: device status word (bit 0 <- non-finite input)
 };
 
 constexpr int kHqMaxThreads = 256;
@@ -87,6 +89,16 @@ __device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, in
         }
     }
     if (!active) return 0;
+    if (J.status != nullptr) {
+        // Inf / NaN anywhere in the block (or a transform that overflows fp32) makes
+        // t * 0 NaN: flag the device status word ("input error")
+        uint64_t z = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z = f2_fma(p[j], 0, z);
+        float z0, z1;
+        f2_unpack(z, z0, z1);
+        if (z0 != 0.0f || z1 != 0.0f) atomicOr(J.status, kStatusNonFinite);
+    }
     // LSQ: v = fl32(t r); code = clamp(rint(v), -7, 7); mask = |v| <= 7.
     // rint on the clamped value by the magic-number add: fl32(c + 1.5 2^23) is
     // exact round-half-even for |c| <= 7 (ulp 1 there), and the low byte of its
@@ -202,8 +214,8 @@ static int hq_rows_per_cta(int64_t cols) {
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     if (a.cols / 32 > kHqMaxThreads) return cudaErrorInvalidValue;   // cols > 8192: not supported
     const int R = hq_rows_per_cta(a.cols);
-    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0};
-    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0};
+    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0, a.status};
+    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0, a.status};
     j0.blocks = int((a.rows0 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
     j1.blocks = int((a.rows1 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
     const int grid = j0.blocks + j1.blocks;
@@ -236,8 +248,9 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
-                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, cudaStream_t s) {
+                                  int8_t* codes, uint32_t* bits, int32_t* sqnorm, int32_t* status, cudaStream_t s) {
     HqArgs a{};
+    a.status = status;
     a.x0 = x; a.rows0 = rows; a.r0 = r; a.codes0 = codes; a.bits0 = bits; a.sqnorm0 = sqnorm;
     a.cols = cols; a.k = k;
     return launch_hadamard_quant2(a, s);
@@ -330,8 +343,8 @@ __device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const P
 
 // Fast phase 2 for one 8-element chunk (reading Z-10 / Z-11, same arithmetic as
 // the generic loop below, restated for the ALU / fma-heavy pipe budget):
-//   y = fl32(|g| R32) with R32 = r8 2^32 (exact power-of-two scaling of
-//       fl32(|g| r8); DESIGN.md notes the subnormal-underflow corner)
+//   y = fl32(fl32(|g| r8) 2^32) on fp32 pairs (FMUL2): the power-of-two scaling
+//       is exact, so y = a 2^32 bit for bit, including a subnormal fl32(|g| r8)
 //   A = ceil(min(y, 119 2^32)) as u64: high word floor(a), low word T
 //   mag = hi(A) + [u < lo(A)]
 // then sign and split on packed bytes, with no cross-byte carries:
@@ -340,18 +353,22 @@ __device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const P
 //        (positive: m + 128 + 8; negative: 127 - m + 1 + 8)
 //   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
 template <bool CLAMP>
-__device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float R32,
+__device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float r8,
                                              uint2& pq, int& shi, int& slo) {
     const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+    const uint64_t r2 = f2_pack(r8, r8), e2 = f2_pack(4294967296.0f, 4294967296.0f);
     uint32_t mag[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t bits = (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
-        float y = __fmul_rn(fabsf(__uint_as_float(bits)), R32);
-        if (CLAMP) y = fminf(y, 511101108224.0f);                       // 119 * 2^32
-        const uint64_t A = __float2ull_ru(y);
-        mag[i] = uint32_t(A >> 32) + (u[i] < uint32_t(A) ? 1u : 0u);
+    for (int i = 0; i < 8; i += 2) {
+        // |g| of elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
+        const uint64_t ag = uint64_t((w[i >> 1] << 16) & 0x7FFFFFFFu) | (uint64_t(w[i >> 1] & 0x7FFF0000u) << 32);
+        float y0, y1;
+        f2_unpack(f2_mul(f2_mul(ag, r2), e2), y0, y1);
+        if (CLAMP) { y0 = fminf(y0, 511101108224.0f); y1 = fminf(y1, 511101108224.0f); }   // 119 * 2^32
+        const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
+        mag[i] = uint32_t(A0 >> 32) + (u[i] < uint32_t(A0) ? 1u : 0u);
+        mag[i + 1] = uint32_t(A1 >> 32) + (u[i + 1] < uint32_t(A1) ? 1u : 0u);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -411,10 +428,9 @@ __device__ __forceinline__ void load_unit(const uint4* src, int64_t un, uint4 (&
     for (int gi = 0; gi < G; ++gi) dst[gi] = ld_nc_v4(src + (un * G + gi) * 32);
 }
 
-// One unit: SR words (Philox, or a fake stream for the timing experiment),
-// codes stored to the Q plane, half-row norms into shi / slo.
-template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG>
-__device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, const float R32, const PhiloxKeys& keys,
+// One unit: SR words (Philox), codes stored to the Q plane, half-row norms into shi / slo.
+template <int G, bool CLAMP, bool C1Z>
+__device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, const float r8, const PhiloxKeys& keys,
                                            uint32_t call_id, uint64_t tbase, int8_t* __restrict__ q8,
                                            int& shi, int& slo) {
     const int lane = lane_id();
@@ -422,15 +438,9 @@ __device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, co
     for (int gi = 0; gi < G; ++gi) {
         const int64_t flat = (un * G + gi) * 256 + lane * 8;
         Philox4 p0, p1;
-        if (FAKE_RNG) {
-            const uint32_t blk = uint32_t(flat);
-            p0 = {blk * 3u, blk * 5u, blk * 7u, blk * 9u};
-            p1 = {p0.x ^ call_id, p0.y ^ call_id, p0.z ^ call_id, p0.w ^ call_id};
-        } else {
-            sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
-        }
+        sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
         uint2 pq;
-        split_chunk8<CLAMP>(cur[gi], p0, p1, R32, pq, shi, slo);
+        split_chunk8<CLAMP>(cur[gi], p0, p1, r8, pq, shi, slo);
         *reinterpret_cast<uint2*>(q8 + flat) = pq;
     }
 }
@@ -448,8 +458,8 @@ __device__ __forceinline__ void flush_norms(int& shi, int& slo, int32_t* __restr
     shi = 0; slo = 0;
 }
 
-template <int G, bool CLAMP, bool C1Z, bool FAKE_RNG = false>
-__device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int64_t N, int C, const float R32,
+template <int G, bool CLAMP, bool C1Z>
+__device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int64_t N, int C, const float r8,
                                             const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset,
                                             int8_t* __restrict__ q8, int32_t* __restrict__ a_sq, int64_t u0,
                                             int64_t u1, uint4 (&buf)[G]) {
@@ -466,7 +476,7 @@ __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int6
 #pragma unroll
             for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
             if (un + 1 < u1) load_unit<G>(src, un + 1, buf);        // next unit's loads in flight
-            split_unit<G, CLAMP, C1Z, FAKE_RNG>(cur, un, R32, keys, call_id, tbase, q8, shi, slo);
+            split_unit<G, CLAMP, C1Z>(cur, un, r8, keys, call_id, tbase, q8, shi, slo);
             if (++seg == upr || un + 1 == u1) {                       // row done (or range end): flush
                 flush_norms(shi, slo, a_sq, N, row);
                 seg = 0; ++row;
@@ -475,9 +485,14 @@ __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int6
     }
 }
 
-// timing experiment (I4_BS_EXP bit 3): per-CTA globaltimer stamps -- start,
-// phase 1 done, barrier passed, amax known, phase 2 done (max over warps)
-__device__ unsigned long long g_gs_stamp[5][kGradSplitMaxBlocks];
+// timing experiment, compiled in only by -DI4_STAMPS=1 (tools/build_variants.sh,
+// tools/gs_stamps.py): per-CTA globaltimer stamps -- start, phase 1 done,
+// barrier passed, amax known, phase 2 done (max over warps)
+#ifndef I4_STAMPS
+#define I4_STAMPS 0
+#endif
+constexpr bool kStamps = I4_STAMPS != 0;
+__device__ unsigned long long g_gs_stamp[kStamps ? 5 : 1][kStamps ? kGradSplitMaxBlocks : 1];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -489,12 +504,12 @@ __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ scratch,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
-                  int exp_flags, bool p1_stream) {
+                  int32_t* __restrict__ status) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     pdl_trigger();
     pdl_wait();
-    const bool stamp = exp_flags & 8;
+    constexpr bool stamp = kStamps;
     if (stamp && threadIdx.x == 0) g_gs_stamp[0][blockIdx.x] = gtimer();
 
     // ---- phase 1: amax ----------------------------------------------------
@@ -508,9 +523,9 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
 #pragma unroll
             for (int j = 0; j < kAmaxUnroll; ++j) {
                 const int64_t i = i0 + j * stride;
-                // streamed past L1 (default) or the cached load (experiment switch)
-                if (p1_stream) u[j] = i < n8 ? ld_nc_v4(g4 + i) : make_uint4(0, 0, 0, 0);
-                else u[j] = i < n8 ? __ldg(g4 + i) : make_uint4(0, 0, 0, 0);
+                // streamed past L1: the phase-2 re-reads come from L2 on other SMs
+                // (measured equal or faster on every config with a flushed L2)
+                u[j] = i < n8 ? ld_nc_v4(g4 + i) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int j = 0; j < kAmaxUnroll; ++j)
@@ -555,12 +570,18 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     __syncthreads();
     const uint32_t amax_b = amax_sh;
     const float amax = __uint_as_float(amax_b << 16);
-    const bool zero = !(amax > 0.0f);
+    // |g| bit patterns >= 0x7F80 are Inf / NaN ("input error"): the
+    // device status word gets bit 0 and the tensor is treated as all-zero (codes 0,
+    // s_down = 0, no items kept, zero gradients); an all-zero grad_Y sets bit 1
+    // ("degenerate")
+    const bool nonfinite = amax_b >= 0x7F80u;
+    const bool zero = nonfinite || !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
     if (stamp && threadIdx.x == 0) { g_gs_stamp[3][blockIdx.x] = gtimer(); g_gs_stamp[4][blockIdx.x] = 0; }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
         *amax_out = amax_b;
+        if (status != nullptr && zero) atomicOr(status, nonfinite ? kStatusNonFinite : kStatusZeroGrad);
     }
 
     // ---- phase 2: SR + bit split ------------------------------------------
@@ -568,22 +589,14 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(q8 + N * C + c) = make_uint4(0, 0, 0, 0);
     if constexpr (G > 0) {
-        if (exp_flags & 3) {                              // timing experiments: phase 1 only / no Philox
-            if (exp_flags & 2)
-                split_units<G, false, C1Z, true>(g, N, C, __fmul_rn(r8, 4294967296.0f), keys, call_id, token_offset,
-                                                 q8, a_sq, pu0, pu1, pbuf);
-            depart(scratch);
-            return;
-        }
         if (zero) {                                       // all-zero grad_Y: codes 0, norms 0 (zeroed above)
             split_units<G, false, C1Z>(g, N, C, 0.0f, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         } else {
-            const float R32 = __fmul_rn(r8, 4294967296.0f);
             // only elements with |g| = amax can land above 119 (fl32(amax r8) may round up by an ulp)
             if (__fmul_rn(amax, r8) > 119.0f)
-                split_units<G, true, C1Z>(g, N, C, R32, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
+                split_units<G, true, C1Z>(g, N, C, r8, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
             else
-                split_units<G, false, C1Z>(g, N, C, R32, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
+                split_units<G, false, C1Z>(g, N, C, r8, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         }
         if (stamp && lane == 0) atomicMax(&g_gs_stamp[4][blockIdx.x], gtimer());
         depart(scratch);
@@ -619,7 +632,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 int qv[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const float sv = __fmul_rn(v[i], r8);
+                    const float sv = zero ? 0.0f : __fmul_rn(v[i], r8);
                     const float a = fminf(fabsf(sv), 119.0f);
                     const uint64_t A = __float2ull_ru(__fmul_rn(a, 4294967296.0f));   // exact ceil(a 2^32)
                     const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
@@ -660,15 +673,19 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
 
 template <int G, bool C1Z>
 static int grad_split_max_blocks() {
-    static int cached = 0;
-    if (cached == 0) {
-        int per_sm = 0, sms = 0, dev = 0;
-        cudaGetDevice(&dev);
+    static std::atomic<int> cached[kMaxDevices];        // per device ordinal (0 = not yet queried)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    int v = cached[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        int per_sm = 0, sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z>, kSplitThreads, 0);
-        cached = per_sm * sms;
+        v = per_sm * sms;
+        cached[dev].store(v, std::memory_order_relaxed);
     }
-    return cached;
+    return v;
 }
 
 int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
@@ -676,16 +693,11 @@ int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
 template <int G, bool C1Z>
 static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
                                        uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
-                                       float* s_down, uint32_t* amax_out, cudaStream_t s) {
-    static const int exp_flags = getenv("I4_BS_EXP") ? atoi(getenv("I4_BS_EXP")) : 0;   // timing experiments only
+                                       float* s_down, uint32_t* amax_out, int32_t* status, cudaStream_t s) {
     int blocks = grad_split_max_blocks<G, C1Z>();
     const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
     if (blocks > kAmaxWord) blocks = kAmaxWord;
-    static const int p1_env = getenv("I4_BS_P1_STREAM") ? atoi(getenv("I4_BS_P1_STREAM")) : -1;   // experiment
-    // amax pass past L1 (the phase-2 re-reads come from L2 on other SMs): measured
-    // equal or faster on every config with a flushed L2 (ViT FFN-up 229 -> 218 us)
-    const bool p1_stream = p1_env >= 0 ? p1_env != 0 : true;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(blocks));
     cfg.blockDim = dim3(kSplitThreads);
@@ -696,12 +708,12 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
     cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id,
-                                       token_offset, q8, a_sq, s_down, amax_out, exp_flags, p1_stream);
+                                       token_offset, q8, a_sq, s_down, amax_out, status);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id, token_offset,
-                               q8, a_sq, s_down, amax_out, exp_flags, p1_stream);
+                               q8, a_sq, s_down, amax_out, status);
     }
     return e;
 }
@@ -709,40 +721,38 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
 template <int G>
 static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint32_t* block_max,
                                        const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* q8,
-                                       int32_t* a_sq, float* s_down, uint32_t* amax_out, cudaStream_t s) {
+                                       int32_t* a_sq, float* s_down, uint32_t* amax_out, int32_t* status,
+                                       cudaStream_t s) {
     // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
     const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
     if (c1z)
         return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
-                                            amax_out, s);
+                                            amax_out, status, s);
     return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
-                                         amax_out, s);
+                                         amax_out, status, s);
 }
 
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, cudaStream_t s) {
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
     const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
     const int Ci = int(C);
-    const char* env = getenv("I4_BS_GENERIC");            // experiment switch: force the generic phase 2
-    const bool generic = env && env[0] == '1';
-    const char* genv = getenv("I4_BS_G");                 // experiment switch: force the unit size
-    const int gforce = genv ? atoi(genv) : 0;
-#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, s)
+#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, status, s)
     // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
-    // measured equal or slower), else 3, 4, 1
-    if (!generic && (gforce == 0 || gforce == 2) && C % 512 == 0) return I4_GS(2);
-    if (!generic && (gforce == 0 || gforce == 3) && C % 768 == 0) return I4_GS(3);
-    if (!generic && (gforce == 0 || gforce == 4) && C % 1024 == 0) return I4_GS(4);
-    if (!generic && C % 256 == 0) return I4_GS(1);
+    // measured equal or slower), else 3, 1; the one-warp-per-row loop otherwise
+    if (C % 512 == 0) return I4_GS(2);
+    if (C % 768 == 0) return I4_GS(3);
+    if (C % 256 == 0) return I4_GS(1);
 #undef I4_GS
-    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, s);
+    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out,
+                                  status, s);
 }
 
-// debug export for the timing experiment: copies the stamps of the last
-// I4_BS_EXP=8 launch ([5][n] u64, n <= kGradSplitMaxBlocks) to host memory
+// debug export for the timing experiment: copies the stamps of the last launch
+// ([5][n] u64, n <= kGradSplitMaxBlocks) to host memory (-DI4_STAMPS=1 builds only)
 int grad_split_stamps(unsigned long long* host, int n) {
+    if (!kStamps) return -1;
     if (n > kGradSplitMaxBlocks) n = kGradSplitMaxBlocks;
     for (int r = 0; r < 5; ++r)
         if (cudaMemcpyFromSymbol(host + size_t(r) * n, g_gs_stamp, sizeof(unsigned long long) * n,

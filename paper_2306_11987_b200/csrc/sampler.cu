@@ -20,6 +20,7 @@
 // The item scores live in shared memory (16384 items per CTA -> N <= 65536,
 // the same bound the grad_W INT32 accumulator imposes).  The kernel is
 // latency-bound (it moves < 2 MB); it is not an HBM-roofline kernel.
+#include <atomic>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -40,8 +41,6 @@ constexpr int kSmallItemsPerCTA = 4096;
 constexpr int kItemsPerCTA = 16384;
 constexpr int kEMaxW = 4;
 constexpr int kEMaxX = 24;
-
-int sampler_max_tokens() { return kClusterCTAs * kItemsPerCTA / 2; }
 
 // fixed part of the shared memory; the per-item arrays follow it, sized for the
 // CTA's share of the items (launch-time: a small N gets a small footprint):
@@ -120,9 +119,14 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
     parity ^= 1;
 }
 
-// timing experiment: globaltimer stamps of CTA (rank 0, mask 0), thread 0:
-// [0] start [1] scores summed [2..] after each A.2 round, then Bernoulli done,
-// compaction done, end; slot 31 = number of stamps
+// timing experiment, compiled in only by -DI4_STAMPS=1 (tools/smp_stamps.py):
+// globaltimer stamps of CTA (rank 0, mask 0), thread 0: [0] start [1] scores
+// summed [2..] after each A.2 round, then Bernoulli done, compaction done, end;
+// slot 31 = number of stamps
+#ifndef I4_STAMPS
+#define I4_STAMPS 0
+#endif
+constexpr bool kSmpStamps = I4_STAMPS != 0;
 __device__ int g_smp_stamp_on = 0;
 __device__ unsigned long long g_smp_stamp[32];
 __device__ __forceinline__ void smp_stamp(int& n, bool on) {
@@ -136,6 +140,7 @@ __device__ __forceinline__ void smp_stamp(int& n, bool on) {
 }
 
 int sampler_stamps(unsigned long long* host, int enable) {
+    if (!kSmpStamps) return -1;
     if (cudaMemcpyToSymbol(g_smp_stamp_on, &enable, sizeof(int)) != cudaSuccess) return -1;
     if (host && cudaMemcpyFromSymbol(host, g_smp_stamp, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
     return 0;
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(NT, 1)
 lss_sampler_kernel(SamplerArgs a) {
     pdl_trigger();
     pdl_wait();                                   // a_sq / s_down of grad_split
-    const bool st_on = g_smp_stamp_on && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
+    const bool st_on = kSmpStamps && g_smp_stamp_on && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
     int st_n = 0;
     smp_stamp(st_n, st_on);
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -341,36 +346,76 @@ lss_sampler_kernel(SamplerArgs a) {
 }
 
 template <int CL, int NT>
-static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
+static void sampler_config(const SamplerArgs& a, cudaStream_t s, cudaLaunchConfig_t& cfg, cudaLaunchAttribute (&attr)[2]) {
     const int per = (2 * a.N + CL - 1) / CL;
     const int per16 = (per + 15) & ~15;
-    const size_t smem = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
-    const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1 + 1);
-    auto kern = lss_sampler_kernel<CL, NT>;
-    static bool attr_set = false;                 // once per instantiation: the largest footprint
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
-        if (e != cudaSuccess) return e;
-        if (CL > 8) {
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
-        }
-        attr_set = true;
-    }
-    cudaLaunchConfig_t cfg{};
+    cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    int n = CL > 1 ? 1 : 0;
-    if (CL == 1) attr[0] = attr[1];
-    cfg.numAttrs = add_pdl_attr(attr, n);
-    return cudaLaunchKernelEx(&cfg, kern, a);
+    cfg.numAttrs = CL > 1 ? 1 : 0;
 }
+
+// function attributes (largest footprint; non-portable cluster size) once per
+// (instantiation, device) -- they are per-device state of the CUDA context
+template <int CL, int NT>
+static cudaError_t set_attrs() {
+    static std::atomic<int> done[kMaxDevices];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (done[dev].load(std::memory_order_relaxed)) return cudaSuccess;
+    auto kern = lss_sampler_kernel<CL, NT>;
+    const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1 + 1);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
+    if (e == cudaSuccess && CL > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) done[dev].store(1, std::memory_order_relaxed);
+    return e;
+}
+
+template <int CL, int NT>
+static cudaError_t launch_cl(const SamplerArgs& a, cudaStream_t s) {
+    const cudaError_t e = set_attrs<CL, NT>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[2];
+    sampler_config<CL, NT>(a, s, cfg, attr);
+    if (CL == 1) attr[0] = attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, CL > 1 ? 1 : 0);
+    return cudaLaunchKernelEx(&cfg, lss_sampler_kernel<CL, NT>, a);
+}
+
+// Whether a 16-CTA cluster of the 1024-thread sampler at its largest shared-memory
+// footprint can be scheduled on this device (it cannot under MIG / MPS SM limits or
+// with GPCs of fewer than 16 usable SMs).  Queried once per device with the
+// occupancy API, outside any stream capture, so a captured launch never fails.
+static bool cluster16_ok() {
+    static std::atomic<int> ok[kMaxDevices];        // 0 unknown, 1 yes, 2 no
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
+    int v = ok[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        v = 2;
+        if (set_attrs<16, 1024>() == cudaSuccess) {
+            SamplerArgs probe{};
+            probe.N = kItemsPerCTA * 16 / 2;            // the largest footprint a 16-CTA launch uses
+            cudaLaunchConfig_t cfg;
+            cudaLaunchAttribute attr[2];
+            sampler_config<16, 1024>(probe, nullptr, cfg, attr);
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, lss_sampler_kernel<16, 1024>, &cfg) == cudaSuccess && n >= 1) v = 1;
+        }
+        (void)cudaGetLastError();
+        ok[dev].store(v, std::memory_order_relaxed);
+    }
+    return v == 1;
+}
+
+int sampler_max_tokens() { return kClusterCTAs * kItemsPerCTA / 2; }
 
 cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
     // an 8-CTA cluster per mask: the A.2 rounds are dominated by the per-item
@@ -378,14 +423,17 @@ cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
     // on binding budgets); tiny problems use one CTA
     if (2 * int64_t(a.N) <= 2048) return launch_cl<1, 1024>(a, s);
     if (2 * int64_t(a.N) <= int64_t(kClusterCTAs) * kSmallItemsPerCTA) return launch_cl<kClusterCTAs, 512>(a, s);
-    static const int big = getenv("I4_SMP_CL16") ? atoi(getenv("I4_SMP_CL16")) : 1;   // experiment switch
-    if (big && 2 * int64_t(a.N) > int64_t(kClusterCTAs) * 2 * kSmallItemsPerCTA) {
-        // > 8 K items per CTA: a 16-CTA (non-portable) cluster halves each CTA's share
-        const cudaError_t e = launch_cl<16, 1024>(a, s);
-        if (e == cudaSuccess) return e;
-        (void)cudaGetLastError();                  // cluster of 16 refused: fall back to 8
-    }
+    // > 8 K items per CTA: a 16-CTA (non-portable) cluster halves each CTA's share
+    // (ViT sizes 22.6 -> 15.5 us), when two of them (one per mask) fit on the device
+    if (2 * int64_t(a.N) > int64_t(kClusterCTAs) * 2 * kSmallItemsPerCTA && cluster16_ok())
+        return launch_cl<16, 1024>(a, s);
     return launch_cl<kClusterCTAs, 1024>(a, s);
+}
+
+int sampler_cluster_ctas(int64_t N) {
+    if (2 * N <= 2048) return 1;
+    if (2 * N > int64_t(kClusterCTAs) * 2 * kSmallItemsPerCTA && cluster16_ok()) return 16;
+    return kClusterCTAs;
 }
 
 }  // namespace i4

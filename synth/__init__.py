@@ -10,8 +10,10 @@ structure of the paper's workloads, as stated in DESIGN.md "Input recipe".
          per-token scale r_t = 1 for 5 % of tokens, 1e-3 for 90 %, 0 for 5 %
          (padding), times lognormal(0, 0.5) jitter; entries r_t N(0,1).
          dense variant: r_t = 1 for every token.
-  steps  s = 2 mean|T| / sqrt(7) (cold-start rule, PAPER.md:652 A.4) with T the
-         raw tensor (reading: the rule is applied to the untransformed tensor).
+  steps  not generated here: they are operator inputs set by the A.4 cold-start
+         rule, which is method arithmetic -- tests take it from
+         oracle.lsq_grad.cold_start_step, bench.py from the library's
+         lsq_cold_start_step kernel (bit-identical, tests/test_gpu_lsq_grad.py).
 
 Arrays are numpy float32 holding exactly-representable bf16 values, so the
 same bytes can be handed to the oracle (as float64) and to the GPU (as bf16).
@@ -62,11 +64,6 @@ def grad_output(N, C, seed=DATA_SEED, dense=False):
     r = r * rng.lognormal(0.0, 0.5, N).astype(np.float32)
     g = rng.standard_normal((N, C), dtype=np.float32) * r[:, None]
     return _to_bf16_values(g)
-
-
-def cold_start_step(t):
-    """2 mean|T| / sqrt(Q_P), Q_P = 7, as an fp32 scalar."""
-    return np.float32(2.0 * np.abs(np.asarray(t, dtype=np.float64)).mean() / np.sqrt(7.0))
 
 
 # BASELINE.json configs (shapes only; k per SURVEY.md §8(d)).

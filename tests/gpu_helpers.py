@@ -30,3 +30,23 @@ def code_mismatch(gpu_codes, oracle_codes):
     o = oracle_codes.astype(np.int64)
     diff = np.abs(g - o)
     return int((diff > 0).sum()), int(diff.max(initial=0))
+
+
+def item_pairs(items, wexp):
+    """(item id, weight exponent) pairs sorted by item id: the kept set of an LSS
+    mask, independent of the order a kernel stores its list in."""
+    items = np.asarray(items, dtype=np.int64)
+    wexp = np.asarray(wexp, dtype=np.int64)
+    order = np.argsort(items, kind="stable")
+    return np.stack([items[order], wexp[order]])
+
+
+def same_item_set(gpu_items, gpu_wexp, ora):
+    """The GPU's kept (item, weight) set equals the oracle mask `ora` exactly, and
+    no item appears twice."""
+    g = item_pairs(gpu_items, gpu_wexp)
+    if g.shape[1] != ora["count"]:
+        return False
+    if g.shape[1] and np.any(np.diff(g[0]) == 0):
+        return False
+    return np.array_equal(g, item_pairs(ora["items"], ora["wexp"]))

@@ -58,3 +58,11 @@ def test_host_validation_without_gpu():
     st = p.lib.int4_gemm_s8s8s32(None, 0, None, 0, 1, 64, 16, None, None, 0, None)
     assert st != 0
     assert p.lib.int4_last_error()
+
+
+def test_library_reads_no_environment():
+    # no environment switches in the product library --
+    # experiment variants are compile-time (-D) builds under tools/
+    srcs = glob.glob(os.path.join(ROOT, "paper_2306_11987_b200", "csrc", "*"))
+    for path in srcs:
+        assert "getenv" not in open(path).read(), path

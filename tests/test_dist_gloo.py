@@ -12,6 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import synth
+from oracle.lsq_grad import cold_start_step
 from oracle import bitsplit, linear
 
 N_LOCAL, D, C, K = 32, 64, 64, 4
@@ -39,7 +40,7 @@ def _worker(rank, world, port, out_path):
     r, ws = pdist.init(backend="gloo")
     assert (r, ws) == (rank, world)
     x, w, g = _global_batch(world)
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     off = pdist.token_offset(rank, N_LOCAL)
     sl = slice(off, off + N_LOCAL)
     f = linear.forward(x[sl], w, K, s_x, s_w)
@@ -60,7 +61,7 @@ def test_two_rank_gloo_allreduce_matches_serial_shards():
     res = np.load(out)
     # serial emulation of the same shards: per-shard budget, per-shard amax, global offsets
     x, w, g = _global_batch(world)
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     ref = np.zeros((C, D))
     for r in range(world):
         sl = slice(r * N_LOCAL, (r + 1) * N_LOCAL)

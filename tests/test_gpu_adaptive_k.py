@@ -5,6 +5,7 @@ import pytest
 import torch
 
 import synth
+from oracle.lsq_grad import cold_start_step
 from oracle import adaptive_k as o_ak
 from oracle import hadamard as o_had
 
@@ -33,7 +34,7 @@ def _run(x, w, s_x, s_w, k_min, k_max):
 def test_select_k_parity(N, D, C, k_min, k_max):
     x = synth.activations(N, D, seed=N)
     w = synth.weights(C, D, seed=N)
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     k_best, mse, xv, wv = _run(x, w, s_x, s_w, k_min, k_max)
     ks = list(range(k_min, k_max + 1))
     ref_k, table = o_ak.select_k(xv, wv, s_x, s_w, ks)

@@ -6,6 +6,7 @@ import pytest
 import torch
 
 import synth
+from oracle.lsq_grad import cold_start_step
 from oracle import bmm as o_bmm
 from oracle import gemm as o_gemm
 from oracle import lss as o_lss
@@ -28,8 +29,8 @@ def test_bmm_parity(B, N, P, M, k, mode):
     q = np.stack([synth.activations(N, M, seed=10 + b) for b in range(B)])
     kk = np.stack([synth.activations(P, M, seed=20 + b) for b in range(B)])
     dt = np.stack([synth.grad_output(N, P, seed=30 + b, dense=(b % 2 == 0)) for b in range(B)])
-    s_q = np.array([synth.cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
-    s_k = np.array([synth.cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
+    s_q = np.array([cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
+    s_k = np.array([cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
     op = p().Int4BMM(B, N, P, M, k)
     T = torch.empty(B, N, P, dtype=torch.float32, device="cuda")
     op.forward(to_bf16_cuda(q), to_bf16_cuda(kk), s_q, s_k, T)
@@ -72,8 +73,8 @@ def test_bmm_chains_bitwise_independent_of_stream_count(monkeypatch):
     q = np.stack([synth.activations(N, M, seed=50 + b) for b in range(B)])
     kk = np.stack([synth.activations(P, M, seed=60 + b) for b in range(B)])
     dt = np.stack([synth.grad_output(N, P, seed=70 + b, dense=(b % 3 == 0)) for b in range(B)])
-    s_q = np.array([synth.cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
-    s_k = np.array([synth.cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
+    s_q = np.array([cold_start_step(q[b]) for b in range(B)], dtype=np.float32)
+    s_k = np.array([cold_start_step(kk[b]) for b in range(B)], dtype=np.float32)
     outs = []
     for streams in ("1", "16"):
         monkeypatch.setenv("I4_BMM_STREAMS", streams)

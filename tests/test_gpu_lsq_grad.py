@@ -5,6 +5,7 @@ import pytest
 import torch
 
 import synth
+from oracle.lsq_grad import cold_start_step
 from oracle import hq as o_hq
 from oracle import linear as o_lin
 from oracle import lsq_grad as o_lg
@@ -24,7 +25,7 @@ def _case(N, D, C, k, mode, dense=False, seed=0, call_id=3, token_offset=0):
     x = synth.activations(N, D, seed=seed)
     w = synth.weights(C, D, seed=seed)
     g = synth.grad_output(N, C, seed=seed, dense=dense)
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     layer = p().Int4Linear(N, D, C, k, step_grads=True)
     Y = torch.empty(N, C, dtype=torch.float32, device="cuda")
     layer.forward(to_bf16_cuda(x), to_bf16_cuda(w), s_x, s_w, Y)

@@ -12,6 +12,7 @@ import pytest
 import torch
 
 import synth
+from oracle.lsq_grad import cold_start_step
 from oracle import bitsplit as o_bs
 from oracle import gemm as o_gemm
 from oracle import hadamard as o_had
@@ -19,7 +20,7 @@ from oracle import hq as o_hq
 from oracle import linear as o_lin
 from oracle import lss as o_lss
 
-from gpu_helpers import code_mismatch, rel_frob, to_bf16_cuda, unpack_bits
+from gpu_helpers import code_mismatch, rel_frob, same_item_set, to_bf16_cuda, unpack_bits
 
 pytestmark = pytest.mark.gpu
 
@@ -68,7 +69,7 @@ def test_gemm_int32_bit_exact(M, N, K, a_mn, b_mn, split_ws):
 @pytest.mark.parametrize("rows,cols", [(200, 256), (64, 1024)])
 def test_hadamard_quant_codes(k, rows, cols):
     x = synth.activations(rows, cols, seed=k)
-    s = synth.cold_start_step(x)
+    s = cold_start_step(x)
     X = to_bf16_cuda(x)
     codes = torch.empty(rows, cols, dtype=torch.int8, device="cuda")
     bits = torch.empty(rows, cols // 32, dtype=torch.int32, device="cuda")
@@ -106,7 +107,7 @@ def test_hadamard_quant_no_fma_contraction_at_ties():
 def _run_forward(N, D, C, k, y_dtype=torch.float32, seed=0):
     x = synth.activations(N, D, seed=seed)
     w = synth.weights(C, D, seed=seed)
-    s_x, s_w = synth.cold_start_step(x), synth.cold_start_step(w)
+    s_x, s_w = cold_start_step(x), cold_start_step(w)
     layer = p().Int4Linear(N, D, C, k)
     Y = torch.empty(N, C, dtype=y_dtype, device="cuda")
     layer.forward(to_bf16_cuda(x), to_bf16_cuda(w), s_x, s_w, Y)
@@ -175,10 +176,8 @@ def _check_backward(layer, g, s_x, s_w, k, dX, dW, mode, call_id=3, token_offset
     mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, call_id, token_offset, mode)
     cw, cx = [int(v) for v in layer.counts().cpu().numpy()]
     assert cw == mw["count"] and cx == mx["count"]
-    assert np.array_equal(layer.items_w.cpu().numpy()[:cw], mw["items"])
-    assert np.array_equal(layer.wexp_w.cpu().numpy()[:cw], mw["wexp"])
-    assert np.array_equal(layer.items_x.cpu().numpy()[:cx], mx["items"])
-    assert np.array_equal(layer.wexp_x.cpu().numpy()[:cx], mx["wexp"])
+    assert same_item_set(layer.items_w.cpu().numpy()[:cw], layer.wexp_w.cpu().numpy()[:cw], mw)
+    assert same_item_set(layer.items_x.cpu().numpy()[:cx], layer.wexp_x.cpu().numpy()[:cx], mx)
     pad_w = layer.items_w.cpu().numpy()[cw:(cw + 127) // 128 * 128]
     assert np.all(pad_w == 2 * N)
     # (iv) outputs from identical codes and lists
@@ -276,7 +275,7 @@ def test_full_size_sampled_parity(cfg):
     # codes: sampled rows exactly vs oracle
     oc, om, osq = o_hq.hadamard_quant(x[rows], k, s_x)
     nbad, maxdiff = code_mismatch(xq[rows], oc)
-    assert maxdiff <= 1 and nbad <= CODE_FRAC_TOL * xq.size
+    assert maxdiff <= 1 and nbad <= CODE_FRAC_TOL * oc.size    # fraction of the codes compared
     # forward rows
     Y = torch.empty(N, C, dtype=torch.float32, device="cuda")
     layer.forward(to_bf16_cuda(x), to_bf16_cuda(w), s_x, s_w, Y, reuse_weight=True)
@@ -291,8 +290,8 @@ def test_full_size_sampled_parity(cfg):
     mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 3, 0)
     cw, cx = [int(v) for v in layer.counts().cpu().numpy()]
     assert (cw, cx) == (mw["count"], mx["count"])
-    assert np.array_equal(layer.items_w.cpu().numpy()[:cw], mw["items"])
-    assert np.array_equal(layer.items_x.cpu().numpy()[:cx], mx["items"])
+    assert same_item_set(layer.items_w.cpu().numpy()[:cw], layer.wexp_w.cpu().numpy()[:cw], mw)
+    assert same_item_set(layer.items_x.cpu().numpy()[:cx], layer.wexp_x.cpu().numpy()[:cx], mx)
     x_mask = unpack_bits(layer.x_mask, D)
     w_mask = unpack_bits(layer.w_mask, D)
     # grad_X rows of sampled tokens
@@ -402,7 +401,9 @@ def test_sampler_16cta_cluster_parity(dense_g):
     mx = o_lss.sample_activation_mask(bs["a_sq"], synth.PHILOX_SEED, 5, 0)
     cw, cx = int(plan.scalars[2].item()), int(plan.scalars[3].item())
     assert cw == mw["count"] and cx == mx["count"]
-    assert np.array_equal(plan.items_w.cpu().numpy()[:cw], mw["items"])
-    assert np.array_equal(plan.wexp_w.cpu().numpy()[:cw].astype(np.int64), mw["wexp"])
-    assert np.array_equal(plan.items_x.cpu().numpy()[:cx], mx["items"])
-    assert np.array_equal(plan.wexp_x.cpu().numpy()[:cx].astype(np.int64), mx["wexp"])
+    assert same_item_set(plan.items_w.cpu().numpy()[:cw], plan.wexp_w.cpu().numpy()[:cw], mw)
+    assert same_item_set(plan.items_x.cpu().numpy()[:cx], plan.wexp_x.cpu().numpy()[:cx], mx)
+    # the 16-CTA variant is the one that ran, whenever the device can schedule it
+    assert mod.lib.int4_sampler_cluster_ctas(N) in (8, 16)
+    if mod.lib.int4_sampler_cluster_ctas(N) != 16:
+        pytest.skip("16-CTA clusters not schedulable on this device: the 8-CTA sampler ran (checked above)")

@@ -106,3 +106,45 @@ def test_p16_whole_backward_unbiased_monte_carlo():
         # and the estimate is not trivially noisy: relative Frobenius bias small
         assert np.linalg.norm(mean - ref) < 0.05 * np.linalg.norm(ref)
     assert np.mean(kept) <= N + 1            # budget N (plus the 1/16 floor)
+
+
+def test_o12_grad_w_folding_matches_the_paper_form_per_sample():
+    """the oracle's grad_W folds the item weight into the A
+    operand (2^wexp code, |.| <= 128) and s_up = 16 s_down into the B operand
+    (16 X_hat on high-half rows).  For single mask draws (not in expectation) the
+    folded accumulator times s_down must equal, exactly in rationals, the paper's
+    form sum_kept (m_i / p_i) s_h code_i (x) X_hat_t (Eq. 5:
+    s_h = s_up for the high half, s_down for the low), with the drawn weight
+    2^wexp in the role of m_i / p_i; and the finished grad_W must equal
+    s_X [P o I_W] H with P summed item by item in float64."""
+    from fractions import Fraction
+
+    weighted = False
+    for seed in range(4):
+        rng, x, w, fwd = _setup(N=24, C=16, D=32, k=3, seed=seed)
+        g = rng.standard_normal((24, 16)).astype(np.float32) * np.where(rng.random(24) < 0.3, 1.0, 0.02)[:, None]
+        g = g.astype(np.float32)
+        out = linear.backward(g, fwd, seed=seed, call_id=2)
+        bs, mw = out["bs"], out["mask_w"]
+        assert mw["count"] > 0
+        weighted |= bool(np.any(mw["wexp"] > 0))            # the draw up-weighted some items
+        N = g.shape[0]
+        s_down = Fraction(float(bs["s_down"]))
+        xq = fwd["xq"].astype(np.int64)
+        P = np.zeros((16, 32))
+        entries = [(0, 0), (3, 7), (15, 31), (8, 16)]
+        exact = {e: Fraction(0) for e in entries}
+        for i, e in zip(mw["items"], mw["wexp"]):
+            h, t = int(i) // N, int(i) % N
+            code = (bs["hi"] if h == 0 else bs["lo"])[t].astype(np.int64)
+            s_h = 16 * s_down if h == 0 else s_down
+            weight = Fraction(2) ** int(e)
+            P += float(weight) * float(s_h) * np.outer(code, xq[t])
+            for (c, d) in entries:
+                exact[(c, d)] += weight * s_h * int(code[c]) * int(xq[t, d])
+        for (c, d) in entries:
+            assert Fraction(int(out["acc_w"][c, d])) * s_down == exact[(c, d)]
+        H = hadamard.block_diag_hadamard(32, fwd["k"])
+        dw_paper = np.float64(fwd["s_x"]) * (P * fwd["w_mask"]) @ H
+        assert np.allclose(out["dw"], dw_paper, rtol=1e-12, atol=1e-12 * np.abs(dw_paper).max())
+    assert weighted

@@ -2,13 +2,14 @@
 import sys, os, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-import synth, paper_2306_11987_b200 as i4
+import synth
+from oracle.lsq_grad import cold_start_step  # tools only (test infrastructure), paper_2306_11987_b200 as i4
 
 cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2_bert_base_ffn1"]
 N, D, C, k = cfg["N"], cfg["D"], cfg["C"], cfg["k"]
 def up(a): return torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
 X, W, G = up(synth.activations(N, D)), up(synth.weights(C, D)), up(synth.grad_output(N, C))
-s_x, s_w = synth.cold_start_step(synth.activations(N, D)), synth.cold_start_step(synth.weights(C, D))
+s_x, s_w = cold_start_step(synth.activations(N, D)), cold_start_step(synth.weights(C, D))
 layer = i4.Int4Linear(N, D, C, k)
 Y = torch.empty(N, C, dtype=torch.bfloat16, device="cuda")
 dX = torch.empty(N, D, device="cuda"); dW = torch.empty(C, D, device="cuda")

@@ -4,6 +4,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
+from oracle.lsq_grad import cold_start_step  # tools only (test infrastructure)
 import paper_2306_11987_b200 as i4
 
 for name in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
@@ -11,7 +12,7 @@ for name in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
     N, D, C, k = cfg["N"], cfg["D"], cfg["C"], cfg["k"]
     up = lambda a: torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
     X, W, G = up(synth.activations(N, D)), up(synth.weights(C, D)), up(synth.grad_output(N, C))
-    s_x, s_w = synth.cold_start_step(synth.activations(N, D)), synth.cold_start_step(synth.weights(C, D))
+    s_x, s_w = cold_start_step(synth.activations(N, D)), cold_start_step(synth.weights(C, D))
     L = i4.Int4Linear(N, D, C, k)
     Y = torch.empty(N, C, dtype=torch.bfloat16, device="cuda")
     L.forward(X, W, s_x, s_w, Y)
