@@ -20,7 +20,7 @@ __all__ = [
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
     "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step", "hq_select_k", "hq_select_k_workspace_size",
     "int4_bmm_fwd", "int4_bmm_bwd", "Int4BMM", "I4BmmCache",
-    "lsq_cold_start_workspace_size", "cold_start_step", "Int4Linear", "LaunchTrace",
+    "lsq_cold_start_workspace_size", "cold_start_step", "Int4Linear", "BwdScratch", "LaunchTrace",
     "STATUS_NONFINITE", "STATUS_ZERO_GRAD",
 ]
 
@@ -286,16 +286,38 @@ class _PlanBuffers:
                                               "items_x", "wexp_x", "x_touched")}
 
 
+class BwdScratch:
+    """Transient backward buffers (sampling plan, workspace, status word) for
+    token count N and shapes up to D_max x C_max.  They are only live during one
+    int4_linear_bwd, so the linears of a network that run their backwards one
+    after another on one stream share one BwdScratch (the forward caches stay
+    per layer)."""
+
+    def __init__(self, N, D_max, C_max, device="cuda"):
+        import torch
+        dev = torch.device(device)
+        self.N, self.D_max, self.C_max = N, D_max, C_max
+        self.plan_bufs = _PlanBuffers(N, C_max, dev)
+        self.ws = torch.empty(int4_bwd_workspace_size(N, D_max, C_max), dtype=torch.uint8, device=dev)
+        self.status_buf = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.plan_bufs.plan.dev_status = self.status_buf.data_ptr()
+
+    def fits(self, N, D, C):
+        return N == self.N and D <= self.D_max and C <= self.C_max
+
+
 class Int4Linear:
     """Caller-side buffers of one INT4 linear layer shape [N, D] x [C, D].
 
-    Allocates (torch, on `device`) the forward cache, the sampling plan and the
-    backward workspace once; forward / backward then only launch kernels.
+    Allocates (torch, on `device`) the forward cache once, and the sampling plan
+    and backward workspace unless a shared BwdScratch is passed; forward /
+    backward then only launch kernels.
     """
 
-    def __init__(self, N, D, C, k, device="cuda", step_grads=False):
+    def __init__(self, N, D, C, k, device="cuda", step_grads=False, scratch=None):
         """step_grads: also keep the A.3 deltas in the forward cache and return the
-        step-size gradients {grad s_X, grad s_W} from backward (see grad_s())."""
+        step-size gradients {grad s_X, grad s_W} from backward (see grad_s()).
+        scratch: a BwdScratch shared with other layers (None: a private one)."""
         import torch
         self.N, self.D, self.C, self.k = N, D, C, k
         dev = torch.device(device)
@@ -308,14 +330,18 @@ class Int4Linear:
         self.cache = I4FwdCache(xq=self.xq.data_ptr(), wq=self.wq.data_ptr(),
                                 x_mask=self.x_mask.data_ptr(), w_mask=self.w_mask.data_ptr(),
                                 x_sqnorm=self.x_sqnorm.data_ptr(), w_valid=0)
-        self._plan_bufs = _PlanBuffers(N, C, dev)
+        if scratch is None:
+            scratch = BwdScratch(N, D, C, dev)
+        elif not scratch.fits(N, D, C):
+            raise ValueError(f"BwdScratch(N={scratch.N}, D<={scratch.D_max}, C<={scratch.C_max}) too small")
+        self.scratch = scratch
+        self._plan_bufs = scratch.plan_bufs
         self.__dict__.update(self._plan_bufs.views())
         self.plan = self._plan_bufs.plan
-        self.ws = torch.empty(int4_bwd_workspace_size(N, D, C), dtype=torch.uint8, device=dev)
+        self.ws = scratch.ws
         # device status word shared by the forward cache and the plan (I4_STATUS_* bits)
-        self.status_buf = torch.zeros(1, dtype=i32, device=dev)
+        self.status_buf = scratch.status_buf
         self.cache.dev_status = self.status_buf.data_ptr()
-        self.plan.dev_status = self.status_buf.data_ptr()
         self.step_grads = bool(step_grads)
         if self.step_grads:
             self.x_delta = torch.empty(N, D, dtype=f32, device=dev)
@@ -323,13 +349,14 @@ class Int4Linear:
             self.grad_s_buf = torch.zeros(2, dtype=f32, device=dev)
             self.cache.x_delta = self.x_delta.data_ptr()
             self.cache.w_delta = self.w_delta.data_ptr()
-            self.plan.grad_s = self.grad_s_buf.data_ptr()
 
     def forward(self, X, W, s_x, s_w, Y, reuse_weight=False, stream=None):
         self.cache.w_valid = 1 if reuse_weight else 0
         int4_linear_fwd(X, W, self.k, s_x, s_w, Y, self.cache, stream)
 
     def backward(self, dY, dX, dW, seed, call_id=0, token_offset=0, mode=LSS_BERNOULLI, stream=None):
+        # the plan may be shared with other layers: point it at this layer's outputs
+        self.plan.grad_s = self.grad_s_buf.data_ptr() if self.step_grads else None
         int4_linear_bwd(dY, self.cache, seed, call_id, token_offset, mode, self.plan, dX, dW, self.ws, stream)
 
     def status(self):
@@ -354,6 +381,10 @@ class Int4Linear:
         import torch
         off = lib.int4_bwd_ws_det_offset(self.N, self.D, self.C)
         return self.ws[off:off + 8].view(torch.int32)
+
+    def q8_codes(self):
+        """The code plane of the last backward as an [N + 1, C] int8 view."""
+        return self.q8.view(-1)[:(self.N + 1) * self.C].view(self.N + 1, self.C)
 
     def grad_s(self):
         """{grad s_X, grad s_W} of the last backward (A.3), a float32 device tensor."""

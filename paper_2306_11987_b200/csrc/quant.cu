@@ -352,23 +352,70 @@ __device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const P
 //   t  = (M ^ S ^ 0x80) + (S & 1) + 8 per byte  == q + 136 in [16, 255]
 //        (positive: m + 128 + 8; negative: 127 - m + 1 + 8)
 //   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
+// How T = ceil(frac(a) 2^32) and floor(a) are formed (compile-time; all three are
+// the same integers, tests/test_gpu_parity*.py):
+//   0  A = ceil(a 2^32) as u64 by one F2I.U64.CEIL per element (XU pipe)
+//   1  floor(a) by the magic add fl32_rm(a + 2^23) (FADD2.RM), f = a - floor(a)
+//      (exact), T = F2I.U32.CEIL(f 2^32) (XU, a 32-bit conversion)
+//   2  no conversion instruction: z = f 2^9 in [0, 512), zt = fl32_rm(z + 2^23)
+//      holds floor(z) = floor(y / 2^23) in its low mantissa bits, the rest
+//      yl = (z - floor(z)) 2^23 in [0, 2^23) is rounded up by fl32_rp(yl + 2^23)
+//      (FFMA2.RP, exact below 2^24), and T = floor(z) 2^23 + ceil(yl) is put
+//      together from the two bit patterns by one LEA (y = f 2^32)
+#ifndef I4_SR_CVT
+#define I4_SR_CVT 2
+#endif
 template <bool CLAMP>
 __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float r8,
                                              uint2& pq, int& shi, int& slo) {
     const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-    const uint64_t r2 = f2_pack(r8, r8), e2 = f2_pack(4294967296.0f, 4294967296.0f);
+    const uint64_t r2 = f2_pack(r8, r8);
     uint32_t mag[8];
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
         // |g| of elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
         const uint64_t ag = uint64_t((w[i >> 1] << 16) & 0x7FFFFFFFu) | (uint64_t(w[i >> 1] & 0x7FFF0000u) << 32);
-        float y0, y1;
-        f2_unpack(f2_mul(f2_mul(ag, r2), e2), y0, y1);
-        if (CLAMP) { y0 = fminf(y0, 511101108224.0f); y1 = fminf(y1, 511101108224.0f); }   // 119 * 2^32
-        const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
-        mag[i] = uint32_t(A0 >> 32) + (u[i] < uint32_t(A0) ? 1u : 0u);
-        mag[i + 1] = uint32_t(A1 >> 32) + (u[i + 1] < uint32_t(A1) ? 1u : 0u);
+        uint64_t a2 = f2_mul(ag, r2);                                   // a = fl32(|g| r8)
+        if (CLAMP) {
+            float a0, a1;
+            f2_unpack(a2, a0, a1);
+            a2 = f2_pack(fminf(a0, 119.0f), fminf(a1, 119.0f));
+        }
+        if constexpr (I4_SR_CVT == 0) {
+            float y0, y1;
+            f2_unpack(f2_mul(a2, f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);   // exact 2^32 scaling
+            const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
+            mag[i] = uint32_t(A0 >> 32) + (u[i] < uint32_t(A0) ? 1u : 0u);
+            mag[i + 1] = uint32_t(A1 >> 32) + (u[i + 1] < uint32_t(A1) ? 1u : 0u);
+        } else {
+            const uint64_t m23 = f2_pack(8388608.0f, 8388608.0f);
+            const uint64_t t2 = f2_add_rm(a2, m23);                      // 2^23 + floor(a), exact
+            const uint64_t f2 = f2_sub(a2, f2_sub(t2, m23));             // frac(a), exact
+            uint32_t T0, T1;
+            if constexpr (I4_SR_CVT == 1) {
+                float y0, y1;
+                f2_unpack(f2_mul(f2, f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
+                T0 = __float2uint_ru(y0);
+                T1 = __float2uint_ru(y1);
+            } else {
+                const uint64_t z2 = f2_mul(f2, f2_pack(512.0f, 512.0f));  // y / 2^23, exact
+                const uint64_t zt = f2_add_rm(z2, m23);                  // 2^23 + floor(z)
+                const uint64_t zr = f2_sub(z2, f2_sub(zt, m23));         // frac(z), exact
+                const uint64_t cw = f2_fma_rp(zr, m23, m23);             // 2^23 + ceil(frac(z) 2^23)
+                float zt0, zt1, cw0, cw1;
+                f2_unpack(zt, zt0, zt1);
+                f2_unpack(cw, cw0, cw1);
+                // (bits(zt) << 23) drops the exponent bits; bits(cw) - 0x4B000000 = ceil(yl)
+                T0 = (__float_as_uint(zt0) << 23) + __float_as_uint(cw0) - 0x4B000000u;
+                T1 = (__float_as_uint(zt1) << 23) + __float_as_uint(cw1) - 0x4B000000u;
+            }
+            float t0, t1;
+            f2_unpack(t2, t0, t1);
+            // the low byte of bits(t) is floor(a) <= 119 (no carry out of it below)
+            mag[i] = __float_as_uint(t0) + (u[i] < T0 ? 1u : 0u);
+            mag[i + 1] = __float_as_uint(t1) + (u[i + 1] < T1 ? 1u : 0u);
+        }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -589,8 +636,11 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(q8 + N * C + c) = make_uint4(0, 0, 0, 0);
     if constexpr (G > 0) {
-        if (zero) {                                       // all-zero grad_Y: codes 0, norms 0 (zeroed above)
-            split_units<G, false, C1Z>(g, N, C, 0.0f, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
+        if (zero) {                                       // all-zero / non-finite grad_Y: codes 0, norms 0
+            for (int64_t un = pu0; un < pu1; ++un)        // (zeroed in phase 1)
+#pragma unroll
+                for (int gi = 0; gi < G; ++gi)
+                    *reinterpret_cast<uint2*>(q8 + (un * G + gi) * 256 + lane * 8) = make_uint2(0u, 0u);
         } else {
             // only elements with |g| = amax can land above 119 (fl32(amax r8) may round up by an ulp)
             if (__fmul_rn(amax, r8) > 119.0f)

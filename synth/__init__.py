@@ -66,7 +66,10 @@ def grad_output(N, C, seed=DATA_SEED, dense=False):
     return _to_bf16_values(g)
 
 
-# BASELINE.json configs (shapes only; k per SURVEY.md §8(d)).
+# BASELINE.json configs (shapes only; k per SURVEY.md §8(d)).  cfgT: the
+# translation layers north_star names (Transformer-base d = 512, FFN 2048, a
+# 4096-token batch ~ fairseq max-tokens) and the
+# 16384-token variant SURVEY.md §8(d) asks for.
 CONFIGS = {
     "cfg1": dict(N=128, D=64, C=64, k=4),
     "cfg2_bert_base_ffn1": dict(N=4096, D=768, C=3072, k=5),
@@ -75,4 +78,21 @@ CONFIGS = {
     "cfg3_bert_large_ffn_down": dict(N=8192, D=4096, C=1024, k=5),
     "cfg4_vit_b16_ffn_up": dict(N=50432, D=768, C=3072, k=5),
     "cfg4_vit_b16_ffn_down": dict(N=50432, D=3072, C=768, k=5),
+    "cfgT_transformer_base_qkv": dict(N=4096, D=512, C=1536, k=5),
+    "cfgT_transformer_base_ffn_up": dict(N=4096, D=512, C=2048, k=5),
+    "cfgT_transformer_base_ffn_down": dict(N=4096, D=2048, C=512, k=5),
+    "cfgT16k_transformer_base_qkv": dict(N=16384, D=512, C=1536, k=5),
+    "cfgT16k_transformer_base_ffn_up": dict(N=16384, D=512, C=2048, k=5),
+    "cfgT16k_transformer_base_ffn_down": dict(N=16384, D=2048, C=512, k=5),
+}
+
+# Stacks of linears (one training step = every linear's forward, then every
+# backward in reverse layer order).  cfg5 = BASELINE configs[4]: the 24-layer
+# BERT-large linear stack (QKV, FFN-up, FFN-down per layer),
+# N tokens per GPU (token-sharded data parallelism, weak scaling).
+STACKS = {
+    "cfg5_bert_large_stack": dict(layers=24, N=8192, k=5,
+                                  linears=[("qkv", 1024, 3072), ("ffn_up", 1024, 4096), ("ffn_down", 4096, 1024)]),
+    "cfgT_transformer_base_stack": dict(layers=6, N=4096, k=5,
+                                        linears=[("qkv", 512, 1536), ("ffn_up", 512, 2048), ("ffn_down", 2048, 512)]),
 }
