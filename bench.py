@@ -293,7 +293,7 @@ def algorithmic_work(name, N, D, C, kx, kw, dense, moved=None):
         return "ops", 2.0 * rx * C * D
     if name == "gemm_i8_wgrad":
         return "ops", 2.0 * rw * C * D
-    if name == GROUP:
+    if name in (GROUP, "gemm_i8_bwd"):       # grad_X and grad_W GEMMs in one launch
         return "ops", 2.0 * (rx + rw) * C * D
     if name == "hadamard_quant":              # X and W: read bf16, write int8 codes + 1-bit mask (+ int32 norm)
         return "bytes", (N + C) * D * (2 + 1 + 1 / 8) + 4 * N
@@ -731,7 +731,8 @@ def cupti_kernel_times(step, n):
 
 KERNEL_NAMES = [("hadamard_quant_kernel", "hadamard_quant"), ("grad_split_kernel", "grad_split"),
                 ("lss_sampler_kernel", "lss_sampler"), ("compact_kernel", "compact")]
-GEMM_EPI = {"0": "gemm_i8_int32", "1": "gemm_i8_fwd", "2": "gemm_i8_dgrad", "3": "gemm_i8_wgrad"}
+GEMM_EPI = {"0": "gemm_i8_int32", "1": "gemm_i8_fwd", "2": "gemm_i8_dgrad", "3": "gemm_i8_wgrad",
+            "4": "gemm_i8_bwd"}
 
 
 def short_kernel_name(full):

@@ -300,13 +300,9 @@ I4_API size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C);
  * tcgen05 path used by every GEMM of the operator ("Multiply the
  * two INT4 matrices").  A is [M, K] (a_mn_major = 0) or [K, M] (a_mn_major = 1);
  * B is [Nn, K] or [K, Nn]; acc [M, Nn] int32.  K % 16 == 0, Nn % 64 == 0.
- * ws (nullable): zero-initialised scratch of int4_gemm_workspace_size() bytes
- * enabling the deterministic split-K the operator uses for under-filled grids
- * (left zeroed on return).  Exposed for the bit-exact accumulator parity check
- * (SURVEY.md §8(c) (iii)). */
+ * Exposed for the bit-exact accumulator parity check. */
 I4_API i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B, int32_t b_mn_major, int64_t M,
-                                   int64_t Nn, int64_t K, int32_t* acc, void* ws, size_t ws_bytes, void* stream);
-I4_API size_t int4_gemm_workspace_size(void);
+                                   int64_t Nn, int64_t K, int32_t* acc, void* stream);
 
 /* Measurement hook (used by bench.py).  int4_trace_begin arms tracing on the
  * calling thread with `capacity` caller-created cudaEvent_t handles (passed as

@@ -79,7 +79,7 @@ def _load():
         "bitsplit_lss": [vp, i64, i64, vp, u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp],
         "int4_linear_bwd": [vp, ctypes.POINTER(I4FwdCache), u64, u32, i64, i32, ctypes.POINTER(I4LssPlan), vp, i32,
                             vp, vp, ctypes.c_size_t, vp],
-        "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp, ctypes.c_size_t, vp],
+        "int4_gemm_s8s8s32": [vp, i32, vp, i32, i64, i64, i64, vp, vp],
         "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
         "hq_select_k": [vp, i64, vp, i64, i64, f32, f32, i32, i32, vp, vp, vp, ctypes.c_size_t, vp],
         "int4_bmm_fwd": [vp, vp, i64, i64, i64, i64, i32, vp, vp, vp, i32, ctypes.POINTER(I4BmmCache), vp],
@@ -90,8 +90,6 @@ def _load():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
-    L.int4_gemm_workspace_size.argtypes = []
-    L.int4_gemm_workspace_size.restype = ctypes.c_size_t
     L.lsq_cold_start_workspace_size.argtypes = []
     L.lsq_cold_start_workspace_size.restype = ctypes.c_size_t
     L.hq_select_k_workspace_size.argtypes = []
@@ -169,19 +167,13 @@ def int4_bwd_workspace_size(N, D, C):
     return int(lib.int4_bwd_workspace_size(N, D, C))
 
 
-def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, ws=None, stream=None):
+def int4_gemm_s8s8s32(A, B, acc, a_mn_major=False, b_mn_major=False, stream=None):
     """acc[m, n] = sum_k A(m, k) B(n, k), int8 x int8 -> int32 on tcgen05.
-    A is [M, K] or, if a_mn_major, [K, M]; B is [Nn, K] or, if b_mn_major, [K, Nn].
-    ws: optional zeroed uint8 tensor of int4_gemm_workspace_size() bytes (split-K)."""
+    A is [M, K] or, if a_mn_major, [K, M]; B is [Nn, K] or, if b_mn_major, [K, Nn]."""
     M, Nn = acc.shape
     K = A.shape[0] if a_mn_major else A.shape[1]
-    nbytes = 0 if ws is None else ws.numel() * ws.element_size()
     _check(lib.int4_gemm_s8s8s32(_ptr(A), int(a_mn_major), _ptr(B), int(b_mn_major), M, Nn, K, _ptr(acc),
-                                 _ptr(ws), nbytes, _stream(stream)))
-
-
-def int4_gemm_workspace_size():
-    return int(lib.int4_gemm_workspace_size())
+                                 _stream(stream)))
 
 
 def hq_select_k_workspace_size():

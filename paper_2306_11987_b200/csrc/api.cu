@@ -69,16 +69,11 @@ void trace_record(cudaEvent_t e, cudaStream_t s) {
     if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);  // graph node
     else cudaEventRecord(e, s);
 }
-// launches inside a fork / join region are traced as one entry (the region's
-// events sit on the caller's stream, before the fork and after the join)
-thread_local bool g_trace_group = false;
-struct TraceGroupReset { ~TraceGroupReset() { g_trace_group = false; } };   // error paths too
 void trace_pre(cudaStream_t s) {
-    if (g_trace_group) return;
     if (g_trace.active && g_trace.n == g_trace.first && g_trace.cap > 0) trace_record(g_trace.ev[0], s);
 }
 void trace_post(const char* name, cudaStream_t s) {
-    if (!g_trace.active || g_trace_group) return;
+    if (!g_trace.active) return;
     const int w = g_trace.n - g_trace.first;                 // position inside the window
     if (w >= 0 && w + 1 < g_trace.cap) trace_record(g_trace.ev[w + 1], s);
     if (g_trace.n < kMaxTrace) g_trace.names[g_trace.n] = name;
@@ -206,7 +201,7 @@ constexpr int64_t kMaxBwdTokens = 65536;
 
 // One operand of a GEMM: `rows` x `inner` int8 with row pitch `pitch` bytes.
 // K-major: rows = M (or Nn), inner = K.  MN-major: rows = K, inner = M (or Nn).
-struct Operand { const int8_t* p; int64_t rows, inner, pitch; bool gather = false; };
+struct Operand { const int8_t* p; int64_t rows, inner, pitch; };
 
 // A_alt (optional): a second A the kernel may read instead, chosen on the device
 // (the grad_X GEMM reads the code plane Q when its mask is deterministic, Z-32);
@@ -215,7 +210,7 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
                const Operand* A_alt = nullptr, const Operand* A_dense = nullptr, const Operand* B_dense = nullptr) {
     CUtensorMap ta, tb, tc, ta2, ta3, tb2;
     const int bn = i4::gemm_block_n(args.Nn, args.b_mn != 0);
-    bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), A.gather ? 1u : 128u) &&
+    bool ok = make_tmap_i8(&ta, A.p, uint64_t(A.inner), uint64_t(A.rows), uint64_t(A.pitch), 128u) &&
               make_tmap_i8(&tb, B.p, uint64_t(B.inner), uint64_t(B.rows), uint64_t(B.pitch),
                            args.b_mn ? 128u : uint32_t(bn / i4::kGemmCG));
     if (A_alt) ok = ok && make_tmap_i8(&ta2, A_alt->p, uint64_t(A_alt->inner), uint64_t(A_alt->rows),
@@ -233,17 +228,38 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
                                   uint64_t(args.Nn), uint64_t(args.M));
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
-    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2};
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, nullptr, nullptr};
     I4_LAUNCH(i4::launch_gemm(maps, args, sms > 0 ? sms : device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
 
-// Side stream + fork / join events of this host thread (per device), used to
-// run the grad_X and grad_W GEMMs concurrently on disjoint SM sets.  Event
-// record / wait are stream-ordered and capturable (a captured step graph gets
-// two parallel branches).
+// The grad_X and grad_W GEMMs of one backward as ONE persistent launch
+// (EPI_BWD): problem 0 = grad_X (A = compacted items A_X or the code plane Q, K-major;
+// B = W_hat read MN-major), problem 1 = grad_W (A = A_W or Q, B = B_W or X_hat, both
+// MN-major; output dW by TMA store).  Which operands each problem reads (compacted or
+// dense, reading Z-32) is decided on the device from the sampler's flags.
+i4_status gemm_bwd(const Operand& a_x, const Operand& q_rows, const Operand& w_mn, const Operand& a_w,
+                   const Operand& b_w, const Operand& q_mn, const Operand& xq_mn, const i4::GemmArgs& gx,
+                   const i4::GemmArgs& gw, cudaStream_t s) {
+    CUtensorMap ta, tb, tc, ta2, ta3, tb2, taw, tbw;
+    bool ok = make_tmap_i8(&ta, a_x.p, uint64_t(a_x.inner), uint64_t(a_x.rows), uint64_t(a_x.pitch), 128u) &&
+              make_tmap_i8(&ta2, q_rows.p, uint64_t(q_rows.inner), uint64_t(q_rows.rows), uint64_t(q_rows.pitch), 128u) &&
+              make_tmap_i8(&tb, w_mn.p, uint64_t(w_mn.inner), uint64_t(w_mn.rows), uint64_t(w_mn.pitch), 128u) &&
+              make_tmap_i8(&taw, a_w.p, uint64_t(a_w.inner), uint64_t(a_w.rows), uint64_t(a_w.pitch), 128u) &&
+              make_tmap_i8(&tbw, b_w.p, uint64_t(b_w.inner), uint64_t(b_w.rows), uint64_t(b_w.pitch), 128u) &&
+              make_tmap_i8(&ta3, q_mn.p, uint64_t(q_mn.inner), uint64_t(q_mn.rows), uint64_t(q_mn.pitch), 128u) &&
+              make_tmap_i8(&tb2, xq_mn.p, uint64_t(xq_mn.inner), uint64_t(xq_mn.rows), uint64_t(xq_mn.pitch), 128u) &&
+              make_tmap_out(&tc, gw.out, false, false, uint64_t(gw.Nn), uint64_t(gw.M));
+    if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, &taw, &tbw};
+    I4_LAUNCH(i4::launch_gemm(maps, gx, device_info().sms, s, &gw), "gemm_i8_bwd", s);
+    return I4_OK;
+}
+
+// Side streams + fork / join events of this host thread (per device), used to
+// run the batch chains of the attention BMM concurrently.  Event record / wait
+// are stream-ordered and capturable (a captured step graph gets parallel branches).
 struct SideStream { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
-thread_local SideStream t_side;
 #ifndef I4_BMM_MAX_STREAMS
 #define I4_BMM_MAX_STREAMS 16
 #endif
@@ -265,48 +281,6 @@ i4_status make_side(SideStream& st) {
     return I4_OK;
 }
 
-i4_status side_stream(SideStream*& out) {
-    I4_RETURN_IF(make_side(t_side));
-    out = &t_side;
-    return I4_OK;
-}
-
-// Work model of one persistent GEMM on P CTA pairs, in k-block units (the
-// kernel's own split-K choice: choose_splits in gemm.cu, hand-over cost H).
-int64_t gemm_cost_kb(int64_t tiles, int64_t nk, int64_t pairs, int max_splits) {
-    if (tiles <= 0 || nk <= 0) return 0;
-    constexpr int64_t H = 24;
-    int64_t best = ((tiles + pairs - 1) / pairs) * nk;
-    if (tiles <= i4::kSplitMaxTiles)
-        for (int sp = 2; sp <= max_splits; ++sp) {
-            if (nk < 2 * sp) break;
-            best = std::min(best, ((sp * tiles + pairs - 1) / pairs) * ((nk + sp - 1) / sp) + H);
-        }
-    return best;
-}
-
-// SM split for running the grad_X GEMM (tiles_x tiles of nk_x k-blocks, no
-// split-K) beside the grad_W GEMM (tiles_w x nk_w, split-K up to kSplitMaxK):
-// returns the pairs given to grad_X, or 0 when running them one after the other
-// is modelled as faster.  Each launch also costs a fixed prologue / last-tile
-// epilogue (kFixedKb, measured 5-8 us ~ 16 k-blocks) that concurrency overlaps.
-int concurrent_split(int64_t tiles_x, int64_t nk_x, int64_t tiles_w, int64_t nk_w, int64_t pairs) {
-    constexpr int64_t kFixedKb = 16;
-    const int64_t seq = gemm_cost_kb(tiles_x, nk_x, pairs, 1) + gemm_cost_kb(tiles_w, nk_w, pairs, i4::kSplitMaxK) +
-                        2 * kFixedKb;
-    int64_t best = -1, best_px = 0;
-    for (int64_t px = 1; px < pairs; ++px) {
-        // concurrent grad_W runs without split-K: its partial-sum chains stalled the
-        // pipeline when it shared the GPU (BERT-large QKV, 4-way split on 42 pairs:
-        // grad_W 28 -> 103 us)
-        const int64_t c = std::max(gemm_cost_kb(tiles_x, nk_x, px, 1), gemm_cost_kb(tiles_w, nk_w, pairs - px, 1)) +
-                          kFixedKb;
-        if (best < 0 || c < best) { best = c; best_px = px; }
-    }
-    // only on a clear modelled win (BERT-large QKV: modelled 136 vs 144 k-blocks,
-    // measured 159 -> 206 us concurrent; BERT-base FFN1: 64 vs 88, 97 -> 88 us)
-    return best >= 0 && 100 * best < 85 * seq ? int(best_px) : 0;
-}
 
 }  // namespace
 
@@ -404,6 +378,7 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     g.out = Y;
     g.out_bf16 = y_dtype == I4_OUT_BF16;
     g.scale = s_x * s_w;                      // fl32(s_x s_w), reading Z-22
+
     I4_RETURN_IF(gemm(Operand{cache->xq, N, D, D}, Operand{cache->wq, C, D, D}, g, s));
     cache->N = N; cache->D = D; cache->C = C; cache->k = k; cache->s_x = s_x; cache->s_w = s_w;
     return I4_OK;
@@ -458,11 +433,10 @@ i4_status bitsplit_lss(const void* dY, int64_t N, int64_t C, const int32_t* x_sq
 namespace {
 
 // Backward workspace layout (bytes, each region 256-aligned):
-//   A_X [2N+128, C] | A_W [kcap, C] | B_W [kcap, D] | split-K partials (dgrad, wgrad) | split-K flags
+//   A_X [2N+128, C] | A_W [kcap, C] | B_W [kcap, D] | A.3 partials (grad_X, grad_W) | det flags
 struct BwdWs {
     int8_t* a_x; int8_t* a_w; int8_t* b_w;
-    int32_t* part_x; int32_t* part_w; uint32_t* flags_x; uint32_t* flags_w;
-    double* lsq_x; double* lsq_w;        // A.3 fp64 partials (zeroed with the flags by the sampler)
+    double* lsq_x; double* lsq_w;        // A.3 fp64 partials (zeroed by the sampler launch)
     int32_t* det;                        // [2] deterministic-mask flags (written by the sampler)
     size_t total;
 };
@@ -475,10 +449,7 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
     const size_t o_ax = take(size_t((2 * N + 128) * C));
     const size_t o_aw = take(size_t(C * kcap));
     const size_t o_bw = take(size_t(D * kcap));
-    const size_t o_px = take(i4::gemm_split_partial_bytes());
-    const size_t o_pw = take(i4::gemm_split_partial_bytes());
-    // split-K flags and the A.3 partials are one contiguous region: the sampler zeroes it
-    const size_t o_f = take(2 * i4::gemm_split_flag_words() * sizeof(uint32_t) + 2 * i4::kLsqPartials * sizeof(double));
+    const size_t o_f = take(2 * i4::kLsqPartials * sizeof(double));   // the sampler zeroes it
     const size_t o_det = take(2 * sizeof(int32_t));
     w.total = off;
     if (ws) {
@@ -486,11 +457,7 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
         w.a_x = reinterpret_cast<int8_t*>(b + o_ax);
         w.a_w = reinterpret_cast<int8_t*>(b + o_aw);
         w.b_w = reinterpret_cast<int8_t*>(b + o_bw);
-        w.part_x = reinterpret_cast<int32_t*>(b + o_px);
-        w.part_w = reinterpret_cast<int32_t*>(b + o_pw);
-        w.flags_x = reinterpret_cast<uint32_t*>(b + o_f);
-        w.flags_w = w.flags_x + i4::gemm_split_flag_words();
-        w.lsq_x = reinterpret_cast<double*>(w.flags_w + i4::gemm_split_flag_words());
+        w.lsq_x = reinterpret_cast<double*>(b + o_f);
         w.lsq_w = w.lsq_x + i4::kLsqPartials;
         w.det = reinterpret_cast<int32_t*>(b + o_det);
     }
@@ -514,22 +481,19 @@ size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C) {
 
 static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                                  int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
-                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream,
-                                 bool allow_concurrent);
+                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream);
 
 i4_status int4_linear_bwd(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                           int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
                           i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream) {
-    return linear_bwd_impl(dY, cache, seed, call_id, token_offset, mode, plan, dX, dx_dtype, dW, ws, ws_bytes, stream,
-                           true);
+    return linear_bwd_impl(dY, cache, seed, call_id, token_offset, mode, plan, dX, dx_dtype, dW, ws, ws_bytes, stream);
 }
 
 }  // extern "C"
 
 static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
                                  int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan, void* dX,
-                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream,
-                                 bool allow_concurrent) {
+                                 i4_out_dtype dx_dtype, float* dW, void* ws, size_t ws_bytes, void* stream) {
     I4_RETURN_IF(check_device());
     if (!cache || !dX || !dW || !ws) return fail(I4_ERR_ARG, "int4_linear_bwd: NULL pointer");
     if (dx_dtype != I4_OUT_F32 && dx_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "int4_linear_bwd: bad dx_dtype");
@@ -545,12 +509,10 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         return fail(I4_ERR_ARG, "int4_linear_bwd: plan->grad_s needs cache->x_delta and cache->w_delta");
     {
         const BwdWs w0 = carve_bwd_ws(ws, N, D, C);
-        // the sampler launch also zeroes the split-K flags of the two GEMMs below (and
-        // the A.3 partial slots that follow them)
-        const int32_t words = int32_t(2 * i4::gemm_split_flag_words() +
-                                      (want_lsq ? 2 * i4::kLsqPartials * sizeof(double) / sizeof(uint32_t) : 0));
+        // the sampler launch also zeroes the A.3 partial slots of the GEMM launch below
+        const int32_t words = int32_t(want_lsq ? 2 * i4::kLsqPartials * sizeof(double) / sizeof(uint32_t) : 0);
         I4_RETURN_IF(bitsplit_lss_impl(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, s,
-                                       w0.flags_x, words, w0.det));
+                                       reinterpret_cast<uint32_t*>(w0.lsq_x), words, w0.det));
     }
 
     const int64_t kcap = round_up(2 * N, 128);
@@ -566,75 +528,38 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         ca.det_flags = w.det;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
-    // The two GEMMs are independent: when the work model says so (each alone
-    // under-fills the GPU, e.g. grad_X with fewer tiles than CTA pairs and a short
-    // grad_W), grad_W runs on a side stream on the SMs grad_X leaves free.
-    // Sizes are modelled with the budget N as the kept-item count (E[K] <= N).
-    const int64_t pairs = device_info().sms / i4::kGemmCG;
-    const int px = !allow_concurrent ? 0 :
-                   concurrent_split(((N + 255) / 256) * ((D + 255) / 256), (C + 127) / 128,
-                                    ((C + 255) / 256) * ((D + 255) / 256), (N + 127) / 128, pairs);
-    SideStream* side = nullptr;
-    TraceGroupReset trace_group_reset;
-    if (px > 0) {
-        trace_pre(s);                            // the concurrent pair is one trace entry
-        g_trace_group = true;
-        I4_RETURN_IF(side_stream(side));
-        if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
-            return fail(I4_ERR_CUDA, "int4_linear_bwd: fork to the side stream failed");
-    }
-    // grad_X: rows = kept items of the grad_X mask (count on device), K = C, N = D
-    {
-        i4::GemmArgs g{};
-        g.M = int32_t(2 * N + 128); g.m_dev = plan->count_x;
-        g.Nn = int32_t(D); g.K = int32_t(C);
-        g.epi = i4::EPI_DGRAD;
-        g.out = dX;
-        g.out_bf16 = dx_dtype == I4_OUT_BF16;
-        g.scale = cache->s_w * inv_sqrt_block(k);
-        g.s_down = plan->s_down;
-        g.k_had = k;
-        g.mask = cache->x_mask;
-        g.items = plan->items_x;
-        g.wexp = plan->wexp_x;
-        g.n_tokens = int32_t(N);
-        g.b_mn = 1;                              // B = W_hat [C, D] read MN-major (K = C, N = D)
-        g.partial = w.part_x; g.flags = w.flags_x;
-        g.max_tiles_split = i4::kSplitMaxTiles; g.max_splits = 1;   // split-K measured no gain here
-        if (want_lsq) { g.delta = cache->x_delta; g.lsq_part = w.lsq_x; }
-        g.dense_flag = w.det + 1;                // grad_X mask deterministic: rows = tokens of Q
-        const Operand q_rows{plan->q8, N + 1, C, C};
-        I4_RETURN_IF(gemm(Operand{w.a_x, 2 * N + 128, C, C}, Operand{cache->wq, C, D, D}, g, s,
-                          px > 0 ? 2 * px : 0, &q_rows));
-    }
-    // grad_W: M = C, N = D, K = kept items of the grad_W mask (count on device)
-    {
-        i4::GemmArgs g{};
-        g.M = int32_t(C); g.Nn = int32_t(D); g.K = int32_t(kcap); g.k_dev = plan->count_w;
-        g.epi = i4::EPI_WGRAD;
-        g.out = dW;
-        g.scale = cache->s_x * inv_sqrt_block(k);
-        g.s_down = plan->s_down;
-        g.k_had = k;
-        g.mask = cache->w_mask;
-        g.a_mn = 1; g.b_mn = 1;                  // A_W [K items, C], B_W [K, D]: both MN-major
-        g.partial = w.part_w; g.flags = w.flags_w;
-        g.max_tiles_split = i4::kSplitMaxTiles;  // few (C/256 x D/256) tiles, long sampled K
-        g.max_splits = px > 0 ? 1 : i4::kSplitMaxK;   // no split-K beside a concurrent grad_X
-        if (want_lsq) { g.delta = cache->w_delta; g.lsq_part = w.lsq_w; }
-        g.dense_flag = w.det;                    // grad_W mask deterministic: K = tokens, A = Q, B = X_hat
-        g.n_tokens = int32_t(N);
-        const Operand q_k{plan->q8, N + 1, C, C};            // Q as the MN-major A (rows = K = tokens)
-        const Operand xq_k{cache->xq, N, D, D};             // X_hat as the MN-major B
-        I4_RETURN_IF(gemm(Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D}, g, px > 0 ? side->s : s,
-                          px > 0 ? device_info().sms - 2 * px : 0, nullptr, &q_k, &xq_k));
-    }
-    if (px > 0) {
-        g_trace_group = false;
-        if (cudaEventRecord(side->join, side->s) != cudaSuccess || cudaStreamWaitEvent(s, side->join, 0) != cudaSuccess)
-            return fail(I4_ERR_CUDA, "int4_linear_bwd: join from the side stream failed");
-        trace_post("gemm_i8_dgrad||gemm_i8_wgrad", s);
-    }
+    // grad_X and grad_W: one persistent launch over both GEMMs' tiles
+    i4::GemmArgs gx{};                           // grad_X: rows = kept items (count on device), K = C, N = D
+    gx.M = int32_t(2 * N + 128); gx.m_dev = plan->count_x;
+    gx.Nn = int32_t(D); gx.K = int32_t(C);
+    gx.epi = i4::EPI_BWD;
+    gx.out = dX;
+    gx.out_bf16 = dx_dtype == I4_OUT_BF16;
+    gx.scale = cache->s_w * inv_sqrt_block(k);
+    gx.s_down = plan->s_down;
+    gx.k_had = k;
+    gx.mask = cache->x_mask;
+    gx.items = plan->items_x;
+    gx.wexp = plan->wexp_x;
+    gx.n_tokens = int32_t(N);
+    gx.b_mn = 1;                                 // B = W_hat [C, D] read MN-major (K = C, N = D)
+    if (want_lsq) { gx.delta = cache->x_delta; gx.lsq_part = w.lsq_x; }
+    gx.dense_flag = w.det + 1;                   // grad_X mask deterministic: rows = tokens of Q
+    i4::GemmArgs gw{};                           // grad_W: M = C, N = D, K = kept items (count on device)
+    gw.M = int32_t(C); gw.Nn = int32_t(D); gw.K = int32_t(kcap); gw.k_dev = plan->count_w;
+    gw.epi = i4::EPI_WGRAD;
+    gw.out = dW;
+    gw.scale = cache->s_x * inv_sqrt_block(k);
+    gw.s_down = plan->s_down;
+    gw.k_had = k;
+    gw.mask = cache->w_mask;
+    gw.a_mn = 1; gw.b_mn = 1;                    // A_W [K items, C], B_W [K, D]: both MN-major
+    if (want_lsq) { gw.delta = cache->w_delta; gw.lsq_part = w.lsq_w; }
+    gw.dense_flag = w.det;                       // grad_W mask deterministic: K = tokens, A = Q, B = X_hat
+    gw.n_tokens = int32_t(N);
+    I4_RETURN_IF(gemm_bwd(Operand{w.a_x, 2 * N + 128, C, C}, Operand{plan->q8, N + 1, C, C},
+                          Operand{cache->wq, C, D, D}, Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D},
+                          Operand{plan->q8, N + 1, C, C}, Operand{cache->xq, N, D, D}, gx, gw, s));
     if (want_lsq) {
         // A.3: g(s) = 1 / sqrt(Q_P N_elem), Q_P = 7 (reading Z-29 for N_elem)
         const double nx = double(plan->n_elem_x > 0 ? plan->n_elem_x : N * D);
@@ -732,7 +657,7 @@ i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s
         I4_RETURN_IF(linear_bwd_impl(static_cast<const uint16_t*>(dT) + b * N * P, &v, seed, call_id, b * N, mode,
                                      plans + j, static_cast<uint8_t*>(dQ) + size_t(b * N * M) * oq, dq_dtype,
                                      dK + b * P * M, static_cast<uint8_t*>(ws) + size_t(j) * per_ws, per_ws,
-                                     j == 0 ? s0 : t_bmm[j - 1].s, S == 1));
+                                     j == 0 ? s0 : t_bmm[j - 1].s));
     }
     for (int j = 1; j < S; ++j)
         if (cudaEventRecord(t_bmm[j - 1].join, t_bmm[j - 1].s) != cudaSuccess ||
@@ -786,32 +711,21 @@ i4_status lsq_cold_start_step(const void* x_bf16, int64_t n, float* step, void* 
 }
 
 i4_status int4_gemm_s8s8s32(const int8_t* A, int32_t a_mn_major, const int8_t* B, int32_t b_mn_major, int64_t M,
-                            int64_t Nn, int64_t K, int32_t* acc, void* ws, size_t ws_bytes, void* stream) {
+                            int64_t Nn, int64_t K, int32_t* acc, void* stream) {
     I4_RETURN_IF(check_device());
     if (!A || !B || !acc) return fail(I4_ERR_ARG, "int4_gemm_s8s8s32: NULL pointer");
     if (M <= 0 || Nn <= 0 || K <= 0 || Nn % 64 || K % 16 || (a_mn_major && M % 16))
         return fail(I4_ERR_SHAPE, "int4_gemm_s8s8s32: unsupported shape M=%lld Nn=%lld K=%lld", (long long)M,
                     (long long)Nn, (long long)K);
-    if (ws && ws_bytes < int4_gemm_workspace_size()) return fail(I4_ERR_WORKSPACE, "int4_gemm_s8s8s32: ws too small");
     if (!aligned16(A) || !aligned16(B) || !aligned16(acc)) return fail(I4_ERR_ALIGN, "int4_gemm_s8s8s32: unaligned pointer");
     i4::GemmArgs g{};
     g.M = int32_t(M); g.Nn = int32_t(Nn); g.K = int32_t(K);
     g.a_mn = a_mn_major != 0; g.b_mn = b_mn_major != 0;
     g.epi = i4::EPI_INT32;
     g.out = acc;
-    if (ws) {                                    // deterministic split-K over the caller's zeroed workspace
-        g.partial = static_cast<int32_t*>(ws);
-        g.flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + i4::gemm_split_partial_bytes());
-        g.max_tiles_split = i4::kSplitMaxTiles;
-        g.max_splits = i4::kSplitMaxK;
-    }
     const Operand a = g.a_mn ? Operand{A, K, M, M} : Operand{A, M, K, K};
     const Operand b = g.b_mn ? Operand{B, K, Nn, Nn} : Operand{B, Nn, K, K};
     return gemm(a, b, g, static_cast<cudaStream_t>(stream));
-}
-
-size_t int4_gemm_workspace_size(void) {
-    return i4::gemm_split_partial_bytes() + i4::gemm_split_flag_words() * sizeof(uint32_t);
 }
 
 }  // extern "C"

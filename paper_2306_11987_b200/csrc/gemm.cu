@@ -9,20 +9,20 @@
 //   transposed in memory (the paper's CUTLASS path needed explicit
 //   transpose+contiguous copies).
 //
-// Structure (one CTA per SM, persistent over output tiles, warp-specialised).
-// CG = 2 (default): a CTA pair (thread-block cluster of 2 on one TPC) computes a
-// 256 x BN tile with tcgen05.mma.cta_group::2: each CTA stages its 128 rows of
-// A and BN/2 rows of B, so per-SM operand traffic is half that of a 1-SM
-// 128 x BN tile; the leader CTA issues the MMAs for both.
+// Structure (one CTA per SM, persistent, warp-specialised).  A CTA pair
+// (thread-block cluster of 2 on one TPC) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2: each CTA stages its 128 rows of A and BN/2 rows of
+// B, so per-SM operand traffic is half that of a 1-SM 128 x BN tile; the leader
+// CTA issues the MMAs for both.
 //   warp 0   TMA producer: 128-byte-swizzled A (128 x 128 B) and B (BN/CG x 128 B)
 //            tiles into a STAGES-deep shared-memory ring; completion counted on
 //            the leader's mbarrier (2-SM TMA), slots released by a multicast commit.
 //   warp 1   allocates 2 x BN TMEM columns (cta_group::CG); the leader's lane 0
-//            issues tcgen05.mma (M = 128 CG, N = BN, K = 32 per instruction, 4 per
+//            issues tcgen05.mma (M = 256, N = BN, K = 32 per instruction, 4 per
 //            128-deep k-block) and tcgen05.commit to release stages / publish
 //            accumulators to both CTAs.
-//   warps 2-5 (2-9)  epilogue, one (two) per TMEM lane group -- with 8 warps each
-//            takes half of the tile's columns: tcgen05.ld (32 lanes x 32 columns) -> registers, then
+//   warps 2-9 (2-5)  epilogue, two (one) per TMEM lane group: tcgen05.ld (32 lanes x
+//            32 columns) -> registers, then
 //            EPI_INT32  raw accumulators (bit-exact parity checks)
 //            EPI_FWD    Y = fl32(acc) * fl32(s_x s_w)   (HQ-MM step 4)
 //            EPI_WGRAD  v = acc * s_x s_down 2^{-k/2}; v = I_W o v; v = v H; dW
@@ -32,11 +32,28 @@
 //                       so s_up = 16 s_down is folded in);
 //                       v = I_X[t] o v; v = v H; rows are token-major, so a token's
 //                       two items are adjacent lanes: summed by a shuffle and stored
-//                       once (pairs straddling a 32-row group: red.add.v4 of 2
+//                       once (pairs straddling a 32-row group: red.add of 2
 //                       addends onto a zeroed row -- order-independent)
+//            EPI_BWD    the grad_X (problem 0, EPI_DGRAD) and grad_W (problem 1,
+//                       EPI_WGRAD) GEMMs of one backward in ONE persistent launch:
+//                       their tiles share one schedule, so neither under-fills the GPU
 //   Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of
 //   tile i+1.  M (grad_X: kept items) or K (grad_W: kept items) may be read
 //   from device memory, so the sampled sizes never travel to the host.
+//
+// Schedule (static, deterministic).  The output tiles of the launch are dealt
+// to the CTA pairs before any work starts; every CTA derives the same
+// assignment from the (device-resident) problem sizes.  One problem: tile
+// p + j P goes to pair p.  EPI_BWD (two problems whose tiles have different
+// lengths in k-blocks, e.g. 64 k-block grad_W tiles next to 24 k-block grad_X
+// tiles for BERT-large QKV): the long tiles are dealt round-robin, then every
+// pair gets a contiguous run of short tiles sized so that its k-block total
+// comes as close as the tile granularity allows to the average W / P (extra
+// tiles first to the pairs with the most room) -- a closed-form longest-first
+// balance (QKV: 96 k-blocks on the busiest pair instead of 112 round-robin).
+// (A stream-K split of tiles across pairs, with exact INT32 partial sums, was
+// built and measured slower on every shape here: each piece costs a full
+// accumulator hand-over through L2.)
 #include <cuda.h>
 
 #include "common.cuh"
@@ -48,6 +65,17 @@ constexpr int kBM = 128;
 constexpr int kBK = 128;                     // bytes = int8 elements along K per stage
 constexpr int kStageOutBytes = 4096;         // per epilogue warp per buffer: 32 rows x 128 B
 constexpr int kMaxEpiWarps = 8;
+#ifndef I4_GEMM_SCHED
+#define I4_GEMM_SCHED 2                      // 0 round-robin, 1 balanced long-first, 2 balanced short-first
+#endif
+constexpr bool kBalance = I4_GEMM_SCHED != 0;
+constexpr bool kShortFirst = I4_GEMM_SCHED == 2;
+#ifndef I4_EPI_KB_DGRAD
+#define I4_EPI_KB_DGRAD 14                   // measured: a 256 x 256 grad_X tile's epilogue ~ 14 k-blocks of MMA
+#endif
+#ifndef I4_EPI_KB_WGRAD
+#define I4_EPI_KB_WGRAD 8
+#endif
 
 // Epilogue warps: 4 (one per TMEM lane group) or 8 (two per lane group, each
 // taking one half of the tile's columns) -- the epilogue (tcgen05.ld, scaling,
@@ -82,30 +110,6 @@ struct GemmCfg {
 // 16-byte chunk c of staging row r (128-byte rows, SWIZZLE_128B pattern)
 __device__ __forceinline__ uint8_t* stage_chunk(uint8_t* buf, int r, int c) {
     return buf + r * 128 + ((c ^ (r & 7)) << 4);
-}
-
-// Deterministic split-K (used when there are fewer output tiles than CTA pairs,
-// e.g. the grad_W GEMM whose K is the sampled-item count): S splits of the K
-// range are separate work units; the unit of the highest K split writes its raw
-// INT32 accumulators to a workspace tile, each lower split waits for it, adds
-// its own accumulators (integer adds: exact and order-independent) and passes
-// it on, and split 0 runs the real epilogue.  Units are numbered so that a unit
-// only ever waits on a lower-numbered one, so a persistent grid of co-resident
-// CTAs cannot deadlock.
-// The partial-sum hand-over costs about kSplitHandoverKb k-blocks of MMA time
-// (measured: a 2-way split of a 32-k-block grad_W took longer than none).
-#ifndef I4_SPLIT_HANDOVER_KB
-#define I4_SPLIT_HANDOVER_KB 24
-#endif
-constexpr int kSplitHandoverKb = I4_SPLIT_HANDOVER_KB;
-__device__ __forceinline__ int choose_splits(int tiles, int pairs, int nk, int max_splits) {
-    int best = 1, best_cost = ((tiles + pairs - 1) / pairs) * nk;
-    for (int s = 2; s <= max_splits; ++s) {
-        if (nk < 2 * s) break;
-        const int cost = ((s * tiles + pairs - 1) / pairs) * ((nk + s - 1) / s) + kSplitHandoverKb;
-        if (cost < best_cost) { best = s; best_cost = cost; }
-    }
-    return best;
 }
 
 // mask word j of a warp's preloaded column range (j is a compile-time index
@@ -144,25 +148,134 @@ __device__ __forceinline__ void masked_scaled_fwht(const uint32_t (&r)[CW / 32][
     for (int j = 0; j < HALF; ++j) f2_unpack(p[j], v[j], v[j + HALF]);
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+// ---------------------------------------------------------------------------- schedule
+// Device-resolved size of one problem of the launch.
+struct ProbSize { int M, K, m_tiles, n_tiles, T, nk; bool dense; };
+
+template <int EPI, int BMP, int BN>
+__device__ __forceinline__ ProbSize prob_size(const GemmArgs& g) {
+    ProbSize s{};
+    // dense mode (the mask kept every nonzero item with weight 1, reading Z-32): the
+    // operands are the 8-bit code plane Q and X_hat themselves, one row per token
+    s.dense = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr && __ldg(g.dense_flag) != 0;
+    s.M = (EPI == EPI_DGRAD && s.dense) ? g.n_tokens : (g.m_dev ? __ldg(g.m_dev) : g.M);
+    s.K = (EPI == EPI_WGRAD && s.dense) ? ((g.n_tokens + kBK - 1) / kBK) * kBK
+                                        : (g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K);
+    s.m_tiles = (s.M + BMP - 1) / BMP;
+    s.n_tiles = (g.Nn + BN - 1) / BN;
+    s.T = s.m_tiles * s.n_tiles;
+    s.nk = (s.K + kBK - 1) / kBK;
+    return s;
 }
 
-// KH: Hadamard order k of the grad epilogues (compile-time, 0 for FWD / INT32)
+// Tile assignment.  Tiles are numbered problem 0 first (T0 tiles of L0 k-blocks)
+// then problem 1 (T1 of L1).  The "long" class (larger k-blocks per tile) is dealt
+// round-robin; the "short" class is cut into contiguous runs, run p of length
+// quota(p) starting at start(p), so that pair p's total approaches W / P.
+struct Sched {
+    int P;                         // CTA pairs
+    int T0, L0, T1, L1;            // tiles and k-blocks per tile of problem 0 and problem 1
+    bool two;                      // two-class balance (else round-robin over all tiles)
+    int long_prob;                 // problem of the long class
+    int TL, LL, TS, LS;            // long / short class: tiles, k-blocks per tile
+    int r1;                        // pairs 0 .. r1-1 hold one long tile more than the others
+    int qx, qy;                    // base short quota of those pairs / of the others
+    int R;                         // short tiles left after the base quotas (>= 0 here)
+    bool y_first;                  // the extra short tiles go to pairs r1.. first
+    // E0, E1: a tile's cost floor in k-blocks (its epilogue time: a short-K grad_X tile
+    // is epilogue-bound), so tile p's weight is max(k-blocks, E)
+    __device__ void init(int P_, int T0_, int L0_, int T1_, int L1_, int E0, int E1) {
+        P = P_; T0 = T0_; L0 = L0_; T1 = T1_; L1 = L1_;
+        two = kBalance && T1 > 0 && T0 > 0 && L0 > 0 && L1 > 0;
+        if (!two) return;
+        const int w0 = L0 > E0 ? L0 : E0, w1 = L1 > E1 ? L1 : E1;
+        long_prob = w1 >= w0 ? 1 : 0;
+        TL = long_prob ? T1 : T0; LL = long_prob ? w1 : w0;
+        TS = long_prob ? T0 : T1; LS = long_prob ? w0 : w1;
+        const int64_t W = int64_t(TL) * LL + int64_t(TS) * LS;
+        const int64_t tau = (W + P - 1) / P;
+        r1 = TL % P;
+        const int64_t lx = int64_t(TL / P + 1) * LL, ly = int64_t(TL / P) * LL;
+        qx = tau > lx ? int((tau - lx) / LS) : 0;
+        qy = tau > ly ? int((tau - ly) / LS) : 0;
+        int64_t base = int64_t(r1) * qx + int64_t(P - r1) * qy;
+        // never more short tiles than there are: trim the base quotas (pairs with long
+        // tiles first) -- only possible through the rounding of tau
+        while (base > TS) {
+            if (qx > 0 && r1 > 0 && lx + int64_t(qx) * LS >= ly + int64_t(qy) * LS) { --qx; base -= r1; }
+            else if (qy > 0) { --qy; base -= P - r1; }
+            else { --qx; base -= r1; }
+        }
+        R = int(TS - base);
+        const int64_t slack_x = tau - lx - int64_t(qx) * LS, slack_y = tau - ly - int64_t(qy) * LS;
+        y_first = r1 == 0 || slack_y >= slack_x;
+    }
+    __device__ int nlong(int p) const { return TL / P + (p < r1 ? 1 : 0); }
+    // number of pairs r < p whose priority rank is below m (the first m of the order
+    // get one extra short tile)
+    __device__ int n_extra_before(int p, int m) const {
+        if (m <= 0) return 0;
+        if (!y_first) return p < m ? p : m;                                   // order 0, 1, ..., P-1
+        const int xs = min(p, r1), ys = max(0, p - r1);                       // order r1.., then 0..r1-1
+        const int cy = min(ys, m);
+        const int cx = max(0, min(xs, m - (P - r1)));
+        return cy + cx;
+    }
+    __device__ bool extra(int p, int m) const {
+        const int rank = y_first ? (p >= r1 ? p - r1 : (P - r1) + p) : p;
+        return rank < m;
+    }
+    __device__ int quota(int p) const { return (p < r1 ? qx : qy) + R / P + (extra(p, R % P) ? 1 : 0); }
+    __device__ int start(int p) const {
+        return min(p, r1) * qx + max(0, p - r1) * qy + p * (R / P) + n_extra_before(p, R % P);
+    }
+};
+
+// j-th tile of pair p
+struct Seg { int prob, tile, nk; bool valid; };
+
+__device__ __forceinline__ Seg seg_at(const Sched& s, int p, int j) {
+    Seg r{};
+    if (!s.two) {
+        const int t = p + j * s.P;
+        if (t >= s.T0 + s.T1) return r;
+        r.prob = t < s.T0 ? 0 : 1;
+        r.tile = t < s.T0 ? t : t - s.T0;
+    } else {
+        const int nl = s.nlong(p), ns = s.quota(p);
+        if (kShortFirst ? j >= ns : j < nl) {          // a long tile
+            const int jl = kShortFirst ? j - ns : j;
+            if (jl >= nl) return r;
+            r.prob = s.long_prob;
+            r.tile = p + jl * s.P;
+        } else {
+            const int js = kShortFirst ? j : j - nl;
+            if (js >= ns) return r;
+            r.prob = 1 - s.long_prob;
+            r.tile = s.start(p) + js;
+        }
+    }
+    r.nk = r.prob == 0 ? s.L0 : s.L1;
+    r.valid = true;
+    return r;
+}
+
+// ---------------------------------------------------------------------------- kernel
+struct GemmMapSet { CUtensorMap m[8]; };
+enum { MAP_A = 0, MAP_B = 1, MAP_C = 2, MAP_A2 = 3, MAP_A3 = 4, MAP_B2 = 5, MAP_AW = 6, MAP_BW = 7 };
+
+// KH: Hadamard order k of the grad epilogues (compile-time, 0 for FWD / INT32).
+// EPI_BWD: problem 0 = grad_X (A K-major, B MN-major, args g), problem 1 = grad_W
+// (A and B MN-major, args g1); A_MN / B_MN describe the single-problem kinds.
 template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG>
-__global__ void __launch_bounds__(EpiShape<BN, EPI, kh_ch(KH)>::THREADS, 1)
-gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
-               const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
+__global__ void __launch_bounds__(EpiShape<BN, (EPI == EPI_BWD ? EPI_WGRAD : EPI), kh_ch(KH)>::THREADS, 1)
+gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const GemmArgs g1) {
+    constexpr bool kBwd = EPI == EPI_BWD;
+    constexpr int EPI0 = kBwd ? EPI_DGRAD : EPI;                 // kind of problem 0
     constexpr int CH = kh_ch(KH);
-    using Epi = EpiShape<BN, EPI, CH>;
+    using Epi = EpiShape<BN, (kBwd ? EPI_WGRAD : EPI), CH>;
     constexpr int kEpiWarps = Epi::WARPS;
-    using Cfg = GemmCfg<BN, CG, kEpiWarps, EPI, Epi::COLS>;
+    using Cfg = GemmCfg<BN, CG, kEpiWarps, (kBwd ? EPI_WGRAD : EPI), Epi::COLS>;
     constexpr int BMP = kBM * CG;                // rows per (pair) tile
     constexpr int BNC = BN / CG;                 // B rows / columns staged by this CTA
     constexpr int STAGES = Cfg::STAGES;
@@ -183,11 +296,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int pair0 = int(blockIdx.x) / CG, n_pairs = int(gridDim.x) / CG;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmA);
-        if (EPI == EPI_DGRAD) tma_prefetch_desc(&tmA2);
-        if (EPI == EPI_WGRAD) { tma_prefetch_desc(&tmA3); tma_prefetch_desc(&tmB2); }
-        tma_prefetch_desc(&tmB);
-        if (EPI != EPI_DGRAD) tma_prefetch_desc(&tmC);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) tma_prefetch_desc(&maps.m[i]);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CG * kEpiWarps); }
         fence_mbar_init();
@@ -200,126 +310,94 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     pdl_trigger();
     pdl_wait();                                  // operands / metadata of the previous kernels
 
-    // problem size (possibly data-dependent, so read after the PDL wait) and work units
-    // dense mode (the mask kept every nonzero item with weight 1, reading Z-12): the
-    // operands are the 8-bit code plane Q and X_hat themselves, one row per token
-    const bool dense = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr && __ldg(g.dense_flag) != 0;
-    const int M = (EPI == EPI_DGRAD && dense) ? g.n_tokens : (g.m_dev ? __ldg(g.m_dev) : g.M);
-    const int K = (EPI == EPI_WGRAD && dense) ? ((g.n_tokens + kBK - 1) / kBK) * kBK
-                                                : (g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K);
-    const int m_tiles = (M + BMP - 1) / BMP;
-    const int n_tiles = (g.Nn + BN - 1) / BN;
-    const int T = m_tiles * n_tiles;
-    const int nk = (K + kBK - 1) / kBK;
-    const int S = (g.partial != nullptr && T <= g.max_tiles_split) ? choose_splits(T, n_pairs, nk, g.max_splits) : 1;
-    const int units = S * T;
-    // unit u: tile = u % T; split s = S - 1 - u / T (s = 0 is the final one), k-blocks [kb0, kb1)
-#define UNIT_DECODE(u)                                          \
-    const int tile = (u) % T;                                   \
-    const int split = S - 1 - (u) / T;                          \
-    const int kb0 = split * nk / S, kb1 = (split + 1) * nk / S;
-
+    // problem sizes (possibly data-dependent, so read after the PDL wait) and the schedule
+    const ProbSize s0 = prob_size<EPI0, BMP, BN>(g);
+    ProbSize s1{};
+    if constexpr (kBwd) s1 = prob_size<EPI_WGRAD, BMP, BN>(g1);
+    Sched sc;
+    sc.init(n_pairs, s0.T, s0.nk, kBwd ? s1.T : 0, kBwd ? s1.nk : 0, I4_EPI_KB_DGRAD, I4_EPI_KB_WGRAD);
+    // per-pair constants of the short-class run (computed once, used by every warp)
+#define SEG(j) seg_at(sc, pair0, (j))
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer (warp 0)
-        // lane 0 issues the TMA; with a gathered A the 32 lanes first fetch the
-        // 128 row indices of the stage (4 per lane) and hand them out by shuffles.
-        const bool gather = g.a_gather != nullptr;
-        const CUtensorMap* pA = &tmA;
-        const CUtensorMap* pB = &tmB;
-        if (EPI == EPI_DGRAD && dense) pA = &tmA2;                     // Q, K-major
-        if (EPI == EPI_WGRAD) {
-            if (dense) { pA = &tmA3; pB = &tmB2; }                    // Q and X_hat, MN-major
-        }
-        const int gcount = gather ? __ldg(g.gather_count) : 0;
-        auto load_idx4 = [&](int r) {
-            int4 v;
-            v.x = r + 0 < gcount ? __ldg(g.a_gather + r + 0) : g.gather_zero_row;
-            v.y = r + 1 < gcount ? __ldg(g.a_gather + r + 1) : g.gather_zero_row;
-            v.z = r + 2 < gcount ? __ldg(g.a_gather + r + 2) : g.gather_zero_row;
-            v.w = r + 3 < gcount ? __ldg(g.a_gather + r + 3) : g.gather_zero_row;
-            return v;
-        };
         int stage = 0; uint32_t phase = 0;
-        for (int u = pair0; u < units; u += n_pairs) {
-            UNIT_DECODE(u)
-            const int m0 = (tile / n_tiles) * BMP + kBM * int(rank);   // this CTA's A rows
-            const int nb = (tile % n_tiles) * BN + BNC * int(rank);    // this CTA's B rows
-            int4 gidx = make_int4(0, 0, 0, 0), gnext = make_int4(0, 0, 0, 0);
-            if (gather && !A_MN) gidx = load_idx4(m0 + 4 * lane);       // rows of the tile (grad_X)
-            if (gather && A_MN && kb0 < kb1) gnext = load_idx4(kb0 * kBK + 4 * lane);   // K rows (grad_W)
-            for (int kb = kb0; kb < kb1; ++kb) {
-                if (gather && A_MN) {                 // indices of this stage; prefetch the next stage's
-                    gidx = gnext;
-                    if (kb + 1 < kb1) gnext = load_idx4((kb + 1) * kBK + 4 * lane);
-                }
+        for (int j = 0;; ++j) {
+            const Seg sg = SEG(j);
+            if (!sg.valid) break;
+            const bool p1 = kBwd && sg.prob == 1;
+            const ProbSize& ps = p1 ? s1 : s0;
+            const bool a_mn = kBwd ? p1 : A_MN;
+            const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank);     // this CTA's A rows
+            const int nb = (sg.tile % ps.n_tiles) * BN + BNC * int(rank);      // this CTA's B rows
+            const CUtensorMap* pA = &maps.m[MAP_A];
+            const CUtensorMap* pB = &maps.m[MAP_B];
+            if ((EPI == EPI_DGRAD || (kBwd && !p1)) && ps.dense) pA = &maps.m[MAP_A2];    // Q, K-major
+            if (EPI == EPI_WGRAD || p1) {
+                if (ps.dense) { pA = &maps.m[MAP_A3]; pB = &maps.m[MAP_B2]; }              // Q and X_hat, MN-major
+                else if (kBwd) { pA = &maps.m[MAP_AW]; pB = &maps.m[MAP_BW]; }
+            }
+            for (int kb = 0; kb < sg.nk; ++kb) {
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
-                }
-                __syncwarp();
-                uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
-                uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
-                const uint32_t fb = CG == 2 ? mapa_shared(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
-                if (gather)                            // every lane issues the gather of its own 4 rows
-                    tma_gather4<CG>(a_dst + lane * 4 * 128, pA, fb, A_MN ? m0 : kb * kBK,
-                                    gidx.x, gidx.y, gidx.z, gidx.w);
-                if (lane == 0) {
+                    uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+                    uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
                     if constexpr (CG == 2) {
-                        if (!gather) {
-                            if (A_MN) tma_load_2d_2sm(a_dst, pA, fb, m0, kb * kBK);
-                            else      tma_load_2d_2sm(a_dst, pA, fb, kb * kBK, m0);
-                        }
-                        if (B_MN) {
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (a_mn) tma_load_2d_2sm(a_dst, pA, fb, m0, kb * kBK);
+                        else      tma_load_2d_2sm(a_dst, pA, fb, kb * kBK, m0);
+                        if (B_MN || kBwd) {
 #pragma unroll
-                            for (int j = 0; j < BNC / 128; ++j)
-                                tma_load_2d_2sm(b_dst + j * 128 * kBK, pB, fb, nb + 128 * j, kb * kBK);
+                            for (int q = 0; q < BNC / 128; ++q)
+                                tma_load_2d_2sm(b_dst + q * 128 * kBK, pB, fb, nb + 128 * q, kb * kBK);
                         } else {
                             tma_load_2d_2sm(b_dst, pB, fb, kb * kBK, nb);
                         }
                     } else {
-                        if (!gather) {
-                            if (A_MN) tma_load_2d(a_dst, pA, &full[stage], m0, kb * kBK);
-                            else      tma_load_2d(a_dst, pA, &full[stage], kb * kBK, m0);
-                        }
-                        if (B_MN) {
+                        if (a_mn) tma_load_2d(a_dst, pA, &full[stage], m0, kb * kBK);
+                        else      tma_load_2d(a_dst, pA, &full[stage], kb * kBK, m0);
+                        if (B_MN || kBwd) {
 #pragma unroll
-                            for (int j = 0; j < BNC / 128; ++j)
-                                tma_load_2d(b_dst + j * 128 * kBK, pB, &full[stage], nb + 128 * j, kb * kBK);
+                            for (int q = 0; q < BNC / 128; ++q)
+                                tma_load_2d(b_dst + q * 128 * kBK, pB, &full[stage], nb + 128 * q, kb * kBK);
                         } else {
                             tma_load_2d(b_dst, pB, &full[stage], kb * kBK, nb);
                         }
                     }
                 }
+                __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer (leader CTA)
         if (lane == 0 && leader) {
-            constexpr uint32_t idesc = idesc_i8(BMP, BN, A_MN, B_MN);
-            // descriptor advance per K = 32 MMA: K-major +32 B; MN-major +32 rows x 128 B
-            constexpr uint64_t a_step = A_MN ? (32 * 128) >> 4 : 32 >> 4;
-            constexpr uint64_t b_step = B_MN ? (32 * 128) >> 4 : 32 >> 4;
-            int stage = 0; uint32_t phase = 0; int it = 0;
-            for (int u = pair0; u < units; u += n_pairs, ++it) {
-                UNIT_DECODE(u)
-                (void)tile;
-                const int as = it & 1;
-                const uint32_t ap = (it >> 1) & 1;
+            int stage = 0; uint32_t phase = 0;
+            for (int j = 0;; ++j) {
+                const Seg sg = SEG(j);
+                if (!sg.valid) break;
+                const bool a_mn = kBwd ? sg.prob == 1 : A_MN;
+                constexpr bool b_mn = B_MN || kBwd;
+                const uint32_t idesc = idesc_i8(BMP, BN, a_mn, b_mn);
+                // descriptor advance per K = 32 MMA: K-major +32 B; MN-major +32 rows x 128 B
+                const uint64_t a_step = a_mn ? (32 * 128) >> 4 : 32 >> 4;
+                constexpr uint64_t b_step = b_mn ? (32 * 128) >> 4 : 32 >> 4;
+                const int as = j & 1;
+                const uint32_t ap = (j >> 1) & 1;
                 mbar_wait(&tempty[as], ap ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(as * BN);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = 0; kb < sg.nk; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
-                    const uint64_t adesc = A_MN ? sdesc_mnmajor_sw128(a_addr, 128 * kBK) : sdesc_kmajor_sw128(a_addr);
-                    const uint64_t bdesc = B_MN ? sdesc_mnmajor_sw128(b_addr, 128 * kBK) : sdesc_kmajor_sw128(b_addr);
+                    const uint64_t adesc = a_mn ? sdesc_mnmajor_sw128(a_addr, 128 * kBK) : sdesc_kmajor_sw128(a_addr);
+                    const uint64_t bdesc = b_mn ? sdesc_mnmajor_sw128(b_addr, 128 * kBK) : sdesc_kmajor_sw128(b_addr);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 32; ++kk) {
-                        const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+                        const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
                         if constexpr (CG == 2) umma_i8_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, acc);
                         else umma_i8(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, idesc, acc);
                     }
@@ -335,97 +413,86 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int ew = warp - 2;                       // epilogue warp index
         const int cbeg = (ew >> 2) * Epi::COLS;        // this warp's column range [cbeg, cbeg + COLS)
         const int r_in_tile = lg * 32 + lane;
-        const int words = g.Nn >> 5;
-        uint8_t* stg = sOut + (warp - 2) * (Cfg::OUT_BYTES / kEpiWarps);
+        uint8_t* stg = sOut + (warp - 2) * (Cfg::OUT_BYTES > 0 ? Cfg::OUT_BYTES / kEpiWarps : 0);
         int sbuf = 0;
         float sd = 1.0f;
-        if (EPI == EPI_DGRAD || EPI == EPI_WGRAD) sd = __ldg(g.s_down);
-        // Row metadata (kept item, its neighbours, its weight exponent) and the mask
-        // words of this warp's columns are loaded two / one tile(s) ahead: the mask
-        // row of a grad_X item depends on the item index, and both loads would
-        // otherwise sit as two dependent global-memory latencies on every tile.
-        constexpr bool kMask = EPI == EPI_DGRAD || EPI == EPI_WGRAD;
+        if (EPI0 == EPI_DGRAD || EPI0 == EPI_WGRAD) sd = __ldg(g.s_down);
+        constexpr bool kMask = EPI0 == EPI_DGRAD || EPI0 == EPI_WGRAD;
         constexpr int NW = kMask ? Epi::COLS / 32 : 1;
         const int two_n = 2 * g.n_tokens;
-        // Loaded two tiles ahead and left raw until the tile is processed (a consumer
-        // right after the load -- e.g. the int8 sign extension of the weight
-        // exponent -- made every tile wait for the load, ncu: long-scoreboard on
-        // the epilogue warps): the item of this lane's row, the items of the rows
-        // just outside the warp's 32 (lanes 31 / 0 only; inner neighbours come by
-        // shuffle at use time) and the 32-bit word holding the weight exponent.
+        // Row metadata (kept item, its neighbours, its weight exponent) and the mask
+        // words of this warp's columns are loaded two / one segment(s) ahead: the mask
+        // row of a grad_X item depends on the item index, and both loads would
+        // otherwise sit as two dependent global-memory latencies on every tile.  Left
+        // raw until the tile is processed (a consumer right after the load made every
+        // tile wait for it, ncu: long-scoreboard on the epilogue warps).
         struct RowInfo { int item, edge, eword, rw; };
-        auto load_ri = [&](int u) {
+        auto is_dg = [&](const Seg& sg) { return EPI0 == EPI_DGRAD && (!kBwd || sg.prob == 0); };
+        auto load_ri = [&](const Seg& sg) {
             RowInfo x{two_n, two_n, 0, 0};
-            if (EPI == EPI_DGRAD && u < units) {
-                const int tl = u % T;
-                const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+            if (sg.valid && is_dg(sg)) {
+                const int rw = (sg.tile / s0.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
                 x.rw = rw;
-                if (rw < M && dense) {
+                if (rw < s0.M && s0.dense) {
                     x.item = rw;                       // token rw, weight 1, never paired
-                } else if (rw < M) {
+                } else if (rw < s0.M) {
                     x.item = __ldg(g.items + rw);
                     x.eword = int(__ldg(reinterpret_cast<const uint32_t*>(g.wexp + (rw & ~3))));
-                    if (lane == 31 && rw + 1 < M) x.edge = __ldg(g.items + rw + 1);
+                    if (lane == 31 && rw + 1 < s0.M) x.edge = __ldg(g.items + rw + 1);
                     if (lane == 0 && rw > 0) x.edge = __ldg(g.items + rw - 1);
                 }
             }
             return x;
         };
-        auto load_mask = [&](int u, const RowInfo& x, uint32_t (&mw)[NW]) {
+        auto load_mask = [&](const Seg& sg, const RowInfo& x, uint32_t (&mw)[NW]) {
 #pragma unroll
             for (int q = 0; q < NW; ++q) mw[q] = 0u;
-            if (!kMask || u >= units) return;
-            const int tl = u % T;
-            const int rw = (tl / n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+            if (!kMask || !sg.valid) return;
+            const bool dg = is_dg(sg);
+            const ProbSize& ps = (kBwd && sg.prob == 1) ? s1 : s0;
+            const GemmArgs& G = (kBwd && sg.prob == 1) ? g1 : g;
+            const int rw = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
             int64_t mrow = rw;
-            if (EPI == EPI_DGRAD) {
+            if (dg) {
                 if (x.item >= two_n) return;
                 mrow = x.item >= g.n_tokens ? x.item - g.n_tokens : x.item;
-            } else if (rw >= M) {
+            } else if (rw >= ps.M) {
                 return;
             }
-            const int cw0 = ((tl % n_tiles) * BN + cbeg) >> 5;
+            const int words = G.Nn >> 5;
+            const int cw0 = ((sg.tile % ps.n_tiles) * BN + cbeg) >> 5;
 #pragma unroll
             for (int q = 0; q < NW; ++q)
-                if (cw0 + q < words) mw[q] = __ldg(g.mask + mrow * words + cw0 + q);
+                if (cw0 + q < words) mw[q] = __ldg(G.mask + mrow * words + cw0 + q);
         };
-        RowInfo ri_cur = load_ri(pair0), ri_next = load_ri(pair0 + n_pairs);
+        Seg sg_cur = SEG(0), sg_next = SEG(1);
+        RowInfo ri_cur = load_ri(sg_cur), ri_next = load_ri(sg_next);
         uint32_t mw_cur[NW];
-        load_mask(pair0, ri_cur, mw_cur);
-        double lsq_acc = 0.0;                          // A.3 partial of this lane
-        int it = 0;
-        for (int u = pair0; u < units; u += n_pairs, ++it) {
-            UNIT_DECODE(u)
+        load_mask(sg_cur, ri_cur, mw_cur);
+        double lsq_acc[2] = {0.0, 0.0};                // A.3 partials of this lane (per problem)
+        for (int j = 0; sg_cur.valid; ++j) {
+            const Seg sg = sg_cur;
+            const Seg sg_next2 = SEG(j + 2);
             uint32_t mw_next[NW];
-            load_mask(u + n_pairs, ri_next, mw_next);  // ri_next arrived during the previous tile
-            const RowInfo ri_next2 = load_ri(u + 2 * n_pairs);
-            const int as = it & 1;
-            const uint32_t ap = (it >> 1) & 1;
-            const int m0 = (tile / n_tiles) * BMP + kBM * int(rank), n0 = (tile % n_tiles) * BN;
+            load_mask(sg_next, ri_next, mw_next);      // ri_next arrived during the previous segment
+            const RowInfo ri_next2 = load_ri(sg_next2);
+            const bool p1 = kBwd && sg.prob == 1;
+            const bool dg = is_dg(sg);
+            const GemmArgs& G = p1 ? g1 : g;
+            const ProbSize& ps = p1 ? s1 : s0;
+            const int as = j & 1;
+            const uint32_t ap = (j >> 1) & 1;
+            const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank), n0 = (sg.tile % ps.n_tiles) * BN;
             const int row = m0 + r_in_tile;
-            const bool no_acc = kb1 == kb0;            // empty K range: accumulator is zero
-            // split-K bookkeeping for this warp's 32 rows of the tile
-            int32_t* part = nullptr;
-            uint32_t* flag = nullptr;
-            if (S > 1) {
-                part = g.partial + (int64_t(tile) * BMP + kBM * int(rank) + r_in_tile) * BN;
-                flag = g.flags + (tile * CG + int(rank)) * kMaxEpiWarps + ew;
-                if (split < S - 1) {                   // wait until the higher splits are in `part`
-                    if (lane == 0) while (ld_acquire_u32(flag) < uint32_t(S - 1 - split)) { }
-                    __syncwarp();
-                }
-            }
+            const bool no_acc = sg.nk == 0;            // empty K range: accumulator is zero
 
             // per-row setup
-            bool valid = row < M;
+            bool valid = row < ps.M;
             int64_t out_row = row;
-            float rscale = g.scale;
-            // grad_X rows are token-major kept items: a token's two items are adjacent
-            // rows; the first adds its neighbour's values (shuffle) and stores plainly;
-            // pairs straddling a 32-row group use red.add onto rows zeroed beforehand
+            float rscale = G.scale;
             int dmode = 0;                             // 0 store, 1 store pair sum, 2 skip, 3 red.add
             int row_e = 0;                             // dgrad: log2 of the item's weight
-            if (EPI == EPI_DGRAD) {
+            if (dg) {
                 const int item = ri_cur.item;
                 valid = valid && item < two_n;
                 const int h = item >= g.n_tokens ? 1 : 0;
@@ -437,10 +504,10 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 int pv = __shfl_up_sync(0xFFFFFFFFu, ri_cur.item, 1);
                 if (lane == 31) nx = ri_cur.edge;
                 if (lane == 0) pv = ri_cur.edge;
-                if (row + 1 >= M || dense) nx = two_n;
-                if (row == 0 || dense) pv = two_n;
+                if (row + 1 >= ps.M || ps.dense) nx = two_n;
+                if (row == 0 || ps.dense) pv = two_n;
                 row_e = e;
-                rscale = ldexpf(__fmul_rn(g.scale, sd), e);   // s_up = 16 s_down is inside the A codes
+                rscale = ldexpf(__fmul_rn(G.scale, sd), e);   // s_up = 16 s_down is inside the A codes
                 const int inext = valid ? nx : two_n;
                 const int iprev = valid ? pv : two_n;
                 const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;
@@ -448,8 +515,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if ((first && lane == 31) || (second && lane == 0)) dmode = 3;
                 else if (second) dmode = 2;
                 else if (first) dmode = 1;
-            } else if (EPI == EPI_WGRAD) {
-                rscale = __fmul_rn(g.scale, sd);
+            } else if (EPI0 == EPI_WGRAD || p1) {
+                rscale = __fmul_rn(G.scale, sd);
             }
             mbar_wait(&tfull[as], ap);
             tc_fence_after();
@@ -470,40 +537,18 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         else mbar_arrive(&tempty[as]);
                     }
                 }
-                if (nk == 0 || no_acc) {
+                if (no_acc) {
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) r[q][i] = 0;
                 }
-                if (S > 1) {
-                    int32_t* pc = part + c;
-                    if (split < S - 1) {               // add the higher splits' partial sums (exact)
-#pragma unroll
-                        for (int q = 0; q < CW / 32; ++q)
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4) {
-                                const int4 v = __ldcg(reinterpret_cast<const int4*>(pc + 32 * q + i));
-                                r[q][i] += uint32_t(v.x); r[q][i + 1] += uint32_t(v.y);
-                                r[q][i + 2] += uint32_t(v.z); r[q][i + 3] += uint32_t(v.w);
-                            }
-                    }
-                    if (split > 0) {                   // pass the running sum on; no output yet
-#pragma unroll
-                        for (int q = 0; q < CW / 32; ++q)
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4)
-                                __stcg(reinterpret_cast<int4*>(pc + 32 * q + i),
-                                       make_int4(int(r[q][i]), int(r[q][i + 1]), int(r[q][i + 2]), int(r[q][i + 3])));
-                        continue;
-                    }
-                }
                 const int col0 = n0 + c;
-                if (col0 >= g.Nn) continue;           // ragged N (MN-major B): nothing to write
-                if (kMask && g.lsq_part != nullptr && valid) {
+                if (col0 >= G.Nn) continue;           // ragged N (MN-major B): nothing to write
+                if (kMask && G.lsq_part != nullptr && valid) {
                     // A.3 step-size gradient: sum_d acc[d] delta[row, d] (fp32 in column order,
                     // then fp64 across chunks; the dgrad item weight 2^e applied exactly)
-                    const float* dp = g.delta + (EPI == EPI_DGRAD ? out_row : int64_t(row)) * g.Nn + col0;
+                    const float* dp = G.delta + (dg ? out_row : int64_t(row)) * G.Nn + col0;
                     float cs = 0.0f;
 #pragma unroll
                     for (int q = 0; q < CW / 32; ++q)
@@ -515,13 +560,13 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             cs = __fmaf_rn(float(int32_t(r[q][i + 2])), d4.z, cs);
                             cs = __fmaf_rn(float(int32_t(r[q][i + 3])), d4.w, cs);
                         }
-                    lsq_acc += EPI == EPI_DGRAD ? ldexp(double(cs), row_e) : double(cs);
+                    lsq_acc[p1 ? 1 : 0] += dg ? ldexp(double(cs), row_e) : double(cs);
                 }
 
-                if (EPI == EPI_DGRAD) {
+                if (dg) {
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
-                    if (!dense) {                           // token rows (dense) have no partner item
+                    if (!ps.dense) {                        // token rows (dense) have no partner item
 #pragma unroll
                         for (int i = 0; i < CW; ++i) {     // warp-wide: every lane takes part
                             const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
@@ -560,39 +605,41 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
 
                 // value transform into 32-bit words, then stage 32 x 128 B sub-tiles
-                if (EPI == EPI_FWD && g.out_bf16) {
-                    // 64 bf16 columns = one 128-byte staging row
-                    uint32_t packed[32];
+                if constexpr (EPI == EPI_FWD) {
+                    if (g.out_bf16) {
+                        // 64 bf16 columns = one 128-byte staging row
+                        uint32_t packed[CW / 2];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float a = __fmul_rn(float(int32_t(r[i >> 4][(2 * i) & 31])), rscale);
-                        const float b = __fmul_rn(float(int32_t(r[i >> 4][(2 * i + 1) & 31])), rscale);
-                        __nv_bfloat162 p2 = __floats2bfloat162_rn(a, b);
-                        packed[i] = *reinterpret_cast<uint32_t*>(&p2);
+                        for (int i = 0; i < CW / 2; ++i) {
+                            const float a = __fmul_rn(float(int32_t(r[(2 * i) >> 5][(2 * i) & 31])), rscale);
+                            const float b = __fmul_rn(float(int32_t(r[(2 * i + 1) >> 5][(2 * i + 1) & 31])), rscale);
+                            __nv_bfloat162 p2 = __floats2bfloat162_rn(a, b);
+                            packed[i] = *reinterpret_cast<uint32_t*>(&p2);
+                        }
+                        if (lane == 0) bulk_wait_read<1>();
+                        __syncwarp();
+                        uint8_t* buf = stg + sbuf * kStageOutBytes;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<uint4*>(stage_chunk(buf, lane, q)) =
+                                make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) { tma_store_2d(&maps.m[MAP_C], buf, col0, m0 + lg * 32); bulk_commit(); }
+                        sbuf ^= 1;
+                        continue;
                     }
-                    if (lane == 0) bulk_wait_read<1>();
-                    __syncwarp();
-                    uint8_t* buf = stg + sbuf * kStageOutBytes;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        *reinterpret_cast<uint4*>(stage_chunk(buf, lane, q)) =
-                            make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) { tma_store_2d(&tmC, buf, col0, m0 + lg * 32); bulk_commit(); }
-                    sbuf ^= 1;
-                    continue;
                 }
 
                 uint32_t wv[CW];                      // 32-bit output words (int32 or fp32 bits)
-                if (EPI == EPI_INT32) {
+                if constexpr (EPI == EPI_INT32) {
 #pragma unroll
                     for (int i = 0; i < CW; ++i) wv[i] = r[i >> 5][i & 31];
-                } else if (EPI == EPI_FWD) {
+                } else if constexpr (EPI == EPI_FWD) {
 #pragma unroll
                     for (int i = 0; i < CW; ++i)
                         wv[i] = __float_as_uint(__fmul_rn(float(int32_t(r[i >> 5][i & 31])), rscale));
-                } else {                              // EPI_WGRAD
+                } else {                              // EPI_WGRAD (or problem 1 of EPI_BWD)
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
 #pragma unroll
@@ -600,38 +647,35 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
 #pragma unroll
                 for (int q = 0; q < CW / 32; ++q) {
-                    if (col0 + 32 * q >= g.Nn) break;
+                    if (col0 + 32 * q >= G.Nn) break;
                     if (lane == 0) bulk_wait_read<1>();
                     __syncwarp();
                     uint8_t* buf = stg + sbuf * kStageOutBytes;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        *reinterpret_cast<uint4*>(stage_chunk(buf, lane, j)) =
-                            make_uint4(wv[32 * q + 4 * j], wv[32 * q + 4 * j + 1], wv[32 * q + 4 * j + 2], wv[32 * q + 4 * j + 3]);
+                    for (int jj = 0; jj < 8; ++jj)
+                        *reinterpret_cast<uint4*>(stage_chunk(buf, lane, jj)) =
+                            make_uint4(wv[32 * q + 4 * jj], wv[32 * q + 4 * jj + 1], wv[32 * q + 4 * jj + 2], wv[32 * q + 4 * jj + 3]);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) { tma_store_2d(&tmC, buf, col0 + 32 * q, m0 + lg * 32); bulk_commit(); }
+                    if (lane == 0) { tma_store_2d(&maps.m[MAP_C], buf, col0 + 32 * q, m0 + lg * 32); bulk_commit(); }
                     sbuf ^= 1;
                 }
             }
             ri_cur = ri_next; ri_next = ri_next2;
 #pragma unroll
             for (int q = 0; q < NW; ++q) mw_cur[q] = mw_next[q];
-            if (S > 1) {
-                __syncwarp();
-                if (split > 0) {                       // publish: this warp's rows now hold S - split splits
-                    __threadfence();
-                    if (lane == 0) st_release_u32(flag, uint32_t(S - split));
-                } else if (lane == 0) {
-                    *flag = 0u;                        // consumed: reset for the next launch
-                }
-            }
+            sg_cur = sg_next; sg_next = sg_next2;
         }
-#undef UNIT_DECODE
+#undef SEG
         if (kMask && g.lsq_part != nullptr) {          // fixed-order warp sum -> this warp's slot
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) lsq_acc += __shfl_xor_sync(0xFFFFFFFFu, lsq_acc, o);
-            if (lane == 0) g.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc;
+            for (int o = 16; o > 0; o >>= 1) lsq_acc[0] += __shfl_xor_sync(0xFFFFFFFFu, lsq_acc[0], o);
+            if (lane == 0) g.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc[0];
+        }
+        if (kBwd && g1.lsq_part != nullptr) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lsq_acc[1] += __shfl_xor_sync(0xFFFFFFFFu, lsq_acc[1], o);
+            if (lane == 0) g1.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc[1];
         }
         bulk_wait<0>();                                // every lane: its own copies are done
         __syncwarp();
@@ -643,9 +687,6 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 1) tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
 }
 
-size_t gemm_split_partial_bytes() { return size_t(kSplitMaxTiles) * (kBM * kGemmCG) * 256 * sizeof(int32_t); }
-size_t gemm_split_flag_words() { return size_t(kSplitMaxTiles) * kGemmCG * kMaxEpiWarps; }
-
 int gemm_block_n(int Nn, bool b_mn) {
     if (Nn % 256 == 0 || b_mn) return 256;      // MN-major B halves are whole 128-byte atoms
     if (Nn % 128 == 0) return 128;
@@ -655,12 +696,16 @@ int gemm_block_n(int Nn, bool b_mn) {
 constexpr int kCG = kGemmCG;                    // CTA pairs (cta_group::2) for every GEMM
 
 template <int BN, int EPI, int KH, bool A_MN, bool B_MN>
-static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
+static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid, cudaStream_t s) {
     auto kern = gemm_i8_kernel<BN, EPI, KH, A_MN, B_MN, kCG>;
-    using Epi = EpiShape<BN, EPI, kh_ch(KH)>;
-    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS, EPI, Epi::COLS>::SMEM;
+    constexpr int EPIC = EPI == EPI_BWD ? EPI_WGRAD : EPI;
+    using Epi = EpiShape<BN, EPIC, kh_ch(KH)>;
+    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS, EPIC, Epi::COLS>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    GemmMapSet ms;
+    const void* src[8] = {m.a, m.b, m.c, m.a2, m.a3, m.b2, m.aw, m.bw};
+    for (int i = 0; i < 8; ++i) ms.m[i] = *reinterpret_cast<const CUtensorMap*>(src[i] ? src[i] : m.a);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(Epi::THREADS);
@@ -671,59 +716,64 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, int grid, cu
     attr[0].val.clusterDim.x = kCG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
-    return cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(m.a),
-                              *reinterpret_cast<const CUtensorMap*>(m.b), *reinterpret_cast<const CUtensorMap*>(m.c),
-                              *reinterpret_cast<const CUtensorMap*>(m.a2 ? m.a2 : m.a),
-                              *reinterpret_cast<const CUtensorMap*>(m.a3 ? m.a3 : m.a),
-                              *reinterpret_cast<const CUtensorMap*>(m.b2 ? m.b2 : m.b), g);
+    return cudaLaunchKernelEx(&cfg, kern, ms, g, g1);
 }
 
 template <int EPI, int KH, bool A_MN, bool B_MN>
-static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    if (bn == 256) return launch_one<256, EPI, KH, A_MN, B_MN>(m, g, grid, s);
-    if constexpr (!B_MN) {
-        if (bn == 128) return launch_one<128, EPI, KH, A_MN, B_MN>(m, g, grid, s);
-        if constexpr (kh_ch(KH) <= 64) return launch_one<64, EPI, KH, A_MN, B_MN>(m, g, grid, s);
+static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid,
+                               cudaStream_t s) {
+    if (bn == 256) return launch_one<256, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
+    if constexpr (!B_MN && EPI != EPI_BWD) {
+        if (bn == 128) return launch_one<128, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
+        if constexpr (kh_ch(KH) <= 64) return launch_one<64, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
     }
     return cudaErrorInvalidValue;
 }
 
 template <int EPI, bool A_MN, bool B_MN>
-static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, int grid, cudaStream_t s) {
-    if constexpr (EPI == EPI_DGRAD || EPI == EPI_WGRAD) {
+static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid,
+                               cudaStream_t s) {
+    if constexpr (EPI == EPI_DGRAD || EPI == EPI_WGRAD || EPI == EPI_BWD) {
         switch (g.k_had) {
-            case 0: return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, grid, s);
-            case 1: return dispatch_bn<EPI, 1, A_MN, B_MN>(bn, m, g, grid, s);
-            case 2: return dispatch_bn<EPI, 2, A_MN, B_MN>(bn, m, g, grid, s);
-            case 3: return dispatch_bn<EPI, 3, A_MN, B_MN>(bn, m, g, grid, s);
-            case 4: return dispatch_bn<EPI, 4, A_MN, B_MN>(bn, m, g, grid, s);
-            case 5: return dispatch_bn<EPI, 5, A_MN, B_MN>(bn, m, g, grid, s);
-            case 6: return dispatch_bn<EPI, 6, A_MN, B_MN>(bn, m, g, grid, s);
-            case 7: return dispatch_bn<EPI, 7, A_MN, B_MN>(bn, m, g, grid, s);
+            case 0: return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 1: return dispatch_bn<EPI, 1, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 2: return dispatch_bn<EPI, 2, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 3: return dispatch_bn<EPI, 3, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 4: return dispatch_bn<EPI, 4, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 5: return dispatch_bn<EPI, 5, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 6: return dispatch_bn<EPI, 6, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 7: return dispatch_bn<EPI, 7, A_MN, B_MN>(bn, m, g, g1, grid, s);
             default: return cudaErrorInvalidValue;
         }
     } else {
-        return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, grid, s);
+        return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, g1, grid, s);
     }
 }
 
-cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s) {
-    const int bn = gemm_block_n(g.Nn, g.b_mn);
-    const int64_t tiles = int64_t((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
+cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s, const GemmArgs* g1) {
+    const int bn = g.epi == EPI_BWD ? 256 : gemm_block_n(g.Nn, g.b_mn);
     const int64_t pairs = num_sms / kCG;
-    // split-K turns each of few tiles into several work units: size the grid for those
-    const int64_t units = (g.partial != nullptr && tiles <= g.max_tiles_split) ? tiles * g.max_splits : tiles;
-    int grid = kCG * int(units < pairs ? units : pairs);
-    if (grid < kCG) grid = kCG;
+    // persistent grid: at most one pair per tile (every pair when two problems share
+    // the launch: their tile counts may come from device memory)
+    int64_t grid_pairs = pairs;
+    if (g.epi != EPI_BWD) {
+        const int64_t tiles = int64_t((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
+        grid_pairs = tiles < pairs ? tiles : pairs;
+    }
+    if (grid_pairs < 1) grid_pairs = 1;
+    const int grid = kCG * int(grid_pairs);
+    const GemmArgs none{};
+    const GemmArgs& gg1 = g1 ? *g1 : none;
     switch (g.epi) {
-        case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, grid, s);
-        case EPI_DGRAD: return dispatch_ch<EPI_DGRAD, false, true>(bn, m, g, grid, s);
-        case EPI_WGRAD: return dispatch_ch<EPI_WGRAD, true, true>(bn, m, g, grid, s);
+        case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, gg1, grid, s);
+        case EPI_DGRAD: return dispatch_ch<EPI_DGRAD, false, true>(bn, m, g, gg1, grid, s);
+        case EPI_WGRAD: return dispatch_ch<EPI_WGRAD, true, true>(bn, m, g, gg1, grid, s);
+        case EPI_BWD: return dispatch_ch<EPI_BWD, false, true>(bn, m, g, gg1, grid, s);
         case EPI_INT32:
-            if (!g.a_mn && !g.b_mn) return dispatch_ch<EPI_INT32, false, false>(bn, m, g, grid, s);
-            if (!g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, false, true>(bn, m, g, grid, s);
-            if (g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, true, true>(bn, m, g, grid, s);
-            return dispatch_ch<EPI_INT32, true, false>(bn, m, g, grid, s);
+            if (!g.a_mn && !g.b_mn) return dispatch_ch<EPI_INT32, false, false>(bn, m, g, gg1, grid, s);
+            if (!g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, false, true>(bn, m, g, gg1, grid, s);
+            if (g.a_mn && g.b_mn) return dispatch_ch<EPI_INT32, true, true>(bn, m, g, gg1, grid, s);
+            return dispatch_ch<EPI_INT32, true, false>(bn, m, g, gg1, grid, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -55,7 +55,7 @@ struct SamplerArgs {
     int8_t* wexp[2];
     int32_t* count[2];
     uint8_t* x_touched;       // [N]: 1 if the token has a kept grad_X item (optional)
-    uint32_t* zero_words;     // optional: words zeroed by the launch (split-K flags of the GEMMs)
+    uint32_t* zero_words;     // optional: words zeroed by the launch (the GEMMs' A.3 partial slots)
     int32_t n_zero_words;
     int32_t* det_flags;       // optional [2]: 1 if mask m kept a deterministic set (all positives / all items)
 };
@@ -82,7 +82,8 @@ struct CompactArgs {
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
 // gemm.cu ---------------------------------------------------------------------
-enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3 };
+enum EpiKind : int { EPI_INT32 = 0, EPI_FWD = 1, EPI_DGRAD = 2, EPI_WGRAD = 3,
+                     EPI_BWD = 4 };           // grad_X (args g) + grad_W (args g1) GEMMs in one launch
 
 struct GemmArgs {
     // problem: acc[M, Nn] = A(M, K) . B(Nn, K)^T; M or K may come from device memory
@@ -99,18 +100,8 @@ struct GemmArgs {
     int32_t k_had;            // Hadamard exponent for the epilogue inverse transform
     const uint32_t* mask;     // dgrad: I_X [N, Nn/32]; wgrad: I_W [M, Nn/32]
     const int32_t* items;     // dgrad: item id of each A row
-    // A rows gathered by TMA (tile::gather4) from a row list: along M for a K-major A
-    // (grad_X: the kept items' plane rows), along K for an MN-major A (grad_W)
-    const int32_t* a_gather;  // row indices, or null (plain tiles)
-    const int32_t* gather_count;   // indices at positions >= *gather_count read the zero row
-    int32_t gather_zero_row;
     const int8_t* wexp;       // dgrad: weight exponent of each A row
     int32_t n_tokens;         // dgrad: N (item id = h*N + t)
-    // deterministic split-K (optional): INT32 partial tiles + per-warp flags (zeroed before use)
-    int32_t* partial;         // [max_tiles_split, 128 CG, BN] int32, or null (no split-K)
-    uint32_t* flags;          // [max_tiles_split, CG, 4]
-    int32_t max_tiles_split;  // split only when the tile count is at most this
-    int32_t max_splits;
     // LSQ step-size gradient (A.3), optional: sum(acc o delta) per CTA epilogue warp
     const float* delta;       // dgrad: delta_X [N, Nn] (row = token); wgrad: delta_W [M, Nn]
     double* lsq_part;         // [gridDim.x * 8] fp64 partials (entries of absent CTAs pre-zeroed)
@@ -119,13 +110,13 @@ struct GemmArgs {
     // A = Q and B = X_hat (maps a3, b2, K = n_tokens)
     const int32_t* dense_flag;
 };
-constexpr int kSplitMaxTiles = 96;        // workspace tiles reserved for split-K
-constexpr int kSplitMaxK = 4;
-size_t gemm_split_partial_bytes();        // bytes of one GEMM's split-K partial workspace
-size_t gemm_split_flag_words();
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
-struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; const void* a3; const void* b2; };   // CUtensorMap* (host)
-cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s);
+// CUtensorMap* (host): A, B, C (output), A2 (grad_X dense A = Q), A3 / B2 (grad_W dense A = Q,
+// B = X_hat), AW / BW (grad_W sampled A_W, B_W in an EPI_BWD launch); null = unused
+struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; const void* a3; const void* b2;
+                  const void* aw; const void* bw; };
+cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s,
+                        const GemmArgs* g1 = nullptr);
 int gemm_block_n(int Nn, bool b_mn);
 
 // lsq.cu ----------------------------------------------------------------------

@@ -283,6 +283,10 @@ constexpr int kSplitThreads = 256;
 #define I4_BS_MINB 3
 #endif
 constexpr int kBsGroup = I4_BS_GROUP;
+#ifndef I4_BS_GMAX
+#define I4_BS_GMAX 3                      // largest unit size (chunks of 256 columns) phase 2 uses
+#endif
+constexpr int kBsGMax = I4_BS_GMAX;
 #ifndef I4_BS_AMAX_UNROLL
 #define I4_BS_AMAX_UNROLL 4
 #endif
@@ -362,8 +366,10 @@ __device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const P
 //      yl = (z - floor(z)) 2^23 in [0, 2^23) is rounded up by fl32_rp(yl + 2^23)
 //      (FFMA2.RP, exact below 2^24), and T = floor(z) 2^23 + ceil(yl) is put
 //      together from the two bit patterns by one LEA (y = f 2^32)
+//   3  as 0, with the sign cleared after the multiplies (folded into the
+//      conversion) and mag = high word of (A + ~u) (one 64-bit add, no select)
 #ifndef I4_SR_CVT
-#define I4_SR_CVT 2
+#define I4_SR_CVT 3
 #endif
 template <bool CLAMP>
 __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float r8,
@@ -372,6 +378,24 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0,
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
     const uint64_t r2 = f2_pack(r8, r8);
     uint32_t mag[8];
+    if constexpr (I4_SR_CVT == 3) {
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+            // elements i (low bf16) and i + 1 (high bf16) as one signed fp32 pair; |.| is taken
+            // after the multiplies (exact: IEEE products are sign-symmetric) and folds into the
+            // conversion; mag = high word of A + ~u = floor(a) + [u < T] (one 64-bit add)
+            const uint32_t wv = w[i >> 1];
+            const uint64_t g2 = f2_pack(__uint_as_float(__byte_perm(wv, 0u, 0x1044u)), __uint_as_float(wv & 0xFFFF0000u));
+            float y0, y1;
+            f2_unpack(f2_mul(f2_mul(g2, r2), f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
+            y0 = fabsf(y0);
+            y1 = fabsf(y1);
+            if (CLAMP) { y0 = fminf(y0, 511101108224.0f); y1 = fminf(y1, 511101108224.0f); }   // 119 * 2^32
+            const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
+            mag[i] = uint32_t((A0 + uint64_t(~u[i])) >> 32);
+            mag[i + 1] = uint32_t((A1 + uint64_t(~u[i + 1])) >> 32);
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
         // |g| of elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
@@ -416,6 +440,7 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0,
             mag[i] = __float_as_uint(t0) + (u[i] < T0 ? 1u : 0u);
             mag[i + 1] = __float_as_uint(t1) + (u[i + 1] < T1 ? 1u : 0u);
         }
+    }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -791,8 +816,8 @@ cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t*
 #define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, status, s)
     // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
     // measured equal or slower), else 3, 1; the one-warp-per-row loop otherwise
-    if (C % 512 == 0) return I4_GS(2);
-    if (C % 768 == 0) return I4_GS(3);
+    if (kBsGMax >= 2 && C % 512 == 0) return I4_GS(2);
+    if (kBsGMax >= 3 && C % 768 == 0) return I4_GS(3);
     if (C % 256 == 0) return I4_GS(1);
 #undef I4_GS
     return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out,

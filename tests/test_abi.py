@@ -21,7 +21,7 @@ def _declared():
 def test_header_declares_the_boundary():
     names = set(_declared())
     assert {"hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd"} <= names
-    assert {"int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_gemm_workspace_size", "int4_last_error"} <= names
+    assert {"int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_last_error"} <= names
 
 
 def test_library_exports_every_declared_symbol():
@@ -55,7 +55,7 @@ def test_host_validation_without_gpu():
         has_gpu = False
     if has_gpu:
         pytest.skip("host has a GPU")
-    st = p.lib.int4_gemm_s8s8s32(None, 0, None, 0, 1, 64, 16, None, None, 0, None)
+    st = p.lib.int4_gemm_s8s8s32(None, 0, None, 0, 1, 64, 16, None, None)
     assert st != 0
     assert p.lib.int4_last_error()
 

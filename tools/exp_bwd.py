@@ -25,6 +25,7 @@ def child(cfg_name):
     rng = np.random.default_rng(1)
     bf = lambda a: torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
     X, W, G = bf(synth.activations(N, D)), bf(synth.weights(C, D)), bf(synth.grad_output(N, C))
+    i4.int4_set_pdl(False)                    # per-kernel durations without early-launch waits
     L = i4.Int4Linear(N, D, C, k)
     Y = torch.empty(N, C, dtype=torch.bfloat16, device="cuda")
     dX = torch.empty(N, D, dtype=torch.bfloat16, device="cuda")
@@ -58,7 +59,6 @@ def main():
     libs = [None] + sorted(glob.glob(os.path.join(ROOT, "build_variants", "*.so")))
     for lib in libs:
         env = dict(os.environ, I4_EXP_CHILD="1")
-        env.setdefault("I4_PDL", "0")             # per-kernel durations without early-launch waits
         if lib:
             env["I4_LIB_OVERRIDE"] = lib
         subprocess.run([sys.executable, __file__, cfg], env=env, timeout=300)

@@ -19,7 +19,6 @@ def tgraph(fn, n=30):
         a.record(); g.replay(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     return statistics.median(ts) * 1e3
 
-ws = torch.zeros(i4.int4_gemm_workspace_size(), dtype=torch.uint8, device="cuda")
 cases = [  # name, M, N, K, a_mn, b_mn
     ("fwd cfg2", 4096, 3072, 768, False, False),
     ("dgrad cfg2", 4096, 768, 3072, False, True),
@@ -34,7 +33,7 @@ for name, M, N, K, a_mn, b_mn in cases:
     C = torch.empty(M, N, dtype=torch.int32, device="cuda")
     ops = 2.0 * M * N * K
     t0 = tgraph(lambda: i4.int4_gemm_s8s8s32(A, B, C, a_mn, b_mn))
-    t1 = tgraph(lambda: i4.int4_gemm_s8s8s32(A, B, C, a_mn, b_mn, ws=ws))
+    t1 = tgraph(lambda: i4.int4_gemm_s8s8s32(A, B, C, a_mn, b_mn))
     Ak = (A.t() if a_mn else A).contiguous(); Bk = (B.t() if b_mn else B).contiguous()
     t_lt = tgraph(lambda: torch._int_mm(Ak, Bk.t()))
     Ab, Bb = Ak.bfloat16(), Bk.bfloat16()
