@@ -153,6 +153,157 @@ __device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, in
     return sq;
 }
 
+#ifndef I4_HQ_TMA
+#define I4_HQ_TMA 0
+#endif
+static int hq_rows_per_cta(int64_t cols) {
+    const int tpr = int(cols / 32);
+    return tpr >= kHqMaxThreads ? 1 : kHqMaxThreads / tpr;
+}
+
+#if I4_HQ_TMA
+// TMA-staged persistent variant (compile with -DI4_HQ_TMA=1).  Measured 4-15 %
+// slower than the register-staged kernel above on every BASELINE shape (B200:
+// BERT-large FFN-up 13.2 vs 11.5 us, ViT FFN-down 106 vs 103 us): the kernel is
+// instruction-issue bound, not latency bound, and the per-stage CTA barriers
+// cost more than the deeper prefetch gains.  A stage is RS whole rows (RS x cols bf16, one
+// contiguous cp.async.bulk copy of ~16 KB); each CTA streams its stages through
+// a kHqStages-deep shared-memory ring (mbarrier completion), so ~64 KB per CTA
+// (~128 KB per SM) of X / W is in flight while the threads transform earlier
+// stages: thread (row slot, 32-column block) pulls its 64 bytes from shared
+// memory into registers for the FWHT + LSQ of hq_block, and stores its codes and
+// mask word straight to global memory (a warp's stores cover contiguous bytes of
+// one row).  Stages never cross the X / W job boundary.  Row norms: shared-memory
+// integer atomics per stage (exact, order-independent).
+constexpr int kHqStages = 4;
+constexpr int kHqStageBytes = 16384;          // target bytes per stage (RS rows)
+
+struct HqSched {
+    int rs;                                    // rows per stage
+    int64_t st0, st1;                          // stages of job 0 (X) and job 1 (W)
+};
+
+template <int K, bool DELTA>
+__global__ void __launch_bounds__(kHqMaxThreads)
+hadamard_quant_tma_kernel(HqJob j0, HqJob j1, int cols, HqSched hs) {
+    extern __shared__ __align__(128) uint8_t hq_smem[];
+    __shared__ uint64_t full[kHqStages];
+    __shared__ int sq_row[kHqMaxThreads];
+    const int tpr = cols >> 5;                       // threads (32-column blocks) per row
+    const int r_local = int(threadIdx.x) / tpr;
+    const int blk = int(threadIdx.x) - r_local * tpr;
+    const int64_t n_stages = hs.st0 + hs.st1;
+    const int64_t row_bytes = int64_t(cols) * 2;
+    const int stage_bytes = hs.rs * int(row_bytes);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kHqStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();                                        // X / W may be written by the previous kernel
+    // stage i of this CTA = global stage blockIdx.x + i * gridDim.x
+    auto issue = [&](int64_t gs, int slot) {
+        const bool second = gs >= hs.st0;
+        const HqJob& J = second ? j1 : j0;
+        const int64_t row0 = (second ? gs - hs.st0 : gs) * hs.rs;
+        const int64_t nrow = min(int64_t(hs.rs), J.rows - row0);
+        const uint32_t bytes = uint32_t(nrow * row_bytes);
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_copy_g2s(hq_smem + slot * stage_bytes, J.x + row0 * cols, bytes, &full[slot]);
+    };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kHqStages; ++s) {
+            const int64_t gs = int64_t(blockIdx.x) + int64_t(s) * gridDim.x;
+            if (gs < n_stages) issue(gs, s);
+        }
+    int it = 0;
+    for (int64_t gs = blockIdx.x; gs < n_stages; gs += gridDim.x, ++it) {
+        const int slot = it % kHqStages;
+        const uint32_t ph = uint32_t(it / kHqStages) & 1u;
+        const bool second = gs >= hs.st0;
+        const HqJob& J = second ? j1 : j0;
+        const int64_t row0 = (second ? gs - hs.st0 : gs) * hs.rs;
+        const int64_t row = row0 + r_local;
+        const bool active = r_local < hs.rs && row < J.rows;
+        if (threadIdx.x < hs.rs) sq_row[threadIdx.x] = 0;
+        mbar_wait(&full[slot], ph);
+        uint4 raw[4];
+        const uint8_t* src = hq_smem + slot * stage_bytes + (active ? r_local * row_bytes + blk * 64 : 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) raw[q] = active ? ld_shared_v4(src + 16 * q) : make_uint4(0, 0, 0, 0);
+        __syncthreads();                               // slot drained (and sq_row zeroed): refill it
+        if (threadIdx.x == 0) {
+            const int64_t nx = gs + int64_t(kHqStages) * gridDim.x;
+            fence_proxy_async_smem();                  // the generic reads above before the async refill
+            if (nx < n_stages) issue(nx, slot);
+        }
+        const int sq = hq_block<K, DELTA>(J, row, blk, tpr, cols, active, raw);
+        if (active && J.sqnorm != nullptr) atomicAdd(&sq_row[r_local], sq);
+        if (J.sqnorm != nullptr) {
+            __syncthreads();
+            if (active && blk == 0) J.sqnorm[row] = sq_row[r_local];
+        }
+        __syncthreads();                               // sq_row reused by the next stage
+    }
+}
+
+static cudaError_t launch_hadamard_quant_tma(const HqArgs& a, cudaStream_t s) {
+    if (a.cols / 32 > kHqMaxThreads) return cudaErrorInvalidValue;   // cols > 8192: not supported
+    // rows per stage: whole rows, one per thread-row slot of the CTA, at most ~16 KB
+    const int R = hq_rows_per_cta(a.cols);
+    int rs = int(kHqStageBytes / (a.cols * 2));
+    if (rs > R) rs = R;
+    if (rs < 1) rs = 1;
+    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0, a.status};
+    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0, a.status};
+    HqSched hs{rs, (a.rows0 + rs - 1) / rs, (a.rows1 + rs - 1) / rs};
+    const int64_t n_stages = hs.st0 + hs.st1;
+    if (n_stages == 0) return cudaSuccess;
+    static std::atomic<int> sms_cache[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    int sms = sms_cache[dev].load(std::memory_order_relaxed);
+    if (sms == 0) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_cache[dev].store(sms, std::memory_order_relaxed);
+    }
+    // persistent: 3 CTAs per SM (3 x 64 KB ring), never more CTAs than stages
+    int64_t grid = int64_t(sms) * 3;
+    if (grid > n_stages) grid = n_stages;
+    const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
+    const int smem = kHqStages * rs * int(a.cols) * 2;
+    void (*kern)(HqJob, HqJob, int, HqSched) = nullptr;
+    const bool delta = a.delta0 != nullptr || a.delta1 != nullptr;
+#define I4_HQ_K(KK) kern = delta ? hadamard_quant_tma_kernel<KK, true> : hadamard_quant_tma_kernel<KK, false>; break;
+    switch (a.k) {
+        case 0: I4_HQ_K(0)
+        case 1: I4_HQ_K(1)
+        case 2: I4_HQ_K(2)
+        case 3: I4_HQ_K(3)
+        case 4: I4_HQ_K(4)
+        case 5: I4_HQ_K(5)
+        case 6: I4_HQ_K(6)
+        case 7: I4_HQ_K(7)
+        default: return cudaErrorInvalidValue;
+    }
+#undef I4_HQ_K
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 0);
+    return cudaLaunchKernelEx(&cfg, kern, j0, j1, int(a.cols), hs);
+}
+
+#endif  // I4_HQ_TMA
+
 // A CTA covers PASSES x R rows: the thread of (row slot, block) handles row
 // slot + pass R for every pass, with the loads of all passes issued before the
 // first block is transformed (measured on B200: 2 and 4 passes are 20-45 %
@@ -206,13 +357,11 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     }
 }
 
-static int hq_rows_per_cta(int64_t cols) {
-    const int tpr = int(cols / 32);
-    return tpr >= kHqMaxThreads ? 1 : kHqMaxThreads / tpr;
-}
-
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     if (a.cols / 32 > kHqMaxThreads) return cudaErrorInvalidValue;   // cols > 8192: not supported
+#if I4_HQ_TMA
+    return launch_hadamard_quant_tma(a, s);
+#endif
     const int R = hq_rows_per_cta(a.cols);
     HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0, a.status};
     HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0, a.status};
