@@ -88,6 +88,9 @@ def parse(argv=None):
     ap.add_argument("--no-per-linear", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the pre-timing oracle parity gate")
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no operator compute")
+    ap.add_argument("--wgrad-reduce", choices=["nccl", "nvls"], default="nccl",
+                    help="N > 1: grad_W all-reduce by NCCL per layer (overlapped), or inside the grad_W GEMM "
+                         "epilogue through an NVLS multicast buffer (SURVEY.md §8(f4); opt-in, unmeasured)")
     return ap.parse_args(argv)
 
 
@@ -306,14 +309,22 @@ def algorithmic_work(name, N, D, C, kx, kw, dense, moved=None):
     return "bytes", 0.0
 
 
-def compact_bytes(layer, N, D, C, kx, kw, dense):
+def compact_bytes(layer, N, D, C, kx, kw, form):
     """Bytes compact actually moves (read + write), from the last backward's lists:
     a sampled grad_X mask reads its tokens' Q rows once (a token's second half hits
     L2), writes K_X half-rows of A_X and zeroes the bf16 grad_X rows of untouched
     tokens; a sampled grad_W mask reads the Q and X_hat rows of its tokens and
-    writes K_W rows of A_W (C) and B_W (D)."""
-    dw, dx = dense
+    writes K_W rows of A_W (C) and B_W (D).  Operand form 2: only the correction rows
+    (grad_W) and the sampled tokens' item rows (grad_X), read + written."""
+    fw, fx = form
+    dw, dx = fw != 0, fx != 0
     b = 0.0
+    if fw == 2 or fx == 2:
+        cw, cx = [int(v) for v in layer.form2_counts().cpu().numpy()]
+        if fw == 2:
+            b += 2.0 * cw * (C + D)
+        if fx == 2:
+            b += 2.0 * cx * C
     if not dx:
         toks = np.unique(layer.items_x[:kx].cpu().numpy() % N).size
         b += toks * C + kx * C + (N - toks) * D * 2
@@ -376,6 +387,22 @@ class Stack:
             self.layers.append(i4.Int4Linear(N, D, C, k, device=dev, scratch=self.scratch))
             self.s.append((i4.cold_start_step(self.X[-1]), i4.cold_start_step(self.W[-1])))   # A.4, library kernel
         self.mode = MODES[args.mode]
+        self.mc = [None] * len(lins)              # NVLS multicast grad_W addresses (--wgrad-reduce nvls)
+        self.sym = None
+
+    def enable_nvls(self):
+        """grad_W buckets in symmetric memory; each linear's grad_W GEMM reduces into its
+        bucket's multicast address.  False when no multicast object is available."""
+        from paper_2306_11987_b200 import dist as pdist
+        self.sym = [pdist.SymmetricGradW(b.numel(), self.dev) for b in self.dW_bucket]
+        if not all(s.available for s in self.sym):
+            self.sym = None
+            return False
+        offs = {layer: 0 for layer in range(self.n_layers)}
+        for i, (nm, _, D, C, k, layer, cid) in enumerate(self.lins):
+            self.mc[i] = self.sym[layer].multicast(offs[layer])
+            offs[layer] += C * D
+        return True
 
     def fwd_one(self, i):
         s_x, s_w = self.s[i]
@@ -383,7 +410,7 @@ class Stack:
 
     def bwd_one(self, i):
         self.layers[i].backward(self.G[i], self.dX[i], self.dW[i], synth.PHILOX_SEED, call_id=self.lins[i][6],
-                                token_offset=self.token_offset, mode=self.mode)
+                                token_offset=self.token_offset, mode=self.mode, dw_multicast=self.mc[i])
 
     # the two halves of a step (graph bodies)
     def fwd_body(self):
@@ -428,6 +455,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     gate = parity_gate(st) if (rank == 0 and not args.no_gate) else None
     st.scratch.status_buf.zero_()
+    nvls = world > 1 and args.wgrad_reduce == "nvls" and st.enable_nvls()
 
     flush_w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     flush_r = torch.ones(32 * 1024 * 1024, dtype=torch.int64, device=dev)
@@ -442,34 +470,39 @@ def run_ours(args):
     g_bwd = [capture(lambda l=l: st.bwd_body(l)) for l in range(n_layers)]
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-    def one_step(gf, gb, buckets):
+    def one_step(gf, gb, buckets, fused=False):
+        if fused:           # NVLS: every rank zeroes its copy; the grad_W GEMMs reduce into all copies
+            for sym in st.sym:
+                sym.zero_()
         gf.replay()
         handles = []
         for layer in reversed(range(n_layers)):
             gb[layer].replay()
-            if world > 1:   # async on NCCL's stream: overlaps the next (lower) layer's backward
+            if world > 1 and not fused:   # async on NCCL's stream: overlaps the next (lower) layer's backward
                 handles.append(dist.all_reduce(buckets[layer], op=dist.ReduceOp.SUM, async_op=True))
         for h in handles:
             h.wait()        # the compute stream waits for every all-reduce before the step ends
+        if fused:
+            st.sym[0].barrier()           # every rank's reductions have landed
 
-    def timed(gf, gb, buckets, n):
+    def timed(gf, gb, buckets, n, fused=False):
         out = []
         for _ in range(n):
             flush()
             torch.cuda.synchronize()
             ev_a.record()
-            one_step(gf, gb, buckets)
+            one_step(gf, gb, buckets, fused)
             ev_b.record()
             torch.cuda.synchronize()
             out.append(ev_a.elapsed_time(ev_b))
         return out
 
-    timed(g_fwd, g_bwd, st.dW_bucket, args.warmup)
+    timed(g_fwd, g_bwd, st.dW_bucket, args.warmup, nvls)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        step_ms = timed(g_fwd, g_bwd, st.dW_bucket, args.steps)
+        step_ms = timed(g_fwd, g_bwd, st.dW_bucket, args.steps, nvls)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -523,9 +556,10 @@ def run_ours(args):
         st.bwd_one(i)
         torch.cuda.synchronize()
         kw, kx = [int(v) for v in st.layers[i].counts().cpu().numpy()]
-        dense = tuple(bool(v) for v in st.layers[i].dense_flags().cpu().numpy())
-        shape_stats[nm] = dict(N=N, D=D, C=C, kw=kw, kx=kx, dense=dense,
-                               compact_bytes=compact_bytes(st.layers[i], N, D, C, kx, kw, dense))
+        form = tuple(int(v) for v in st.layers[i].dense_flags().cpu().numpy())
+        dense = tuple(f == 1 for f in form)
+        shape_stats[nm] = dict(N=N, D=D, C=C, kw=kw, kx=kx, dense=dense, form=form,
+                               compact_bytes=compact_bytes(st.layers[i], N, D, C, kx, kw, form))
     step_us = ms * 1e3
     kernels = {nm: {"us_per_step": tot, "launches_per_step": n_launch.get(nm, 0), "share": tot / step_us}
                for nm, tot in cupti.items()}
@@ -552,7 +586,7 @@ def run_ours(args):
     e2e = None if args.no_e2e else run_e2e(st, args, dev, world, ops, flush)
 
     if rank == 0:
-        gemm_names = ("gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad")
+        gemm_names = ("gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad", "gemm_i8_bwd")
         gemm_us = sum(kernels[nm]["us_per_step"] for nm in gemm_names if nm in kernels)
         if GROUP in kernels:                  # concurrent pairs: count their union, not both kernels
             gemm_us = kernels.get("gemm_i8_fwd", {}).get("us_per_step", 0.0) + kernels[GROUP]["us_per_step"]
@@ -568,15 +602,19 @@ def run_ours(args):
                 "speedup_vs_bf16_cublas": bf16_ms / ms_max, "bf16_cublas_ms_per_step": bf16_ms,
                 "gemm_int8_peak_frac": gemm_ops / (gemm_us * 1e-6) / 1e12 / int8_peak if gemm_us else None,
                 "kept_items": {nm: {"grad_W": v["kw"], "grad_X": v["kx"], "budget": v["N"],
-                                    "dense_masks": {"grad_W": v["dense"][0], "grad_X": v["dense"][1]}}
+                                    "operand_form": {"grad_W": v["form"][0], "grad_X": v["form"][1],
+                                                     "legend": "0 compacted kept items, 1 dense Q/X_hat (Z-32), "
+                                                               "2 dense + correction rows (Z-33)"}}
                                for nm, v in shape_stats.items()},
                 "roofline": roof, "kernels": kernels,
                 "kernels_timing": "CUPTI kernel records (torch.profiler) over extra flushed PDL-off replays; per step",
                 "gpu_launches": sum(n_launch.values()) * args.steps,
                 "clocks": clocks.summary(), "e2e": e2e, "parity_gate": gate, "status_word": status_word,
                 "per_linear": per_linear,
-                "allreduce": ("per layer grad_W bucket (fp32), async on NCCL's stream after the layer's backward "
-                              "graph, overlapping the next layer's backward; waited before the step's end event")
+                "allreduce": (("grad_W reduced inside the grad_W GEMM epilogue into NVLS multicast buffers "
+                               "(multimem.red.add; symmetric-memory barrier at the step's end)") if nvls else
+                              ("per layer grad_W bucket (fp32), async on NCCL's stream after the layer's backward "
+                               "graph, overlapping the next layer's backward; waited before the step's end event"))
                 if world > 1 else None}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(lins, args.grad, args.mode)

@@ -147,6 +147,17 @@ typedef struct {
  *                              Z-27..Z-29), computed when the cache holds x_delta and w_delta
  *   n_elem_x, n_elem_w         host: N_X, N_W of g(s) = 1/sqrt(Q_P N) (0 = this call's
  *                              N*D and C*D; a token-sharded caller passes the global counts)
+ *   dw_multicast float [C, D]  nullable (int4_linear_bwd): multicast (NVLS) address of a
+ *                              symmetric grad_W buffer spanning the data-parallel ranks (e.g.
+ *                              torch symmetric memory's multicast_ptr).  When set, the grad_W
+ *                              epilogue reduces each finished tile into EVERY rank's copy with
+ *                              multimem.red.add.f32 instead of storing to dW: the all-reduce of
+ *                              grad_W happens inside the GEMM, tile by tile (
+ *                              PAPER.md:978).  The caller zeroes the buffer on every rank before
+ *                              the backward and synchronises the ranks after it before reading.
+ *                              fp32 sums of G addends onto zero: bit-identical to a serial sum
+ *                              for G <= 2, addition order of the switch otherwise; subnormal
+ *                              sums flush to zero.  dW is not written in this mode.
  *   dev_status int32 [1]       nullable: device status word, bits ORed in by the backward:
  *                              I4_STATUS_NONFINITE when grad_Y holds an Inf / NaN (the
  *                              tensor is then treated as all-zero: codes 0, s_down = 0, no
@@ -170,6 +181,7 @@ typedef struct {
     float* grad_s;
     int64_t n_elem_x, n_elem_w;
     int32_t* dev_status;
+    float* dw_multicast;
 } i4_lss_plan;
 
 /* F1+F2 / F3: block-Hadamard transform + LSQ quantize of a bf16 matrix
@@ -293,8 +305,15 @@ I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);
  * flags the last backward left there: [0] the grad_W mask, [1] the grad_X mask was
  * deterministic (every item with a positive score kept with weight 1; DESIGN.md
  * reading Z-32), so that GEMM ran on the 8-bit code plane q8 (and X_hat) with no
- * compaction.  Informational only: results do not depend on which form ran. */
+ * compaction; 0: the GEMM ran on the compacted kept items; 2: a binding budget left
+ * few items sampled, so the GEMM ran on q8 / X_hat plus correction rows (reading
+ * Z-33).  Informational only: results do not depend on which form ran. */
 I4_API size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C);
+
+/* Introspection: byte offset, inside the backward workspace, of two int32 counts of the
+ * last backward's operand form 2 (dense + correction, reading Z-33; flag
+ * value 2 above): [0] grad_W correction rows, [1] grad_X rows of the sampled tokens. */
+I4_API size_t int4_bwd_ws_form2_offset(int64_t N, int64_t D, int64_t C);
 
 /* Exact INT8 x INT8 -> INT32 product acc[m, n] = sum_k A(m, k) B(n, k) on the
  * tcgen05 path used by every GEMM of the operator ("Multiply the

@@ -57,7 +57,8 @@ class I4LssPlan(ctypes.Structure):
                 ("wexp_w", ctypes.c_void_p),
                 ("count_w", ctypes.c_void_p), ("items_x", ctypes.c_void_p), ("wexp_x", ctypes.c_void_p),
                 ("count_x", ctypes.c_void_p), ("x_touched", ctypes.c_void_p), ("grad_s", ctypes.c_void_p),
-                ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64), ("dev_status", ctypes.c_void_p)]
+                ("n_elem_x", ctypes.c_int64), ("n_elem_w", ctypes.c_int64), ("dev_status", ctypes.c_void_p),
+                ("dw_multicast", ctypes.c_void_p)]
 
 
 class I4BmmCache(ctypes.Structure):
@@ -94,6 +95,8 @@ def _load():
     L.lsq_cold_start_workspace_size.restype = ctypes.c_size_t
     L.hq_select_k_workspace_size.argtypes = []
     L.hq_select_k_workspace_size.restype = ctypes.c_size_t
+    L.int4_bwd_ws_form2_offset.argtypes = [i64, i64, i64]
+    L.int4_bwd_ws_form2_offset.restype = ctypes.c_size_t
     L.int4_bwd_ws_det_offset.argtypes = [i64, i64, i64]
     L.int4_bwd_ws_det_offset.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
@@ -346,9 +349,13 @@ class Int4Linear:
         self.cache.w_valid = 1 if reuse_weight else 0
         int4_linear_fwd(X, W, self.k, s_x, s_w, Y, self.cache, stream)
 
-    def backward(self, dY, dX, dW, seed, call_id=0, token_offset=0, mode=LSS_BERNOULLI, stream=None):
+    def backward(self, dY, dX, dW, seed, call_id=0, token_offset=0, mode=LSS_BERNOULLI, stream=None,
+                 dw_multicast=None):
+        """dw_multicast: optional multicast address (int) of a symmetric grad_W buffer; the
+        grad_W GEMM then all-reduces into it in its epilogue (NVLS, see the header)."""
         # the plan may be shared with other layers: point it at this layer's outputs
         self.plan.grad_s = self.grad_s_buf.data_ptr() if self.step_grads else None
+        self.plan.dw_multicast = dw_multicast
         int4_linear_bwd(dY, self.cache, seed, call_id, token_offset, mode, self.plan, dX, dW, self.ws, stream)
 
     def status(self):
@@ -372,6 +379,13 @@ class Int4Linear:
         (reading Z-32: the GEMMs then ran on Q / X_hat), an int32 device tensor."""
         import torch
         off = lib.int4_bwd_ws_det_offset(self.N, self.D, self.C)
+        return self.ws[off:off + 8].view(torch.int32)
+
+    def form2_counts(self):
+        """[grad_W correction rows, grad_X sampled-token rows] of the last backward when a
+        mask ran in operand form 2 (reading Z-33), an int32 device tensor."""
+        import torch
+        off = lib.int4_bwd_ws_form2_offset(self.N, self.D, self.C)
         return self.ws[off:off + 8].view(torch.int32)
 
     def q8_codes(self):

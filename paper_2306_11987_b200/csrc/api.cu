@@ -384,10 +384,14 @@ i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_t D, in
     return I4_OK;
 }
 
+// Operand form 2 buffers of the backward workspace (reading Z-33), handed to the sampler.
+struct Form2 { int32_t* corr_items; int8_t* corr_wexp; int32_t* counts2; int32_t* sub_items; int8_t* sub_wexp;
+               uint8_t* tok_flag; };
+
 static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const int32_t* x_sqnorm, uint64_t seed,
                             uint32_t call_id, int64_t token_offset, i4_lss_mode mode, const i4_lss_plan* plan,
                             cudaStream_t s, uint32_t* zero_words, int32_t n_zero_words,
-                            int32_t* det_flags = nullptr) {
+                            int32_t* det_flags = nullptr, const Form2* f2 = nullptr) {
     I4_RETURN_IF(check_device());
     if (!dY || !plan || !plan->q8 || !plan->a_sq || !plan->amax_bits || !plan->s_down || !plan->scratch || !plan->items_w ||
         !plan->wexp_w || !plan->count_w || !plan->items_x || !plan->wexp_x || !plan->count_x || !plan->x_touched)
@@ -418,6 +422,11 @@ static i4_status bitsplit_lss_impl(const void* dY, int64_t N, int64_t C, const i
     a.zero_words = zero_words; a.n_zero_words = n_zero_words;
     a.det_flags = det_flags;
     a.x_touched = plan->x_touched;
+    if (f2 != nullptr) {                         // int4_linear_bwd: operand form 2 available
+        a.corr_items = f2->corr_items; a.corr_wexp = f2->corr_wexp; a.corr_count = f2->counts2;
+        a.sub_items = f2->sub_items; a.sub_wexp = f2->sub_wexp; a.sub_count = f2->counts2 + 1;
+        a.tok_flag = f2->tok_flag;
+    }
     I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
     return I4_OK;
 }
@@ -437,7 +446,12 @@ namespace {
 struct BwdWs {
     int8_t* a_x; int8_t* a_w; int8_t* b_w;
     double* lsq_x; double* lsq_w;        // A.3 fp64 partials (zeroed by the sampler launch)
-    int32_t* det;                        // [2] deterministic-mask flags (written by the sampler)
+    int32_t* det;                        // [2] operand forms of the two masks (written by the sampler)
+    // operand form 2 (dense + correction, reading Z-33): grad_W correction rows, grad_X
+    // sub-list of the tokens with sampled items, their counts and per-token flags
+    int32_t* corr_items; int8_t* corr_wexp; int32_t* sub_items; int8_t* sub_wexp;
+    int32_t* counts2;                    // [0] correction rows, [1] sub-list items
+    uint8_t* tok_flag;                   // [N]
     size_t total;
 };
 
@@ -451,6 +465,12 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
     const size_t o_bw = take(size_t(D * kcap));
     const size_t o_f = take(2 * i4::kLsqPartials * sizeof(double));   // the sampler zeroes it
     const size_t o_det = take(2 * sizeof(int32_t));
+    const size_t o_ci = take(size_t(2 * N + 128) * sizeof(int32_t));
+    const size_t o_ce = take(size_t(2 * N + 128));
+    const size_t o_si = take(size_t(2 * N + 128) * sizeof(int32_t));
+    const size_t o_se = take(size_t(2 * N + 128));
+    const size_t o_c2 = take(2 * sizeof(int32_t));
+    const size_t o_tf = take(size_t(N));
     w.total = off;
     if (ws) {
         uint8_t* b = static_cast<uint8_t*>(ws);
@@ -460,6 +480,12 @@ BwdWs carve_bwd_ws(void* ws, int64_t N, int64_t D, int64_t C) {
         w.lsq_x = reinterpret_cast<double*>(b + o_f);
         w.lsq_w = w.lsq_x + i4::kLsqPartials;
         w.det = reinterpret_cast<int32_t*>(b + o_det);
+        w.corr_items = reinterpret_cast<int32_t*>(b + o_ci);
+        w.corr_wexp = reinterpret_cast<int8_t*>(b + o_ce);
+        w.sub_items = reinterpret_cast<int32_t*>(b + o_si);
+        w.sub_wexp = reinterpret_cast<int8_t*>(b + o_se);
+        w.counts2 = reinterpret_cast<int32_t*>(b + o_c2);
+        w.tok_flag = b + o_tf;
     }
     return w;
 }
@@ -477,6 +503,12 @@ size_t int4_bwd_ws_det_offset(int64_t N, int64_t D, int64_t C) {
     uint8_t* const base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);
     const BwdWs w = carve_bwd_ws(base, N, D, C);
     return size_t(reinterpret_cast<uint8_t*>(w.det) - base);
+}
+
+size_t int4_bwd_ws_form2_offset(int64_t N, int64_t D, int64_t C) {
+    uint8_t* const base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);
+    const BwdWs w = carve_bwd_ws(base, N, D, C);
+    return size_t(reinterpret_cast<uint8_t*>(w.counts2) - base);
 }
 
 static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint64_t seed, uint32_t call_id,
@@ -509,10 +541,11 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         return fail(I4_ERR_ARG, "int4_linear_bwd: plan->grad_s needs cache->x_delta and cache->w_delta");
     {
         const BwdWs w0 = carve_bwd_ws(ws, N, D, C);
+        const Form2 f2{w0.corr_items, w0.corr_wexp, w0.counts2, w0.sub_items, w0.sub_wexp, w0.tok_flag};
         // the sampler launch also zeroes the A.3 partial slots of the GEMM launch below
         const int32_t words = int32_t(want_lsq ? 2 * i4::kLsqPartials * sizeof(double) / sizeof(uint32_t) : 0);
         I4_RETURN_IF(bitsplit_lss_impl(dY, N, C, cache->x_sqnorm, seed, call_id, token_offset, mode, plan, s,
-                                       reinterpret_cast<uint32_t*>(w0.lsq_x), words, w0.det));
+                                       reinterpret_cast<uint32_t*>(w0.lsq_x), words, w0.det, &f2));
     }
 
     const int64_t kcap = round_up(2 * N, 128);
@@ -526,6 +559,8 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
         ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
         ca.x_touched = plan->x_touched; ca.dx = dX; ca.dx_bf16 = dx_dtype == I4_OUT_BF16;
         ca.det_flags = w.det;
+        ca.corr_items = w.corr_items; ca.corr_wexp = w.corr_wexp; ca.corr_count = w.counts2;
+        ca.sub_items = w.sub_items; ca.sub_count = w.counts2 + 1; ca.tok_flag = w.tok_flag;
         I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
     }
     // grad_X and grad_W: one persistent launch over both GEMMs' tiles
@@ -544,7 +579,9 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
     gx.n_tokens = int32_t(N);
     gx.b_mn = 1;                                 // B = W_hat [C, D] read MN-major (K = C, N = D)
     if (want_lsq) { gx.delta = cache->x_delta; gx.lsq_part = w.lsq_x; }
-    gx.dense_flag = w.det + 1;                   // grad_X mask deterministic: rows = tokens of Q
+    gx.dense_flag = w.det + 1;                   // grad_X operand form (sampler): 1 rows = tokens of Q,
+                                                 // 2 Q rows + sub-list rows of the sampled tokens
+    gx.items2 = w.sub_items; gx.wexp2 = w.sub_wexp; gx.m_dev2 = w.counts2 + 1; gx.tok_flag = w.tok_flag;
     i4::GemmArgs gw{};                           // grad_W: M = C, N = D, K = kept items (count on device)
     gw.M = int32_t(C); gw.Nn = int32_t(D); gw.K = int32_t(kcap); gw.k_dev = plan->count_w;
     gw.epi = i4::EPI_WGRAD;
@@ -555,7 +592,9 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
     gw.mask = cache->w_mask;
     gw.a_mn = 1; gw.b_mn = 1;                    // A_W [K items, C], B_W [K, D]: both MN-major
     if (want_lsq) { gw.delta = cache->w_delta; gw.lsq_part = w.lsq_w; }
-    gw.dense_flag = w.det;                       // grad_W mask deterministic: K = tokens, A = Q, B = X_hat
+    gw.dense_flag = w.det;                       // grad_W operand form: 1 K = tokens (A = Q, B = X_hat),
+    gw.k_dev2 = w.counts2;                       // 2 the same plus the correction rows (A_W, B_W)
+    if (plan) gw.out_mc = plan->dw_multicast;    // f4: grad_W all-reduced inside the GEMM (NVLS)
     gw.n_tokens = int32_t(N);
     I4_RETURN_IF(gemm_bwd(Operand{w.a_x, 2 * N + 128, C, C}, Operand{plan->q8, N + 1, C, C},
                           Operand{cache->wq, C, D, D}, Operand{w.a_w, kcap, C, C}, Operand{w.b_w, kcap, D, D},

@@ -286,6 +286,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void red_add_bf16x2(void* dst, uint32_t v) {
     asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" :: "l"(dst), "r"(v) : "memory");
 }
+// NVLS reduction through a multicast address: the switch adds the 4 values into the
+// same offset of every member GPU's buffer (fp32, subnormals flushed)
+__device__ __forceinline__ void multimem_red_add_v4(float* mc, float a, float b, float c, float d) {
+    asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(mc), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }

@@ -67,56 +67,63 @@ __device__ __forceinline__ void zero_row(void* base, int64_t row, int n, bool bf
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     pdl_trigger();
     pdl_wait();                                               // counts / lists of the sampler
-    const int64_t cnt_x = __ldg(a.count_x);
-    int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
-    const int64_t pad_w = (int64_t(__ldg(a.count_w)) + 127) & ~int64_t(127);
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    // deterministic masks (the sampler's flags; the GEMMs pick their operands by the
-    // same tests): grad_X dense -> no A_X rows and no zero rows (its GEMM writes every
-    // token row from Q); grad_W dense -> no A_W / B_W rows (Q and X_hat are read)
-    const bool dense_x = a.det_flags != nullptr && __ldg(a.det_flags + 1) != 0;
-    const bool dense_w = a.det_flags != nullptr && __ldg(a.det_flags) != 0;
-    const int64_t n_straddle = dense_x ? 0 : (cnt_x + 31) / 32;   // candidate positions 31, 63, ...
-    if (dense_x) pad_x = 0;
-    const int64_t pad_aw = dense_w ? 0 : pad_w;
-    const int64_t pad_bw = dense_w ? 0 : pad_w;
-    const int64_t seg_bw = pad_x + pad_aw;                   // first B_W row job
-    const int64_t n_zero = dense_x ? 0 : a.N;
-    const int64_t total = seg_bw + pad_bw + n_zero + n_straddle;
+    // operand forms (the sampler's flags; the GEMMs pick their operands by the same
+    // values): 1 dense -> nothing to move (the GEMM reads Q / X_hat and writes every
+    // grad_X token row); 0 sampled -> every kept item; 2 dense + correction -> the
+    // grad_W correction rows and the grad_X sub list of the tokens with sampled items
+    const int fx = a.det_flags != nullptr ? __ldg(a.det_flags + 1) : 0;
+    const int fw = a.det_flags != nullptr ? __ldg(a.det_flags) : 0;
+    const int32_t* lx = fx == 2 ? a.sub_items : a.items_x;   // grad_X rows to gather
+    const int64_t cnt_x = fx == 1 ? 0 : __ldg(fx == 2 ? a.sub_count : a.count_x);
+    const int32_t* lw = fw == 2 ? a.corr_items : a.items_w;  // grad_W rows to gather
+    const int8_t* ew = fw == 2 ? a.corr_wexp : a.wexp_w;
+    const int64_t cnt_w = fw == 1 ? 0 : __ldg(fw == 2 ? a.corr_count : a.count_w);
+    const int64_t pad_x = (cnt_x + 127) & ~int64_t(127);
+    const int64_t pad_w = (cnt_w + 127) & ~int64_t(127);
+    const int64_t n_straddle = (cnt_x + 31) / 32;            // candidate positions 31, 63, ...
+    const int64_t seg_bw = pad_x + pad_w;                    // first B_W row job
+    const int64_t n_zero = fx == 1 ? 0 : a.N;
+    const int64_t total = seg_bw + pad_w + n_zero + n_straddle;
     const int two_n = 2 * a.N;
     for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
-        if (j >= seg_bw + pad_bw) {
-            // grad_X rows the GEMM epilogue does not store: tokens without a kept
-            // item, and tokens whose two items straddle a 32-row group (both red.add)
-            const int64_t r = j - seg_bw - pad_bw;
+        if (j >= seg_bw + pad_w) {
+            // grad_X rows the GEMM epilogue does not store: tokens without a kept item
+            // (form 2: only among the flagged tokens -- the others are Q rows), and tokens
+            // whose two items straddle a 32-row group (both red.add)
+            const int64_t r = j - seg_bw - pad_w;
             if (r < a.N) {
-                if (__ldg(a.x_touched + r) == 0) zero_row(a.dx, r, a.D, a.dx_bf16, lane);
+                if (__ldg(a.x_touched + r) == 0 && (fx != 2 || __ldg(a.tok_flag + r) != 0))
+                    zero_row(a.dx, r, a.D, a.dx_bf16, lane);
             } else {
                 const int64_t p = 32 * (r - a.N) + 31;
                 if (p + 1 < cnt_x) {
-                    const int32_t i0 = __ldg(a.items_x + p), i1 = __ldg(a.items_x + p + 1);
+                    const int32_t i0 = __ldg(lx + p), i1 = __ldg(lx + p + 1);
                     const int t0 = i0 >= a.N ? i0 - a.N : i0, t1 = i1 >= a.N ? i1 - a.N : i1;
                     if (t0 == t1) zero_row(a.dx, t0, a.D, a.dx_bf16, lane);
                 }
             }
         } else if (j < pad_x) {
-            const int32_t item = __ldg(a.items_x + j);
+            const int32_t item = __ldg(lx + j);
             const bool pad = item >= two_n;
             const int h = item >= a.N ? 1 : 0;
             copy_row(a.q8 + int64_t(pad ? 0 : item - h * a.N) * a.C, a.a_x + j * a.C, a.C, lane, pad, 1, h);
         } else if (j < seg_bw) {
             const int64_t r = j - pad_x;
-            const int32_t item = __ldg(a.items_w + r);
+            const int32_t item = __ldg(lw + r);
             const bool pad = item >= two_n;
             const int h = item >= a.N ? 1 : 0;
             copy_row(a.q8 + int64_t(pad ? 0 : item - h * a.N) * a.C, a.a_w + r * a.C, a.C, lane, pad, 1, h);
         } else {
+            // B_W row = weight x X_hat[t]: 2^wexp for kept items, -1 for a form-2
+            // correction row that removes the item's dense term (|.| <= 112)
             const int64_t r = j - seg_bw;
-            const int32_t item = __ldg(a.items_w + r);
+            const int32_t item = __ldg(lw + r);
             const bool pad = item >= two_n;
             const int t = pad ? 0 : (item >= a.N ? item - a.N : item);
-            copy_row(a.xq + int64_t(t) * a.D, a.b_w + r * a.D, a.D, lane, pad, pad ? 1 : (1 << __ldg(a.wexp_w + r)));
+            const int e = pad ? 0 : int(__ldg(ew + r));
+            copy_row(a.xq + int64_t(t) * a.D, a.b_w + r * a.D, a.D, lane, pad, e < 0 ? -1 : (1 << e));
         }
     }
 }

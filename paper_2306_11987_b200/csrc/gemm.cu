@@ -150,17 +150,23 @@ __device__ __forceinline__ void masked_scaled_fwht(const uint32_t (&r)[CW / 32][
 
 // ---------------------------------------------------------------------------- schedule
 // Device-resolved size of one problem of the launch.
-struct ProbSize { int M, K, m_tiles, n_tiles, T, nk; bool dense; };
+// form: the operand form the sampler chose for this mask -- 0 the compacted kept items,
+// 1 dense (reading Z-32: Q and X_hat, one row per token), 2 dense + correction (reading
+// Z-33): grad_X = Q token rows (m-tiles 0 .. mtd-1) then sub-list item rows; grad_W = Q /
+// X_hat token k-blocks (0 .. nkd-1) then correction k-blocks
+struct ProbSize { int M, K, m_tiles, n_tiles, T, nk; int form, mtd, nkd; };
 
 template <int EPI, int BMP, int BN>
 __device__ __forceinline__ ProbSize prob_size(const GemmArgs& g) {
     ProbSize s{};
-    // dense mode (the mask kept every nonzero item with weight 1, reading Z-32): the
-    // operands are the 8-bit code plane Q and X_hat themselves, one row per token
-    s.dense = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr && __ldg(g.dense_flag) != 0;
-    s.M = (EPI == EPI_DGRAD && s.dense) ? g.n_tokens : (g.m_dev ? __ldg(g.m_dev) : g.M);
-    s.K = (EPI == EPI_WGRAD && s.dense) ? ((g.n_tokens + kBK - 1) / kBK) * kBK
-                                        : (g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K);
+    s.form = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr ? __ldg(g.dense_flag) : 0;
+    const int tok_kb = (g.n_tokens + kBK - 1) / kBK;
+    if (EPI == EPI_DGRAD && s.form == 1) s.M = g.n_tokens;
+    else if (EPI == EPI_DGRAD && s.form == 2) { s.mtd = (g.n_tokens + BMP - 1) / BMP; s.M = s.mtd * BMP + __ldg(g.m_dev2); }
+    else s.M = g.m_dev ? __ldg(g.m_dev) : g.M;
+    if (EPI == EPI_WGRAD && s.form == 1) s.K = tok_kb * kBK;
+    else if (EPI == EPI_WGRAD && s.form == 2) { s.nkd = tok_kb; s.K = (tok_kb + (__ldg(g.k_dev2) + kBK - 1) / kBK) * kBK; }
+    else s.K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
     s.m_tiles = (s.M + BMP - 1) / BMP;
     s.n_tiles = (g.Nn + BN - 1) / BN;
     s.T = s.m_tiles * s.n_tiles;
@@ -328,16 +334,25 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             const bool p1 = kBwd && sg.prob == 1;
             const ProbSize& ps = p1 ? s1 : s0;
             const bool a_mn = kBwd ? p1 : A_MN;
-            const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank);     // this CTA's A rows
+            const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank);     // this CTA's output rows
             const int nb = (sg.tile % ps.n_tiles) * BN + BNC * int(rank);      // this CTA's B rows
+            const bool is_w = EPI == EPI_WGRAD || p1;
             const CUtensorMap* pA = &maps.m[MAP_A];
             const CUtensorMap* pB = &maps.m[MAP_B];
-            if ((EPI == EPI_DGRAD || (kBwd && !p1)) && ps.dense) pA = &maps.m[MAP_A2];    // Q, K-major
-            if (EPI == EPI_WGRAD || p1) {
-                if (ps.dense) { pA = &maps.m[MAP_A3]; pB = &maps.m[MAP_B2]; }              // Q and X_hat, MN-major
-                else if (kBwd) { pA = &maps.m[MAP_AW]; pB = &maps.m[MAP_BW]; }
+            int a_row = m0;                                                    // this CTA's A rows
+            if (EPI == EPI_DGRAD || (kBwd && !p1)) {
+                const int mb = sg.tile / ps.n_tiles;
+                if (ps.form == 1 || (ps.form == 2 && mb < ps.mtd)) pA = &maps.m[MAP_A2];   // Q token rows, K-major
+                else if (ps.form == 2) a_row -= ps.mtd * BMP;                                // sub-list rows of A_X
             }
+            const CUtensorMap* pAs = kBwd ? &maps.m[MAP_AW] : &maps.m[MAP_A];  // grad_W gathered rows
+            const CUtensorMap* pBs = kBwd ? &maps.m[MAP_BW] : &maps.m[MAP_B];
             for (int kb = 0; kb < sg.nk; ++kb) {
+                int kr = kb;                                                   // k-block of the map
+                if (is_w) {
+                    if (ps.form == 1 || (ps.form == 2 && kb < ps.nkd)) { pA = &maps.m[MAP_A3]; pB = &maps.m[MAP_B2]; }
+                    else { pA = pAs; pB = pBs; if (ps.form == 2) kr = kb - ps.nkd; }   // Q / X_hat, then A_W / B_W
+                }
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
@@ -345,24 +360,24 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                     uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
                     if constexpr (CG == 2) {
                         const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (a_mn) tma_load_2d_2sm(a_dst, pA, fb, m0, kb * kBK);
-                        else      tma_load_2d_2sm(a_dst, pA, fb, kb * kBK, m0);
+                        if (a_mn) tma_load_2d_2sm(a_dst, pA, fb, a_row, kr * kBK);
+                        else      tma_load_2d_2sm(a_dst, pA, fb, kr * kBK, a_row);
                         if (B_MN || kBwd) {
 #pragma unroll
                             for (int q = 0; q < BNC / 128; ++q)
-                                tma_load_2d_2sm(b_dst + q * 128 * kBK, pB, fb, nb + 128 * q, kb * kBK);
+                                tma_load_2d_2sm(b_dst + q * 128 * kBK, pB, fb, nb + 128 * q, kr * kBK);
                         } else {
-                            tma_load_2d_2sm(b_dst, pB, fb, kb * kBK, nb);
+                            tma_load_2d_2sm(b_dst, pB, fb, kr * kBK, nb);
                         }
                     } else {
-                        if (a_mn) tma_load_2d(a_dst, pA, &full[stage], m0, kb * kBK);
-                        else      tma_load_2d(a_dst, pA, &full[stage], kb * kBK, m0);
+                        if (a_mn) tma_load_2d(a_dst, pA, &full[stage], a_row, kr * kBK);
+                        else      tma_load_2d(a_dst, pA, &full[stage], kr * kBK, a_row);
                         if (B_MN || kBwd) {
 #pragma unroll
                             for (int q = 0; q < BNC / 128; ++q)
-                                tma_load_2d(b_dst + q * 128 * kBK, pB, &full[stage], nb + 128 * q, kb * kBK);
+                                tma_load_2d(b_dst + q * 128 * kBK, pB, &full[stage], nb + 128 * q, kr * kBK);
                         } else {
-                            tma_load_2d(b_dst, pB, &full[stage], kb * kBK, nb);
+                            tma_load_2d(b_dst, pB, &full[stage], kr * kBK, nb);
                         }
                     }
                 }
@@ -426,20 +441,32 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
         // otherwise sit as two dependent global-memory latencies on every tile.  Left
         // raw until the tile is processed (a consumer right after the load made every
         // tile wait for it, ncu: long-scoreboard on the epilogue warps).
-        struct RowInfo { int item, edge, eword, rw; };
+        // dense: a Q token row (weight 1, never paired); skip: its token's grad_X row comes
+        // from sub-list item rows (form 2), so this row is not stored; li: list index
+        struct RowInfo { int item, edge, eword, li; bool dense, skip; };
         auto is_dg = [&](const Seg& sg) { return EPI0 == EPI_DGRAD && (!kBwd || sg.prob == 0); };
         auto load_ri = [&](const Seg& sg) {
-            RowInfo x{two_n, two_n, 0, 0};
+            RowInfo x{two_n, two_n, 0, 0, false, false};
             if (sg.valid && is_dg(sg)) {
                 const int rw = (sg.tile / s0.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
-                x.rw = rw;
-                if (rw < s0.M && s0.dense) {
-                    x.item = rw;                       // token rw, weight 1, never paired
-                } else if (rw < s0.M) {
-                    x.item = __ldg(g.items + rw);
-                    x.eword = int(__ldg(reinterpret_cast<const uint32_t*>(g.wexp + (rw & ~3))));
-                    if (lane == 31 && rw + 1 < s0.M) x.edge = __ldg(g.items + rw + 1);
-                    if (lane == 0 && rw > 0) x.edge = __ldg(g.items + rw - 1);
+                if (s0.form == 1 || (s0.form == 2 && rw < s0.mtd * BMP)) {
+                    x.dense = true;
+                    if (rw < g.n_tokens) {
+                        x.item = rw;                   // token rw, weight 1, never paired
+                        x.skip = s0.form == 2 && __ldg(g.tok_flag + rw) != 0;
+                    }
+                } else {
+                    const int li = s0.form == 2 ? rw - s0.mtd * BMP : rw;        // index into the item list
+                    const int cnt = s0.form == 2 ? s0.M - s0.mtd * BMP : s0.M;
+                    const int32_t* items = s0.form == 2 ? g.items2 : g.items;
+                    const int8_t* wexp = s0.form == 2 ? g.wexp2 : g.wexp;
+                    x.li = li;
+                    if (li < cnt) {
+                        x.item = __ldg(items + li);
+                        x.eword = int(__ldg(reinterpret_cast<const uint32_t*>(wexp + (li & ~3))));
+                        if (lane == 31 && li + 1 < cnt) x.edge = __ldg(items + li + 1);
+                        if (lane == 0 && li > 0) x.edge = __ldg(items + li - 1);
+                    }
                 }
             }
             return x;
@@ -494,18 +521,17 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             int row_e = 0;                             // dgrad: log2 of the item's weight
             if (dg) {
                 const int item = ri_cur.item;
-                valid = valid && item < two_n;
+                valid = item < two_n && !ri_cur.skip;
                 const int h = item >= g.n_tokens ? 1 : 0;
                 out_row = item - h * g.n_tokens;
-                const int e = valid ? int(int8_t(uint32_t(ri_cur.eword) >> (8 * (ri_cur.rw & 3)))) : 0;
-                // neighbours: rows rw + 1 / rw - 1 (lanes 31 / 0 loaded them; others shuffle);
-                // rows at or past M read as the sentinel
+                const int e = valid && !ri_cur.dense ? int(int8_t(uint32_t(ri_cur.eword) >> (8 * (ri_cur.li & 3)))) : 0;
+                // neighbours: list rows li + 1 / li - 1 (lanes 31 / 0 loaded them; others shuffle);
+                // rows past the list read as the sentinel; token rows have none
                 int nx = __shfl_down_sync(0xFFFFFFFFu, ri_cur.item, 1);
                 int pv = __shfl_up_sync(0xFFFFFFFFu, ri_cur.item, 1);
                 if (lane == 31) nx = ri_cur.edge;
                 if (lane == 0) pv = ri_cur.edge;
-                if (row + 1 >= ps.M || ps.dense) nx = two_n;
-                if (row == 0 || ps.dense) pv = two_n;
+                if (ri_cur.dense) { nx = two_n; pv = two_n; }
                 row_e = e;
                 rscale = ldexpf(__fmul_rn(G.scale, sd), e);   // s_up = 16 s_down is inside the A codes
                 const int inext = valid ? nx : two_n;
@@ -566,7 +592,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 if (dg) {
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
-                    if (!ps.dense) {                        // token rows (dense) have no partner item
+                    if (!ri_cur.dense) {                    // token rows have no partner item (warp-uniform:
+                                                            // the form-2 segment border is 256-row aligned)
 #pragma unroll
                         for (int i = 0; i < CW; ++i) {     // warp-wide: every lane takes part
                             const float o = __shfl_down_sync(0xFFFFFFFFu, v[i], 1);
@@ -642,6 +669,15 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 } else {                              // EPI_WGRAD (or problem 1 of EPI_BWD)
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
+                    if (G.out_mc != nullptr) {        // f4: the data-parallel all-reduce inside the GEMM
+                        if (row < ps.M) {
+                            float* dst = G.out_mc + int64_t(row) * G.Nn + col0;
+#pragma unroll
+                            for (int i = 0; i < CW; i += 4)
+                                if (col0 + i < G.Nn) multimem_red_add_v4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int i = 0; i < CW; ++i) wv[i] = __float_as_uint(v[i]);
                 }
@@ -678,6 +714,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             if (lane == 0) g1.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc[1];
         }
         bulk_wait<0>();                                // every lane: its own copies are done
+        if ((EPI0 == EPI_WGRAD && g.out_mc != nullptr) || (kBwd && g1.out_mc != nullptr))
+            __threadfence_system();                    // multimem reductions performed before the kernel ends
         __syncwarp();
     }
 

@@ -57,7 +57,16 @@ struct SamplerArgs {
     uint8_t* x_touched;       // [N]: 1 if the token has a kept grad_X item (optional)
     uint32_t* zero_words;     // optional: words zeroed by the launch (the GEMMs' A.3 partial slots)
     int32_t n_zero_words;
-    int32_t* det_flags;       // optional [2]: 1 if mask m kept a deterministic set (all positives / all items)
+    int32_t* det_flags;       // optional [2]: operand form of mask m's GEMM: 1 deterministic (every
+                              // positive item kept with weight 1: dense Q / X_hat), 0 sampled
+                              // (compacted kept items), 2 dense + correction (a binding budget
+                              // that left few items sampled: see corr_* / sub_*)
+    // optional, form 2 (all null: form 2 never chosen):
+    int32_t* corr_items; int8_t* corr_wexp; int32_t* corr_count;   // grad_W: per sampled item a
+                              // -1 row (removes its dense term) and, if kept, a +2^wexp row
+    int32_t* sub_items; int8_t* sub_wexp; int32_t* sub_count;      // grad_X: the kept items of the
+                              // tokens with a sampled item (token-major)
+    uint8_t* tok_flag;        // [N] 1: token's grad_X row comes from sub-list rows, not Q
 };
 int sampler_max_tokens();
 int sampler_cluster_ctas(int64_t N);      // CTAs per mask the sampler launches for N tokens (introspection)
@@ -76,8 +85,10 @@ struct CompactArgs {
     int8_t* a_x;              // [2N+128, C]
     int8_t* a_w;              // [kcap, C]
     int8_t* b_w;              // [kcap, D]
-    const int32_t* det_flags; // optional [2] (sampler): [1] set: grad_X GEMM dense (no A_X, no zero
-                              // rows); [0] set: grad_W GEMM dense (no A_W / B_W)
+    const int32_t* det_flags; // optional [2] (sampler) operand forms: [1] grad_X, [0] grad_W:
+                              // 1 dense (nothing to move), 0 sampled, 2 dense + correction
+    const int32_t* corr_items; const int8_t* corr_wexp; const int32_t* corr_count;   // form 2
+    const int32_t* sub_items; const int32_t* sub_count; const uint8_t* tok_flag;
 };
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
@@ -109,6 +120,15 @@ struct GemmArgs {
     // with weight 1): dgrad reads A = Q (map a2, M = n_tokens rows = tokens), wgrad reads
     // A = Q and B = X_hat (maps a3, b2, K = n_tokens)
     const int32_t* dense_flag;
+    // operand form 2 (dense + correction): grad_X sub list (rows after the token rows of Q,
+    // which start at row round_up(N, 256)) and the per-token flags; grad_W correction-row
+    // count (k-blocks after the round_up(N, 128) token rows)
+    const int32_t* items2; const int8_t* wexp2; const int32_t* m_dev2; const uint8_t* tok_flag;
+    const int32_t* k_dev2;
+    // grad_W only, optional: multicast (NVLS) address of a symmetric [M, Nn] fp32 buffer that
+    // spans the data-parallel ranks; the epilogue reduces its tile into every rank's copy with
+    // multimem.red.add instead of storing to `out`
+    float* out_mc;
 };
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
 // CUtensorMap* (host): A, B, C (output), A2 (grad_X dense A = Q), A3 / B2 (grad_W dense A = Q,

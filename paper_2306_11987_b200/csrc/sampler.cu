@@ -52,6 +52,8 @@ struct SamplerSmem {
     uint32_t warp_c[kSamplerThreads / 32];
     uint32_t scan[32];
     uint32_t cta_tot[16];
+    uint32_t scan2[32];
+    uint32_t cta_tot2[16];
 };
 
 
@@ -79,6 +81,47 @@ template <> struct Group<1> {
     __device__ void sync() const { __syncthreads(); }
     template <class T> __device__ T* map(T* p, int) const { return p; }
 };
+
+// items per CTA of a CL-CTA group: even, so a token's two items (slots 2t, 2t+1)
+// never straddle two CTAs
+__host__ __device__ inline int sampler_per(int N, int CL) { return ((2 * N + CL - 1) / CL + 1) & ~1; }
+
+// Exclusive prefix of v over all threads of the CTA group (thread order within a CTA,
+// CTA rank order across the cluster) and the group total.  Collective: every thread of
+// every CTA of the group calls it; scan / tot are shared arrays of the caller.
+template <int CL, int NT>
+__device__ uint32_t group_scan(const Group<CL>& cl, uint32_t v, uint32_t* scan, uint32_t* tot, uint32_t& total) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = int(cl.rank());
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    if (lane == 31) scan[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < NT / 32 ? scan[lane] : 0u;
+        uint32_t x = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += n;
+        }
+        if (lane < NT / 32) scan[lane] = x - w;            // exclusive warp offsets
+        if (lane == 31)
+            for (int r = 0; r < CL; ++r) *cl.map(&tot[rank], r) = x;
+    }
+    cl.sync();
+    uint32_t cta_off = 0;
+    total = 0;
+    for (int r = 0; r < CL; ++r) {
+        if (r < rank) cta_off += tot[r];
+        total += tot[r];
+    }
+    return cta_off + scan[warp] + (incl - v);
+}
 
 // Exact floor(num 2^32 / W) for 0 < num < W < 2^64 without a 128-bit division:
 // a double-precision estimate (relative error < 2^-52, so off by at most a few
@@ -161,7 +204,7 @@ lss_sampler_kernel(SamplerArgs a) {
     const int mask_id = blockIdx.y;                      // 0: grad_W, 1: grad_X
     const int N = a.N;
     const int n_items = 2 * N;
-    const int per = (n_items + CL - 1) / CL;
+    const int per = sampler_per(N, CL);
     const int per16 = (per + 15) & ~15;
     uint64_t* sw = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SamplerSmem));
     uint8_t* scl = reinterpret_cast<uint8_t*>(sw + per16);
@@ -231,10 +274,10 @@ lss_sampler_kernel(SamplerArgs a) {
     // deterministic set (every positive item with weight 1, or all items): the
     // grad_W set is then a subset of the grad_X set (w_W > 0 implies w_X > 0), so
     // equal counts mean equal lists
-    if (a.det_flags && rank == 0 && threadIdx.x == 0) a.det_flags[mask_id] = binding ? 0 : 1;
+
     uint64_t R = B, W = Wall;
+    uint32_t s_cnt = 0;                                   // |S|: items clamped to p = 1 by A.2
     if (binding) {
-        uint32_t s_cnt = 0;
         for (int round = 0; round <= n_items + 1; ++round) {
             uint64_t wun = 0; uint32_t sc = 0;
             for (int j = t_lo; j < t_hi; ++j) {
@@ -252,6 +295,13 @@ lss_sampler_kernel(SamplerArgs a) {
             W = Wn;
         }
     }
+
+    // operand form of this mask's GEMM (reading Z-33): a binding budget that
+    // leaves only a few items sampled (0 < p < 1) runs the dense Q / X_hat GEMM plus
+    // correction rows for those items instead of compacting every kept item
+    const uint32_t n_samp = binding ? Z - s_cnt : 0u;
+    const bool corr = binding && a.corr_items != nullptr && uint64_t(n_samp) * 16 <= B;
+    if (a.det_flags && rank == 0 && threadIdx.x == 0) a.det_flags[mask_id] = binding ? (corr ? 2 : 0) : 1;
 
     // ---- Bernoulli with dyadic weights ---------------------------------------
     uint32_t my_keep = 0;
@@ -292,36 +342,8 @@ lss_sampler_kernel(SamplerArgs a) {
 
     smp_stamp(st_n, st_on);
     // ---- compaction: block exclusive scan + cluster prefix --------------------
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t incl = my_keep;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += n;
-    }
-    if (lane == 31) sm.scan[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = lane < NT / 32 ? sm.scan[lane] : 0u;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t n = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (lane >= o) x += n;
-        }
-        if (lane < NT / 32) sm.scan[lane] = x - v;          // exclusive warp offsets
-        if (lane == 31) {
-            for (int r = 0; r < CL; ++r)
-                *cl.map(&sm.cta_tot[rank], r) = x;
-        }
-    }
-    cl.sync();
-    uint32_t cta_off = 0, total = 0;
-    for (int r = 0; r < CL; ++r) {
-        if (r < rank) cta_off += sm.cta_tot[r];
-        total += sm.cta_tot[r];
-    }
-    uint32_t pos = cta_off + sm.scan[warp] + (incl - my_keep);
+    uint32_t total = 0;
+    uint32_t pos = group_scan<CL, NT>(cl, my_keep, sm.scan, sm.cta_tot, total);
     int32_t* items = a.items[mask_id];
     int8_t* wexp = a.wexp[mask_id];
     for (int j = t_lo; j < t_hi; ++j) {
@@ -340,6 +362,40 @@ lss_sampler_kernel(SamplerArgs a) {
         }
         if (threadIdx.x == 0) *a.count[mask_id] = int32_t(total);
     }
+    if (corr) {
+        // form 2 lists.  An item is sampled when its score is positive and A.2 did not
+        // clamp it.  grad_W: per sampled item a -1 row and, when kept, a +2^e row (the
+        // dense Q^T X_hat already holds weight 1 for every item).  grad_X: every kept
+        // item of a token that has a sampled item (its Q row is not used; tok_flag).
+        __syncthreads();                       // swe of the whole CTA written
+        auto sampled = [&](int j) { return sw[j] > 0 && !scl[j]; };
+        uint32_t my_n = 0;
+        for (int j = t_lo; j < t_hi; ++j) {
+            if (mask_id == 0) my_n += sampled(j) ? 1u + (swe[j] >= 0 ? 1u : 0u) : 0u;
+            else my_n += ((sampled(j) || sampled(j ^ 1)) && swe[j] >= 0) ? 1u : 0u;
+        }
+        uint32_t tot2 = 0;
+        uint32_t p2 = group_scan<CL, NT>(cl, my_n, sm.scan2, sm.cta_tot2, tot2);
+        int32_t* li = mask_id == 0 ? a.corr_items : a.sub_items;
+        int8_t* le = mask_id == 0 ? a.corr_wexp : a.sub_wexp;
+        for (int j = t_lo; j < t_hi; ++j) {
+            const int it = item_of(base + j);
+            if (mask_id == 0) {
+                if (!sampled(j)) continue;
+                li[p2] = it; le[p2] = -1; ++p2;
+                if (swe[j] >= 0) { li[p2] = it; le[p2] = swe[j]; ++p2; }
+            } else {
+                const bool ts = sampled(j) || sampled(j ^ 1);
+                if ((j & 1) == 0) a.tok_flag[it] = ts ? 1 : 0;            // slot 2t: item t (h = 0)
+                if (ts && swe[j] >= 0) { li[p2] = it; le[p2] = swe[j]; ++p2; }
+            }
+        }
+        if (rank == 0) {
+            const uint32_t padded = (tot2 + 127u) & ~127u;
+            for (uint32_t p = tot2 + threadIdx.x; p < padded; p += NT) { li[p] = n_items; le[p] = 0; }
+            if (threadIdx.x == 0) *(mask_id == 0 ? a.corr_count : a.sub_count) = int32_t(tot2);
+        }
+    }
     smp_stamp(st_n, st_on);
     cl.sync();
     smp_stamp(st_n, st_on);                                 // keep DSMEM alive until all remote writes landed
@@ -347,7 +403,7 @@ lss_sampler_kernel(SamplerArgs a) {
 
 template <int CL, int NT>
 static void sampler_config(const SamplerArgs& a, cudaStream_t s, cudaLaunchConfig_t& cfg, cudaLaunchAttribute (&attr)[2]) {
-    const int per = (2 * a.N + CL - 1) / CL;
+    const int per = sampler_per(a.N, CL);
     const int per16 = (per + 15) & ~15;
     cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask

@@ -56,3 +56,38 @@ def max_over_ranks(value, device):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class SymmetricGradW:
+    """A grad_W buffer in PyTorch symmetric memory with an NVLS multicast address
+    (SURVEY.md §8(f4)): pass `multicast(offset)` as `dw_multicast` to
+    Int4Linear.backward and the grad_W GEMM epilogue reduces its tiles into every
+    rank's copy (multimem.red.add) -- no separate all-reduce pass.  Per step:
+    zero_() on every rank before the backwards, barrier() after them.
+    Plumbing only (allocation, rendezvous, barrier); the reduction runs in the
+    library's kernel.  `available` is False when the device / driver offers no
+    multicast object for this group (then use allreduce_grad_w)."""
+
+    def __init__(self, numel, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group or dist.group.WORLD
+        self.group_name = group.group_name
+        try:
+            symm_mem.enable_symm_mem_for_group(self.group_name)
+        except Exception:
+            pass
+        self.tensor = symm_mem.empty(int(numel), dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.tensor, self.group_name)
+        self.mc = int(getattr(self.handle, "multicast_ptr", 0) or 0)
+        self.available = self.mc != 0
+
+    def multicast(self, offset_elems=0):
+        return self.mc + 4 * int(offset_elems)
+
+    def zero_(self):
+        self.tensor.zero_()
+
+    def barrier(self):
+        """Device-side barrier of the group on the current stream (every rank's
+        reductions have landed in every copy once it returns on the device)."""
+        self.handle.barrier(channel=0)

@@ -227,3 +227,29 @@ def test_status_word_nonfinite_and_zero_grad():
     torch.cuda.synchronize()
     assert int(layer.status()[0]) == 0
     _check_backward(layer, g, s_x, s_w, k, dX.cpu().numpy(), dW.cpu().numpy(), o_lss.MODE_BERNOULLI, call_id=1)
+
+
+# ----------------------------------------------------------------------------- operand form 2
+@pytest.mark.parametrize("N,D,C,seed,k", [(2048, 256, 2048, 0, 5), (4096, 256, 2048, 2, 5), (4096, 256, 2048, 1, 3)])
+def test_binding_few_sampled_dense_plus_correction(N, D, C, seed, k):
+    """Reading Z-33: a binding budget that leaves few items sampled (sparse grad_Y
+    just over the budget: these seeds give 18-220 sampled items, found with the
+    oracle's A.2) runs the dense Q / X_hat GEMMs plus correction rows -- grad_W gets
+    a -1 row per sampled item and a +2^e row per kept one, grad_X takes the sampled
+    tokens' rows from their kept items.  Gradients equal the oracle's item-by-item
+    sums; the kept lists are unchanged."""
+    x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=False, seed=seed, token_offset=0)
+    assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == (2, 2)
+    _check_backward(layer, g, s_x, s_w, k, dX, dW, o_lss.MODE_BERNOULLI)
+
+
+def test_form2_bf16_grad_x_matches_fp32():
+    N, D, C, k = 2048, 256, 2048, 5
+    x, w, s_x, s_w, layer, g, dX32, dW32 = _bwd_case(N, D, C, k, dense=False, seed=0)
+    dX = torch.empty(N, D, dtype=torch.bfloat16, device="cuda")
+    dW = torch.empty(C, D, dtype=torch.float32, device="cuda")
+    layer.backward(to_bf16_cuda(g), dX, dW, synth.PHILOX_SEED, 3, 0, 0)
+    torch.cuda.synchronize()
+    assert tuple(int(v) for v in layer.dense_flags().cpu().numpy()) == (2, 2)
+    assert np.array_equal(dW.cpu().numpy(), dW32)
+    assert rel_frob(dX.float().cpu().numpy(), dX32) < 4e-3
