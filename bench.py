@@ -124,8 +124,9 @@ def workload_config(args, lins, world):
             "parallelism": f"dp{world} (token-sharded)",
             "l2": "a step's inputs (GBs for the stack) exceed the 126 MB L2; L2 is also flushed before every timed "
                   "step (256 MiB write + 256 MiB read of another buffer)",
-            "graph": "forward and each layer's backward captured as CUDA graphs, kernels chained by programmatic "
-                     "dependent launch; per-kernel breakdown from PDL-off captures"}
+            "graph": ("the whole step captured as one CUDA graph" if world == 1 else
+                      "forward and each layer's backward captured as CUDA graphs (the all-reduces between them)")
+                     + ", kernels chained by programmatic dependent launch; per-kernel breakdown from PDL-off captures"}
 
 
 # ---------------------------------------------------------------------------- launcher
@@ -466,8 +467,16 @@ def run_ours(args):
         flush_w.zero_()
         torch.sum(flush_r)
 
-    g_fwd = capture(st.fwd_body)
-    g_bwd = [capture(lambda l=l: st.bwd_body(l)) for l in range(n_layers)]
+    def whole_step():
+        st.fwd_body()
+        for layer in reversed(range(n_layers)):
+            st.bwd_body(layer)
+
+    if world == 1:      # no exchange: the whole step is one graph (no gaps between graph launches)
+        g_fwd, g_bwd = capture(whole_step), [None] * n_layers
+    else:               # the all-reduces go between the per-layer backward graphs
+        g_fwd = capture(st.fwd_body)
+        g_bwd = [capture(lambda l=l: st.bwd_body(l)) for l in range(n_layers)]
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def one_step(gf, gb, buckets, fused=False):
@@ -477,7 +486,8 @@ def run_ours(args):
         gf.replay()
         handles = []
         for layer in reversed(range(n_layers)):
-            gb[layer].replay()
+            if gb[layer] is not None:
+                gb[layer].replay()
             if world > 1 and not fused:   # async on NCCL's stream: overlaps the next (lower) layer's backward
                 handles.append(dist.all_reduce(buckets[layer], op=dist.ReduceOp.SUM, async_op=True))
         for h in handles:
@@ -530,12 +540,18 @@ def run_ours(args):
             torch.matmul(st.G[i], st.W[i], out=dXb[i])
             torch.matmul(st.G[i].t(), st.X[i], out=bf_dW[i])
 
-    bf_fwd()
-    for layer in range(n_layers):
-        bf_bwd(layer)
+    def bf_step():
+        bf_fwd()
+        for layer in reversed(range(n_layers)):
+            bf_bwd(layer)
+
+    bf_step()
     torch.cuda.synchronize()
-    gb_fwd = capture(bf_fwd)
-    gb_bwd = [capture(lambda l=l: bf_bwd(l)) for l in range(n_layers)]
+    if world == 1:
+        gb_fwd, gb_bwd = capture(bf_step), [None] * n_layers
+    else:
+        gb_fwd = capture(bf_fwd)
+        gb_bwd = [capture(lambda l=l: bf_bwd(l)) for l in range(n_layers)]
     timed(gb_fwd, gb_bwd, bf_bucket, args.warmup)
     bf16_ms = max_over_ranks(statistics.mean(timed(gb_fwd, gb_bwd, bf_bucket, args.steps)), dev, world)
     del gb_fwd, gb_bwd, Yb, dXb, bf_bucket, bf_dW

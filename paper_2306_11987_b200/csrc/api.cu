@@ -228,7 +228,7 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
                                   uint64_t(args.Nn), uint64_t(args.M));
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     static const char* kNames[] = {"gemm_i8_int32", "gemm_i8_fwd", "gemm_i8_dgrad", "gemm_i8_wgrad"};
-    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, nullptr, nullptr};
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, nullptr, nullptr, nullptr};
     I4_LAUNCH(i4::launch_gemm(maps, args, sms > 0 ? sms : device_info().sms, s), kNames[args.epi], s);
     return I4_OK;
 }
@@ -241,7 +241,7 @@ i4_status gemm(const Operand& A, const Operand& B, const i4::GemmArgs& args, cud
 i4_status gemm_bwd(const Operand& a_x, const Operand& q_rows, const Operand& w_mn, const Operand& a_w,
                    const Operand& b_w, const Operand& q_mn, const Operand& xq_mn, const i4::GemmArgs& gx,
                    const i4::GemmArgs& gw, cudaStream_t s) {
-    CUtensorMap ta, tb, tc, ta2, ta3, tb2, taw, tbw;
+    CUtensorMap ta, tb, tc, ta2, ta3, tb2, taw, tbw, tdx;
     bool ok = make_tmap_i8(&ta, a_x.p, uint64_t(a_x.inner), uint64_t(a_x.rows), uint64_t(a_x.pitch), 128u) &&
               make_tmap_i8(&ta2, q_rows.p, uint64_t(q_rows.inner), uint64_t(q_rows.rows), uint64_t(q_rows.pitch), 128u) &&
               make_tmap_i8(&tb, w_mn.p, uint64_t(w_mn.inner), uint64_t(w_mn.rows), uint64_t(w_mn.pitch), 128u) &&
@@ -249,9 +249,10 @@ i4_status gemm_bwd(const Operand& a_x, const Operand& q_rows, const Operand& w_m
               make_tmap_i8(&tbw, b_w.p, uint64_t(b_w.inner), uint64_t(b_w.rows), uint64_t(b_w.pitch), 128u) &&
               make_tmap_i8(&ta3, q_mn.p, uint64_t(q_mn.inner), uint64_t(q_mn.rows), uint64_t(q_mn.pitch), 128u) &&
               make_tmap_i8(&tb2, xq_mn.p, uint64_t(xq_mn.inner), uint64_t(xq_mn.rows), uint64_t(xq_mn.pitch), 128u) &&
-              make_tmap_out(&tc, gw.out, false, false, uint64_t(gw.Nn), uint64_t(gw.M));
+              make_tmap_out(&tc, gw.out, false, false, uint64_t(gw.Nn), uint64_t(gw.M)) &&
+              make_tmap_out(&tdx, gx.out, gx.out_bf16 != 0, false, uint64_t(gx.Nn), uint64_t(gx.n_tokens));
     if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, &taw, &tbw};
+    const i4::GemmMaps maps{&ta, &tb, &tc, &ta2, &ta3, &tb2, &taw, &tbw, &tdx};
     I4_LAUNCH(i4::launch_gemm(maps, gx, device_info().sms, s, &gw), "gemm_i8_bwd", s);
     return I4_OK;
 }

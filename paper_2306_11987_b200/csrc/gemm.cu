@@ -267,8 +267,8 @@ __device__ __forceinline__ Seg seg_at(const Sched& s, int p, int j) {
 }
 
 // ---------------------------------------------------------------------------- kernel
-struct GemmMapSet { CUtensorMap m[8]; };
-enum { MAP_A = 0, MAP_B = 1, MAP_C = 2, MAP_A2 = 3, MAP_A3 = 4, MAP_B2 = 5, MAP_AW = 6, MAP_BW = 7 };
+struct GemmMapSet { CUtensorMap m[9]; };
+enum { MAP_A = 0, MAP_B = 1, MAP_C = 2, MAP_A2 = 3, MAP_A3 = 4, MAP_B2 = 5, MAP_AW = 6, MAP_BW = 7, MAP_DX = 8 };
 
 // KH: Hadamard order k of the grad epilogues (compile-time, 0 for FWD / INT32).
 // EPI_BWD: problem 0 = grad_X (A K-major, B MN-major, args g), problem 1 = grad_W
@@ -303,7 +303,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
 
     if (warp == 0 && lane == 0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) tma_prefetch_desc(&maps.m[i]);
+        for (int i = 0; i < 9; ++i) tma_prefetch_desc(&maps.m[i]);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], CG * kEpiWarps); }
         fence_mbar_init();
@@ -592,6 +592,54 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 if (dg) {
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
+                    if constexpr (kBwd && CW == 32) {
+                        if (ps.form == 1) {
+                            // token rows of Q (form 1): the tile's rows are contiguous grad_X rows, so
+                            // they go out through swizzled shared-memory staging and TMA tensor
+                            // stores (full-line writes) instead of one row per lane
+                            const int part = ((c - cbeg) / 32) & 1;        // bf16: two chunks per 128 B row
+                            if (!g.out_bf16 || part == 0) {
+                                if (lane == 0) bulk_wait_read<1>();
+                                __syncwarp();
+                            }
+                            uint8_t* buf = stg + sbuf * kStageOutBytes;
+                            if (g.out_bf16) {
+                                uint32_t pk[16];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                                    pk[i] = *reinterpret_cast<uint32_t*>(&p2);
+                                }
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    *reinterpret_cast<uint4*>(stage_chunk(buf, lane, 4 * part + q)) =
+                                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                                if (part == 1 || c + CW >= cbeg + Epi::COLS) {
+                                    fence_proxy_async_smem();
+                                    __syncwarp();
+                                    if (lane == 0) {
+                                        tma_store_2d(&maps.m[MAP_DX], buf, col0 - 32 * part, m0 + lg * 32);
+                                        bulk_commit();
+                                    }
+                                    sbuf ^= 1;
+                                }
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 8; ++q)
+                                    *reinterpret_cast<uint4*>(stage_chunk(buf, lane, q)) =
+                                        make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                                                   __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+                                fence_proxy_async_smem();
+                                __syncwarp();
+                                if (lane == 0) {
+                                    tma_store_2d(&maps.m[MAP_DX], buf, col0, m0 + lg * 32);
+                                    bulk_commit();
+                                }
+                                sbuf ^= 1;
+                            }
+                            continue;
+                        }
+                    }
                     if (!ri_cur.dense) {                    // token rows have no partner item (warp-uniform:
                                                             // the form-2 segment border is 256-row aligned)
 #pragma unroll
@@ -742,8 +790,8 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, const GemmAr
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     GemmMapSet ms;
-    const void* src[8] = {m.a, m.b, m.c, m.a2, m.a3, m.b2, m.aw, m.bw};
-    for (int i = 0; i < 8; ++i) ms.m[i] = *reinterpret_cast<const CUtensorMap*>(src[i] ? src[i] : m.a);
+    const void* src[9] = {m.a, m.b, m.c, m.a2, m.a3, m.b2, m.aw, m.bw, m.dx};
+    for (int i = 0; i < 9; ++i) ms.m[i] = *reinterpret_cast<const CUtensorMap*>(src[i] ? src[i] : m.a);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(Epi::THREADS);

@@ -134,7 +134,7 @@ constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_grou
 // CUtensorMap* (host): A, B, C (output), A2 (grad_X dense A = Q), A3 / B2 (grad_W dense A = Q,
 // B = X_hat), AW / BW (grad_W sampled A_W, B_W in an EPI_BWD launch); null = unused
 struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; const void* a3; const void* b2;
-                  const void* aw; const void* bw; };
+                  const void* aw; const void* bw; const void* dx; };   // dx: grad_X output (EPI_BWD)
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s,
                         const GemmArgs* g1 = nullptr);
 int gemm_block_n(int Nn, bool b_mn);

@@ -36,7 +36,7 @@ def launches(r):
     order = []
     for x in rows[hi + 1:]:
         nm = x[ki]
-        mine = "i4::" in nm or "gemm_i8" in nm or "nvjet" in nm
+        mine = ("i4::" in nm or "nvjet" in nm or short_kernel_name(nm) is not None)
         if not mine:
             continue
         v = float(x[vi].replace(",", ""))
@@ -47,6 +47,19 @@ def launches(r):
             order.append(key)
         per.setdefault(key, []).append(us)
     ours = [k for k in order if not k.startswith("cuBLAS")]
+    if STEP:                                   # a one-step capture (tools/stack_step.py): totals per kernel
+        tot = sum(sum(per[k]) for k in ours)
+        lines = [f"# {r}: ncu launch list of ONE step of {CONFIG} (`--metrics gpu__time_duration.sum --clock-control none`)",
+                 "", "Command: `ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none "
+                 f"python tools/stack_step.py {CONFIG}` (the bench step: every forward, then every backward in "
+                 "reverse layer order, PDL on, eager launches).  Per-launch times under ncu are cold-cache and "
+                 "serialised: compare SHARES with the bench's CUPTI breakdown, not absolutes.", "",
+                 "| kernel | launches | total us | median us | share of the step |", "|---|---|---|---|---|"]
+        for k in ours:
+            lines.append(f"| {k} | {len(per[k])} | {sum(per[k]):.1f} | {statistics.median(per[k]):.1f} | "
+                         f"{sum(per[k]) / tot:.3f} |")
+        lines.append(f"| **sum of our kernels per step** | | **{tot:.1f}** | | 1.000 |")
+        return "\n".join(lines) + "\n", {k: sum(per[k]) for k in ours}
     tot = sum(statistics.median(per[k]) for k in ours)
     lines = [f"# {r}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)", "",
              f"Command: `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 3 "
@@ -95,10 +108,15 @@ def full(r):
                     continue
                 d[key] = v * UNIT_SCALE.get(units[i], 1)
         res.append(d)
+    cmd = (f"ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:\"grad_split|"
+           f"gemm_i8|hadamard_quant|lss_sampler|compact\" -s 213 -c 12 python tools/stack_step.py {CONFIG}` "
+           "(one layer's three backwards, in backward order FFN-down, FFN-up, QKV, inside the one-step run)"
+           if STEP else
+           f"ncu --set full --clock-control none --import-source on -k regex:\"grad_split|gemm_i8|hadamard_quant|"
+           f"lss_sampler|compact\" -s 7 -c 7 python bench.py --steps 1 --warmup 1 --config {CONFIG} ...` "
+           "(tools/profile_round.sh)")
     lines = [f"# {r}: ncu --set full (one launch each, cold cache, --clock-control none)", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:\"grad_split|gemm_i8|"
-             f"hadamard_quant|lss_sampler|compact\" -s 7 -c 7 python bench.py --steps 1 --warmup 1 --config {CONFIG} ...` "
-             "(tools/profile_round.sh).  DRAM write bytes stay in L2 within one replayed launch.", "",
+             "Command: `" + cmd + ".  DRAM write bytes stay in L2 within one replayed launch.", "",
              "| kernel | us | DRAM read MB | DRAM write MB | DRAM % | L2 % | INT8 tensor % | issue active % | warps active % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in res:
@@ -112,6 +130,7 @@ def full(r):
 
 
 CONFIG = sys.argv[2] if len(sys.argv) > 2 else "cfg2_bert_base_ffn1"
+STEP = "--step" in sys.argv
 
 
 def main():
@@ -120,6 +139,9 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md, _ = launches(r)
     open(os.path.join(ROOT, "profiles", f"{r}_launches.md"), "w").write(md)
+    if not os.path.exists(os.path.join(ROOT, "gpurun_out", f"{r}_full.ncu-rep")):
+        print(open(os.path.join(ROOT, "profiles", f"{r}_launches.md")).read())
+        return
     md, res = full(r)
     open(os.path.join(ROOT, "profiles", f"{r}_ncu_full.md"), "w").write(md)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
