@@ -616,8 +616,12 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0,
 // the first ones issued before the phase-1 -> phase-2 wait), accumulates the row
 // norms in registers and flushes them (exact int32 atomics onto the zeroed a_sq)
 // when the row changes.  (Measured and dropped: a dynamic pool of units claimed
-// from a counter -- the per-CTA finish spread is not load imbalance; and Philox
-// words precomputed into shared memory during phase 1 -- no gain.)
+// from a counter -- the per-CTA finish spread is not load imbalance; Philox words
+// precomputed into shared memory during phase 1 -- no gain; a software pipeline that
+// generates unit u+1's Philox words beside unit u's split, at 2 or 3 CTAs / SM --
+// 1-4 % slower; a threshold / floor without the F2I conversion (FADD2.RM magic
+// numbers) -- more ALU work, 15 % slower.  Phase 2 is ALU-pipe bound: ~12 LOP3 /
+// PRMT / IADD3 per element, 5 of them Philox's XORs.)
 
 // scratch words (uint32 [kGradSplitMaxBlocks], zero before the first call; every
 // launch returns them to zero): amax word, arrival / departure counters
