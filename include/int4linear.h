@@ -16,13 +16,8 @@
  *     workspace); the library never allocates device memory and keeps no
  *     per-call state.  Buffer sizes are stated per field below.  Library-owned
  *     global state: per-device caches of launch parameters (SM count, occupancy,
- *     the sampler's cluster size), the PDL switch (int4_set_pdl), and per
- *     (host thread, device) side streams + fork / join events (created on first
- *     use, never destroyed) that int4_linear_bwd uses to run the grad_X and
- *     grad_W GEMMs concurrently when they under-fill the GPU, and that
- *     int4_bmm_fwd / int4_bmm_bwd use for concurrent batch chains.  Work on
- *     them is forked from and joined back into `stream` by event record / wait,
- *     so stream order, graph capture and results are unaffected.
+ *     the sampler's cluster size) and the PDL switch (int4_set_pdl).  The
+ *     library creates no streams: every launch goes to `stream`.
  *   - No environment variables are read by the library.
  *   - Execution: stream-ordered and asynchronous on `stream` (a cudaStream_t
  *     passed as void*; NULL = legacy default stream).  No entry point
@@ -260,21 +255,29 @@ I4_API size_t hq_select_k_workspace_size(void);
 /* BMM in attention (A.1; reading Z-31): T = BMM(Q, K^T) with
  * Q [B, N, M], K [B, P, M] bf16 and per-batch step sizes s_q[B], s_k[B] (HOST
  * float arrays).  Batch b is the linear operator above with
- * X = Q_b, W = K_b (D = M, C = P): T_b = s_q[b] s_k[b] Q_hat_b K_hat_b^T.  The
- * cache holds all batches (device buffers, caller-allocated):
+ * X = Q_b, W = K_b (D = M, C = P): T_b = s_q[b] s_k[b] Q_hat_b K_hat_b^T, and
+ * H_hat = Repeat_B(BlockDiag(H_k, ...)) is the per-row block
+ * transform of the linear operator.  The batch dimension is inside the kernels:
+ * the forward is 3 launches for all B batches (step table, hadamard_quant over
+ * the B N + B P rows, one batched GEMM over 3-D tensor maps), the backward 4
+ * (grad_split with per-batch amax, one sampler cluster per (mask, batch), compact,
+ * one GEMM launch over every batch's grad_Q and grad_K tiles).
+ * The cache holds all batches (device buffers, caller-allocated):
  *   qq int8 [B, N, M], kq int8 [B, P, M], q_mask uint32 [B, N, M/32],
- *   k_mask uint32 [B, P, M/32], q_sqnorm int32 [B, N];
- * B, N, P, M, k are filled by int4_bmm_fwd.  Shape rules as for the linear
- * operator (M, P multiples of 64; N <= 65536 for the backward).
- * This version runs the per-batch operator for b = 0 .. B-1 (every step in the
- * library's kernels; the batch loop is host orchestration): batch b on stream
- * b % S, S = min(B, 16), library-owned streams forked from / joined into `stream`. */
+ *   k_mask uint32 [B, P, M/32], q_sqnorm int32 [B, N],
+ *   steps float [B, 8] (library-written per-batch step table: 1/s_q and 1/s_k
+ *   scaled by 2^{-k/2}, fl32(s_q s_k), fl32(s_k 2^{-k/2}), fl32(s_q 2^{-k/2}), s_q, s_k),
+ *   dev_status int32 (optional, NULL = off; status bits as i4_fwd_cache);
+ * B, N, P, M, k are filled by int4_bmm_fwd.  Shape rules: M, P positive multiples
+ * of 64 (M <= 8192, M % 2^k == 0); N > 0; the backward needs N <= 65536. */
 typedef struct {
     int8_t* qq;
     int8_t* kq;
     uint32_t* q_mask;
     uint32_t* k_mask;
     int32_t* q_sqnorm;
+    float* steps;
+    int32_t* dev_status;
     int64_t B, N, P, M;
     int32_t k;
 } i4_bmm_cache;
@@ -284,19 +287,26 @@ I4_API i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N
                               const float* s_q, const float* s_k, void* T, i4_out_dtype t_dtype, i4_bmm_cache* cache,
                               void* stream);
 
-/* Per-batch LSS-MM backward: dQ [B, N, M] (fp32 or bf16), dK [B, P, M] fp32.  Batch b
- * uses token_offset = b N (its Philox streams are distinct, reading Z-31), its own
- * amax and budget N.  plans: n_plans i4_lss_plan structs, each sized for ONE batch
- * (N tokens, C = P; scratch zeroed before first use); ws: n_plans x
- * int4_bwd_workspace_size(N, M, P) bytes.  Batch b runs as chain j = b % S,
- * S = min(B, n_plans, 16), with plans[j], workspace slice j and, for j > 0, a
- * library-owned stream forked from and joined back into `stream` (event
- * record / wait only: capturable, no host synchronisation).  Results do not
- * depend on S. */
-I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k,
-                              uint64_t seed, uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plans,
-                              int32_t n_plans, void* dQ, i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes,
-                              void* stream);
+/* Per-batch LSS-MM backward, batched inside the kernels: dQ [B, N, M] (fp32 or
+ * bf16), dK [B, P, M] fp32.  Batch b is int4_linear_bwd of its forward with
+ * token_offset = b N (distinct Philox streams, reading Z-31), its own amax and
+ * budget N, the step sizes of the forward (cache->steps), operand form 0 (the
+ * compacted kept items) for both masks.  ws: int4_bmm_bwd_workspace_size(B, N, P, M)
+ * bytes, ZERO-INITIALISED BEFORE ITS FIRST USE (it holds grad_split's barrier and
+ * per-batch amax words; every call leaves them zero again).  B is processed in
+ * chunks of at most 2048 batches (one launch sequence per chunk). */
+I4_API size_t int4_bmm_bwd_workspace_size(int64_t B, int64_t N, int64_t P, int64_t M);
+I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, uint64_t seed, uint32_t call_id,
+                              i4_lss_mode mode, void* dQ, i4_out_dtype dq_dtype, float* dK, void* ws,
+                              size_t ws_bytes, void* stream);
+/* Introspection (tests): byte offset inside the BMM backward workspace of
+ *   what = 0  s_down float [B]           1  amax bits uint32 [B]
+ *          2  kept counts int32 [2][B] ([0][b] grad_K mask, [1][b] grad_Q mask)
+ *          3  grad_K item list int32 [B][2N + 128]   4  its weight exponents int8 [B][2N + 128]
+ *          5  grad_Q item list int32 [B][2N + 128]   6  its weight exponents int8 [B][2N + 128]
+ *          7  8-bit SR codes q int8 [B N + 1, P]
+ * of the last call's first chunk; (size_t)-1 for an unknown `what`. */
+I4_API size_t int4_bmm_bwd_ws_offset(int64_t B, int64_t N, int64_t P, int64_t M, int32_t what);
 
 /* Bytes of device scratch int4_linear_bwd needs for these shapes. */
 I4_API size_t int4_bwd_workspace_size(int64_t N, int64_t D, int64_t C);

@@ -19,7 +19,7 @@ __all__ = [
     "LSS_BERNOULLI", "LSS_KEEP_POSITIVE", "LSS_NONE", "OUT_F32", "OUT_BF16",
     "hadamard_quant", "int4_linear_fwd", "bitsplit_lss", "int4_linear_bwd",
     "int4_bwd_workspace_size", "int4_gemm_s8s8s32", "int4_set_pdl", "lsq_cold_start_step", "hq_select_k", "hq_select_k_workspace_size",
-    "int4_bmm_fwd", "int4_bmm_bwd", "Int4BMM", "I4BmmCache",
+    "int4_bmm_fwd", "int4_bmm_bwd", "int4_bmm_bwd_workspace_size", "Int4BMM", "I4BmmCache",
     "lsq_cold_start_workspace_size", "cold_start_step", "Int4Linear", "BwdScratch", "LaunchTrace",
     "STATUS_NONFINITE", "STATUS_ZERO_GRAD",
 ]
@@ -63,7 +63,8 @@ class I4LssPlan(ctypes.Structure):
 
 class I4BmmCache(ctypes.Structure):
     _fields_ = [("qq", ctypes.c_void_p), ("kq", ctypes.c_void_p), ("q_mask", ctypes.c_void_p),
-                ("k_mask", ctypes.c_void_p), ("q_sqnorm", ctypes.c_void_p),
+                ("k_mask", ctypes.c_void_p), ("q_sqnorm", ctypes.c_void_p), ("steps", ctypes.c_void_p),
+                ("dev_status", ctypes.c_void_p),
                 ("B", ctypes.c_int64), ("N", ctypes.c_int64), ("P", ctypes.c_int64), ("M", ctypes.c_int64),
                 ("k", ctypes.c_int32)]
 
@@ -84,8 +85,7 @@ def _load():
         "lsq_cold_start_step": [vp, i64, vp, vp, ctypes.c_size_t, vp],
         "hq_select_k": [vp, i64, vp, i64, i64, f32, f32, i32, i32, vp, vp, vp, ctypes.c_size_t, vp],
         "int4_bmm_fwd": [vp, vp, i64, i64, i64, i64, i32, vp, vp, vp, i32, ctypes.POINTER(I4BmmCache), vp],
-        "int4_bmm_bwd": [vp, ctypes.POINTER(I4BmmCache), vp, vp, u64, u32, i32, ctypes.POINTER(I4LssPlan), i32, vp,
-                         i32, vp, vp, ctypes.c_size_t, vp],
+        "int4_bmm_bwd": [vp, ctypes.POINTER(I4BmmCache), u64, u32, i32, vp, i32, vp, vp, ctypes.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -97,6 +97,10 @@ def _load():
     L.hq_select_k_workspace_size.restype = ctypes.c_size_t
     L.int4_bwd_ws_form2_offset.argtypes = [i64, i64, i64]
     L.int4_bwd_ws_form2_offset.restype = ctypes.c_size_t
+    L.int4_bmm_bwd_workspace_size.argtypes = [i64, i64, i64, i64]
+    L.int4_bmm_bwd_workspace_size.restype = ctypes.c_size_t
+    L.int4_bmm_bwd_ws_offset.argtypes = [i64, i64, i64, i64, i32]
+    L.int4_bmm_bwd_ws_offset.restype = ctypes.c_size_t
     L.int4_bwd_ws_det_offset.argtypes = [i64, i64, i64]
     L.int4_bwd_ws_det_offset.restype = ctypes.c_size_t
     L.int4_bwd_workspace_size.argtypes = [i64, i64, i64]
@@ -412,17 +416,18 @@ def int4_bmm_fwd(Q, K, k, s_q, s_k, T, cache, stream=None):
                             ctypes.byref(cache), _stream(stream)))
 
 
-def int4_bmm_bwd(dT, cache, s_q, s_k, seed, call_id, mode, plans, dQ, dK, ws, stream=None):
-    """A.1 BMM backward: per-batch LSS-MM with token offsets b N (reading Z-31).
-    plans: a ctypes array of I4LssPlan (one per concurrent batch chain)."""
-    import numpy as np
+def int4_bmm_bwd(dT, cache, seed, call_id, mode, dQ, dK, ws, stream=None):
+    """A.1 BMM backward, batched inside the kernels: per-batch LSS-MM with token offsets
+    b N (reading Z-31).  ws: uint8 device tensor of int4_bmm_bwd_workspace_size bytes,
+    zeroed before its first use."""
     import torch
-    sq = np.ascontiguousarray(s_q, dtype=np.float32)
-    sk = np.ascontiguousarray(s_k, dtype=np.float32)
     dq_dtype = OUT_BF16 if dQ.dtype == torch.bfloat16 else OUT_F32
-    _check(lib.int4_bmm_bwd(_ptr(dT), ctypes.byref(cache), sq.ctypes.data, sk.ctypes.data, int(seed), int(call_id),
-                            int(mode), plans, len(plans), _ptr(dQ), dq_dtype, _ptr(dK), _ptr(ws),
-                            ws.numel() * ws.element_size(), _stream(stream)))
+    _check(lib.int4_bmm_bwd(_ptr(dT), ctypes.byref(cache), int(seed), int(call_id), int(mode), _ptr(dQ), dq_dtype,
+                            _ptr(dK), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def int4_bmm_bwd_workspace_size(B, N, P, M):
+    return int(lib.int4_bmm_bwd_workspace_size(B, N, P, M))
 
 
 class Int4BMM:
@@ -438,18 +443,36 @@ class Int4BMM:
         self.q_mask = torch.empty(B, N, M // 32, dtype=i32, device=dev)
         self.k_mask = torch.empty(B, P, M // 32, dtype=i32, device=dev)
         self.q_sqnorm = torch.empty(B, N, dtype=i32, device=dev)
+        self.steps = torch.zeros(B, 8, dtype=torch.float32, device=dev)
+        self.status_buf = torch.zeros(1, dtype=i32, device=dev)
         self.cache = I4BmmCache(qq=self.qq.data_ptr(), kq=self.kq.data_ptr(), q_mask=self.q_mask.data_ptr(),
-                                k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr())
-        # one plan + workspace slice per concurrent batch chain (batch b -> chain b % S)
-        S = min(B, 16)
-        self._plan_bufs = [_PlanBuffers(N, P, dev) for _ in range(S)]
-        self.plans = (I4LssPlan * S)(*[pb.plan for pb in self._plan_bufs])
-        self.plan = self.plans[0]
-        self.ws = torch.empty(S * int4_bwd_workspace_size(N, M, P), dtype=torch.uint8, device=dev)
+                                k_mask=self.k_mask.data_ptr(), q_sqnorm=self.q_sqnorm.data_ptr(),
+                                steps=self.steps.data_ptr(), dev_status=self.status_buf.data_ptr())
+        self.ws = torch.zeros(int4_bmm_bwd_workspace_size(B, N, P, M), dtype=torch.uint8, device=dev)
 
     def forward(self, Q, K, s_q, s_k, T, stream=None):
-        self.s_q, self.s_k = s_q, s_k
         int4_bmm_fwd(Q, K, self.k, s_q, s_k, T, self.cache, stream)
 
     def backward(self, dT, dQ, dK, seed, call_id=0, mode=LSS_BERNOULLI, stream=None):
-        int4_bmm_bwd(dT, self.cache, self.s_q, self.s_k, seed, call_id, mode, self.plans, dQ, dK, self.ws, stream)
+        int4_bmm_bwd(dT, self.cache, seed, call_id, mode, dQ, dK, self.ws, stream)
+
+    def status(self):
+        return int(self.status_buf.item())
+
+    def ws_view(self, what):
+        """A region of the last backward's workspace (its first chunk of <= 2048 batches) as a
+        device tensor: 0 s_down [B] f32, 1 amax bits [B] i32, 2 kept counts [2, B] i32
+        ([0] grad_K mask, [1] grad_Q mask), 3 / 5 grad_K / grad_Q item lists [B, 2N+128] i32,
+        4 / 6 their weight exponents [B, 2N+128] i8, 7 SR codes q [B N + 1, P] i8."""
+        import torch
+        B, N, P, M = min(self.B, 2048), self.N, self.P, self.M
+        off = int(lib.int4_bmm_bwd_ws_offset(self.B, N, P, M, what))
+        L = 2 * N + 128
+        dt, shape = {0: (torch.float32, (B,)), 1: (torch.int32, (B,)), 2: (torch.int32, (2, B)),
+                     3: (torch.int32, (B, L)), 4: (torch.int8, (B, L)), 5: (torch.int32, (B, L)),
+                     6: (torch.int8, (B, L)), 7: (torch.int8, (B * N + 1, P))}[what]
+        n = 1
+        for d in shape:
+            n *= d
+        esz = torch.tensor([], dtype=dt).element_size()
+        return self.ws[off:off + n * esz].view(dt).view(*shape)

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/int4linear.h"
 #include "kernels.h"
@@ -257,31 +258,35 @@ i4_status gemm_bwd(const Operand& a_x, const Operand& q_rows, const Operand& w_m
     return I4_OK;
 }
 
-// Side streams + fork / join events of this host thread (per device), used to
-// run the batch chains of the attention BMM concurrently.  Event record / wait
-// are stream-ordered and capturable (a captured step graph gets parallel branches).
-struct SideStream { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
-#ifndef I4_BMM_MAX_STREAMS
-#define I4_BMM_MAX_STREAMS 16
-#endif
-constexpr int kBmmStreams = I4_BMM_MAX_STREAMS;                       // batch chains of int4_bmm_fwd run on this many streams
-thread_local SideStream t_bmm[kBmmStreams - 1];
-
-i4_status make_side(SideStream& st) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return fail(I4_ERR_CUDA, "cudaGetDevice failed");
-    if (st.dev != dev) {
-        if (st.s) { cudaStreamDestroy(st.s); cudaEventDestroy(st.fork); cudaEventDestroy(st.join); }
-        st = SideStream{};
-        if (cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&st.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&st.join, cudaEventDisableTiming) != cudaSuccess)
-            return fail(I4_ERR_CUDA, "side stream / event creation failed");
-        st.dev = dev;
-    }
-    return I4_OK;
+// 3-D variants for the batched BMM launches: [batches, rows, inner] with batch pitch
+// `bpitch` bytes; coordinate 2 = batch, so a box never crosses into another batch.
+bool make_tmap_i8_3d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t pitch,
+                     uint64_t batches, uint64_t bpitch, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {inner, rows, batches};
+    cuuint64_t strides[2] = {pitch, bpitch};
+    cuuint32_t box[3] = {128, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_out_3d(CUtensorMap* m, void* ptr, bool bf16, uint64_t cols, uint64_t rows, uint64_t batches) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const uint32_t esz = bf16 ? 2 : 4;
+    cuuint64_t dims[3] = {cols, rows, batches};
+    cuuint64_t strides[2] = {cols * esz, cols * rows * esz};
+    cuuint32_t box[3] = {128 / esz, 32, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = fn(m, dt, 3, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 }  // namespace
 
@@ -614,95 +619,242 @@ static i4_status linear_bwd_impl(const void* dY, const i4_fwd_cache* cache, uint
 extern "C" {
 
 namespace {
-i4_fwd_cache bmm_view(const i4_bmm_cache* c, int64_t b, float s_q, float s_k) {
-    i4_fwd_cache v{};
-    const int64_t N = c->N, P = c->P, M = c->M;
-    v.xq = c->qq + b * N * M;
-    v.wq = c->kq + b * P * M;
-    v.x_mask = c->q_mask + b * N * (M / 32);
-    v.w_mask = c->k_mask + b * P * (M / 32);
-    v.x_sqnorm = c->q_sqnorm + b * N;
-    v.N = N; v.D = M; v.C = P; v.k = c->k; v.s_x = s_q; v.s_w = s_k;
-    return v;
+
+// Backward workspace of the batched BMM (int4_bmm_bwd), for a chunk of Bc <= 2048
+// batches; each region 256-aligned.  The first two regions must be zero before the
+// first call (grad_split's barrier words and per-batch amax words; left zero).
+struct BmmWs {
+    uint32_t* scratch; uint32_t* bamax; uint32_t* amax; float* s_down; int32_t* counts;
+    int32_t* items_w; int8_t* wexp_w; int32_t* items_x; int8_t* wexp_x;
+    uint8_t* x_touched; int32_t* a_sq; int8_t* q8; int8_t* a_x; int8_t* a_w; int8_t* b_w;
+    size_t off[8];
+    size_t total;
+};
+
+BmmWs carve_bmm_ws(void* ws, int64_t B, int64_t N, int64_t P, int64_t M) {
+    const int64_t Bc = std::min<int64_t>(B, i4::kMaxGemmBatch);
+    const int64_t L = 2 * N + 128, kcap = round_up(2 * N, 128);
+    BmmWs w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += size_t(round_up(int64_t(bytes), 256)); return o; };
+    const size_t o_scr = take(size_t(i4::kGradSplitMaxBlocks) * 4);
+    const size_t o_bam = take(size_t(Bc) * 4);
+    const size_t o_am = take(size_t(Bc) * 4);
+    const size_t o_sd = take(size_t(Bc) * 4);
+    const size_t o_cn = take(size_t(2 * Bc) * 4);
+    const size_t o_iw = take(size_t(Bc * L) * 4);
+    const size_t o_ew = take(size_t(Bc * L));
+    const size_t o_ix = take(size_t(Bc * L) * 4);
+    const size_t o_ex = take(size_t(Bc * L));
+    const size_t o_xt = take(size_t(Bc * N));
+    const size_t o_sq = take(size_t(Bc * 2 * N) * 4);
+    const size_t o_q8 = take(size_t(Bc * N + 1) * size_t(P));
+    const size_t o_ax = take(size_t(Bc * L) * size_t(P));
+    const size_t o_aw = take(size_t(Bc * kcap) * size_t(P));
+    const size_t o_bw = take(size_t(Bc * kcap) * size_t(M));
+    w.total = off;
+    const size_t offs[8] = {o_sd, o_am, o_cn, o_iw, o_ew, o_ix, o_ex, o_q8};
+    for (int i = 0; i < 8; ++i) w.off[i] = offs[i];
+    if (ws) {
+        uint8_t* b = static_cast<uint8_t*>(ws);
+        w.scratch = reinterpret_cast<uint32_t*>(b + o_scr);
+        w.bamax = reinterpret_cast<uint32_t*>(b + o_bam);
+        w.amax = reinterpret_cast<uint32_t*>(b + o_am);
+        w.s_down = reinterpret_cast<float*>(b + o_sd);
+        w.counts = reinterpret_cast<int32_t*>(b + o_cn);
+        w.items_w = reinterpret_cast<int32_t*>(b + o_iw);
+        w.wexp_w = reinterpret_cast<int8_t*>(b + o_ew);
+        w.items_x = reinterpret_cast<int32_t*>(b + o_ix);
+        w.wexp_x = reinterpret_cast<int8_t*>(b + o_ex);
+        w.x_touched = b + o_xt;
+        w.a_sq = reinterpret_cast<int32_t*>(b + o_sq);
+        w.q8 = reinterpret_cast<int8_t*>(b + o_q8);
+        w.a_x = reinterpret_cast<int8_t*>(b + o_ax);
+        w.a_w = reinterpret_cast<int8_t*>(b + o_aw);
+        w.b_w = reinterpret_cast<int8_t*>(b + o_bw);
+    }
+    return w;
 }
+
 }  // namespace
 
 i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64_t P, int64_t M, int32_t k,
                        const float* s_q, const float* s_k, void* T, i4_out_dtype t_dtype, i4_bmm_cache* cache,
                        void* stream) {
+    I4_RETURN_IF(check_device());
     if (!Q || !K || !T || !cache || !s_q || !s_k || !cache->qq || !cache->kq || !cache->q_mask || !cache->k_mask ||
-        !cache->q_sqnorm)
+        !cache->q_sqnorm || !cache->steps)
         return fail(I4_ERR_ARG, "int4_bmm_fwd: NULL pointer");
     if (B <= 0) return fail(I4_ERR_SHAPE, "int4_bmm_fwd: B must be positive");
-    if (N <= 0 || P <= 0 || M <= 0 || M % 64 || P % 64)
-        return fail(I4_ERR_SHAPE, "int4_bmm_fwd: need N > 0 and M, P positive multiples of 64");
-    cache->B = B; cache->N = N; cache->P = P; cache->M = M; cache->k = k;
-    const size_t ob = t_dtype == I4_OUT_BF16 ? 2 : 4;
-    // the batches are independent (each writes its own cache slices and T slice):
-    // batch b runs on stream b % S (S = min(B, kBmmStreams); the caller's stream
-    // and side streams joined back into it), so the small per-batch kernels overlap
-    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
-    const int S = int(std::min<int64_t>(B, kBmmStreams));
-    cudaEvent_t fork_ev = nullptr;
-    for (int j = 1; j < S; ++j) {
-        I4_RETURN_IF(make_side(t_bmm[j - 1]));
-        if (j == 1) fork_ev = t_bmm[0].fork;
-    }
-    if (S > 1) {
-        if (cudaEventRecord(fork_ev, s0) != cudaSuccess) return fail(I4_ERR_CUDA, "int4_bmm_fwd: fork failed");
-        for (int j = 1; j < S; ++j)
-            if (cudaStreamWaitEvent(t_bmm[j - 1].s, fork_ev, 0) != cudaSuccess)
-                return fail(I4_ERR_CUDA, "int4_bmm_fwd: fork failed");
-    }
+    if (N <= 0 || P <= 0 || M <= 0 || M % 64 || P % 64 || M > 8192)
+        return fail(I4_ERR_SHAPE, "int4_bmm_fwd: need N > 0 and M, P positive multiples of 64 (M <= 8192)");
+    if (B * N > (int64_t(1) << 31) || B * P > (int64_t(1) << 31))
+        return fail(I4_ERR_SHAPE, "int4_bmm_fwd: B N and B P must stay below 2^31 rows");
+    I4_RETURN_IF(check_k(k, M));
     for (int64_t b = 0; b < B; ++b) {
-        i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
-        cudaStream_t sb = (b % S) == 0 ? s0 : t_bmm[b % S - 1].s;
-        I4_RETURN_IF(int4_linear_fwd(static_cast<const uint16_t*>(Q) + b * N * M, static_cast<const uint16_t*>(K) + b * P * M,
-                                     N, M, P, k, s_q[b], s_k[b], static_cast<uint8_t*>(T) + size_t(b * N * P) * ob, t_dtype,
-                                     &v, sb));
+        I4_RETURN_IF(check_step(s_q[b], "s_q[b]"));
+        I4_RETURN_IF(check_step(s_k[b], "s_k[b]"));
     }
-    for (int j = 1; j < S; ++j)
-        if (cudaEventRecord(t_bmm[j - 1].join, t_bmm[j - 1].s) != cudaSuccess ||
-            cudaStreamWaitEvent(s0, t_bmm[j - 1].join, 0) != cudaSuccess)
-            return fail(I4_ERR_CUDA, "int4_bmm_fwd: join failed");
+    if (t_dtype != I4_OUT_F32 && t_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "int4_bmm_fwd: bad t_dtype");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(T) || !aligned16(cache->qq) || !aligned16(cache->kq))
+        return fail(I4_ERR_ALIGN, "int4_bmm_fwd: unaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // per-batch step table (the same host arithmetic as int4_linear_fwd / _bwd per batch)
+    std::vector<float> tab(size_t(B) * 8, 0.0f);
+    const float isb = inv_sqrt_block(k);
+    for (int64_t b = 0; b < B; ++b) {
+        float* t = tab.data() + 8 * b;
+        t[0] = step_recip(k, s_q[b]);
+        t[1] = step_recip(k, s_k[b]);
+        t[2] = s_q[b] * s_k[b];                  // fwd scale fl32(s_q s_k), reading Z-22
+        t[3] = s_k[b] * isb;                     // grad_Q GEMM scale (as gx.scale of the linear backward)
+        t[4] = s_q[b] * isb;                     // grad_K GEMM scale
+        t[5] = s_q[b];
+        t[6] = s_k[b];
+    }
+    I4_LAUNCH(i4::launch_step_table(tab.data(), B, cache->steps, s), "step_table", s);
+    {
+        // F1-F3 for every row of Q and K (one launch; per-row r from the batch's table entry)
+        i4::HqArgs h{};
+        h.x0 = static_cast<const uint16_t*>(Q); h.rows0 = B * N; h.r0 = 1.0f;
+        h.codes0 = cache->qq; h.bits0 = cache->q_mask; h.sqnorm0 = cache->q_sqnorm;
+        h.r_tab0 = cache->steps; h.rpb0 = N;
+        h.x1 = static_cast<const uint16_t*>(K); h.rows1 = B * P; h.r1 = 1.0f;
+        h.codes1 = cache->kq; h.bits1 = cache->k_mask; h.sqnorm1 = nullptr;
+        h.r_tab1 = cache->steps + 1; h.rpb1 = P;
+        h.cols = M; h.k = k;
+        h.status = cache->dev_status;
+        I4_LAUNCH(i4::launch_hadamard_quant2(h, s), "hadamard_quant", s);
+    }
+    {
+        // T_b = fl32(s_q s_k) (Q_hat_b K_hat_b^T): one GEMM launch over every batch's tiles
+        i4::GemmArgs g{};
+        g.M = int32_t(N); g.Nn = int32_t(P); g.K = int32_t(M);
+        g.epi = i4::EPI_FWD;
+        g.out = T;
+        g.out_bf16 = t_dtype == I4_OUT_BF16;
+        g.batch = int32_t(B);
+        g.tab = cache->steps; g.tab_idx = 2;
+        const int bn = i4::gemm_block_n(int(P), false);
+        CUtensorMap ta, tb, tc;
+        const bool ok =
+            make_tmap_i8_3d(&ta, cache->qq, uint64_t(M), uint64_t(N), uint64_t(M), uint64_t(B), uint64_t(N * M), 128u) &&
+            make_tmap_i8_3d(&tb, cache->kq, uint64_t(M), uint64_t(P), uint64_t(M), uint64_t(B), uint64_t(P * M),
+                            uint32_t(bn / i4::kGemmCG)) &&
+            make_tmap_out_3d(&tc, T, g.out_bf16 != 0, uint64_t(P), uint64_t(N), uint64_t(B));
+        if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        const i4::GemmMaps maps{&ta, &tb, &tc, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        I4_LAUNCH(i4::launch_gemm(maps, g, device_info().sms, s), "gemm_i8_fwd", s);
+    }
+    cache->B = B; cache->N = N; cache->P = P; cache->M = M; cache->k = k;
     return I4_OK;
 }
 
-i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, const float* s_q, const float* s_k, uint64_t seed,
-                       uint32_t call_id, i4_lss_mode mode, const i4_lss_plan* plans, int32_t n_plans, void* dQ,
-                       i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes, void* stream) {
-    if (!dT || !cache || !s_q || !s_k || !dQ || !dK || !plans) return fail(I4_ERR_ARG, "int4_bmm_bwd: NULL pointer");
-    if (cache->B <= 0) return fail(I4_ERR_ARG, "int4_bmm_bwd: cache not filled by int4_bmm_fwd");
-    if (n_plans < 1) return fail(I4_ERR_ARG, "int4_bmm_bwd: n_plans must be >= 1");
+size_t int4_bmm_bwd_workspace_size(int64_t B, int64_t N, int64_t P, int64_t M) {
+    if (B <= 0 || N <= 0 || P <= 0 || M <= 0) return 0;
+    return carve_bmm_ws(nullptr, B, N, P, M).total;
+}
+
+size_t int4_bmm_bwd_ws_offset(int64_t B, int64_t N, int64_t P, int64_t M, int32_t what) {
+    if (what < 0 || what > 7 || B <= 0 || N <= 0 || P <= 0 || M <= 0) return size_t(-1);
+    return carve_bmm_ws(nullptr, B, N, P, M).off[what];
+}
+
+i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, uint64_t seed, uint32_t call_id, i4_lss_mode mode,
+                       void* dQ, i4_out_dtype dq_dtype, float* dK, void* ws, size_t ws_bytes, void* stream) {
+    I4_RETURN_IF(check_device());
+    if (!dT || !cache || !dQ || !dK || !ws) return fail(I4_ERR_ARG, "int4_bmm_bwd: NULL pointer");
+    if (cache->B <= 0 || !cache->steps) return fail(I4_ERR_ARG, "int4_bmm_bwd: cache not filled by int4_bmm_fwd");
+    if (mode != I4_LSS_BERNOULLI && mode != I4_LSS_KEEP_POSITIVE && mode != I4_LSS_NONE)
+        return fail(I4_ERR_ARG, "int4_bmm_bwd: bad mode");
+    if (dq_dtype != I4_OUT_F32 && dq_dtype != I4_OUT_BF16) return fail(I4_ERR_ARG, "int4_bmm_bwd: bad dq_dtype");
     const int64_t B = cache->B, N = cache->N, P = cache->P, M = cache->M;
+    const int32_t k = cache->k;
+    if (N > kMaxBwdTokens || N > i4::sampler_max_tokens())
+        return fail(I4_ERR_SHAPE, "int4_bmm_bwd: N = %lld exceeds %lld tokens per batch (reading Z-21)", (long long)N,
+                    (long long)kMaxBwdTokens);
+    if (ws_bytes < int4_bmm_bwd_workspace_size(B, N, P, M))
+        return fail(I4_ERR_WORKSPACE, "int4_bmm_bwd: ws_bytes %zu < %zu", ws_bytes, int4_bmm_bwd_workspace_size(B, N, P, M));
+    if (!aligned16(dT) || !aligned16(dQ) || !aligned16(dK) || !aligned16(ws))
+        return fail(I4_ERR_ALIGN, "int4_bmm_bwd: unaligned pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const BmmWs w = carve_bmm_ws(ws, B, N, P, M);
+    const int64_t Bc = std::min<int64_t>(B, i4::kMaxGemmBatch);
+    const int64_t L = 2 * N + 128, kcap = round_up(2 * N, 128);
     const size_t oq = dq_dtype == I4_OUT_BF16 ? 2 : 4;
-    // chain j = b % S owns plan j and workspace slice j and runs on stream j (the
-    // caller's stream for j = 0, library side streams joined back otherwise), so
-    // the per-batch kernel chains overlap; S = min(B, n_plans, kBmmStreams)
-    const size_t per_ws = int4_bwd_workspace_size(N, M, P);
-    const int S = int(std::min<int64_t>(B, std::min<int64_t>(n_plans, kBmmStreams)));
-    if (ws_bytes < size_t(S) * per_ws)
-        return fail(I4_ERR_WORKSPACE, "int4_bmm_bwd: ws_bytes %zu < %d x %zu", ws_bytes, S, per_ws);
-    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
-    for (int j = 1; j < S; ++j) I4_RETURN_IF(make_side(t_bmm[j - 1]));
-    if (S > 1) {
-        if (cudaEventRecord(t_bmm[0].fork, s0) != cudaSuccess) return fail(I4_ERR_CUDA, "int4_bmm_bwd: fork failed");
-        for (int j = 1; j < S; ++j)
-            if (cudaStreamWaitEvent(t_bmm[j - 1].s, t_bmm[0].fork, 0) != cudaSuccess)
-                return fail(I4_ERR_CUDA, "int4_bmm_bwd: fork failed");
+    for (int64_t b0 = 0; b0 < B; b0 += Bc) {
+        const int64_t nb = std::min<int64_t>(Bc, B - b0);
+        const int64_t toff = b0 * N;                  // Philox token index of the chunk's first row (Z-31)
+        // B1 + B2: per-batch amax, SR codes, half-row norms
+        I4_LAUNCH(i4::launch_grad_split(static_cast<const uint16_t*>(dT) + b0 * N * P, nb * N, P, w.scratch, seed,
+                                        call_id, toff, w.q8, w.a_sq, w.s_down, w.amax, cache->dev_status, s, N,
+                                        w.bamax),
+                  "grad_split", s);
+        // LSS steps 2-4: one cluster per (mask, batch)
+        i4::SamplerArgs a{};
+        a.a_sq = w.a_sq;
+        a.x_sqnorm = cache->q_sqnorm + b0 * N;
+        a.N = int32_t(N);
+        a.mode = int32_t(mode);
+        a.seed_lo = uint32_t(seed);
+        a.seed_hi = uint32_t(seed >> 32);
+        a.call_id = call_id;
+        a.token_offset = toff;
+        a.items[0] = w.items_w; a.wexp[0] = w.wexp_w; a.count[0] = w.counts;
+        a.items[1] = w.items_x; a.wexp[1] = w.wexp_x; a.count[1] = w.counts + Bc;
+        a.x_touched = w.x_touched;
+        a.batch = int32_t(nb);
+        a.bs_list = L;
+        I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);
+        void* dq_chunk = static_cast<uint8_t*>(dQ) + size_t(b0 * N * M) * oq;
+        float* dk_chunk = dK + b0 * P * M;
+        i4::CompactArgs ca{};
+        ca.q8 = w.q8; ca.xq = cache->qq + b0 * N * M;
+        ca.N = int32_t(N); ca.C = int32_t(P); ca.D = int32_t(M);
+        ca.items_x = w.items_x; ca.count_x = w.counts + Bc;
+        ca.items_w = w.items_w; ca.wexp_w = w.wexp_w; ca.count_w = w.counts;
+        ca.a_x = w.a_x; ca.a_w = w.a_w; ca.b_w = w.b_w;
+        ca.x_touched = w.x_touched; ca.dx = dq_chunk; ca.dx_bf16 = dq_dtype == I4_OUT_BF16;
+        ca.batch = int32_t(nb); ca.bs_list = L;
+        I4_LAUNCH(i4::launch_compact(ca, s), "compact", s);
+        // grad_Q and grad_K of every batch: one persistent launch
+        i4::GemmArgs gx{};
+        gx.M = int32_t(L); gx.m_dev = w.counts + Bc;
+        gx.Nn = int32_t(M); gx.K = int32_t(P);
+        gx.epi = i4::EPI_BWD;
+        gx.out = dq_chunk;
+        gx.out_bf16 = dq_dtype == I4_OUT_BF16;
+        gx.s_down = w.s_down;
+        gx.k_had = k;
+        gx.mask = cache->q_mask + b0 * N * (M / 32);
+        gx.items = w.items_x; gx.wexp = w.wexp_x;
+        gx.n_tokens = int32_t(N);
+        gx.b_mn = 1;
+        gx.batch = int32_t(nb); gx.bs_items = L;
+        gx.tab = cache->steps + 8 * b0; gx.tab_idx = 3;
+        i4::GemmArgs gw{};
+        gw.M = int32_t(P); gw.Nn = int32_t(M); gw.K = int32_t(kcap); gw.k_dev = w.counts;
+        gw.epi = i4::EPI_WGRAD;
+        gw.out = dk_chunk;
+        gw.s_down = w.s_down;
+        gw.k_had = k;
+        gw.mask = cache->k_mask + b0 * P * (M / 32);
+        gw.a_mn = 1; gw.b_mn = 1;
+        gw.n_tokens = int32_t(N);
+        gw.batch = int32_t(nb);
+        gw.tab = cache->steps + 8 * b0; gw.tab_idx = 4;
+        CUtensorMap ta, tb, tc, taw, tbw;
+        const bool ok =
+            make_tmap_i8_3d(&ta, w.a_x, uint64_t(P), uint64_t(L), uint64_t(P), uint64_t(nb), uint64_t(L * P), 128u) &&
+            make_tmap_i8_3d(&tb, cache->kq + b0 * P * M, uint64_t(M), uint64_t(P), uint64_t(M), uint64_t(nb),
+                            uint64_t(P * M), 128u) &&
+            make_tmap_i8_3d(&taw, w.a_w, uint64_t(P), uint64_t(kcap), uint64_t(P), uint64_t(nb), uint64_t(kcap * P), 128u) &&
+            make_tmap_i8_3d(&tbw, w.b_w, uint64_t(M), uint64_t(kcap), uint64_t(M), uint64_t(nb), uint64_t(kcap * M), 128u) &&
+            make_tmap_out_3d(&tc, dk_chunk, false, uint64_t(M), uint64_t(P), uint64_t(nb));
+        if (!ok) return fail(I4_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        const i4::GemmMaps maps{&ta, &tb, &tc, nullptr, nullptr, nullptr, &taw, &tbw, nullptr};
+        I4_LAUNCH(i4::launch_gemm(maps, gx, device_info().sms, s, &gw), "gemm_i8_bwd", s);
     }
-    for (int64_t b = 0; b < B; ++b) {
-        const int j = int(b % S);
-        const i4_fwd_cache v = bmm_view(cache, b, s_q[b], s_k[b]);
-        I4_RETURN_IF(linear_bwd_impl(static_cast<const uint16_t*>(dT) + b * N * P, &v, seed, call_id, b * N, mode,
-                                     plans + j, static_cast<uint8_t*>(dQ) + size_t(b * N * M) * oq, dq_dtype,
-                                     dK + b * P * M, static_cast<uint8_t*>(ws) + size_t(j) * per_ws, per_ws,
-                                     j == 0 ? s0 : t_bmm[j - 1].s));
-    }
-    for (int j = 1; j < S; ++j)
-        if (cudaEventRecord(t_bmm[j - 1].join, t_bmm[j - 1].s) != cudaSuccess ||
-            cudaStreamWaitEvent(s0, t_bmm[j - 1].join, 0) != cudaSuccess)
-            return fail(I4_ERR_CUDA, "int4_bmm_bwd: join failed");
     return I4_OK;
 }
 

@@ -5,6 +5,8 @@
 //   compact_kernel builds the grad_X GEMM's A and the grad_W GEMM's A and B in
 //   one launch (row copies; TMA tile::gather4 inside the GEMM producers measured
 //   ~3x slower than these copies on B200).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -67,6 +69,15 @@ __device__ __forceinline__ void zero_row(void* base, int64_t row, int n, bool bf
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     pdl_trigger();
     pdl_wait();                                               // counts / lists of the sampler
+    if (a.batch > 1) {                                        // this CTA's batch: its slices
+        const int64_t b = blockIdx.y, N = a.N, kcap = (2 * N + 127) / 128 * 128;
+        a.q8 += b * N * a.C; a.xq += b * N * a.D;
+        a.items_x += b * a.bs_list; a.items_w += b * a.bs_list; a.wexp_w += b * a.bs_list;
+        a.count_x += b; a.count_w += b;
+        a.x_touched += b * N;
+        a.dx = static_cast<uint8_t*>(a.dx) + b * N * a.D * (a.dx_bf16 ? 2 : 4);
+        a.a_x += b * (2 * N + 128) * a.C; a.a_w += b * kcap * a.C; a.b_w += b * kcap * a.D;
+    }
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     // operand forms (the sampler's flags; the GEMMs pick their operands by the same
@@ -133,7 +144,9 @@ cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
     int64_t blocks = (rows + 7) / 8;
     if (blocks > 148 * 4) blocks = 148 * 4;        // grid-stride rows; a smaller grid launches faster when little is to move
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(blocks));
+    const int64_t nbat = a.batch > 1 ? a.batch : 1;
+    if (nbat > 1) blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (148 * 4 + nbat - 1) / nbat));
+    cfg.gridDim = dim3(unsigned(blocks), unsigned(nbat));
     cfg.blockDim = dim3(256);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -93,17 +93,17 @@ struct EpiShape {
     static constexpr int THREADS = 64 + 32 * WARPS;
 };
 
-template <int BN, int CG, int EPW, int EPI, int COLS>
+template <int BN, int CG, int EPW, int EPI, int COLS, int EXTRA = 0>
 struct GemmCfg {
     static constexpr int A_BYTES = kBM * kBK;
     static constexpr int B_BYTES = (BN / CG) * kBK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int OUT_BYTES = EPI == EPI_DGRAD ? 0 : EPW * 2 * kStageOutBytes;   // grad_X: direct stores
     static constexpr int MAX_SMEM = 232448 - 1024 - 256;
-    static constexpr int STAGES_FIT = (MAX_SMEM - OUT_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = (MAX_SMEM - OUT_BYTES - EXTRA) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT < 6 ? STAGES_FIT : 6;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + 1024 + 256;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + 1024 + 256 + EXTRA;
     static_assert(STAGES >= 3, "shared memory ring too shallow");
 };
 
@@ -237,8 +237,12 @@ struct Sched {
     }
 };
 
-// j-th tile of pair p
-struct Seg { int prob, tile, nk; bool valid; };
+// j-th tile of pair p (b: its batch in a batched launch)
+struct Seg { int prob, tile, nk, b; bool valid; };
+
+// batched backward launches: per-batch tile table in shared memory after the barriers
+// ([B + 1] prefix of tiles per batch, [B] grad_X tiles per batch)
+constexpr int kBatSmem = ((2 * kMaxGemmBatch + 1) * 4 + 15) / 16 * 16;
 
 __device__ __forceinline__ Seg seg_at(const Sched& s, int p, int j) {
     Seg r{};
@@ -273,7 +277,9 @@ enum { MAP_A = 0, MAP_B = 1, MAP_C = 2, MAP_A2 = 3, MAP_A3 = 4, MAP_B2 = 5, MAP_
 // KH: Hadamard order k of the grad epilogues (compile-time, 0 for FWD / INT32).
 // EPI_BWD: problem 0 = grad_X (A K-major, B MN-major, args g), problem 1 = grad_W
 // (A and B MN-major, args g1); A_MN / B_MN describe the single-problem kinds.
-template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG>
+// BAT: batched launch (EPI_FWD / EPI_BWD of the attention BMM): 3-D maps, tiles of
+// every batch dealt round-robin to the pairs (GemmArgs::batch).
+template <int BN, int EPI, int KH, bool A_MN, bool B_MN, int CG, bool BAT>
 __global__ void __launch_bounds__(EpiShape<BN, (EPI == EPI_BWD ? EPI_WGRAD : EPI), kh_ch(KH)>::THREADS, 1)
 gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const GemmArgs g1) {
     constexpr bool kBwd = EPI == EPI_BWD;
@@ -281,7 +287,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     constexpr int CH = kh_ch(KH);
     using Epi = EpiShape<BN, (kBwd ? EPI_WGRAD : EPI), CH>;
     constexpr int kEpiWarps = Epi::WARPS;
-    using Cfg = GemmCfg<BN, CG, kEpiWarps, (kBwd ? EPI_WGRAD : EPI), Epi::COLS>;
+    using Cfg = GemmCfg<BN, CG, kEpiWarps, (kBwd ? EPI_WGRAD : EPI), Epi::COLS, (BAT && kBwd) ? kBatSmem : 0>;
+    static_assert(!BAT || (CG == 2 && (EPI == EPI_FWD || EPI == EPI_BWD)), "batched: FWD / BWD pairs only");
     constexpr int BMP = kBM * CG;                // rows per (pair) tile
     constexpr int BNC = BN / CG;                 // B rows / columns staged by this CTA
     constexpr int STAGES = Cfg::STAGES;
@@ -295,6 +302,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* bpref = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + 256);   // BAT bwd: [B + 1]
+    int* btd = bpref + kMaxGemmBatch + 1;                                         // BAT bwd: [B]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -321,9 +330,73 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     ProbSize s1{};
     if constexpr (kBwd) s1 = prob_size<EPI_WGRAD, BMP, BN>(g1);
     Sched sc;
-    sc.init(n_pairs, s0.T, s0.nk, kBwd ? s1.T : 0, kBwd ? s1.nk : 0, I4_EPI_KB_DGRAD, I4_EPI_KB_WGRAD);
-    // per-pair constants of the short-class run (computed once, used by every warp)
-#define SEG(j) seg_at(sc, pair0, (j))
+    if constexpr (!BAT)
+        sc.init(n_pairs, s0.T, s0.nk, kBwd ? s1.T : 0, kBwd ? s1.nk : 0, I4_EPI_KB_DGRAD, I4_EPI_KB_WGRAD);
+    if constexpr (BAT && kBwd) {
+        // tile table: batch b has ceil(M_b / 256) grad_X m-tiles (M_b = its kept items, from
+        // the sampler) and a fixed number of grad_W tiles; prefix over the batches by warp 0
+        // (lane l scans a contiguous chunk).  Identical in both CTAs of a pair.
+        const int B = g.batch;
+        for (int b = threadIdx.x; b < B; b += blockDim.x) {
+            const int td = ((__ldg(g.m_dev + b) + BMP - 1) / BMP) * s0.n_tiles;
+            btd[b] = td;
+            bpref[b + 1] = td + s1.T;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int ch = (B + 31) / 32, lo = min(B, lane * ch), hi = min(B, lo + ch);
+            int run = 0;
+            for (int b = lo; b < hi; ++b) { run += bpref[b + 1]; bpref[b + 1] = run; }
+            int incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += n;
+            }
+            const int off = incl - run;
+            for (int b = lo; b < hi; ++b) bpref[b + 1] += off;
+            if (lane == 0) bpref[0] = 0;
+        }
+        __syncthreads();
+    }
+    // j-th tile of this pair.  Batched: global tile t = pair + j P over all batches (forward:
+    // uniform tiles per batch; backward: the tile table above, binary-searched)
+    auto seg = [&](int j) -> Seg {
+        if constexpr (!BAT) {
+            return seg_at(sc, pair0, j);
+        } else {
+            Seg r{};
+            const int t = pair0 + j * n_pairs;
+            if constexpr (!kBwd) {
+                if (t >= g.batch * s0.T) return r;
+                r.b = t / s0.T; r.tile = t - r.b * s0.T; r.prob = 0; r.nk = s0.nk;
+            } else {
+                if (t >= bpref[g.batch]) return r;
+                int lo = 0, hi = g.batch - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (bpref[mid] <= t) lo = mid; else hi = mid - 1;
+                }
+                r.b = lo;
+                const int l = t - bpref[lo];
+                if (l < btd[lo]) { r.prob = 0; r.tile = l; r.nk = s0.nk; }
+                else { r.prob = 1; r.tile = l - btd[lo]; r.nk = (__ldg(g1.k_dev + lo) + kBK - 1) / kBK; }
+            }
+            r.valid = true;
+            return r;
+        }
+    };
+    // size of a tile's problem (batched backward: the batch's kept-item counts)
+    auto psz = [&](const Seg& sg) -> ProbSize {
+        const bool p1 = kBwd && sg.prob == 1;
+        ProbSize ps = p1 ? s1 : s0;
+        if constexpr (BAT && kBwd) {
+            if (!p1) { ps.M = __ldg(g.m_dev + sg.b); ps.m_tiles = (ps.M + BMP - 1) / BMP; ps.T = ps.m_tiles * ps.n_tiles; }
+            else { ps.nk = sg.nk; ps.K = sg.nk * kBK; }
+        }
+        return ps;
+    };
+#define SEG(j) seg(j)
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer (warp 0)
@@ -332,7 +405,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             const Seg sg = SEG(j);
             if (!sg.valid) break;
             const bool p1 = kBwd && sg.prob == 1;
-            const ProbSize& ps = p1 ? s1 : s0;
+            const ProbSize ps = psz(sg);
             const bool a_mn = kBwd ? p1 : A_MN;
             const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank);     // this CTA's output rows
             const int nb = (sg.tile % ps.n_tiles) * BN + BNC * int(rank);      // this CTA's B rows
@@ -358,7 +431,18 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                     if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
                     uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
                     uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
-                    if constexpr (CG == 2) {
+                    if constexpr (BAT) {                   // 3-D maps: coordinate 2 = batch
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (a_mn) tma_load_3d_2sm(a_dst, pA, fb, a_row, kr * kBK, sg.b);
+                        else      tma_load_3d_2sm(a_dst, pA, fb, kr * kBK, a_row, sg.b);
+                        if (B_MN || kBwd) {
+#pragma unroll
+                            for (int q = 0; q < BNC / 128; ++q)
+                                tma_load_3d_2sm(b_dst + q * 128 * kBK, pB, fb, nb + 128 * q, kr * kBK, sg.b);
+                        } else {
+                            tma_load_3d_2sm(b_dst, pB, fb, kr * kBK, nb, sg.b);
+                        }
+                    } else if constexpr (CG == 2) {
                         const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
                         if (a_mn) tma_load_2d_2sm(a_dst, pA, fb, a_row, kr * kBK);
                         else      tma_load_2d_2sm(a_dst, pA, fb, kr * kBK, a_row);
@@ -448,18 +532,20 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
         auto load_ri = [&](const Seg& sg) {
             RowInfo x{two_n, two_n, 0, 0, false, false};
             if (sg.valid && is_dg(sg)) {
-                const int rw = (sg.tile / s0.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
-                if (s0.form == 1 || (s0.form == 2 && rw < s0.mtd * BMP)) {
+                const ProbSize q0 = psz(sg);
+                const int rw = (sg.tile / q0.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
+                if (q0.form == 1 || (q0.form == 2 && rw < q0.mtd * BMP)) {
                     x.dense = true;
                     if (rw < g.n_tokens) {
                         x.item = rw;                   // token rw, weight 1, never paired
-                        x.skip = s0.form == 2 && __ldg(g.tok_flag + rw) != 0;
+                        x.skip = q0.form == 2 && __ldg(g.tok_flag + rw) != 0;
                     }
                 } else {
-                    const int li = s0.form == 2 ? rw - s0.mtd * BMP : rw;        // index into the item list
-                    const int cnt = s0.form == 2 ? s0.M - s0.mtd * BMP : s0.M;
-                    const int32_t* items = s0.form == 2 ? g.items2 : g.items;
-                    const int8_t* wexp = s0.form == 2 ? g.wexp2 : g.wexp;
+                    const int li = q0.form == 2 ? rw - q0.mtd * BMP : rw;        // index into the item list
+                    const int cnt = q0.form == 2 ? q0.M - q0.mtd * BMP : q0.M;
+                    const int64_t lo = BAT ? int64_t(sg.b) * g.bs_items : 0;   // this batch's list
+                    const int32_t* items = (q0.form == 2 ? g.items2 : g.items) + lo;
+                    const int8_t* wexp = (q0.form == 2 ? g.wexp2 : g.wexp) + lo;
                     x.li = li;
                     if (li < cnt) {
                         x.item = __ldg(items + li);
@@ -476,15 +562,18 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             for (int q = 0; q < NW; ++q) mw[q] = 0u;
             if (!kMask || !sg.valid) return;
             const bool dg = is_dg(sg);
-            const ProbSize& ps = (kBwd && sg.prob == 1) ? s1 : s0;
+            const ProbSize ps = psz(sg);
             const GemmArgs& G = (kBwd && sg.prob == 1) ? g1 : g;
             const int rw = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank) + r_in_tile;
             int64_t mrow = rw;
             if (dg) {
                 if (x.item >= two_n) return;
                 mrow = x.item >= g.n_tokens ? x.item - g.n_tokens : x.item;
+                if (BAT) mrow += int64_t(sg.b) * g.n_tokens;
             } else if (rw >= ps.M) {
                 return;
+            } else if (BAT) {
+                mrow += int64_t(sg.b) * ps.M;
             }
             const int words = G.Nn >> 5;
             const int cw0 = ((sg.tile % ps.n_tiles) * BN + cbeg) >> 5;
@@ -506,7 +595,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             const bool p1 = kBwd && sg.prob == 1;
             const bool dg = is_dg(sg);
             const GemmArgs& G = p1 ? g1 : g;
-            const ProbSize& ps = p1 ? s1 : s0;
+            const ProbSize ps = psz(sg);
             const int as = j & 1;
             const uint32_t ap = (j >> 1) & 1;
             const int m0 = (sg.tile / ps.n_tiles) * BMP + kBM * int(rank), n0 = (sg.tile % ps.n_tiles) * BN;
@@ -516,7 +605,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             // per-row setup
             bool valid = row < ps.M;
             int64_t out_row = row;
-            float rscale = G.scale;
+            float rscale = BAT ? __ldg(G.tab + 8 * sg.b + G.tab_idx) : G.scale;
+            if (BAT && kMask) sd = __ldg(g.s_down + sg.b);
             int dmode = 0;                             // 0 store, 1 store pair sum, 2 skip, 3 red.add
             int row_e = 0;                             // dgrad: log2 of the item's weight
             if (dg) {
@@ -533,7 +623,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 if (lane == 0) pv = ri_cur.edge;
                 if (ri_cur.dense) { nx = two_n; pv = two_n; }
                 row_e = e;
-                rscale = ldexpf(__fmul_rn(G.scale, sd), e);   // s_up = 16 s_down is inside the A codes
+                rscale = ldexpf(__fmul_rn(rscale, sd), e);    // s_up = 16 s_down is inside the A codes
                 const int inext = valid ? nx : two_n;
                 const int iprev = valid ? pv : two_n;
                 const bool first = inext < two_n && (inext >= g.n_tokens ? inext - g.n_tokens : inext) == out_row;
@@ -542,8 +632,9 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 else if (second) dmode = 2;
                 else if (first) dmode = 1;
             } else if (EPI0 == EPI_WGRAD || p1) {
-                rscale = __fmul_rn(G.scale, sd);
+                rscale = __fmul_rn(rscale, sd);
             }
+            if (BAT && dg) out_row += int64_t(sg.b) * g.n_tokens;      // global grad_X row of the batch
             mbar_wait(&tfull[as], ap);
             tc_fence_after();
             const uint32_t t_row = tmem_base + (uint32_t(lg * 32) << 16) + uint32_t(as * BN);
@@ -592,7 +683,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 if (dg) {
                     float v[CW];
                     masked_scaled_fwht<CW, KH>(r, mw_cur, (c - cbeg) / 32, rscale, v);
-                    if constexpr (kBwd && CW == 32) {
+                    if constexpr (kBwd && CW == 32 && !BAT) {
                         if (ps.form == 1) {
                             // token rows of Q (form 1): the tile's rows are contiguous grad_X rows, so
                             // they go out through swizzled shared-memory staging and TMA tensor
@@ -700,7 +791,11 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                                 make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
                         fence_proxy_async_smem();
                         __syncwarp();
-                        if (lane == 0) { tma_store_2d(&maps.m[MAP_C], buf, col0, m0 + lg * 32); bulk_commit(); }
+                        if (lane == 0) {
+                            if constexpr (BAT) tma_store_3d(&maps.m[MAP_C], buf, col0, m0 + lg * 32, sg.b);
+                            else tma_store_2d(&maps.m[MAP_C], buf, col0, m0 + lg * 32);
+                            bulk_commit();
+                        }
                         sbuf ^= 1;
                         continue;
                     }
@@ -741,7 +836,11 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                             make_uint4(wv[32 * q + 4 * jj], wv[32 * q + 4 * jj + 1], wv[32 * q + 4 * jj + 2], wv[32 * q + 4 * jj + 3]);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) { tma_store_2d(&maps.m[MAP_C], buf, col0 + 32 * q, m0 + lg * 32); bulk_commit(); }
+                    if (lane == 0) {
+                        if constexpr (BAT) tma_store_3d(&maps.m[MAP_C], buf, col0 + 32 * q, m0 + lg * 32, sg.b);
+                        else tma_store_2d(&maps.m[MAP_C], buf, col0 + 32 * q, m0 + lg * 32);
+                        bulk_commit();
+                    }
                     sbuf ^= 1;
                 }
             }
@@ -781,12 +880,12 @@ int gemm_block_n(int Nn, bool b_mn) {
 
 constexpr int kCG = kGemmCG;                    // CTA pairs (cta_group::2) for every GEMM
 
-template <int BN, int EPI, int KH, bool A_MN, bool B_MN>
+template <int BN, int EPI, int KH, bool A_MN, bool B_MN, bool BAT>
 static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid, cudaStream_t s) {
-    auto kern = gemm_i8_kernel<BN, EPI, KH, A_MN, B_MN, kCG>;
+    auto kern = gemm_i8_kernel<BN, EPI, KH, A_MN, B_MN, kCG, BAT>;
     constexpr int EPIC = EPI == EPI_BWD ? EPI_WGRAD : EPI;
     using Epi = EpiShape<BN, EPIC, kh_ch(KH)>;
-    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS, EPIC, Epi::COLS>::SMEM;
+    constexpr int smem = GemmCfg<BN, kCG, Epi::WARPS, EPIC, Epi::COLS, (BAT && EPI == EPI_BWD) ? kBatSmem : 0>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     GemmMapSet ms;
@@ -805,34 +904,34 @@ static cudaError_t launch_one(const GemmMaps& m, const GemmArgs& g, const GemmAr
     return cudaLaunchKernelEx(&cfg, kern, ms, g, g1);
 }
 
-template <int EPI, int KH, bool A_MN, bool B_MN>
+template <int EPI, int KH, bool A_MN, bool B_MN, bool BAT>
 static cudaError_t dispatch_bn(int bn, const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid,
                                cudaStream_t s) {
-    if (bn == 256) return launch_one<256, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
+    if (bn == 256) return launch_one<256, EPI, KH, A_MN, B_MN, BAT>(m, g, g1, grid, s);
     if constexpr (!B_MN && EPI != EPI_BWD) {
-        if (bn == 128) return launch_one<128, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
-        if constexpr (kh_ch(KH) <= 64) return launch_one<64, EPI, KH, A_MN, B_MN>(m, g, g1, grid, s);
+        if (bn == 128) return launch_one<128, EPI, KH, A_MN, B_MN, BAT>(m, g, g1, grid, s);
+        if constexpr (kh_ch(KH) <= 64) return launch_one<64, EPI, KH, A_MN, B_MN, BAT>(m, g, g1, grid, s);
     }
     return cudaErrorInvalidValue;
 }
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, bool BAT = false>
 static cudaError_t dispatch_ch(int bn, const GemmMaps& m, const GemmArgs& g, const GemmArgs& g1, int grid,
                                cudaStream_t s) {
     if constexpr (EPI == EPI_DGRAD || EPI == EPI_WGRAD || EPI == EPI_BWD) {
         switch (g.k_had) {
-            case 0: return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 1: return dispatch_bn<EPI, 1, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 2: return dispatch_bn<EPI, 2, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 3: return dispatch_bn<EPI, 3, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 4: return dispatch_bn<EPI, 4, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 5: return dispatch_bn<EPI, 5, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 6: return dispatch_bn<EPI, 6, A_MN, B_MN>(bn, m, g, g1, grid, s);
-            case 7: return dispatch_bn<EPI, 7, A_MN, B_MN>(bn, m, g, g1, grid, s);
+            case 0: return dispatch_bn<EPI, 0, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 1: return dispatch_bn<EPI, 1, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 2: return dispatch_bn<EPI, 2, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 3: return dispatch_bn<EPI, 3, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 4: return dispatch_bn<EPI, 4, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 5: return dispatch_bn<EPI, 5, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 6: return dispatch_bn<EPI, 6, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
+            case 7: return dispatch_bn<EPI, 7, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
             default: return cudaErrorInvalidValue;
         }
     } else {
-        return dispatch_bn<EPI, 0, A_MN, B_MN>(bn, m, g, g1, grid, s);
+        return dispatch_bn<EPI, 0, A_MN, B_MN, BAT>(bn, m, g, g1, grid, s);
     }
 }
 
@@ -842,14 +941,24 @@ cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaS
     // persistent grid: at most one pair per tile (every pair when two problems share
     // the launch: their tile counts may come from device memory)
     int64_t grid_pairs = pairs;
+    const int64_t nb = g.batch > 0 ? g.batch : 1;
     if (g.epi != EPI_BWD) {
-        const int64_t tiles = int64_t((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
+        const int64_t tiles = nb * ((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn);   // g.M = bound
+        grid_pairs = tiles < pairs ? tiles : pairs;
+    } else if (g.batch > 0 && g1) {             // batched backward: capacity tiles (g.M = list capacity)
+        const int64_t tiles = nb * (((g.M + kBM * kCG - 1) / (kBM * kCG)) * ((g.Nn + bn - 1) / bn) +
+                                    ((g1->M + kBM * kCG - 1) / (kBM * kCG)) * ((g1->Nn + bn - 1) / bn));
         grid_pairs = tiles < pairs ? tiles : pairs;
     }
     if (grid_pairs < 1) grid_pairs = 1;
     const int grid = kCG * int(grid_pairs);
     const GemmArgs none{};
     const GemmArgs& gg1 = g1 ? *g1 : none;
+    if (g.batch > 0) {
+        if (g.epi == EPI_FWD) return dispatch_ch<EPI_FWD, false, false, true>(bn, m, g, gg1, grid, s);
+        if (g.epi == EPI_BWD && g.batch <= kMaxGemmBatch) return dispatch_ch<EPI_BWD, false, true, true>(bn, m, g, gg1, grid, s);
+        return cudaErrorInvalidValue;
+    }
     switch (g.epi) {
         case EPI_FWD: return dispatch_ch<EPI_FWD, false, false>(bn, m, g, gg1, grid, s);
         case EPI_DGRAD: return dispatch_ch<EPI_DGRAD, false, true>(bn, m, g, gg1, grid, s);

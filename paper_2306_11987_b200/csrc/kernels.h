@@ -32,6 +32,8 @@ struct HqArgs {                          // two independent hadamard_quant jobs 
     int64_t cols; int k;
     float* delta0; float* delta1;        // optional A.3 delta = <v> - I o v (fp32, exact)
     int32_t* status;                     // optional device status word (bit 0: non-finite input)
+    // batched (BMM): row i of job j uses r = r_tabj[8 (i / rpbj)] (device table) instead of rj
+    const float* r_tab0; int64_t rpb0; const float* r_tab1; int64_t rpb1;
 };
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
@@ -39,9 +41,13 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 constexpr int kGradSplitMaxBlocks = 2048;   // block-max scratch words the plan provides
 int grad_split_stamps(unsigned long long* host, int n);
 int sampler_stamps(unsigned long long* host, int enable);   // timing experiment (-DI4_STAMPS=1 builds)
+// bamax != null: batched (attention BMM): N = B nb rows, batch b = rows [b nb, (b+1) nb) with
+// its own amax word bamax[b] (zero on entry, returned to zero), s_down[b], amax_out[b] and
+// norm block a_sq[b][2 nb]
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, int32_t* status, cudaStream_t s);
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s, int64_t nb = 0,
+                              uint32_t* bamax = nullptr);
 
 // sampler.cu ------------------------------------------------------------------
 struct SamplerArgs {
@@ -67,6 +73,11 @@ struct SamplerArgs {
     int32_t* sub_items; int8_t* sub_wexp; int32_t* sub_count;      // grad_X: the kept items of the
                               // tokens with a sampled item (token-major)
     uint8_t* tok_flag;        // [N] 1: token's grad_X row comes from sub-list rows, not Q
+    // batched (attention BMM): `batch` > 1 independent masks pairs, one cluster per (mask,
+    // batch); batch b reads a_sq + 2 N b, x_sqnorm + N b, writes items / wexp + b bs_list,
+    // count + b, x_touched + N b, Philox token index token_offset + N b + t (no form 2)
+    int32_t batch;
+    int64_t bs_list;
 };
 int sampler_max_tokens();
 int sampler_cluster_ctas(int64_t N);      // CTAs per mask the sampler launches for N tokens (introspection)
@@ -89,6 +100,11 @@ struct CompactArgs {
                               // 1 dense (nothing to move), 0 sampled, 2 dense + correction
     const int32_t* corr_items; const int8_t* corr_wexp; const int32_t* corr_count;   // form 2
     const int32_t* sub_items; const int32_t* sub_count; const uint8_t* tok_flag;
+    // batched (attention BMM, form 0 only): blockIdx.y = batch b; q8 / xq / x_touched / dx rows
+    // offset by N b, lists by bs_list b, counts by b, a_x / a_w / b_w by their per-batch extents
+    // (2N + 128, kcap, kcap rows)
+    int32_t batch;
+    int64_t bs_list;
 };
 cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s);
 
@@ -129,7 +145,17 @@ struct GemmArgs {
     // spans the data-parallel ranks; the epilogue reduces its tile into every rank's copy with
     // multimem.red.add instead of storing to `out`
     float* out_mc;
+    // batched launches only (attention BMM; batch > 0): `batch` independent
+    // problems of these sizes in one launch.  Every tensor map is 3-D (coordinate 2 = batch);
+    // m_dev / k_dev / s_down point at per-batch entries; grad_X item lists of batch b start at
+    // items + b * bs_items; output and mask rows of batch b are b * rows + r (rows = n_tokens
+    // for grad_X, M for grad_W); scale = tab[8 b + tab_idx].  Operand form 0 only.
+    int32_t batch;
+    int64_t bs_items;
+    const float* tab;
+    int32_t tab_idx;
 };
+constexpr int kMaxGemmBatch = 2048;       // batches per batched backward GEMM launch (shared-memory tile table)
 constexpr int kGemmCG = 2;                // CTAs per MMA tile (tcgen05 cta_group::2)
 // CUtensorMap* (host): A, B, C (output), A2 (grad_X dense A = Q), A3 / B2 (grad_W dense A = Q,
 // B = X_hat), AW / BW (grad_W sampled A_W, B_W in an EPI_BWD launch); null = unused
@@ -145,6 +171,9 @@ cudaError_t launch_lsq_finalize(const double* part_x, const double* part_w, cons
                                 float s_w, double g_x, double g_w, float* grad_s, cudaStream_t s);
 size_t lsq_cold_start_ws_bytes();
 cudaError_t launch_lsq_cold_start(const uint16_t* x, int64_t n, float* step, void* ws, cudaStream_t s);
+
+constexpr int kStepTabChunk = 128;       // batches per step-table launch (8 floats each, kernel parameters)
+cudaError_t launch_step_table(const float* host, int64_t n, float* dst, cudaStream_t s);   // host [n][8] -> dst
 
 // adaptive_k.cu -----------------------------------------------------------------
 size_t select_k_ws_bytes();

@@ -125,4 +125,34 @@ cudaError_t launch_lsq_cold_start(const uint16_t* x, int64_t n, float* step, voi
     return cudaLaunchKernelEx(&cfg, lsq_cold_start_kernel, x, n, step, static_cast<ColdWs*>(ws));
 }
 
+// ---------------------------------------------------------------------------
+// Step table of a batched BMM (host values -> device): the values travel as kernel
+// parameters, so the copy is stream-ordered and graph-capturable without pinned
+// host memory.  One launch per kStepTabChunk batches.
+struct StepTab { float v[kStepTabChunk * 8]; };
+
+__global__ void __launch_bounds__(256) step_table_kernel(const StepTab t, int n, float* __restrict__ dst) {
+    pdl_trigger();
+    pdl_wait();                                   // earlier kernels may still read the previous table
+    for (int i = threadIdx.x; i < n * 8; i += blockDim.x) dst[i] = t.v[i];
+}
+
+cudaError_t launch_step_table(const float* host, int64_t n, float* dst, cudaStream_t s) {
+    for (int64_t b0 = 0; b0 < n; b0 += kStepTabChunk) {
+        const int m = int(n - b0 < kStepTabChunk ? n - b0 : kStepTabChunk);
+        StepTab t{};
+        for (int i = 0; i < m * 8; ++i) t.v[i] = host[b0 * 8 + i];
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(1);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        cfg.attrs = attr;
+        cfg.numAttrs = add_pdl_attr(attr, 0);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, step_table_kernel, t, m, dst + b0 * 8);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace i4

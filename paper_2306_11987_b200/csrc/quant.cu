@@ -48,6 +48,8 @@ struct HqJob {
     float* delta;                        // optional: A.3 delta = code - I o v (fp32, exact)
     int blocks;                          // CTAs assigned to this job
     int32_t* status;                     // optional: device status word (bit 0 <- non-finite input)
+    const float* r_tab;                  // batched (BMM): r of row i = r_tab[8 (i / rpb)] (else r)
+    int64_t rpb;
 };
 
 constexpr int kHqMaxThreads = 256;
@@ -55,8 +57,8 @@ constexpr int kHqMaxThreads = 256;
 // One 32-column block of one row: FWHT (registers, + xor-shuffle stages for
 // k = 6, 7), LSQ, code / mask / delta stores; returns the block's sum of squared codes.
 template <int K, bool DELTA>
-__device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, int tpr, int cols, bool active,
-                                        const uint4 (&raw)[4]) {
+__device__ __forceinline__ int hq_block(const HqJob& J, float r, int64_t row, int blk, int tpr, int cols,
+                                        bool active, const uint4 (&raw)[4]) {
     // column pairs (j, j + 16) in fp32x2 registers: the in-register FWHT stages
     // (strides 1 .. 8) and the LSQ scaling run as packed FADD2 / FMUL2
     uint64_t p[16];
@@ -103,7 +105,7 @@ __device__ __forceinline__ int hq_block(const HqJob& J, int64_t row, int blk, in
     // rint on the clamped value by the magic-number add: fl32(c + 1.5 2^23) is
     // exact round-half-even for |c| <= 7 (ulp 1 there), and the low byte of its
     // bits is the int8 code (0x4B400000 + q) -- one FADD instead of an F2I.
-    const uint64_t r2 = f2_pack(J.r, J.r);
+    const uint64_t r2 = f2_pack(r, r);
     uint32_t qb[32];                                // code in byte 0
     uint32_t mask = 0;
     int sq = 0;
@@ -238,7 +240,7 @@ hadamard_quant_tma_kernel(HqJob j0, HqJob j1, int cols, HqSched hs) {
             fence_proxy_async_smem();                  // the generic reads above before the async refill
             if (nx < n_stages) issue(nx, slot);
         }
-        const int sq = hq_block<K, DELTA>(J, row, blk, tpr, cols, active, raw);
+        const int sq = hq_block<K, DELTA>(J, J.r, row, blk, tpr, cols, active, raw);
         if (active && J.sqnorm != nullptr) atomicAdd(&sq_row[r_local], sq);
         if (J.sqnorm != nullptr) {
             __syncthreads();
@@ -343,7 +345,8 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     for (int ps = 0; ps < kHqPasses; ++ps) {
         const int64_t row = row0 + int64_t(ps) * rows_per_cta;
         const bool active = r_local < rows_per_cta && row < J.rows;
-        const int sq = hq_block<K, DELTA>(J, row, blk, tpr, cols, active, raw[ps]);
+        const float r = J.r_tab != nullptr && active ? __ldg(J.r_tab + 8 * (row / J.rpb)) : J.r;
+        const int sq = hq_block<K, DELTA>(J, r, row, blk, tpr, cols, active, raw[ps]);
         if (active && J.sqnorm != nullptr) atomicAdd(&sq_row[ps][r_local], sq);
     }
     if (J.sqnorm != nullptr) {
@@ -363,8 +366,8 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     return launch_hadamard_quant_tma(a, s);
 #endif
     const int R = hq_rows_per_cta(a.cols);
-    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0, a.status};
-    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0, a.status};
+    HqJob j0{a.x0, a.rows0, a.r0, a.codes0, a.bits0, a.sqnorm0, a.delta0, 0, a.status, a.r_tab0, a.rpb0};
+    HqJob j1{a.x1, a.rows1, a.r1, a.codes1, a.bits1, a.sqnorm1, a.delta1, 0, a.status, a.r_tab1, a.rpb1};
     j0.blocks = int((a.rows0 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
     j1.blocks = int((a.rows1 + int64_t(R) * kHqPasses - 1) / (int64_t(R) * kHqPasses));
     const int grid = j0.blocks + j1.blocks;
@@ -635,7 +638,8 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 
 // last CTA out returns the counters to zero for the next launch (every CTA read
 // the amax word and the arrival count before it departed)
-__device__ __forceinline__ void depart(uint32_t* scratch) {
+template <bool BAT>
+__device__ __forceinline__ void depart(uint32_t* scratch, uint32_t* bamax, int64_t nbat) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -643,6 +647,8 @@ __device__ __forceinline__ void depart(uint32_t* scratch) {
             scratch[kAmaxWord] = 0u;
             scratch[kArriveWord] = 0u;
             scratch[kDepartWord] = 0u;
+            if (BAT)
+                for (int64_t b = 0; b < nbat; ++b) bamax[b] = 0u;
         }
     }
 }
@@ -710,6 +716,50 @@ __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int6
     }
 }
 
+// Batched (attention BMM, reading Z-31): batch b = rows [b nb, (b+1) nb) has its own
+// amax word bamax[b] (so its own r8 / s_down) and its own [2 nb] norm block of a_sq.
+__device__ __forceinline__ void batch_scale(const uint32_t* bamax, int64_t b, float& r8, bool& zero) {
+    const uint32_t ab = ld_acquire_gpu(bamax + b);
+    const float amax = __uint_as_float(ab << 16);
+    zero = ab >= 0x7F80u || !(amax > 0.0f);
+    r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
+}
+
+template <int G, bool C1Z>
+__device__ __forceinline__ void split_units_bat(const uint16_t* __restrict__ g, int C, const PhiloxKeys& keys,
+                                                uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
+                                                int32_t* __restrict__ a_sq, int64_t u0, int64_t u1, uint4 (&buf)[G],
+                                                int64_t nb, const uint32_t* bamax) {
+    const int upr = C / (256 * G);
+    const uint4* src = reinterpret_cast<const uint4*>(g) + lane_id();
+    const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);
+    int shi = 0, slo = 0;
+    if (u0 >= u1) return;
+    int64_t row = u0 / upr;
+    int seg = int(u0 - row * upr);
+    int64_t b = row / nb;
+    float r8; bool zero;
+    batch_scale(bamax, b, r8, zero);
+    for (int64_t un = u0; un < u1; ++un) {
+        uint4 cur[G];
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
+        if (un + 1 < u1) load_unit<G>(src, un + 1, buf);
+        if (zero) {
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi)
+                *reinterpret_cast<uint2*>(q8 + (un * G + gi) * 256 + lane_id() * 8) = make_uint2(0u, 0u);
+        } else {
+            split_unit<G, true, C1Z>(cur, un, r8, keys, call_id, tbase, q8, shi, slo);
+        }
+        if (++seg == upr || un + 1 == u1) {
+            flush_norms(shi, slo, a_sq + b * 2 * nb, nb, row - b * nb);
+            seg = 0; ++row;
+            if (un + 1 < u1 && row / nb != b) { b = row / nb; batch_scale(bamax, b, r8, zero); }
+        }
+    }
+}
+
 // timing experiment, compiled in only by -DI4_STAMPS=1 (tools/build_variants.sh,
 // tools/gs_stamps.py): per-CTA globaltimer stamps -- start, phase 1 done,
 // barrier passed, amax known, phase 2 done (max over warps)
@@ -724,12 +774,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-template <int G, bool C1Z>
+// BAT: batched (N = B nb rows; per-batch amax words bamax[B], zero on entry and returned
+// to zero; s_down_out / amax_out [B]; a_sq [B][2 nb])
+template <int G, bool C1Z, bool BAT>
 __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ scratch,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
-                  int32_t* __restrict__ status) {
+                  int32_t* __restrict__ status, int64_t nb, uint32_t* __restrict__ bamax) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     pdl_trigger();
@@ -738,7 +790,39 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     if (stamp && threadIdx.x == 0) g_gs_stamp[0][blockIdx.x] = gtimer();
 
     // ---- phase 1: amax ----------------------------------------------------
-    {
+    if constexpr (BAT) {
+        // contiguous row range per warp; the running max goes to its batch's word when
+        // the batch changes (rows never straddle batches)
+        const int64_t nwarps = int64_t(gridDim.x) * (kSplitThreads / 32);
+        const int64_t wid = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
+        const int64_t r0 = N * wid / nwarps, r1 = N * (wid + 1) / nwarps;
+        const int c8 = C / 8;
+        uint32_t m = 0;
+        int64_t cb = r0 / nb;
+        auto flush = [&](int64_t b) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+            if (lane == 0) atomicMax(bamax + b, m);
+            m = 0;
+        };
+        for (int64_t row = r0; row < r1; ++row) {
+            if (row / nb != cb) { flush(cb); cb = row / nb; }
+            const uint4* g4 = reinterpret_cast<const uint4*>(g + row * C);
+            for (int i = lane; i < c8; i += 32) {
+                const uint4 u = ld_nc_v4(g4 + i);
+                m = max(m, max(max(bf16x2_absmax(u.x), bf16x2_absmax(u.y)), max(bf16x2_absmax(u.z), bf16x2_absmax(u.w))));
+            }
+        }
+        if (r0 < r1) flush(cb);
+        const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+        if (G > 0)
+            for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * N; i += stride) a_sq[i] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(scratch + kArriveWord, 1u);
+        }
+    } else {
         const uint4* g4 = reinterpret_cast<const uint4*>(g);
         const int64_t n8 = N * int64_t(C) / 8;
         const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -803,7 +887,16 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     const bool zero = nonfinite || !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
     if (stamp && threadIdx.x == 0) { g_gs_stamp[3][blockIdx.x] = gtimer(); g_gs_stamp[4][blockIdx.x] = 0; }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (BAT && blockIdx.x == 0) {
+        for (int64_t b = threadIdx.x; b < N / nb; b += blockDim.x) {
+            const uint32_t ab = ld_acquire_gpu(bamax + b);
+            const float am = __uint_as_float(ab << 16);
+            const bool nf = ab >= 0x7F80u, zr = nf || !(am > 0.0f);
+            s_down_out[b] = zr ? 0.0f : __fdiv_rn(am, 119.0f);
+            amax_out[b] = ab;
+            if (status != nullptr && zr) atomicOr(status, nf ? kStatusNonFinite : kStatusZeroGrad);
+        }
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
         *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
         *amax_out = amax_b;
         if (status != nullptr && zero) atomicOr(status, nonfinite ? kStatusNonFinite : kStatusZeroGrad);
@@ -813,7 +906,12 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     if (blockIdx.x == gridDim.x - 1)                      // code row N: the all-zero pad row
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(q8 + N * C + c) = make_uint4(0, 0, 0, 0);
-    if constexpr (G > 0) {
+    if constexpr (G > 0 && BAT) {
+        split_units_bat<G, C1Z>(g, C, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf, nb, bamax);
+        depart<BAT>(scratch, bamax, N / nb);
+        return;
+    }
+    if constexpr (G > 0 && !BAT) {
         if (zero) {                                       // all-zero / non-finite grad_Y: codes 0, norms 0
             for (int64_t un = pu0; un < pu1; ++un)        // (zeroed in phase 1)
 #pragma unroll
@@ -827,9 +925,11 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 split_units<G, false, C1Z>(g, N, C, r8, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         }
         if (stamp && lane == 0) atomicMax(&g_gs_stamp[4][blockIdx.x], gtimer());
-        depart(scratch);
+        depart<BAT>(scratch, bamax, 0);
         return;
     }
+    const float r8g = r8;
+    const bool zerog = zero;
     // generic path (C not a multiple of 256): one warp per row
     const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
     const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
@@ -839,6 +939,10 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         int8_t* qr = q8 + row * C;
         const uint64_t tglob = uint64_t(token_offset + row);
         int shi = 0, slo = 0;
+        float r8 = r8g;
+        bool zero = zerog;
+        const int64_t bb = BAT ? row / nb : 0;
+        if (BAT) batch_scale(bamax, bb, r8, zero);
         for (int g0 = 0; g0 < nch; g0 += kBsGroup) {
             uint4 raw[kBsGroup];
 #pragma unroll
@@ -892,14 +996,15 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
         }
         if (lane == 0) {
-            a_sq[row] = shi >> 8;                             // exact: every term is 256 hi^2
-            a_sq[N + row] = slo;
+            const int64_t base = BAT ? bb * 2 * nb : 0, nrow = BAT ? nb : N, lr = BAT ? row - bb * nb : row;
+            a_sq[base + lr] = shi >> 8;                       // exact: every term is 256 hi^2
+            a_sq[base + nrow + lr] = slo;
         }
     }
-    depart(scratch);
+    depart<BAT>(scratch, bamax, BAT ? N / nb : 0);
 }
 
-template <int G, bool C1Z>
+template <int G, bool C1Z, bool BAT>
 static int grad_split_max_blocks() {
     static std::atomic<int> cached[kMaxDevices];        // per device ordinal (0 = not yet queried)
     int dev = 0;
@@ -909,21 +1014,25 @@ static int grad_split_max_blocks() {
     if (v == 0) {
         int per_sm = 0, sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z>, kSplitThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z, BAT>, kSplitThreads, 0);
         v = per_sm * sms;
         cached[dev].store(v, std::memory_order_relaxed);
     }
     return v;
 }
 
-int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
+int grad_split_max_blocks() { return grad_split_max_blocks<0, false, false>(); }
 
-template <int G, bool C1Z>
-static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
-                                       uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
-                                       float* s_down, uint32_t* amax_out, int32_t* status, cudaStream_t s) {
-    int blocks = grad_split_max_blocks<G, C1Z>();
-    const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
+struct SplitLaunch {
+    const uint16_t* g; int64_t N; int C; uint32_t* block_max; PhiloxKeys keys; uint32_t call_id;
+    int64_t token_offset; int8_t* q8; int32_t* a_sq; float* s_down; uint32_t* amax_out; int32_t* status;
+    int64_t nb; uint32_t* bamax;
+};
+
+template <int G, bool C1Z, bool BAT>
+static cudaError_t launch_grad_split_g(const SplitLaunch& L, cudaStream_t s) {
+    int blocks = grad_split_max_blocks<G, C1Z, BAT>();
+    const int64_t want = G > 0 ? (L.N * (L.C / (256 * G)) + 7) / 8 : (L.N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
     if (blocks > kAmaxWord) blocks = kAmaxWord;
     cudaLaunchConfig_t cfg{};
@@ -935,46 +1044,39 @@ static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id,
-                                       token_offset, q8, a_sq, s_down, amax_out, status);
+    auto kern = grad_split_kernel<G, C1Z, BAT>;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, L.g, L.N, L.C, L.block_max, L.keys, L.call_id, L.token_offset,
+                                       L.q8, L.a_sq, L.s_down, L.amax_out, L.status, L.nb, L.bamax);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id, token_offset,
-                               q8, a_sq, s_down, amax_out, status);
+        e = cudaLaunchKernelEx(&cfg, kern, L.g, L.N, L.C, L.block_max, L.keys, L.call_id, L.token_offset, L.q8,
+                               L.a_sq, L.s_down, L.amax_out, L.status, L.nb, L.bamax);
     }
     return e;
 }
 
 template <int G>
-static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint32_t* block_max,
-                                       const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* q8,
-                                       int32_t* a_sq, float* s_down, uint32_t* amax_out, int32_t* status,
-                                       cudaStream_t s) {
+static cudaError_t launch_grad_split_c(const SplitLaunch& L, cudaStream_t s) {
     // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
-    const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
-    if (c1z)
-        return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
-                                            amax_out, status, s);
-    return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
-                                         amax_out, status, s);
+    const bool c1z = (uint64_t(L.token_offset) + uint64_t(L.N)) * uint64_t(L.C) <= (uint64_t(1) << 34);
+    if (L.bamax != nullptr)
+        return c1z ? launch_grad_split_g<G, true, true>(L, s) : launch_grad_split_g<G, false, true>(L, s);
+    return c1z ? launch_grad_split_g<G, true, false>(L, s) : launch_grad_split_g<G, false, false>(L, s);
 }
 
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, int32_t* status, cudaStream_t s) {
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s, int64_t nb, uint32_t* bamax) {
     if (N == 0) return cudaSuccess;
-    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
-    const int Ci = int(C);
-#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, status, s)
+    const SplitLaunch L{g, N, int(C), block_max, philox_keys(uint32_t(seed), uint32_t(seed >> 32)), call_id,
+                        token_offset, q8, a_sq, s_down, amax_out, status, bamax ? nb : N, bamax};
     // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
     // measured equal or slower), else 3, 1; the one-warp-per-row loop otherwise
-    if (kBsGMax >= 2 && C % 512 == 0) return I4_GS(2);
-    if (kBsGMax >= 3 && C % 768 == 0) return I4_GS(3);
-    if (C % 256 == 0) return I4_GS(1);
-#undef I4_GS
-    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out,
-                                  status, s);
+    if (kBsGMax >= 2 && C % 512 == 0) return launch_grad_split_c<2>(L, s);
+    if (kBsGMax >= 3 && C % 768 == 0) return launch_grad_split_c<3>(L, s);
+    if (C % 256 == 0) return launch_grad_split_c<1>(L, s);
+    return launch_grad_split_c<0>(L, s);
 }
 
 // debug export for the timing experiment: copies the stamps of the last launch

@@ -203,6 +203,12 @@ lss_sampler_kernel(SamplerArgs a) {
     const int rank = int(cl.rank());
     const int mask_id = blockIdx.y;                      // 0: grad_W, 1: grad_X
     const int N = a.N;
+    // batch of this cluster (batched launches: blockIdx.z) and its slices
+    const int64_t bz = blockIdx.z;
+    const int32_t* const a_sq = a.a_sq + bz * 2 * N;
+    const int32_t* const x_sqnorm = a.x_sqnorm != nullptr ? a.x_sqnorm + bz * N : nullptr;
+    uint8_t* const x_touched = a.x_touched != nullptr ? a.x_touched + bz * N : nullptr;
+    const int64_t tok_off = a.token_offset + bz * N;
     const int n_items = 2 * N;
     const int per = sampler_per(N, CL);
     const int per16 = (per + 15) & ~15;
@@ -223,7 +229,7 @@ lss_sampler_kernel(SamplerArgs a) {
     // grad_X GEMM's compacted A and compact skips its own copy
     auto item_of = [&](int slot) { return (slot & 1) * N + (slot >> 1); };
     int parity = 0;
-    if (blockIdx.y == 0 && rank == 0)
+    if (blockIdx.y == 0 && blockIdx.z == 0 && rank == 0)
         for (int i = threadIdx.x; i < a.n_zero_words; i += NT) a.zero_words[i] = 0u;
 
     // ---- scores -------------------------------------------------------------
@@ -239,8 +245,8 @@ lss_sampler_kernel(SamplerArgs a) {
             if (j < t_hi && a.mode != 2) {
                 const int i = item_of(base + j);
                 const int t = i >= N ? i - N : i;
-                av[q] = __ldg(a.a_sq + i);
-                if (mask_id == 0) bv[q] = __ldg(a.x_sqnorm + t);
+                av[q] = __ldg(a_sq + i);
+                if (mask_id == 0) bv[q] = __ldg(x_sqnorm + t);
             }
         }
 #pragma unroll
@@ -250,7 +256,7 @@ lss_sampler_kernel(SamplerArgs a) {
             const int i = item_of(base + j);
             const int h = i >= N ? 1 : 0;
             const int t = i - h * N;
-            if (mask_id == 1 && h == 0 && a.x_touched) a.x_touched[t] = 0;   // set below for kept items
+            if (mask_id == 1 && h == 0 && x_touched) x_touched[t] = 0;   // set below for kept items
             uint64_t w = 0;
             if (a.mode != 2) {                                       // I4_LSS_NONE needs no scores
                 const double prod = double(av[q]) * double(bv[q]);   // exact: < 2^53
@@ -328,7 +334,7 @@ lss_sampler_kernel(SamplerArgs a) {
                     T2 = floor_mul2_32_div(num, W);
                     T1 = 2 * T2 - (1ull << (32 - e));
                 }
-                const uint64_t idx = 2ull * uint64_t(a.token_offset + t) + uint64_t(h);
+                const uint64_t idx = 2ull * uint64_t(tok_off + t) + uint64_t(h);
                 const Philox4 p = philox4x32_10(uint32_t(idx), uint32_t(idx >> 32), purpose, a.call_id,
                                                 a.seed_lo, a.seed_hi);
                 const uint64_t u = p.x;
@@ -337,15 +343,15 @@ lss_sampler_kernel(SamplerArgs a) {
         }
         swe[j] = out;
         my_keep += (out >= 0);
-        if (mask_id == 1 && out >= 0 && a.x_touched) a.x_touched[t] = 1;
+        if (mask_id == 1 && out >= 0 && x_touched) x_touched[t] = 1;
     }
 
     smp_stamp(st_n, st_on);
     // ---- compaction: block exclusive scan + cluster prefix --------------------
     uint32_t total = 0;
     uint32_t pos = group_scan<CL, NT>(cl, my_keep, sm.scan, sm.cta_tot, total);
-    int32_t* items = a.items[mask_id];
-    int8_t* wexp = a.wexp[mask_id];
+    int32_t* items = a.items[mask_id] + bz * a.bs_list;
+    int8_t* wexp = a.wexp[mask_id] + bz * a.bs_list;
     for (int j = t_lo; j < t_hi; ++j) {
         const int8_t e = swe[j];
         if (e >= 0) {
@@ -360,7 +366,7 @@ lss_sampler_kernel(SamplerArgs a) {
             items[p] = n_items;                // sentinel: an all-zero row
             wexp[p] = 0;
         }
-        if (threadIdx.x == 0) *a.count[mask_id] = int32_t(total);
+        if (threadIdx.x == 0) a.count[mask_id][bz] = int32_t(total);
     }
     if (corr) {
         // form 2 lists.  An item is sampled when its score is positive and A.2 did not
@@ -406,7 +412,7 @@ static void sampler_config(const SamplerArgs& a, cudaStream_t s, cudaLaunchConfi
     const int per = sampler_per(a.N, CL);
     const int per16 = (per + 15) & ~15;
     cfg = cudaLaunchConfig_t{};
-    cfg.gridDim = dim3(CL, 2, 1);                 // y: 0 = grad_W mask, 1 = grad_X mask
+    cfg.gridDim = dim3(CL, 2, unsigned(a.batch > 1 ? a.batch : 1));   // y: 0 = grad_W mask, 1 = grad_X mask; z: batch
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
     cfg.stream = s;
