@@ -292,8 +292,8 @@ I4_API i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N
  * token_offset = b N (distinct Philox streams, reading Z-31), its own amax and
  * budget N, the step sizes of the forward (cache->steps), operand form 0 (the
  * compacted kept items) for both masks.  ws: int4_bmm_bwd_workspace_size(B, N, P, M)
- * bytes, ZERO-INITIALISED BEFORE ITS FIRST USE (it holds grad_split's barrier and
- * per-batch amax words; every call leaves them zero again).  B is processed in
+ * bytes, ZERO-INITIALISED BEFORE ITS FIRST USE (it holds grad_split's per-batch
+ * amax words; every call leaves them zero again).  B is processed in
  * chunks of at most 2048 batches (one launch sequence per chunk). */
 I4_API size_t int4_bmm_bwd_workspace_size(int64_t B, int64_t N, int64_t P, int64_t M);
 I4_API i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, uint64_t seed, uint32_t call_id,

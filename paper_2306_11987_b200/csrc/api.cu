@@ -621,10 +621,10 @@ extern "C" {
 namespace {
 
 // Backward workspace of the batched BMM (int4_bmm_bwd), for a chunk of Bc <= 2048
-// batches; each region 256-aligned.  The first two regions must be zero before the
-// first call (grad_split's barrier words and per-batch amax words; left zero).
+// batches; each region 256-aligned.  The first region (grad_split's per-batch amax
+// words) must be zero before the first call; every call leaves it zero.
 struct BmmWs {
-    uint32_t* scratch; uint32_t* bamax; uint32_t* amax; float* s_down; int32_t* counts;
+    uint32_t* bamax; uint32_t* amax; float* s_down; int32_t* counts;
     int32_t* items_w; int8_t* wexp_w; int32_t* items_x; int8_t* wexp_x;
     uint8_t* x_touched; int32_t* a_sq; int8_t* q8; int8_t* a_x; int8_t* a_w; int8_t* b_w;
     size_t off[8];
@@ -637,7 +637,6 @@ BmmWs carve_bmm_ws(void* ws, int64_t B, int64_t N, int64_t P, int64_t M) {
     BmmWs w{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += size_t(round_up(int64_t(bytes), 256)); return o; };
-    const size_t o_scr = take(size_t(i4::kGradSplitMaxBlocks) * 4);
     const size_t o_bam = take(size_t(Bc) * 4);
     const size_t o_am = take(size_t(Bc) * 4);
     const size_t o_sd = take(size_t(Bc) * 4);
@@ -657,7 +656,6 @@ BmmWs carve_bmm_ws(void* ws, int64_t B, int64_t N, int64_t P, int64_t M) {
     for (int i = 0; i < 8; ++i) w.off[i] = offs[i];
     if (ws) {
         uint8_t* b = static_cast<uint8_t*>(ws);
-        w.scratch = reinterpret_cast<uint32_t*>(b + o_scr);
         w.bamax = reinterpret_cast<uint32_t*>(b + o_bam);
         w.amax = reinterpret_cast<uint32_t*>(b + o_am);
         w.s_down = reinterpret_cast<float*>(b + o_sd);
@@ -712,7 +710,8 @@ i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64
         t[5] = s_q[b];
         t[6] = s_k[b];
     }
-    I4_LAUNCH(i4::launch_step_table(tab.data(), B, cache->steps, s), "step_table", s);
+    const bool tab_in_hq = B <= i4::kStepTabChunk;     // the table rides on the quantizer launch
+    if (!tab_in_hq) I4_LAUNCH(i4::launch_step_table(tab.data(), B, cache->steps, s), "step_table", s);
     {
         // F1-F3 for every row of Q and K (one launch; per-row r from the batch's table entry)
         i4::HqArgs h{};
@@ -724,6 +723,7 @@ i4_status int4_bmm_fwd(const void* Q, const void* K, int64_t B, int64_t N, int64
         h.r_tab1 = cache->steps + 1; h.rpb1 = P;
         h.cols = M; h.k = k;
         h.status = cache->dev_status;
+        if (tab_in_hq) { h.tab_host = tab.data(); h.tab_n = int(B); h.tab_dst = cache->steps; }
         I4_LAUNCH(i4::launch_hadamard_quant2(h, s), "hadamard_quant", s);
     }
     {
@@ -786,9 +786,9 @@ i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, uint64_t seed,
         const int64_t nb = std::min<int64_t>(Bc, B - b0);
         const int64_t toff = b0 * N;                  // Philox token index of the chunk's first row (Z-31)
         // B1 + B2: per-batch amax, SR codes, half-row norms
-        I4_LAUNCH(i4::launch_grad_split(static_cast<const uint16_t*>(dT) + b0 * N * P, nb * N, P, w.scratch, seed,
-                                        call_id, toff, w.q8, w.a_sq, w.s_down, w.amax, cache->dev_status, s, N,
-                                        w.bamax),
+        I4_LAUNCH(i4::launch_grad_split_batched(static_cast<const uint16_t*>(dT) + b0 * N * P, nb * N, P, N, seed,
+                                                call_id, toff, w.q8, w.a_sq, w.s_down, w.amax, cache->dev_status,
+                                                w.bamax, s),
                   "grad_split", s);
         // LSS steps 2-4: one cluster per (mask, batch)
         i4::SamplerArgs a{};
@@ -803,6 +803,7 @@ i4_status int4_bmm_bwd(const void* dT, const i4_bmm_cache* cache, uint64_t seed,
         a.items[0] = w.items_w; a.wexp[0] = w.wexp_w; a.count[0] = w.counts;
         a.items[1] = w.items_x; a.wexp[1] = w.wexp_x; a.count[1] = w.counts + Bc;
         a.x_touched = w.x_touched;
+        a.zero_words = w.bamax; a.n_zero_words = int32_t(nb);   // grad_split's amax words, for the next call
         a.batch = int32_t(nb);
         a.bs_list = L;
         I4_LAUNCH(i4::launch_lss_sampler(a, s), "lss_sampler", s);

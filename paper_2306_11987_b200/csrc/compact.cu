@@ -39,6 +39,18 @@ __device__ __forceinline__ uint32_t split_word(uint32_t q, int half) {
 // half: -1 copy (optionally scaled by mul), 0 / 1: the high (16 hi) / low half of the codes
 __device__ __forceinline__ void copy_row(const int8_t* __restrict__ src, int8_t* __restrict__ dst, int n, int lane,
                                          bool zero, int mul, int half = -1) {
+    if (n <= 512) {                                   // short row (attention head dims): one chunk per lane
+        const int c = lane * 16;
+        if (c < n) {
+            uint4 v = zero ? make_uint4(0, 0, 0, 0) : ld_nc_v4(src + c);
+            if (half >= 0)
+                v = make_uint4(split_word(v.x, half), split_word(v.y, half), split_word(v.z, half), split_word(v.w, half));
+            else if (mul != 1)
+                v = scale_i8x16(v, mul);
+            *reinterpret_cast<uint4*>(dst + c) = v;
+        }
+        return;
+    }
     for (int c0 = 0; c0 < n; c0 += 512 * kGroup) {
         uint4 u[kGroup];
 #pragma unroll
@@ -95,25 +107,38 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
     const int64_t pad_w = (cnt_w + 127) & ~int64_t(127);
     const int64_t n_straddle = (cnt_x + 31) / 32;            // candidate positions 31, 63, ...
     const int64_t seg_bw = pad_x + pad_w;                    // first B_W row job
-    const int64_t n_zero = fx == 1 ? 0 : a.N;
-    const int64_t total = seg_bw + pad_w + n_zero + n_straddle;
+    // short rows (D < 512 bytes, e.g. attention head dims) share a warp: rpj rows per job,
+    // D / 16 lanes per row, so every lane moves 16 bytes
+    const int rpj_b = a.D < 512 ? 512 / a.D : 1;
+    const int64_t n_bw = (pad_w + rpj_b - 1) / rpj_b;
+    const int zb = a.D * (a.dx_bf16 ? 2 : 4);                // bytes of a grad_X row
+    const int rpj_z = zb < 512 ? 512 / zb : 1;
+    const int64_t n_zero = fx == 1 ? 0 : (a.N + rpj_z - 1) / rpj_z;
+    const int64_t seg_z = seg_bw + n_bw, seg_s = seg_z + n_zero;
+    const int64_t total = seg_s + n_straddle;
     const int two_n = 2 * a.N;
     for (int64_t j = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); j < total; j += warps) {
-        if (j >= seg_bw + pad_w) {
+        if (j >= seg_s) {
+            // tokens whose two items straddle a 32-row group (both red.add onto a zero row)
+            const int64_t p = 32 * (j - seg_s) + 31;
+            if (p + 1 < cnt_x) {
+                const int32_t i0 = __ldg(lx + p), i1 = __ldg(lx + p + 1);
+                const int t0 = i0 >= a.N ? i0 - a.N : i0, t1 = i1 >= a.N ? i1 - a.N : i1;
+                if (t0 == t1) zero_row(a.dx, t0, a.D, a.dx_bf16, lane);
+            }
+        } else if (j >= seg_z) {
             // grad_X rows the GEMM epilogue does not store: tokens without a kept item
-            // (form 2: only among the flagged tokens -- the others are Q rows), and tokens
-            // whose two items straddle a 32-row group (both red.add)
-            const int64_t r = j - seg_bw - pad_w;
-            if (r < a.N) {
+            // (form 2: only among the flagged tokens -- the others are Q rows)
+            if (rpj_z == 1) {
+                const int64_t r = j - seg_z;
                 if (__ldg(a.x_touched + r) == 0 && (fx != 2 || __ldg(a.tok_flag + r) != 0))
                     zero_row(a.dx, r, a.D, a.dx_bf16, lane);
             } else {
-                const int64_t p = 32 * (r - a.N) + 31;
-                if (p + 1 < cnt_x) {
-                    const int32_t i0 = __ldg(lx + p), i1 = __ldg(lx + p + 1);
-                    const int t0 = i0 >= a.N ? i0 - a.N : i0, t1 = i1 >= a.N ? i1 - a.N : i1;
-                    if (t0 == t1) zero_row(a.dx, t0, a.D, a.dx_bf16, lane);
-                }
+                const int lpr = zb / 16;
+                const int64_t r = (j - seg_z) * rpj_z + lane / lpr;
+                if (r < a.N && __ldg(a.x_touched + r) == 0 && (fx != 2 || __ldg(a.tok_flag + r) != 0))
+                    *reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.dx) + r * zb + (lane % lpr) * 16) =
+                        make_uint4(0, 0, 0, 0);
             }
         } else if (j < pad_x) {
             const int32_t item = __ldg(lx + j);
@@ -129,12 +154,27 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
         } else {
             // B_W row = weight x X_hat[t]: 2^wexp for kept items, -1 for a form-2
             // correction row that removes the item's dense term (|.| <= 112)
-            const int64_t r = j - seg_bw;
-            const int32_t item = __ldg(lw + r);
-            const bool pad = item >= two_n;
-            const int t = pad ? 0 : (item >= a.N ? item - a.N : item);
-            const int e = pad ? 0 : int(__ldg(ew + r));
-            copy_row(a.xq + int64_t(t) * a.D, a.b_w + r * a.D, a.D, lane, pad, e < 0 ? -1 : (1 << e));
+            if (rpj_b == 1) {
+                const int64_t r = j - seg_bw;
+                const int32_t item = __ldg(lw + r);
+                const bool pad = item >= two_n;
+                const int t = pad ? 0 : (item >= a.N ? item - a.N : item);
+                const int e = pad ? 0 : int(__ldg(ew + r));
+                copy_row(a.xq + int64_t(t) * a.D, a.b_w + r * a.D, a.D, lane, pad, e < 0 ? -1 : (1 << e));
+            } else {
+                const int lpr = a.D / 16;
+                const int64_t r = (j - seg_bw) * rpj_b + lane / lpr;
+                if (r < pad_w) {
+                    const int32_t item = __ldg(lw + r);
+                    const bool pad = item >= two_n;
+                    const int t = pad ? 0 : (item >= a.N ? item - a.N : item);
+                    const int e = pad ? 0 : int(__ldg(ew + r));
+                    const int c = (lane % lpr) * 16;
+                    uint4 v = pad ? make_uint4(0, 0, 0, 0) : ld_nc_v4(a.xq + int64_t(t) * a.D + c);
+                    if (!pad) v = scale_i8x16(v, e < 0 ? -1 : (1 << e));
+                    *reinterpret_cast<uint4*>(a.b_w + r * a.D + c) = v;
+                }
+            }
         }
     }
 }
@@ -145,7 +185,8 @@ cudaError_t launch_compact(const CompactArgs& a, cudaStream_t s) {
     if (blocks > 148 * 4) blocks = 148 * 4;        // grid-stride rows; a smaller grid launches faster when little is to move
     cudaLaunchConfig_t cfg{};
     const int64_t nbat = a.batch > 1 ? a.batch : 1;
-    if (nbat > 1) blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (148 * 4 + nbat - 1) / nbat));
+    // batched: one warp per row job where the device holds them (8 CTAs of 8 warps per SM)
+    if (nbat > 1) blocks = std::max<int64_t>(1, std::min<int64_t>((rows + 7) / 8, (148 * 8 + nbat - 1) / nbat));
     cfg.gridDim = dim3(unsigned(blocks), unsigned(nbat));
     cfg.blockDim = dim3(256);
     cfg.stream = s;

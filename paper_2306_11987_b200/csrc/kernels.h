@@ -26,6 +26,7 @@ constexpr int32_t kStatusNonFinite = 1;  // an input element is Inf / NaN (SPEC.
 constexpr int32_t kStatusZeroGrad = 2;   // grad_Y is all zero ("degenerate")
 
 // quant.cu --------------------------------------------------------------------
+constexpr int kStepTabChunk = 128;       // batches per step-table launch (8 floats each, kernel parameters)
 struct HqArgs {                          // two independent hadamard_quant jobs in one launch
     const uint16_t* x0; int64_t rows0; float r0; int8_t* codes0; uint32_t* bits0; int32_t* sqnorm0;
     const uint16_t* x1; int64_t rows1; float r1; int8_t* codes1; uint32_t* bits1; int32_t* sqnorm1;
@@ -34,6 +35,9 @@ struct HqArgs {                          // two independent hadamard_quant jobs 
     int32_t* status;                     // optional device status word (bit 0: non-finite input)
     // batched (BMM): row i of job j uses r = r_tabj[8 (i / rpbj)] (device table) instead of rj
     const float* r_tab0; int64_t rpb0; const float* r_tab1; int64_t rpb1;
+    // batched, <= kStepTabChunk batches: the host step table [tab_n][8] travels as a kernel
+    // parameter (r of job j = entry j of the row's batch) and is written to tab_dst
+    const float* tab_host; int tab_n; float* tab_dst;
 };
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s);
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
@@ -41,13 +45,16 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 constexpr int kGradSplitMaxBlocks = 2048;   // block-max scratch words the plan provides
 int grad_split_stamps(unsigned long long* host, int n);
 int sampler_stamps(unsigned long long* host, int enable);   // timing experiment (-DI4_STAMPS=1 builds)
-// bamax != null: batched (attention BMM): N = B nb rows, batch b = rows [b nb, (b+1) nb) with
-// its own amax word bamax[b] (zero on entry, returned to zero), s_down[b], amax_out[b] and
-// norm block a_sq[b][2 nb]
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, int32_t* status, cudaStream_t s, int64_t nb = 0,
-                              uint32_t* bamax = nullptr);
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s);
+// batched (attention BMM): rows = B nb, batch b = rows [b nb, (b+1) nb) with its own amax word
+// bamax[b] (zero on entry; the caller zeroes it again after use), s_down[b], amax_out[b] and
+// norm block a_sq[b][2 nb]; two launches (amax, split)
+cudaError_t launch_grad_split_batched(const uint16_t* g, int64_t rows, int64_t C, int64_t nb, uint64_t seed,
+                                      uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
+                                      float* s_down, uint32_t* amax_out, int32_t* status, uint32_t* bamax,
+                                      cudaStream_t s);
 
 // sampler.cu ------------------------------------------------------------------
 struct SamplerArgs {
@@ -172,7 +179,6 @@ cudaError_t launch_lsq_finalize(const double* part_x, const double* part_w, cons
 size_t lsq_cold_start_ws_bytes();
 cudaError_t launch_lsq_cold_start(const uint16_t* x, int64_t n, float* step, void* ws, cudaStream_t s);
 
-constexpr int kStepTabChunk = 128;       // batches per step-table launch (8 floats each, kernel parameters)
 cudaError_t launch_step_table(const float* host, int64_t n, float* dst, cudaStream_t s);   // host [n][8] -> dst
 
 // adaptive_k.cu -----------------------------------------------------------------

@@ -7,6 +7,7 @@
 //                    Z-9), then Philox SR to the 8-bit code q (stored), its high /
 //                    low 4-bit halves' per-row integer norms (PAPER.md:234-239,
 //                    :680); one cooperative launch with one grid barrier
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 
@@ -315,9 +316,15 @@ static cudaError_t launch_hadamard_quant_tma(const HqArgs& a, cudaStream_t s) {
 #endif
 constexpr int kHqPasses = I4_HQ_PASSES;
 
-template <int K, bool DELTA>
+// TAB: batched BMM forward with at most kStepTabChunk batches: the per-batch step table
+// travels as a kernel parameter (row i of job j uses r = v[8 (i / rpb) + j]) and CTA 0
+// writes it to device memory for the GEMM and the backward (no separate launch)
+template <bool TAB> struct HqTab { int n; float* dst; float v[kStepTabChunk * 8]; };
+template <> struct HqTab<false> {};
+
+template <int K, bool DELTA, bool TAB>
 __global__ void __launch_bounds__(kHqMaxThreads)
-hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
+hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta, const HqTab<TAB> tab) {
     const bool second = int(blockIdx.x) >= j0.blocks;
     const HqJob& J = second ? j1 : j0;
     const int bid = second ? int(blockIdx.x) - j0.blocks : int(blockIdx.x);
@@ -327,6 +334,10 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     const int64_t row0 = int64_t(bid) * rows_per_cta * kHqPasses + r_local;
     pdl_trigger();
     pdl_wait();                                        // X / W may be written by the previous kernel
+    if constexpr (TAB) {
+        if (blockIdx.x == 0)
+            for (int i = threadIdx.x; i < tab.n * 8; i += blockDim.x) tab.dst[i] = tab.v[i];
+    }
     __shared__ int sq_row[kHqPasses][kHqMaxThreads];
     if (threadIdx.x < rows_per_cta)
 #pragma unroll
@@ -345,7 +356,12 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
     for (int ps = 0; ps < kHqPasses; ++ps) {
         const int64_t row = row0 + int64_t(ps) * rows_per_cta;
         const bool active = r_local < rows_per_cta && row < J.rows;
-        const float r = J.r_tab != nullptr && active ? __ldg(J.r_tab + 8 * (row / J.rpb)) : J.r;
+        float r = J.r;
+        if constexpr (TAB) {
+            if (active) r = tab.v[8 * int(row / J.rpb) + (second ? 1 : 0)];
+        } else {
+            if (J.r_tab != nullptr && active) r = __ldg(J.r_tab + 8 * (row / J.rpb));
+        }
         const int sq = hq_block<K, DELTA>(J, r, row, blk, tpr, cols, active, raw[ps]);
         if (active && J.sqnorm != nullptr) atomicAdd(&sq_row[ps][r_local], sq);
     }
@@ -358,6 +374,35 @@ hadamard_quant_kernel(HqJob j0, HqJob j1, int cols, int rows_per_cta) {
                 if (row < J.rows) J.sqnorm[row] = sq_row[ps][r_local];
             }
     }
+}
+
+static cudaError_t launch_hq_tab(const HqArgs& a, const HqJob& j0, const HqJob& j1, int R, int grid, int threads,
+                                 cudaStream_t s) {
+    if (a.tab_n < 1 || a.tab_n > kStepTabChunk || a.delta0 != nullptr || a.delta1 != nullptr) return cudaErrorInvalidValue;
+    HqTab<true> t{};
+    t.n = a.tab_n;
+    t.dst = a.tab_dst;
+    for (int i = 0; i < a.tab_n * 8; ++i) t.v[i] = a.tab_host[i];
+    void (*kern)(HqJob, HqJob, int, int, HqTab<true>) = nullptr;
+    switch (a.k) {
+        case 0: kern = hadamard_quant_kernel<0, false, true>; break;
+        case 1: kern = hadamard_quant_kernel<1, false, true>; break;
+        case 2: kern = hadamard_quant_kernel<2, false, true>; break;
+        case 3: kern = hadamard_quant_kernel<3, false, true>; break;
+        case 4: kern = hadamard_quant_kernel<4, false, true>; break;
+        case 5: kern = hadamard_quant_kernel<5, false, true>; break;
+        case 6: kern = hadamard_quant_kernel<6, false, true>; break;
+        case 7: kern = hadamard_quant_kernel<7, false, true>; break;
+        default: return cudaErrorInvalidValue;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 0);
+    return cudaLaunchKernelEx(&cfg, kern, j0, j1, int(a.cols), R, t);
 }
 
 cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
@@ -373,9 +418,10 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     const int grid = j0.blocks + j1.blocks;
     if (grid == 0) return cudaSuccess;
     const int threads = (R * int(a.cols / 32) + 31) / 32 * 32;   // whole warps (xor-shuffle stages)
-    void (*kern)(HqJob, HqJob, int, int) = nullptr;
+    if (a.tab_host != nullptr) return launch_hq_tab(a, j0, j1, R, grid, threads, s);
+    void (*kern)(HqJob, HqJob, int, int, HqTab<false>) = nullptr;
     const bool delta = a.delta0 != nullptr || a.delta1 != nullptr;
-#define I4_HQ_K(KK) kern = delta ? hadamard_quant_kernel<KK, true> : hadamard_quant_kernel<KK, false>; break;
+#define I4_HQ_K(KK) kern = delta ? hadamard_quant_kernel<KK, true, false> : hadamard_quant_kernel<KK, false, false>; break;
     switch (a.k) {
         case 0: I4_HQ_K(0)
         case 1: I4_HQ_K(1)
@@ -395,8 +441,7 @@ cudaError_t launch_hadamard_quant2(const HqArgs& a, cudaStream_t s) {
     cudaLaunchAttribute attr[1];
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 0);
-    return cudaLaunchKernelEx(&cfg, kern, j0, j1, int(a.cols), R);
-    return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, kern, j0, j1, int(a.cols), R, HqTab<false>{});
 }
 
 cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols, int k, float r,
@@ -638,8 +683,7 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 
 // last CTA out returns the counters to zero for the next launch (every CTA read
 // the amax word and the arrival count before it departed)
-template <bool BAT>
-__device__ __forceinline__ void depart(uint32_t* scratch, uint32_t* bamax, int64_t nbat) {
+__device__ __forceinline__ void depart(uint32_t* scratch) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -647,8 +691,6 @@ __device__ __forceinline__ void depart(uint32_t* scratch, uint32_t* bamax, int64
             scratch[kAmaxWord] = 0u;
             scratch[kArriveWord] = 0u;
             scratch[kDepartWord] = 0u;
-            if (BAT)
-                for (int64_t b = 0; b < nbat; ++b) bamax[b] = 0u;
         }
     }
 }
@@ -716,50 +758,6 @@ __device__ __forceinline__ void split_units(const uint16_t* __restrict__ g, int6
     }
 }
 
-// Batched (attention BMM, reading Z-31): batch b = rows [b nb, (b+1) nb) has its own
-// amax word bamax[b] (so its own r8 / s_down) and its own [2 nb] norm block of a_sq.
-__device__ __forceinline__ void batch_scale(const uint32_t* bamax, int64_t b, float& r8, bool& zero) {
-    const uint32_t ab = ld_acquire_gpu(bamax + b);
-    const float amax = __uint_as_float(ab << 16);
-    zero = ab >= 0x7F80u || !(amax > 0.0f);
-    r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
-}
-
-template <int G, bool C1Z>
-__device__ __forceinline__ void split_units_bat(const uint16_t* __restrict__ g, int C, const PhiloxKeys& keys,
-                                                uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
-                                                int32_t* __restrict__ a_sq, int64_t u0, int64_t u1, uint4 (&buf)[G],
-                                                int64_t nb, const uint32_t* bamax) {
-    const int upr = C / (256 * G);
-    const uint4* src = reinterpret_cast<const uint4*>(g) + lane_id();
-    const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);
-    int shi = 0, slo = 0;
-    if (u0 >= u1) return;
-    int64_t row = u0 / upr;
-    int seg = int(u0 - row * upr);
-    int64_t b = row / nb;
-    float r8; bool zero;
-    batch_scale(bamax, b, r8, zero);
-    for (int64_t un = u0; un < u1; ++un) {
-        uint4 cur[G];
-#pragma unroll
-        for (int gi = 0; gi < G; ++gi) cur[gi] = buf[gi];
-        if (un + 1 < u1) load_unit<G>(src, un + 1, buf);
-        if (zero) {
-#pragma unroll
-            for (int gi = 0; gi < G; ++gi)
-                *reinterpret_cast<uint2*>(q8 + (un * G + gi) * 256 + lane_id() * 8) = make_uint2(0u, 0u);
-        } else {
-            split_unit<G, true, C1Z>(cur, un, r8, keys, call_id, tbase, q8, shi, slo);
-        }
-        if (++seg == upr || un + 1 == u1) {
-            flush_norms(shi, slo, a_sq + b * 2 * nb, nb, row - b * nb);
-            seg = 0; ++row;
-            if (un + 1 < u1 && row / nb != b) { b = row / nb; batch_scale(bamax, b, r8, zero); }
-        }
-    }
-}
-
 // timing experiment, compiled in only by -DI4_STAMPS=1 (tools/build_variants.sh,
 // tools/gs_stamps.py): per-CTA globaltimer stamps -- start, phase 1 done,
 // barrier passed, amax known, phase 2 done (max over warps)
@@ -774,14 +772,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// BAT: batched (N = B nb rows; per-batch amax words bamax[B], zero on entry and returned
-// to zero; s_down_out / amax_out [B]; a_sq [B][2 nb])
-template <int G, bool C1Z, bool BAT>
+template <int G, bool C1Z>
 __global__ void __launch_bounds__(kSplitThreads, I4_BS_MINB)
 grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __restrict__ scratch,
                   const PhiloxKeys keys, uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8,
                   int32_t* __restrict__ a_sq, float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out,
-                  int32_t* __restrict__ status, int64_t nb, uint32_t* __restrict__ bamax) {
+                  int32_t* __restrict__ status) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     pdl_trigger();
@@ -790,39 +786,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     if (stamp && threadIdx.x == 0) g_gs_stamp[0][blockIdx.x] = gtimer();
 
     // ---- phase 1: amax ----------------------------------------------------
-    if constexpr (BAT) {
-        // contiguous row range per warp; the running max goes to its batch's word when
-        // the batch changes (rows never straddle batches)
-        const int64_t nwarps = int64_t(gridDim.x) * (kSplitThreads / 32);
-        const int64_t wid = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
-        const int64_t r0 = N * wid / nwarps, r1 = N * (wid + 1) / nwarps;
-        const int c8 = C / 8;
-        uint32_t m = 0;
-        int64_t cb = r0 / nb;
-        auto flush = [&](int64_t b) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-            if (lane == 0) atomicMax(bamax + b, m);
-            m = 0;
-        };
-        for (int64_t row = r0; row < r1; ++row) {
-            if (row / nb != cb) { flush(cb); cb = row / nb; }
-            const uint4* g4 = reinterpret_cast<const uint4*>(g + row * C);
-            for (int i = lane; i < c8; i += 32) {
-                const uint4 u = ld_nc_v4(g4 + i);
-                m = max(m, max(max(bf16x2_absmax(u.x), bf16x2_absmax(u.y)), max(bf16x2_absmax(u.z), bf16x2_absmax(u.w))));
-            }
-        }
-        if (r0 < r1) flush(cb);
-        const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-        if (G > 0)
-            for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * N; i += stride) a_sq[i] = 0;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(scratch + kArriveWord, 1u);
-        }
-    } else {
+    {
         const uint4* g4 = reinterpret_cast<const uint4*>(g);
         const int64_t n8 = N * int64_t(C) / 8;
         const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -887,16 +851,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     const bool zero = nonfinite || !(amax > 0.0f);
     const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
     if (stamp && threadIdx.x == 0) { g_gs_stamp[3][blockIdx.x] = gtimer(); g_gs_stamp[4][blockIdx.x] = 0; }
-    if (BAT && blockIdx.x == 0) {
-        for (int64_t b = threadIdx.x; b < N / nb; b += blockDim.x) {
-            const uint32_t ab = ld_acquire_gpu(bamax + b);
-            const float am = __uint_as_float(ab << 16);
-            const bool nf = ab >= 0x7F80u, zr = nf || !(am > 0.0f);
-            s_down_out[b] = zr ? 0.0f : __fdiv_rn(am, 119.0f);
-            amax_out[b] = ab;
-            if (status != nullptr && zr) atomicOr(status, nf ? kStatusNonFinite : kStatusZeroGrad);
-        }
-    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         *s_down_out = zero ? 0.0f : __fdiv_rn(amax, 119.0f);
         *amax_out = amax_b;
         if (status != nullptr && zero) atomicOr(status, nonfinite ? kStatusNonFinite : kStatusZeroGrad);
@@ -906,12 +861,7 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
     if (blockIdx.x == gridDim.x - 1)                      // code row N: the all-zero pad row
         for (int c = threadIdx.x * 16; c < C; c += kSplitThreads * 16)
             *reinterpret_cast<uint4*>(q8 + N * C + c) = make_uint4(0, 0, 0, 0);
-    if constexpr (G > 0 && BAT) {
-        split_units_bat<G, C1Z>(g, C, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf, nb, bamax);
-        depart<BAT>(scratch, bamax, N / nb);
-        return;
-    }
-    if constexpr (G > 0 && !BAT) {
+    if constexpr (G > 0) {
         if (zero) {                                       // all-zero / non-finite grad_Y: codes 0, norms 0
             for (int64_t un = pu0; un < pu1; ++un)        // (zeroed in phase 1)
 #pragma unroll
@@ -925,11 +875,9 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
                 split_units<G, false, C1Z>(g, N, C, r8, keys, call_id, token_offset, q8, a_sq, pu0, pu1, pbuf);
         }
         if (stamp && lane == 0) atomicMax(&g_gs_stamp[4][blockIdx.x], gtimer());
-        depart<BAT>(scratch, bamax, 0);
+        depart(scratch);
         return;
     }
-    const float r8g = r8;
-    const bool zerog = zero;
     // generic path (C not a multiple of 256): one warp per row
     const int64_t warp0 = int64_t(blockIdx.x) * (kSplitThreads / 32) + warp;
     const int64_t wstride = int64_t(gridDim.x) * (kSplitThreads / 32);
@@ -939,10 +887,6 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
         int8_t* qr = q8 + row * C;
         const uint64_t tglob = uint64_t(token_offset + row);
         int shi = 0, slo = 0;
-        float r8 = r8g;
-        bool zero = zerog;
-        const int64_t bb = BAT ? row / nb : 0;
-        if (BAT) batch_scale(bamax, bb, r8, zero);
         for (int g0 = 0; g0 < nch; g0 += kBsGroup) {
             uint4 raw[kBsGroup];
 #pragma unroll
@@ -996,15 +940,14 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
         }
         if (lane == 0) {
-            const int64_t base = BAT ? bb * 2 * nb : 0, nrow = BAT ? nb : N, lr = BAT ? row - bb * nb : row;
-            a_sq[base + lr] = shi >> 8;                       // exact: every term is 256 hi^2
-            a_sq[base + nrow + lr] = slo;
+            a_sq[row] = shi >> 8;                             // exact: every term is 256 hi^2
+            a_sq[N + row] = slo;
         }
     }
-    depart<BAT>(scratch, bamax, BAT ? N / nb : 0);
+    depart(scratch);
 }
 
-template <int G, bool C1Z, bool BAT>
+template <int G, bool C1Z>
 static int grad_split_max_blocks() {
     static std::atomic<int> cached[kMaxDevices];        // per device ordinal (0 = not yet queried)
     int dev = 0;
@@ -1014,25 +957,21 @@ static int grad_split_max_blocks() {
     if (v == 0) {
         int per_sm = 0, sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z, BAT>, kSplitThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_split_kernel<G, C1Z>, kSplitThreads, 0);
         v = per_sm * sms;
         cached[dev].store(v, std::memory_order_relaxed);
     }
     return v;
 }
 
-int grad_split_max_blocks() { return grad_split_max_blocks<0, false, false>(); }
+int grad_split_max_blocks() { return grad_split_max_blocks<0, false>(); }
 
-struct SplitLaunch {
-    const uint16_t* g; int64_t N; int C; uint32_t* block_max; PhiloxKeys keys; uint32_t call_id;
-    int64_t token_offset; int8_t* q8; int32_t* a_sq; float* s_down; uint32_t* amax_out; int32_t* status;
-    int64_t nb; uint32_t* bamax;
-};
-
-template <int G, bool C1Z, bool BAT>
-static cudaError_t launch_grad_split_g(const SplitLaunch& L, cudaStream_t s) {
-    int blocks = grad_split_max_blocks<G, C1Z, BAT>();
-    const int64_t want = G > 0 ? (L.N * (L.C / (256 * G)) + 7) / 8 : (L.N + 7) / 8;   // one warp per unit at most
+template <int G, bool C1Z>
+static cudaError_t launch_grad_split_g(const uint16_t* g, int64_t N, int C, uint32_t* block_max, const PhiloxKeys& keys,
+                                       uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
+                                       float* s_down, uint32_t* amax_out, int32_t* status, cudaStream_t s) {
+    int blocks = grad_split_max_blocks<G, C1Z>();
+    const int64_t want = G > 0 ? (N * (C / (256 * G)) + 7) / 8 : (N + 7) / 8;   // one warp per unit at most
     if (want < blocks) blocks = int(want);
     if (blocks > kAmaxWord) blocks = kAmaxWord;
     cudaLaunchConfig_t cfg{};
@@ -1044,39 +983,196 @@ static cudaError_t launch_grad_split_g(const SplitLaunch& L, cudaStream_t s) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = add_pdl_attr(attr, 1);
-    auto kern = grad_split_kernel<G, C1Z, BAT>;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, L.g, L.N, L.C, L.block_max, L.keys, L.call_id, L.token_offset,
-                                       L.q8, L.a_sq, L.s_down, L.amax_out, L.status, L.nb, L.bamax);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id,
+                                       token_offset, q8, a_sq, s_down, amax_out, status);
     if (e != cudaSuccess && cfg.numAttrs == 2) {       // cooperative + PDL refused: plain cooperative
         (void)cudaGetLastError();
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, L.g, L.N, L.C, L.block_max, L.keys, L.call_id, L.token_offset, L.q8,
-                               L.a_sq, L.s_down, L.amax_out, L.status, L.nb, L.bamax);
+        e = cudaLaunchKernelEx(&cfg, grad_split_kernel<G, C1Z>, g, N, C, block_max, keys, call_id, token_offset,
+                               q8, a_sq, s_down, amax_out, status);
     }
     return e;
 }
 
 template <int G>
-static cudaError_t launch_grad_split_c(const SplitLaunch& L, cudaStream_t s) {
+static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint32_t* block_max,
+                                       const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* q8,
+                                       int32_t* a_sq, float* s_down, uint32_t* amax_out, int32_t* status,
+                                       cudaStream_t s) {
     // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
-    const bool c1z = (uint64_t(L.token_offset) + uint64_t(L.N)) * uint64_t(L.C) <= (uint64_t(1) << 34);
-    if (L.bamax != nullptr)
-        return c1z ? launch_grad_split_g<G, true, true>(L, s) : launch_grad_split_g<G, false, true>(L, s);
-    return c1z ? launch_grad_split_g<G, true, false>(L, s) : launch_grad_split_g<G, false, false>(L, s);
+    const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
+    if (c1z)
+        return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
+                                            amax_out, status, s);
+    return launch_grad_split_g<G, false>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
+                                         amax_out, status, s);
 }
 
 cudaError_t launch_grad_split(const uint16_t* g, int64_t N, int64_t C, uint32_t* block_max, uint64_t seed,
                               uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq, float* s_down,
-                              uint32_t* amax_out, int32_t* status, cudaStream_t s, int64_t nb, uint32_t* bamax) {
+                              uint32_t* amax_out, int32_t* status, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
-    const SplitLaunch L{g, N, int(C), block_max, philox_keys(uint32_t(seed), uint32_t(seed >> 32)), call_id,
-                        token_offset, q8, a_sq, s_down, amax_out, status, bamax ? nb : N, bamax};
+    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
+    const int Ci = int(C);
+#define I4_GS(GG) launch_grad_split_c<GG>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out, status, s)
     // unit size: 2 chunks when C allows (no register spills at 3 CTAs / SM; 4 and 3
     // measured equal or slower), else 3, 1; the one-warp-per-row loop otherwise
-    if (kBsGMax >= 2 && C % 512 == 0) return launch_grad_split_c<2>(L, s);
-    if (kBsGMax >= 3 && C % 768 == 0) return launch_grad_split_c<3>(L, s);
-    if (C % 256 == 0) return launch_grad_split_c<1>(L, s);
-    return launch_grad_split_c<0>(L, s);
+    if (kBsGMax >= 2 && C % 512 == 0) return I4_GS(2);
+    if (kBsGMax >= 3 && C % 768 == 0) return I4_GS(3);
+    if (C % 256 == 0) return I4_GS(1);
+#undef I4_GS
+    return launch_grad_split_c<0>(g, N, Ci, block_max, keys, call_id, token_offset, q8, a_sq, s_down, amax_out,
+                                  status, s);
+}
+
+// ---------------------------------------------------------------------------
+// Batched grad_split (attention BMM, reading Z-31): rows [b nb, (b+1) nb) are batch b,
+// with its own amax, s_down and [2 nb] norm block.  Two launches and no grid-wide
+// barrier (a cooperative barrier and one cluster per batch both measured slower on the
+// BMM shapes: the SR pass needs every SM and many warps, the batches are small):
+//   batch_amax_kernel   warp w takes R consecutive rows; its running max goes to the
+//                       batch's word by atomicMax when the batch changes (the words are
+//                       zero on entry: the sampler launch of the previous call zeroes them)
+//   batch_split_kernel  warp per row: r8 of the row's batch, Philox SR codes, half-row
+//                       norms stored directly; CTA 0 writes s_down[b] / amax[b] / status
+constexpr int kBatchSplitKB = 4;                 // 256-column chunks per lane in flight
+
+__global__ void __launch_bounds__(256)
+batch_amax_kernel(const uint16_t* __restrict__ g, int64_t rows, int C, int64_t nb, int R,
+                  uint32_t* __restrict__ bamax) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = lane_id();
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r0 = w * R, r1 = min(rows, r0 + R);
+    if (r0 >= rows) return;
+    const int c8 = C / 8;
+    uint32_t m = 0;
+    int64_t cb = r0 / nb;
+    auto flush = [&](int64_t b) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (lane == 0) atomicMax(bamax + b, m);
+        m = 0;
+    };
+    for (int64_t row = r0; row < r1; ++row) {
+        if (row / nb != cb) { flush(cb); cb = row / nb; }
+        const uint4* g4 = reinterpret_cast<const uint4*>(g + row * C);
+        for (int i0 = lane; i0 < c8; i0 += 32 * kBatchSplitKB) {
+            uint4 u[kBatchSplitKB];
+#pragma unroll
+            for (int q = 0; q < kBatchSplitKB; ++q)
+                u[q] = i0 + 32 * q < c8 ? ld_nc_v4(g4 + i0 + 32 * q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int q = 0; q < kBatchSplitKB; ++q)
+                m = max(m, max(max(bf16x2_absmax(u[q].x), bf16x2_absmax(u[q].y)),
+                               max(bf16x2_absmax(u[q].z), bf16x2_absmax(u[q].w))));
+        }
+    }
+    flush(cb);
+}
+
+template <bool C1Z>
+__global__ void __launch_bounds__(256)
+batch_split_kernel(const uint16_t* __restrict__ g, int64_t rows, int C, int64_t nb, const PhiloxKeys keys,
+                   uint32_t call_id, int64_t token_offset, int8_t* __restrict__ q8, int32_t* __restrict__ a_sq,
+                   float* __restrict__ s_down_out, uint32_t* __restrict__ amax_out, int32_t* __restrict__ status,
+                   const uint32_t* __restrict__ bamax) {
+    pdl_trigger();
+    pdl_wait();                                   // the batch amax words
+    const int lane = lane_id();
+    if (blockIdx.x == 0)
+        for (int64_t b = threadIdx.x; b < rows / nb; b += blockDim.x) {
+            const uint32_t ab = bamax[b];
+            const float am = __uint_as_float(ab << 16);
+            const bool nf = ab >= 0x7F80u, zr = nf || !(am > 0.0f);
+            s_down_out[b] = zr ? 0.0f : __fdiv_rn(am, 119.0f);
+            amax_out[b] = ab;
+            if (status != nullptr && zr) atomicOr(status, nf ? kStatusNonFinite : kStatusZeroGrad);
+        }
+    if (blockIdx.x == gridDim.x - 1)               // code row B nb: the all-zero pad row
+        for (int c = threadIdx.x * 16; c < C; c += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(q8 + rows * C + c) = make_uint4(0, 0, 0, 0);
+    const uint64_t tbase = uint64_t(token_offset) * uint64_t(C);
+    const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < rows; row += nwarps) {
+        const int64_t b = row / nb;
+        const uint32_t ab = bamax[b];
+        const float amax = __uint_as_float(ab << 16);
+        const bool zero = ab >= 0x7F80u || !(amax > 0.0f);
+        const float r8 = zero ? 0.0f : __fdiv_rn(119.0f, amax);
+        int shi = 0, slo = 0;
+        for (int c0 = 0; c0 < C; c0 += 256 * kBatchSplitKB) {
+            uint4 u[kBatchSplitKB];
+#pragma unroll
+            for (int q = 0; q < kBatchSplitKB; ++q) {
+                const int col = c0 + 256 * q + lane * 8;
+                u[q] = col < C ? ld_nc_v4(g + row * C + col) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < kBatchSplitKB; ++q) {
+                const int col = c0 + 256 * q + lane * 8;
+                if (col >= C) break;
+                const int64_t flat = row * C + col;
+                uint2 pq = make_uint2(0u, 0u);
+                if (!zero) {
+                    Philox4 p0, p1;
+                    sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
+                    split_chunk8<true>(u[q], p0, p1, r8, pq, shi, slo);
+                }
+                *reinterpret_cast<uint2*>(q8 + flat) = pq;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            shi += __shfl_xor_sync(0xFFFFFFFFu, shi, o);
+            slo += __shfl_xor_sync(0xFFFFFFFFu, slo, o);
+        }
+        if (lane == 0) {
+            const int64_t lr = row - b * nb;
+            a_sq[b * 2 * nb + lr] = shi >> 8;                          // exact: every term is 256 hi^2
+            a_sq[b * 2 * nb + nb + lr] = slo;
+        }
+    }
+}
+
+cudaError_t launch_grad_split_batched(const uint16_t* g, int64_t rows, int64_t C, int64_t nb, uint64_t seed,
+                                      uint32_t call_id, int64_t token_offset, int8_t* q8, int32_t* a_sq,
+                                      float* s_down, uint32_t* amax_out, int32_t* status, uint32_t* bamax,
+                                      cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    static std::atomic<int> sms_cache[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    int sms = sms_cache[dev].load(std::memory_order_relaxed);
+    if (sms == 0) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_cache[dev].store(sms, std::memory_order_relaxed);
+    }
+    // amax: R consecutive rows per warp, about 32 warps per SM
+    const int64_t target_warps = int64_t(sms) * 32;
+    const int R = int(std::max<int64_t>(1, (rows + target_warps - 1) / target_warps));
+    const int64_t warps_a = (rows + R - 1) / R;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((warps_a + 7) / 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = add_pdl_attr(attr, 0);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, batch_amax_kernel, g, rows, int(C), nb, R, bamax);
+    if (e != cudaSuccess) return e;
+    // split: one warp per row (grid-stride beyond 16 warps per SM)
+    const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(sms) * 8);
+    cfg.gridDim = dim3(unsigned(blocks));
+    const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
+    const bool c1z = (uint64_t(token_offset) + uint64_t(rows)) * uint64_t(C) <= (uint64_t(1) << 34);
+    if (c1z)
+        return cudaLaunchKernelEx(&cfg, batch_split_kernel<true>, g, rows, int(C), nb, keys, call_id, token_offset,
+                                  q8, a_sq, s_down, amax_out, status, static_cast<const uint32_t*>(bamax));
+    return cudaLaunchKernelEx(&cfg, batch_split_kernel<false>, g, rows, int(C), nb, keys, call_id, token_offset, q8,
+                              a_sq, s_down, amax_out, status, static_cast<const uint32_t*>(bamax));
 }
 
 // debug export for the timing experiment: copies the stamps of the last launch

@@ -145,13 +145,14 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
     c = warp_sum_u32(c);
     if (lane == 0) { sm.warp_w[warp] = w; sm.warp_c[warp] = c; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t bw = 0; uint32_t bc = 0;
-        for (int i = 0; i < int(blockDim.x) / 32; ++i) { bw += sm.warp_w[i]; bc += sm.warp_c[i]; }
+    if (warp == 0) {                              // CTA sum by warp 0 (integer sums: exact, any order)
+        const bool in = lane < int(blockDim.x) / 32;
+        uint64_t bw = warp_sum_u64(in ? sm.warp_w[lane] : 0ull);
+        uint32_t bc = warp_sum_u32(in ? sm.warp_c[lane] : 0u);
         const unsigned me = cl.rank();
-        for (int r = 0; r < CL; ++r) {
-            uint64_t* rw = cl.map(&sm.red_w[parity][me], r);
-            uint32_t* rc = cl.map(&sm.red_c[parity][me], r);
+        if (lane < CL) {                          // lane r writes CTA r's slot
+            uint64_t* rw = cl.map(&sm.red_w[parity][me], lane);
+            uint32_t* rc = cl.map(&sm.red_c[parity][me], lane);
             *rw = bw; *rc = bc;
         }
     }
@@ -194,7 +195,8 @@ __global__ void __launch_bounds__(NT, 1)
 lss_sampler_kernel(SamplerArgs a) {
     pdl_trigger();
     pdl_wait();                                   // a_sq / s_down of grad_split
-    const bool st_on = kSmpStamps && g_smp_stamp_on && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
+    const bool st_on = kSmpStamps && g_smp_stamp_on && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 &&
+                       blockIdx.z == 0;
     int st_n = 0;
     smp_stamp(st_n, st_on);
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -483,7 +485,10 @@ cudaError_t launch_lss_sampler(const SamplerArgs& a, cudaStream_t s) {
     // an 8-CTA cluster per mask: the A.2 rounds are dominated by the per-item
     // work, which the cluster spreads over 8 SMs (a single CTA measured 6x slower
     // on binding budgets); tiny problems use one CTA
-    if (2 * int64_t(a.N) <= 2048) return launch_cl<1, 1024>(a, s);
+    // tiny problems (attention BMM batches): one CTA, fewer threads the fewer the items
+    // (a barrier of 8 warps is cheaper than one of 32; 4 items per thread at most)
+    if (2 * int64_t(a.N) <= 1024) return launch_cl<1, 256>(a, s);
+    if (2 * int64_t(a.N) <= 2048) return launch_cl<1, 512>(a, s);
     if (2 * int64_t(a.N) <= int64_t(kClusterCTAs) * kSmallItemsPerCTA) return launch_cl<kClusterCTAs, 512>(a, s);
     // > 8 K items per CTA: a 16-CTA (non-portable) cluster halves each CTA's share
     // (ViT sizes 22.6 -> 15.5 us), when two of them (one per mask) fit on the device
