@@ -302,6 +302,10 @@ __attribute__((visibility("default"))) int32_t int4_debug_sampler_stamps(unsigne
     return i4::sampler_stamps(host, enable);
 }
 
+__attribute__((visibility("default"))) int32_t int4_debug_gemm_stamps(unsigned long long* host) {
+    return i4::gemm_stamps(host);
+}
+
 int32_t int4_sampler_cluster_ctas(int64_t N) { return i4::sampler_cluster_ctas(N); }
 
 int32_t int4_set_pdl(int32_t enable) {

@@ -159,14 +159,21 @@ struct ProbSize { int M, K, m_tiles, n_tiles, T, nk; int form, mtd, nkd; };
 template <int EPI, int BMP, int BN>
 __device__ __forceinline__ ProbSize prob_size(const GemmArgs& g) {
     ProbSize s{};
-    s.form = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr ? __ldg(g.dense_flag) : 0;
+    // every word the size may depend on is loaded up front (independent loads: one
+    // L2 round trip after the PDL wait instead of a dependent chain)
+    const int f = (EPI == EPI_DGRAD || EPI == EPI_WGRAD) && g.dense_flag != nullptr ? __ldg(g.dense_flag) : 0;
+    const int md = g.m_dev != nullptr ? __ldg(g.m_dev) : g.M;
+    const int md2 = EPI == EPI_DGRAD && g.m_dev2 != nullptr ? __ldg(g.m_dev2) : 0;
+    const int kd = g.k_dev != nullptr ? __ldg(g.k_dev) : 0;
+    const int kd2 = EPI == EPI_WGRAD && g.k_dev2 != nullptr ? __ldg(g.k_dev2) : 0;
+    s.form = f;
     const int tok_kb = (g.n_tokens + kBK - 1) / kBK;
     if (EPI == EPI_DGRAD && s.form == 1) s.M = g.n_tokens;
-    else if (EPI == EPI_DGRAD && s.form == 2) { s.mtd = (g.n_tokens + BMP - 1) / BMP; s.M = s.mtd * BMP + __ldg(g.m_dev2); }
-    else s.M = g.m_dev ? __ldg(g.m_dev) : g.M;
+    else if (EPI == EPI_DGRAD && s.form == 2) { s.mtd = (g.n_tokens + BMP - 1) / BMP; s.M = s.mtd * BMP + md2; }
+    else s.M = md;
     if (EPI == EPI_WGRAD && s.form == 1) s.K = tok_kb * kBK;
-    else if (EPI == EPI_WGRAD && s.form == 2) { s.nkd = tok_kb; s.K = (tok_kb + (__ldg(g.k_dev2) + kBK - 1) / kBK) * kBK; }
-    else s.K = g.k_dev ? ((__ldg(g.k_dev) + kBK - 1) / kBK) * kBK : g.K;
+    else if (EPI == EPI_WGRAD && s.form == 2) { s.nkd = tok_kb; s.K = (tok_kb + (kd2 + kBK - 1) / kBK) * kBK; }
+    else s.K = g.k_dev != nullptr ? ((kd + kBK - 1) / kBK) * kBK : g.K;
     s.m_tiles = (s.M + BMP - 1) / BMP;
     s.n_tiles = (g.Nn + BN - 1) / BN;
     s.T = s.m_tiles * s.n_tiles;
@@ -188,9 +195,11 @@ struct Sched {
     int qx, qy;                    // base short quota of those pairs / of the others
     int R;                         // short tiles left after the base quotas (>= 0 here)
     bool y_first;                  // the extra short tiles go to pairs r1.. first
+    int my_nl, my_ns, my_start;    // this pair's long tiles, short quota, first short tile
     // E0, E1: a tile's cost floor in k-blocks (its epilogue time: a short-K grad_X tile
-    // is epilogue-bound), so tile p's weight is max(k-blocks, E)
-    __device__ void init(int P_, int T0_, int L0_, int T1_, int L1_, int E0, int E1) {
+    // is epilogue-bound), so tile p's weight is max(k-blocks, E).  32-bit arithmetic (every
+    // quantity is below 2^31): this runs between the PDL wait and the first TMA load.
+    __device__ void init(int P_, int T0_, int L0_, int T1_, int L1_, int E0, int E1, int p) {
         P = P_; T0 = T0_; L0 = L0_; T1 = T1_; L1 = L1_;
         two = kBalance && T1 > 0 && T0 > 0 && L0 > 0 && L1 > 0;
         if (!two) return;
@@ -198,25 +207,29 @@ struct Sched {
         long_prob = w1 >= w0 ? 1 : 0;
         TL = long_prob ? T1 : T0; LL = long_prob ? w1 : w0;
         TS = long_prob ? T0 : T1; LS = long_prob ? w0 : w1;
-        const int64_t W = int64_t(TL) * LL + int64_t(TS) * LS;
-        const int64_t tau = (W + P - 1) / P;
-        r1 = TL % P;
-        const int64_t lx = int64_t(TL / P + 1) * LL, ly = int64_t(TL / P) * LL;
-        qx = tau > lx ? int((tau - lx) / LS) : 0;
-        qy = tau > ly ? int((tau - ly) / LS) : 0;
-        int64_t base = int64_t(r1) * qx + int64_t(P - r1) * qy;
+        const int W = TL * LL + TS * LS;
+        const int tau = (W + P - 1) / P;
+        const int tlp = TL / P;
+        r1 = TL - tlp * P;
+        const int lx = (tlp + 1) * LL, ly = tlp * LL;
+        qx = tau > lx ? (tau - lx) / LS : 0;
+        qy = tau > ly ? (tau - ly) / LS : 0;
+        int base = r1 * qx + (P - r1) * qy;
         // never more short tiles than there are: trim the base quotas (pairs with long
         // tiles first) -- only possible through the rounding of tau
         while (base > TS) {
-            if (qx > 0 && r1 > 0 && lx + int64_t(qx) * LS >= ly + int64_t(qy) * LS) { --qx; base -= r1; }
+            if (qx > 0 && r1 > 0 && lx + qx * LS >= ly + qy * LS) { --qx; base -= r1; }
             else if (qy > 0) { --qy; base -= P - r1; }
             else { --qx; base -= r1; }
         }
-        R = int(TS - base);
-        const int64_t slack_x = tau - lx - int64_t(qx) * LS, slack_y = tau - ly - int64_t(qy) * LS;
+        R = TS - base;
+        const int slack_x = tau - lx - qx * LS, slack_y = tau - ly - qy * LS;
         y_first = r1 == 0 || slack_y >= slack_x;
+        my_nl = tlp + (p < r1 ? 1 : 0);
+        const int rp = R / P, rm = R - rp * P;
+        my_ns = (p < r1 ? qx : qy) + rp + (extra(p, rm) ? 1 : 0);
+        my_start = min(p, r1) * qx + max(0, p - r1) * qy + p * rp + n_extra_before(p, rm);
     }
-    __device__ int nlong(int p) const { return TL / P + (p < r1 ? 1 : 0); }
     // number of pairs r < p whose priority rank is below m (the first m of the order
     // get one extra short tile)
     __device__ int n_extra_before(int p, int m) const {
@@ -230,10 +243,6 @@ struct Sched {
     __device__ bool extra(int p, int m) const {
         const int rank = y_first ? (p >= r1 ? p - r1 : (P - r1) + p) : p;
         return rank < m;
-    }
-    __device__ int quota(int p) const { return (p < r1 ? qx : qy) + R / P + (extra(p, R % P) ? 1 : 0); }
-    __device__ int start(int p) const {
-        return min(p, r1) * qx + max(0, p - r1) * qy + p * (R / P) + n_extra_before(p, R % P);
     }
 };
 
@@ -252,7 +261,7 @@ __device__ __forceinline__ Seg seg_at(const Sched& s, int p, int j) {
         r.prob = t < s.T0 ? 0 : 1;
         r.tile = t < s.T0 ? t : t - s.T0;
     } else {
-        const int nl = s.nlong(p), ns = s.quota(p);
+        const int nl = s.my_nl, ns = s.my_ns;             // p is the pair Sched::init was given
         if (kShortFirst ? j >= ns : j < nl) {          // a long tile
             const int jl = kShortFirst ? j - ns : j;
             if (jl >= nl) return r;
@@ -262,12 +271,39 @@ __device__ __forceinline__ Seg seg_at(const Sched& s, int p, int j) {
             const int js = kShortFirst ? j : j - nl;
             if (js >= ns) return r;
             r.prob = 1 - s.long_prob;
-            r.tile = s.start(p) + js;
+            r.tile = s.my_start + js;
         }
     }
     r.nk = r.prob == 0 ? s.L0 : s.L1;
     r.valid = true;
     return r;
+}
+
+// timing experiment, compiled in only by -DI4_STAMPS=1 (tools/gemm_stamps.py): globaltimer
+// stamps of CTA 0 -- [0] entry [1] setup done [2] PDL wait done [3] first TMA issued [4] first
+// stage full (MMA) [5] last MMA committed [6] first accumulator ready (epilogue warp 2)
+// [7] epilogue done [8] exit; [9] earliest CTA entry, [10] latest CTA exit (all CTAs)
+#ifndef I4_STAMPS
+#define I4_STAMPS 0
+#endif
+constexpr bool kGemmStamps = I4_STAMPS != 0;
+__device__ unsigned long long g_gemm_stamp[16];
+__device__ __forceinline__ void gstamp(int i, bool on) {
+    if (kGemmStamps && on) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        if (i == 9) atomicMin(&g_gemm_stamp[9], t);
+        else if (i == 10) atomicMax(&g_gemm_stamp[10], t);
+        else g_gemm_stamp[i] = t;
+    }
+}
+
+int gemm_stamps(unsigned long long* host) {
+    if (!kGemmStamps) return -1;
+    if (cudaMemcpyFromSymbol(host, g_gemm_stamp, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    unsigned long long init[16] = {};
+    init[9] = ~0ull;
+    return cudaMemcpyToSymbol(g_gemm_stamp, init, sizeof(init)) == cudaSuccess ? 0 : -1;
 }
 
 // ---------------------------------------------------------------------------- kernel
@@ -309,6 +345,9 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int pair0 = int(blockIdx.x) / CG, n_pairs = int(gridDim.x) / CG;
+    const bool st0 = blockIdx.x == 0;
+    gstamp(0, st0 && threadIdx.x == 0);
+    gstamp(9, threadIdx.x == 0);
 
     if (warp == 0 && lane == 0) {
 #pragma unroll
@@ -322,16 +361,19 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    gstamp(1, st0 && threadIdx.x == 0);
     pdl_trigger();
     pdl_wait();                                  // operands / metadata of the previous kernels
+    gstamp(2, st0 && threadIdx.x == 0);
 
     // problem sizes (possibly data-dependent, so read after the PDL wait) and the schedule
     const ProbSize s0 = prob_size<EPI0, BMP, BN>(g);
     ProbSize s1{};
     if constexpr (kBwd) s1 = prob_size<EPI_WGRAD, BMP, BN>(g1);
+    gstamp(11, st0 && threadIdx.x == 0 && (s0.M + s1.M) >= 0);
     Sched sc;
     if constexpr (!BAT)
-        sc.init(n_pairs, s0.T, s0.nk, kBwd ? s1.T : 0, kBwd ? s1.nk : 0, I4_EPI_KB_DGRAD, I4_EPI_KB_WGRAD);
+        sc.init(n_pairs, s0.T, s0.nk, kBwd ? s1.T : 0, kBwd ? s1.nk : 0, I4_EPI_KB_DGRAD, I4_EPI_KB_WGRAD, pair0);
     if constexpr (BAT && kBwd) {
         // tile table: batch b has ceil(M_b / 256) grad_X m-tiles (M_b = its kept items, from
         // the sampler) and a fixed number of grad_W tiles; prefix over the batches by warp 0
@@ -397,6 +439,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
         return ps;
     };
 #define SEG(j) seg(j)
+    gstamp(12, st0 && threadIdx.x == 0);
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer (warp 0)
@@ -404,6 +447,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
         for (int j = 0;; ++j) {
             const Seg sg = SEG(j);
             if (!sg.valid) break;
+            gstamp(13, st0 && lane == 0 && j == 0);
             const bool p1 = kBwd && sg.prob == 1;
             const ProbSize ps = psz(sg);
             const bool a_mn = kBwd ? p1 : A_MN;
@@ -466,6 +510,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                     }
                 }
                 __syncwarp();
+                gstamp(3, st0 && lane == 0 && j == 0 && kb == 0);
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
@@ -490,6 +535,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                 for (int kb = 0; kb < sg.nk; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    gstamp(4, st0 && j == 0 && kb == 0);
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
                     const uint64_t adesc = a_mn ? sdesc_mnmajor_sw128(a_addr, 128 * kBK) : sdesc_kmajor_sw128(a_addr);
@@ -504,6 +550,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 if constexpr (CG == 2) umma_commit_2sm(&tfull[as]); else umma_commit(&tfull[as]);
+                gstamp(5, st0);
             }
         }
     } else {
@@ -637,6 +684,7 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             if (BAT && dg) out_row += int64_t(sg.b) * g.n_tokens;      // global grad_X row of the batch
             mbar_wait(&tfull[as], ap);
             tc_fence_after();
+            gstamp(6, st0 && warp == 2 && lane == 0 && j == 0);
             const uint32_t t_row = tmem_base + (uint32_t(lg * 32) << 16) + uint32_t(as * BN);
 
             constexpr int CW = Epi::CW;
@@ -860,7 +908,9 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
             for (int o = 16; o > 0; o >>= 1) lsq_acc[1] += __shfl_xor_sync(0xFFFFFFFFu, lsq_acc[1], o);
             if (lane == 0) g1.lsq_part[int(blockIdx.x) * kMaxEpiWarps + ew] = lsq_acc[1];
         }
-        bulk_wait<0>();                                // every lane: its own copies are done
+        bulk_wait_read<0>();                           // every lane: its staging buffers were read (the
+                                                       // global writes complete with the grid)
+        gstamp(7, st0 && warp == 2 && lane == 0);
         if ((EPI0 == EPI_WGRAD && g.out_mc != nullptr) || (kBwd && g1.out_mc != nullptr))
             __threadfence_system();                    // multimem reductions performed before the kernel ends
         __syncwarp();
@@ -870,6 +920,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     if (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     if (warp == 1) tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
+    gstamp(8, st0 && threadIdx.x == 0);
+    gstamp(10, threadIdx.x == 0);
 }
 
 int gemm_block_n(int Nn, bool b_mn) {

@@ -171,6 +171,7 @@ struct GemmMaps { const void* a; const void* b; const void* c; const void* a2; c
 cudaError_t launch_gemm(const GemmMaps& m, const GemmArgs& g, int num_sms, cudaStream_t s,
                         const GemmArgs* g1 = nullptr);
 int gemm_block_n(int Nn, bool b_mn);
+int gemm_stamps(unsigned long long* host);     // timing experiment (-DI4_STAMPS=1 builds): [16] u64, resets
 
 // lsq.cu ----------------------------------------------------------------------
 constexpr int kLsqPartials = 2048;        // fp64 partial slots per GEMM (>= max grid x 8 warps)
