@@ -598,6 +598,9 @@ def run_ours(args):
     if rank == 0 and not args.no_per_linear and args.config == DEFAULT_CONFIG:
         per_linear = {cfg: {g: time_single(cfg, g, args, dev, flush) for g in ("sparse", "dense")}
                       for cfg in PER_LINEAR}
+    attention_bmm = None
+    if rank == 0 and not args.no_per_linear and args.config == DEFAULT_CONFIG:
+        attention_bmm = {f"B{b}_N{n}_P{p}_M{m}": time_bmm(b, n, p, m, 5, args, dev, flush) for b, n, p, m in BMM_SHAPES}
 
     e2e = None if args.no_e2e else run_e2e(st, args, dev, world, ops, flush)
 
@@ -627,6 +630,7 @@ def run_ours(args):
                 "gpu_launches": sum(n_launch.values()) * args.steps,
                 "clocks": clocks.summary(), "e2e": e2e, "parity_gate": gate, "status_word": status_word,
                 "per_linear": per_linear,
+                "attention_bmm": attention_bmm,
                 "allreduce": (("grad_W reduced inside the grad_W GEMM epilogue into NVLS multicast buffers "
                                "(multimem.red.add; symmetric-memory barrier at the step's end)") if nvls else
                               ("per layer grad_W bucket (fp32), async on NCCL's stream after the layer's backward "
@@ -949,6 +953,62 @@ def time_single(config, grad, args, dev, flush):
     return {"int4_us": out["int4"], "bf16_cublas_us": out["bf16"], "speedup": out["bf16"] / out["int4"],
             "eff_tops": 6.0 * N * C * D / (out["int4"] * 1e-6) / 1e12,
             "kept": {"grad_W": kw, "grad_X": kx, "budget": N}, "dense_masks": {"grad_W": dense[0], "grad_X": dense[1]}}
+
+
+# attention BMM shapes (A.1; BERT-base heads: 12 heads x 512 tokens x 64, and 48 x 128)
+BMM_SHAPES = [(12, 512, 512, 64), (48, 128, 128, 64)]
+
+
+def time_bmm(B, N, P, M, k, args, dev, flush):
+    """T = BMM(Q, K^T) fwd + bwd (A.1, batched inside the kernels: 7 launches) and cuBLAS
+    BF16 torch.bmm (T = Q K^T, dQ = dT K, dK = dT^T Q) beside it; graphs, flushed L2."""
+    import torch
+
+    import paper_2306_11987_b200 as i4
+
+    def up(a):
+        return torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).to(dev)
+
+    q = up(np.stack([synth.activations(N, M, seed=b) for b in range(B)]))
+    kk = up(np.stack([synth.activations(P, M, seed=100 + b) for b in range(B)]))
+    dt = up(np.stack([synth.grad_output(N, P, seed=200 + b, dense=(b % 2 == 0)) for b in range(B)]))
+    s_q = np.array([float(i4.cold_start_step(q[b])) for b in range(B)], np.float32)
+    s_k = np.array([float(i4.cold_start_step(kk[b])) for b in range(B)], np.float32)
+    op = i4.Int4BMM(B, N, P, M, k, device=dev)
+    T = torch.empty(B, N, P, dtype=torch.bfloat16, device=dev)
+    dQ = torch.empty(B, N, M, dtype=torch.bfloat16, device=dev)
+    dK = torch.empty(B, P, M, dtype=torch.float32, device=dev)
+    Tb, dQb, dKb = torch.empty_like(T), torch.empty_like(dQ), torch.empty(B, P, M, dtype=torch.bfloat16, device=dev)
+
+    def body():
+        op.forward(q, kk, s_q, s_k, T)
+        op.backward(dt, dQ, dK, synth.PHILOX_SEED, call_id=1, mode=MODES[args.mode])
+
+    def bf_body():
+        torch.bmm(q, kk.transpose(1, 2), out=Tb)
+        torch.bmm(dt, kk, out=dQb)
+        torch.bmm(dt.transpose(1, 2), q, out=dKb)
+
+    out = {}
+    for nm, fn in (("int4", body), ("bf16", bf_body)):
+        fn()
+        torch.cuda.synchronize()
+        g = capture(fn)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for it in range(3 + max(10, args.steps)):
+            flush()
+            torch.cuda.synchronize()
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            if it >= 3:
+                ts.append(a.elapsed_time(b) * 1e3)
+        out[nm] = statistics.mean(ts)
+    return {"int4_us": out["int4"], "bf16_cublas_us": out["bf16"], "speedup": out["bf16"] / out["int4"],
+            "eff_tops": 6.0 * B * N * P * M / (out["int4"] * 1e-6) / 1e12, "launches_per_step": 7,
+            "status_word": op.status()}
 
 
 def run_e2e(st, args, dev, world, ops, flush):

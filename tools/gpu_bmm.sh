@@ -1,5 +1,5 @@
 #!/bin/bash
-# batched BMM: parity, bench, regression suite
+# batched attention BMM: parity tests, bench_bmm lines, the whole GPU suite, the default bench (run under gpurun)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_bmm.py -x -q 2>&1 | tail -30 > gpurun_out/bmm_tests.log
 for cfg in "12 512 512 64 5" "48 128 128 64 5"; do

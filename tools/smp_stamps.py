@@ -7,11 +7,12 @@ import synth
 from oracle.lsq_grad import cold_start_step  # tools only (test infrastructure)
 import paper_2306_11987_b200 as i4
 
-for name in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
+for arg in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
+    name, _, kind = arg.partition(":")
     cfg = synth.CONFIGS[name]
     N, D, C, k = cfg["N"], cfg["D"], cfg["C"], cfg["k"]
     up = lambda a: torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).cuda()
-    X, W, G = up(synth.activations(N, D)), up(synth.weights(C, D)), up(synth.grad_output(N, C))
+    X, W, G = up(synth.activations(N, D)), up(synth.weights(C, D)), up(synth.grad_output(N, C, dense=(kind == "dense")))
     s_x, s_w = cold_start_step(synth.activations(N, D)), cold_start_step(synth.weights(C, D))
     L = i4.Int4Linear(N, D, C, k)
     Y = torch.empty(N, C, dtype=torch.bfloat16, device="cuda")
@@ -32,4 +33,4 @@ for name in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
         n = int(a[31])
         res.append(np.diff(a[:n]) / 1e3)
     i4.lib.int4_debug_sampler_stamps(None, 0)
-    print(name, "stamps", n, "intervals us:", np.round(np.median(np.array(res[2:]), 0), 2))
+    print(arg, "stamps", n, "intervals us:", np.round(np.median(np.array(res[2:]), 0), 2))
