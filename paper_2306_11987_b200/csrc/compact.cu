@@ -79,8 +79,9 @@ __device__ __forceinline__ void zero_row(void* base, int64_t row, int n, bool bf
 }
 
 __global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
-    pdl_trigger();
     pdl_wait();                                               // counts / lists of the sampler
+    pdl_trigger();                                            // after the wait: the backward GEMM reads the
+                                                              // sampler's sizes before its own PDL wait
     if (a.batch > 1) {                                        // this CTA's batch: its slices
         const int64_t b = blockIdx.y, N = a.N, kcap = (2 * N + 127) / 128 * 128;
         a.q8 += b * N * a.C; a.xq += b * N * a.D;

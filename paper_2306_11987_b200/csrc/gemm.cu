@@ -363,10 +363,13 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     const uint32_t tmem_base = *tmem_slot;
     gstamp(1, st0 && threadIdx.x == 0);
     pdl_trigger();
-    pdl_wait();                                  // operands / metadata of the previous kernels
-    gstamp(2, st0 && threadIdx.x == 0);
 
-    // problem sizes (possibly data-dependent, so read after the PDL wait) and the schedule
+    // Problem sizes and the schedule, BEFORE the PDL wait: the only device-resident sizes
+    // (kept counts, operand forms) are the sampler's, two launches back, and the backward
+    // GEMM's predecessor (compact_kernel) signals its dependents only after its own PDL
+    // wait, i.e. after the sampler grid completed -- so they are final when this grid
+    // starts, and their L2 round trip overlaps compact instead of delaying the first TMA.
+    // Everything compact writes (the gathered operands, zeroed rows) is read after the wait.
     const ProbSize s0 = prob_size<EPI0, BMP, BN>(g);
     ProbSize s1{};
     if constexpr (kBwd) s1 = prob_size<EPI_WGRAD, BMP, BN>(g1);
@@ -440,6 +443,8 @@ gemm_i8_kernel(const __grid_constant__ GemmMapSet maps, const GemmArgs g, const 
     };
 #define SEG(j) seg(j)
     gstamp(12, st0 && threadIdx.x == 0);
+    pdl_wait();                                  // operands of the previous kernels
+    gstamp(2, st0 && threadIdx.x == 0);
 
     if (warp == 0) {
         // ------------------------------------------------------------- producer (warp 0)

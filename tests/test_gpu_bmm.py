@@ -166,3 +166,29 @@ def test_bmm_bad_shape():
     with pytest.raises(p().I4Error):
         op.forward(to_bf16_cuda(synth.activations(64, 64)[None]), to_bf16_cuda(synth.activations(96, 64)[None]),
                    np.ones(1, np.float32), np.ones(1, np.float32), T)
+
+
+@pytest.mark.parametrize("B", [200, 2100])
+def test_bmm_many_batches_sampled(B):
+    """B > 128 (the step table needs its own launch) and B > 2048 (the backward runs in
+    chunks of 2048 batches with token offsets b0 N): every batch's T, dQ, dK against the
+    oracle on a sample of batches spread over the chunks."""
+    N, P, M, k = 64, 64, 64, 3
+    q, kk, dt, s_q, s_k = _inputs(B, N, P, M, seed0=1000, dense_every=2)
+    op, T, dQ, dK = _run(B, N, P, M, k, q, kk, dt, s_q, s_k, o_lss.MODE_BERNOULLI, call_id=11)
+    assert torch.allclose(op.steps[:, 5].cpu(), torch.from_numpy(s_q)) and torch.allclose(op.steps[:, 6].cpu(), torch.from_numpy(s_k))
+    qq, kq = op.qq.cpu().numpy(), op.kq.cpu().numpy()
+    sample = sorted({0, 1, 127, 128, B // 2, 2047 % B, min(2048, B - 1), B - 1})
+    for b in sample:
+        fo = o_bmm.forward(q[b:b + 1], kk[b:b + 1], k, s_q[b:b + 1], s_k[b:b + 1])[0][0]
+        for g, o in ((qq[b], fo["xq"]), (kq[b], fo["wq"])):
+            nbad, maxdiff = code_mismatch(g, o)
+            assert maxdiff <= 1 and nbad <= 1e-6 * o.size
+        t_ref = o_gemm.int_matmul_abt(qq[b], kq[b]).astype(np.float64) * (np.float64(s_q[b]) * np.float64(s_k[b]))
+        assert rel_frob(T[b].cpu().numpy(), t_ref) < FROB_TOL
+        fwd = dict(xq=qq[b], wq=kq[b], x_mask=unpack_bits(op.q_mask[b], M), w_mask=unpack_bits(op.k_mask[b], M),
+                   x_sq=op.q_sqnorm[b].cpu().numpy().astype(np.int64), k=k, s_x=s_q[b], s_w=s_k[b])
+        from oracle import linear as o_lin
+        o = o_lin.backward(dt[b], fwd, synth.PHILOX_SEED, 11, token_offset=b * N, mode=o_lss.MODE_BERNOULLI)
+        assert rel_frob(dQ[b].cpu().numpy(), o["dx"]) < FROB_TOL
+        assert rel_frob(dK[b].cpu().numpy(), o["dw"]) < FROB_TOL
