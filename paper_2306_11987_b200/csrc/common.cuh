@@ -334,6 +334,14 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* tmap
         : "memory");
 }
 
+// DSMEM store of 16 bytes to a shared::cluster address, its completion counted (in
+// bytes) on the destination CTA's mbarrier (st.async, sm_90+)
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 :: "r"(cluster_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(cluster_bar) : "memory");
+}
+
 // 3-D variants (batched BMM: coordinate c2 = batch; rows past a batch's extent
 // are out of bounds of the map, zero-filled on load and clipped on store, so a
 // tile never reads or writes a neighbouring batch)

@@ -46,10 +46,11 @@ constexpr int kEMaxX = 24;
 // CTA's share of the items (launch-time: a small N gets a small footprint):
 //   uint64_t w[per] (scores), uint8_t clamped[per] (A.2 set S), int8_t wexp[per]
 struct SamplerSmem {
-    uint64_t red_w[2][16];                // per-CTA partials (clusters of up to 16)
-    uint32_t red_c[2][16];
-    uint64_t warp_w[kSamplerThreads / 32];
-    uint32_t warp_c[kSamplerThreads / 32];
+    // group sums: one 16-byte {w lo, w hi, c, 0} partial per (CTA, warp) and parity, written
+    // by st.async into every CTA of the cluster; mbar[p] counts their bytes
+    uint4 wpart[2][kSamplerThreads / 32];     // this CTA's warp partials
+    uint4 part[2][16];                        // CTA partials of the cluster (clusters of up to 16)
+    uint64_t mbar[2];
     uint32_t scan[32];
     uint32_t cta_tot[16];
     uint32_t scan2[32];
@@ -66,6 +67,21 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     return v;
+}
+
+#ifndef I4_STAMPS
+#define I4_STAMPS 0
+#endif
+constexpr bool kSmpStamps = I4_STAMPS != 0;
+__device__ int g_smp_stamp_on = 0;
+__device__ unsigned long long g_smp_stamp[32];
+// fixed-slot stamp (slots 24..30: the phases inside one A.2 round)
+__device__ __forceinline__ void smp_mark(int slot, bool on) {
+    if (kSmpStamps && on) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_smp_stamp[slot] = t;
+    }
 }
 
 // CTA group of one mask: a single CTA (2N <= 16384 items) or an 8-CTA cluster
@@ -136,30 +152,43 @@ __device__ __forceinline__ uint64_t floor_mul2_32_div(uint64_t num, uint64_t W) 
     return q;
 }
 
-// Group-wide (sum w, sum c); every thread of every CTA receives the totals.
+// Group-wide (sum w, sum c); every thread of every CTA receives the totals.  Warp sums go
+// to shared memory; after one block barrier every warp forms the CTA total itself (a
+// single CTA is done); in a cluster, warp 0's lanes r < CL send it to CTA r with st.async
+// into part[parity][rank], completion counted in bytes on CTA r's mbar[parity], and every
+// warp sums the CL partials after its CTA's barrier phase completes -- no cluster barrier.
+// Integer sums: exact in any order.  Buffers of parity p are reused two rounds later, when
+// every CTA has read them (a CTA sends round k + 2 only after receiving everyone's round
+// k + 1, which each sent after reading round k).
 template <int CL>
-__device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, uint64_t w, uint32_t c,
-                            uint64_t& W, uint32_t& Cn) {
+__device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, uint32_t& mph, uint64_t w,
+                            uint32_t c, uint64_t& W, uint32_t& Cn, bool mark = false) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NW = int(blockDim.x) >> 5;
     w = warp_sum_u64(w);
     c = warp_sum_u32(c);
-    if (lane == 0) { sm.warp_w[warp] = w; sm.warp_c[warp] = c; }
+    smp_mark(26, mark && (w + c) != 1234567);
+    if (lane == 0) sm.wpart[parity][warp] = make_uint4(uint32_t(w), uint32_t(w >> 32), c, 0u);
     __syncthreads();
-    if (warp == 0) {                              // CTA sum by warp 0 (integer sums: exact, any order)
-        const bool in = lane < int(blockDim.x) / 32;
-        uint64_t bw = warp_sum_u64(in ? sm.warp_w[lane] : 0ull);
-        uint32_t bc = warp_sum_u32(in ? sm.warp_c[lane] : 0u);
-        const unsigned me = cl.rank();
-        if (lane < CL) {                          // lane r writes CTA r's slot
-            uint64_t* rw = cl.map(&sm.red_w[parity][me], lane);
-            uint32_t* rc = cl.map(&sm.red_c[parity][me], lane);
-            *rw = bw; *rc = bc;
-        }
+    if (CL == 1 || warp == 0) {
+        const uint4 v = lane < NW ? sm.wpart[parity][lane] : make_uint4(0u, 0u, 0u, 0u);
+        W = warp_sum_u64(uint64_t(v.x) | (uint64_t(v.y) << 32));
+        Cn = warp_sum_u32(v.z);
     }
-    cl.sync();
-    W = 0; Cn = 0;
-#pragma unroll
-    for (int r = 0; r < CL; ++r) { W += sm.red_w[parity][r]; Cn += sm.red_c[parity][r]; }
+    if constexpr (CL > 1) {
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&sm.mbar[parity], uint32_t(CL * 16));
+        if (warp == 0 && lane < CL)
+            st_async_v4(mapa_shared(smem_u32(&sm.part[parity][cl.rank()]), uint32_t(lane)), uint32_t(W),
+                        uint32_t(W >> 32), Cn, 0u, mapa_shared(smem_u32(&sm.mbar[parity]), uint32_t(lane)));
+        smp_mark(27, mark);
+        mbar_wait(&sm.mbar[parity], (mph >> parity) & 1u);
+        mph ^= 1u << parity;
+        smp_mark(28, mark);
+        const uint4 v = lane < CL ? sm.part[parity][lane] : make_uint4(0u, 0u, 0u, 0u);
+        W = warp_sum_u64(uint64_t(v.x) | (uint64_t(v.y) << 32));
+        Cn = warp_sum_u32(v.z);
+    }
+    smp_mark(29, mark && (W + Cn) != 1234567);
     parity ^= 1;
 }
 
@@ -167,12 +196,6 @@ __device__ void cluster_sum(const Group<CL>& cl, SamplerSmem& sm, int& parity, u
 // globaltimer stamps of CTA (rank 0, mask 0), thread 0: [0] start [1] scores
 // summed [2..] after each A.2 round, then Bernoulli done, compaction done, end;
 // slot 31 = number of stamps
-#ifndef I4_STAMPS
-#define I4_STAMPS 0
-#endif
-constexpr bool kSmpStamps = I4_STAMPS != 0;
-__device__ int g_smp_stamp_on = 0;
-__device__ unsigned long long g_smp_stamp[32];
 __device__ __forceinline__ void smp_stamp(int& n, bool on) {
     if (on) {
         unsigned long long t;
@@ -215,8 +238,10 @@ lss_sampler_kernel(SamplerArgs a) {
     const int per = sampler_per(N, CL);
     const int per16 = (per + 15) & ~15;
     uint64_t* sw = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SamplerSmem));
-    uint8_t* scl = reinterpret_cast<uint8_t*>(sw + per16);
-    int8_t* swe = reinterpret_cast<int8_t*>(scl + per16);
+    int8_t* swe = reinterpret_cast<int8_t*>(sw + per16);
+    // sw[j]: score (< 2^47: floor(sqrt(a b) 2^20) with a b < 2^53) | kClamped once A.2 clamped
+    // the item to p = 1 (the set S) -- one 8-byte word per item, read and written by the rounds
+    constexpr uint64_t kClamped = 1ull << 63;
     const int base = rank * per;
     const int nloc = max(0, min(per, n_items - base));
     const int ipt = (per + NT - 1) / NT;                 // items per thread
@@ -231,6 +256,15 @@ lss_sampler_kernel(SamplerArgs a) {
     // grad_X GEMM's compacted A and compact skips its own copy
     auto item_of = [&](int slot) { return (slot & 1) * N + (slot >> 1); };
     int parity = 0;
+    uint32_t mph = 0;                                    // phase bit of mbar[0] / mbar[1]
+    if constexpr (CL > 1) {
+        if (threadIdx.x == 0) {
+            mbar_init(&sm.mbar[0], 1);
+            mbar_init(&sm.mbar[1], 1);
+            fence_mbar_init();
+        }
+        cl.sync();                                       // barriers initialised before any st.async
+    }
     if (blockIdx.y == 0 && blockIdx.z == 0 && rank == 0)
         for (int i = threadIdx.x; i < a.n_zero_words; i += NT) a.zero_words[i] = 0u;
 
@@ -266,13 +300,12 @@ lss_sampler_kernel(SamplerArgs a) {
                 w = uint64_t(root * (h == 0 ? 1048576.0 : 65536.0));   // floor(root 2^(16+4[up]))
             }
             sw[j] = w;
-            scl[j] = 0;
             sum_pos += w;
             cnt_pos += (w > 0);
         }
     }
     uint64_t Wall; uint32_t Z;
-    cluster_sum(cl, sm, parity, sum_pos, cnt_pos, Wall, Z);
+    cluster_sum(cl, sm, parity, mph, sum_pos, cnt_pos, Wall, Z);
     smp_stamp(st_n, st_on);
 
     // ---- A.2 water-filling ----------------------------------------------------
@@ -288,14 +321,27 @@ lss_sampler_kernel(SamplerArgs a) {
     if (binding) {
         for (int round = 0; round <= n_items + 1; ++round) {
             uint64_t wun = 0; uint32_t sc = 0;
-            for (int j = t_lo; j < t_hi; ++j) {
-                const uint64_t w = sw[j];
-                if (w == 0) continue;
-                if (!scl[j] && R * w >= W) scl[j] = 1;
-                if (scl[j]) sc += 1; else wun += w;
+            const bool mk = st_on && round == 2;
+            smp_mark(24, mk);
+            for (int j0 = t_lo; j0 < t_hi; j0 += 4) {      // 4 items' loads in flight
+                uint64_t v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = j0 + q < t_hi ? sw[j0 + q] : 0ull;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint64_t w = v[q] & ~kClamped;
+                    bool c = (v[q] & kClamped) != 0;
+                    if (w != 0 && !c && R * w >= W) {
+                        c = true;
+                        sw[j0 + q] = v[q] | kClamped;
+                    }
+                    sc += (w != 0 && c) ? 1u : 0u;
+                    wun += (w != 0 && !c) ? w : 0ull;
+                }
             }
+            smp_mark(25, mk && (wun + sc) != 1234567);
             uint64_t Wn; uint32_t Sc;
-            cluster_sum(cl, sm, parity, wun, sc, Wn, Sc);
+            cluster_sum(cl, sm, parity, mph, wun, sc, Wn, Sc, mk);
             smp_stamp(st_n, st_on);
             if (Sc == s_cnt) break;
             s_cnt = Sc;
@@ -317,12 +363,13 @@ lss_sampler_kernel(SamplerArgs a) {
         const int i = item_of(base + j);
         const int h = i >= N ? 1 : 0;
         const int t = i - h * N;
-        const uint64_t w = sw[j];
+        const uint64_t w = sw[j] & ~kClamped;
+        const bool clamped = (sw[j] & kClamped) != 0;
         int8_t out = -1;
         if (a.mode == 2) {                 // I4_LSS_NONE: every item, weight 1
             out = 0;
         } else if (w > 0) {
-            if (!binding || scl[j]) {
+            if (!binding || clamped) {
                 out = 0;                   // p = 1 (Z-16 / clamped by A.2)
             } else {
                 const uint64_t num = R * w;                       // R w < W
@@ -376,7 +423,7 @@ lss_sampler_kernel(SamplerArgs a) {
         // dense Q^T X_hat already holds weight 1 for every item).  grad_X: every kept
         // item of a token that has a sampled item (its Q row is not used; tok_flag).
         __syncthreads();                       // swe of the whole CTA written
-        auto sampled = [&](int j) { return sw[j] > 0 && !scl[j]; };
+        auto sampled = [&](int j) { return sw[j] != 0 && (sw[j] & kClamped) == 0; };
         uint32_t my_n = 0;
         for (int j = t_lo; j < t_hi; ++j) {
             if (mask_id == 0) my_n += sampled(j) ? 1u + (swe[j] >= 0 ? 1u : 0u) : 0u;
@@ -416,7 +463,7 @@ static void sampler_config(const SamplerArgs& a, cudaStream_t s, cudaLaunchConfi
     cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3(CL, 2, unsigned(a.batch > 1 ? a.batch : 1));   // y: 0 = grad_W mask, 1 = grad_X mask; z: batch
     cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = sizeof(SamplerSmem) + size_t(per16) * (8 + 1 + 1);
+    cfg.dynamicSmemBytes = sizeof(SamplerSmem) + size_t(per16) * (8 + 1);
     cfg.stream = s;
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
@@ -433,7 +480,7 @@ static cudaError_t set_attrs() {
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
     if (done[dev].load(std::memory_order_relaxed)) return cudaSuccess;
     auto kern = lss_sampler_kernel<CL, NT>;
-    const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1 + 1);
+    const size_t smem_max = sizeof(SamplerSmem) + size_t(kItemsPerCTA) * (8 + 1);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max));
     if (e == cudaSuccess && CL > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess) done[dev].store(1, std::memory_order_relaxed);

@@ -21,7 +21,7 @@ for arg in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
     i4.lib.int4_debug_sampler_stamps(None, 1)
     fn = i4.lib.bitsplit_lss
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    res = []
+    res, rnd = [], []
     for it in range(6):
         st = fn(ctypes.c_void_p(G.data_ptr()), N, C, ctypes.c_void_p(xsq.data_ptr()), 1, 0, 0, 0,
                 ctypes.byref(L.plan), stream)
@@ -32,5 +32,7 @@ for arg in sys.argv[1:] or ["cfg2_bert_base_ffn1"]:
         a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
         n = int(a[31])
         res.append(np.diff(a[:n]) / 1e3)
+        rnd.append(np.diff(a[24:30]) / 1e3)
     i4.lib.int4_debug_sampler_stamps(None, 0)
-    print(arg, "stamps", n, "intervals us:", np.round(np.median(np.array(res[2:]), 0), 2))
+    print(arg, "stamps", n, "intervals us:", np.round(np.median(np.array(res[2:]), 0), 2),
+          "| round 2: items, warp sums, send, wait, final sums:", np.round(np.median(np.array(rnd[2:]), 0), 3))
