@@ -142,9 +142,11 @@ __device__ uint32_t group_scan(const Group<CL>& cl, uint32_t v, uint32_t* scan, 
 // Exact floor(num 2^32 / W) for 0 < num < W < 2^64 without a 128-bit division:
 // a double-precision estimate (relative error < 2^-52, so off by at most a few
 // units) corrected by exact 128-bit products.
-__device__ __forceinline__ uint64_t floor_mul2_32_div(uint64_t num, uint64_t W) {
+// est: num 2^32 / W in double precision -- here num * fl(2^32 / W) with the reciprocal
+// computed once per CTA (relative error a few 2^-53: the start is off by at most a few
+// units, which the exact loops below remove).
+__device__ __forceinline__ uint64_t floor_mul2_32_div(uint64_t num, uint64_t W, double est) {
     const unsigned __int128 lhs = (unsigned __int128)num << 32;
-    double est = (double(num) / double(W)) * 4294967296.0;
     uint64_t q = uint64_t(est);
     if (q > 0) q -= 1;                                  // start at or below the true quotient
     while ((unsigned __int128)(q + 1) * W <= lhs) ++q;  // at most a few steps
@@ -359,40 +361,60 @@ lss_sampler_kernel(SamplerArgs a) {
 
     // ---- Bernoulli with dyadic weights ---------------------------------------
     uint32_t my_keep = 0;
-    for (int j = t_lo; j < t_hi; ++j) {
-        const int i = item_of(base + j);
-        const int h = i >= N ? 1 : 0;
-        const int t = i - h * N;
-        const uint64_t w = sw[j] & ~kClamped;
-        const bool clamped = (sw[j] & kClamped) != 0;
-        int8_t out = -1;
-        if (a.mode == 2) {                 // I4_LSS_NONE: every item, weight 1
-            out = 0;
-        } else if (w > 0) {
-            if (!binding || clamped) {
-                out = 0;                   // p = 1 (Z-16 / clamped by A.2)
-            } else {
-                const uint64_t num = R * w;                       // R w < W
-                int e = (63 - __clzll((long long)W)) - (63 - __clzll((long long)num));
-                if ((num << e) > W) --e;
-                uint64_t T1, T2;
-                if (e >= e_max) {
-                    e = e_max;
-                    T1 = T2 = 1ull << (32 - e_max);
-                } else {
-                    T2 = floor_mul2_32_div(num, W);
-                    T1 = 2 * T2 - (1ull << (32 - e));
-                }
-                const uint64_t idx = 2ull * uint64_t(tok_off + t) + uint64_t(h);
-                const Philox4 p = philox4x32_10(uint32_t(idx), uint32_t(idx >> 32), purpose, a.call_id,
-                                                a.seed_lo, a.seed_hi);
-                const uint64_t u = p.x;
-                if (u < T2) out = int8_t(u < T1 ? e : e + 1);
-            }
-        }
+    auto emit = [&](int j, int8_t out) {
         swe[j] = out;
         my_keep += (out >= 0);
-        if (mask_id == 1 && out >= 0 && x_touched) x_touched[t] = 1;
+        if (mask_id == 1 && out >= 0 && x_touched) {
+            const int i = item_of(base + j);
+            x_touched[i >= N ? i - N : i] = 1;
+        }
+    };
+    if (a.mode == 2 || !binding) {
+        // deterministic: every item (I4_LSS_NONE) or every positive item, weight 1
+        // (Z-16: a non-binding budget gives every positive item p = 1)
+        for (int j = t_lo; j < t_hi; ++j) emit(j, (a.mode == 2 || (sw[j] & ~kClamped) != 0) ? int8_t(0) : int8_t(-1));
+    } else {
+        // 4 items per step: their Philox words (computed for every item, straight-line code)
+        // and threshold divisions are independent chains whose latencies overlap
+        const double rW = 4294967296.0 / double(W);
+        for (int j0 = t_lo; j0 < t_hi; j0 += 4) {
+            uint64_t v[4];
+            uint32_t u[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = j0 + q < t_hi ? j0 + q : t_lo;
+                v[q] = sw[j];
+                const int i = item_of(base + j);
+                const int h = i >= N ? 1 : 0;
+                const uint64_t idx = 2ull * uint64_t(tok_off + (i - h * N)) + uint64_t(h);
+                u[q] = philox4x32_10(uint32_t(idx), uint32_t(idx >> 32), purpose, a.call_id, a.seed_lo, a.seed_hi).x;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (j0 + q >= t_hi) break;
+                const uint64_t w = v[q] & ~kClamped;
+                int8_t out = -1;
+                if (w > 0) {
+                    if ((v[q] & kClamped) != 0) {
+                        out = 0;               // p = 1 (clamped by A.2)
+                    } else {
+                        const uint64_t num = R * w;                       // R w < W
+                        int e = (63 - __clzll((long long)W)) - (63 - __clzll((long long)num));
+                        if ((num << e) > W) --e;
+                        uint64_t T1, T2;
+                        if (e >= e_max) {
+                            e = e_max;
+                            T1 = T2 = 1ull << (32 - e_max);
+                        } else {
+                            T2 = floor_mul2_32_div(num, W, double(num) * rW);
+                            T1 = 2 * T2 - (1ull << (32 - e));
+                        }
+                        if (u[q] < T2) out = int8_t(u[q] < T1 ? e : e + 1);
+                    }
+                }
+                emit(j0 + q, out);
+            }
+        }
     }
 
     smp_stamp(st_n, st_on);
