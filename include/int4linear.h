@@ -203,6 +203,10 @@ I4_API i4_status int4_linear_fwd(const void* X, const void* W, int64_t N, int64_
  * 8-bit code, bit split (Eq. 5), integer leverage scores of both masks
  * (PAPER.md:296 with b = x_sqnorm, :365), A.2 probabilities (PAPER.md:606-610,
  * budget N per mask), Philox Bernoulli masks with dyadic weights, compaction.
+ * The 8-bit code is floor-form stochastic rounding (reading Z-10):
+ *   q = floor((ceil(v 2^32) + u) / 2^32), v = clamp(fl32(dY r8), -119, 119),
+ * u = (16-bit half L mod 8 of Philox block L/8, purpose 1) << 16 | (the same half
+ * of purpose 4), L = (token_offset + t) C + c (Z-20).
  *   dY [N, C] bf16; x_sqnorm int32 [N] (from the forward cache; may be NULL
  *   only for mode I4_LSS_NONE).  seed/call_id/token_offset select the Philox
  *   streams (Z-20).  Outputs in *plan (see i4_lss_plan). */

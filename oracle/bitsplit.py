@@ -7,9 +7,11 @@ representation"; grad_Y is quantized dynamically for each MM.
 Readings (listed in DESIGN.md):
   Z-9  one per-tensor dynamic 8-bit code q in [-119, 119] with
        s_down = fl32(amax / 119), s_up = 16 s_down, r8 = fl32(119 / amax).
-  Z-10 unbiased stochastic rounding with Philox words, sign-magnitude form:
-       v = clamp(fl32(g * r8), -119, 119); a = |v|; fl = floor(a);
-       f = a - fl (exact); T = ceil(f * 2^32) (exact); q = sign(v) (fl + [u < T]).
+  Z-10 unbiased stochastic rounding with 32-bit uniforms u, floor form:
+       v = clamp(fl32(g * r8), -119, 119); A = ceil(v * 2^32) (an exact integer);
+       q = floor((A + u) / 2^32), i.e. q = floor(v) + 1 with probability
+       ceil(frac(v) 2^32) / 2^32 and floor(v) otherwise ("round up with
+       probability x - floor(x)", Gupta et al. 2015, on a 2^-32 grid).
   Z-11 balanced base-16 split: hi = floor((q + 8) / 16), lo = q - 16 hi,
        hi in [-7, 7], lo in [-8, 7].
 amax == 0 is the degenerate case (SPEC bit_split errors): s_down = 0, q = 0.
@@ -33,18 +35,16 @@ def scales(g):
 
 
 def stochastic_round(v, u):
-    """Sign-magnitude SR of fp32 values v in [-119, 119] with uint32 words u (Z-10).
+    """Floor-form SR of fp32 values v in [-119, 119] with uint32 words u (Z-10).
 
-    Element-wise: P(round away from zero) = T / 2^32 with T = ceil(frac(|v|) 2^32).
+    Element-wise q = floor((ceil(v 2^32) + u) / 2^32): P(q = floor(v) + 1) =
+    T / 2^32 with T = ceil(frac(v) 2^32), the event u >= 2^32 - T.
     """
     v = np.asarray(v, dtype=np.float32)
-    a = np.abs(v)
-    fl = np.floor(a)
-    f = a - fl                                        # exact in fp32
-    T = np.ceil(f.astype(np.float64) * TWO32)         # exact integer in [0, 2^32]
-    up = (np.asarray(u, dtype=np.float64) < T)
-    mag = fl.astype(np.int64) + up.astype(np.int64)
-    return np.where(v < 0, -mag, mag).astype(np.int64)
+    # exact: v 2^32 has <= 24 significant bits and |A| < 2^39, so A + u fits int64
+    A = np.ceil(v.astype(np.float64) * TWO32).astype(np.int64)
+    u = np.asarray(u, dtype=np.uint64).astype(np.int64)
+    return np.floor_divide(A + u, np.int64(1) << 32)
 
 
 def split(q):

@@ -13,8 +13,10 @@ tests/test_oracle_philox.py.
 Stream layout (reading Z-20; shard-invariant because indices are global):
     key     = (seed & 0xffffffff, seed >> 32)
     counter = (idx & 0xffffffff, idx >> 32, purpose, call_id)
-  purpose 1: stochastic rounding of grad_Y; element L = (token_offset+t)*C + c
-             uses word L % 4 of the block with idx = L // 4.
+  purposes 1 and 4: stochastic rounding of grad_Y.  Element L = (token_offset+t)*C + c
+             takes the 16-bit half j = L % 8 (word j // 2; low half for even j) of
+             the block with idx = L // 8 from both streams; its 32-bit uniform is
+             (half of purpose 1) * 2^16 + (half of purpose 4).
   purpose 2: Bernoulli mask of the weight-gradient LSS; item (h, t) uses word 0
              of idx = 2*(token_offset+t) + h   (h = 0 high half, 1 low half).
   purpose 3: same for the activation-gradient LSS.
@@ -30,6 +32,7 @@ MASK32 = 0xFFFFFFFF
 PURPOSE_SR = 1
 PURPOSE_MASK_W = 2
 PURPOSE_MASK_X = 3
+PURPOSE_SR_LOW = 4
 
 
 def philox4x32_10(ctr, key):
@@ -71,16 +74,20 @@ def _counter(idx, purpose, call_id):
 
 
 def sr_uniforms(seed, call_id, token_offset, n_rows, n_cols):
-    """32-bit uniform word for every grad_Y element (purpose 1, Z-20).
+    """32-bit uniform for every grad_Y element (purposes 1 and 4, Z-20).
 
     Returns uint64 array [n_rows, n_cols] with values in [0, 2^32).
     """
     t = np.arange(n_rows, dtype=np.uint64)[:, None] + np.uint64(token_offset)
     c = np.arange(n_cols, dtype=np.uint64)[None, :]
     L = t * np.uint64(n_cols) + c
-    blocks = philox4x32_10(_counter(L >> np.uint64(2), PURPOSE_SR, call_id), _key(seed))
-    word = (L & np.uint64(3)).astype(np.int64)
-    return np.take_along_axis(blocks, word[..., None], axis=-1)[..., 0].astype(np.uint64)
+    j = (L & np.uint64(7)).astype(np.int64)
+    halves = []
+    for purpose in (PURPOSE_SR, PURPOSE_SR_LOW):
+        blocks = philox4x32_10(_counter(L >> np.uint64(3), purpose, call_id), _key(seed))
+        word = np.take_along_axis(blocks, (j // 2)[..., None], axis=-1)[..., 0].astype(np.uint64)
+        halves.append(np.where(j % 2 == 0, word & np.uint64(0xFFFF), word >> np.uint64(16)))
+    return halves[0] * np.uint64(65536) + halves[1]
 
 
 def mask_uniforms(seed, call_id, token_offset, n_tokens, purpose):

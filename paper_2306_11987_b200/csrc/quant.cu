@@ -460,16 +460,17 @@ cudaError_t launch_hadamard_quant(const uint16_t* x, int64_t rows, int64_t cols,
 //            order-independent; each CTA folds its maximum into one scratch
 //            word (atomicMax) and counts itself in (fence + atomicAdd)
 //   --- every CTA spins until all arrived (one acquire load per poll) ---
-//   phase 2  s_down = fl32(amax / 119),
-//            r8 = fl32(119 / amax); v = fl32(g r8), a = min(|v|, 119);
-//            A = ceil(a 2^32) (a 2^32 is exact in fp32, the conversion rounds up):
-//            high word = floor(a) (+1 when frac's threshold wraps), low word =
-//            T = ceil(frac(a) 2^32) mod 2^32; q = sign(v) (hi(A) + [u < lo(A)])
-//            with u the element's Philox word: P(round up) = frac(a) exactly
-//            (reading Z-10); the code plane stores q itself; hi = floor((q+8)/16),
-//            lo = q - 16 hi (Z-11) are formed in registers for the per-row
-//            sum hi^2, sum lo^2 (the leverage scores' INT data) and
-//            split again on the fly where a half-row is an operand (compact).
+//   phase 2  s_down = fl32(amax / 119), r8 = fl32(119 / amax); v = fl32(g r8)
+//            clamped to [-119, 119]; A = ceil(v 2^32) (v 2^32 is exact in fp32, the
+//            conversion rounds up); q = floor((A + u) / 2^32) with u the element's
+//            32-bit uniform: the floor form of SR, P(q = floor(v) + 1) =
+//            ceil(frac(v) 2^32) / 2^32 (reading Z-10); u's high 16 bits come from
+//            the purpose-1 Philox stream, its low 16 bits from purpose 4, drawn only
+//            when the high half leaves the decision open (Z-20).  The code plane
+//            stores q itself; hi = floor((q+8)/16), lo = q - 16 hi (Z-11) are formed
+//            in registers for the per-row sum hi^2, sum lo^2 (the leverage scores'
+//            INT data) and split again on the fly where a half-row is
+//            an operand (compact).
 //            grad_Y is re-read right after phase 1, mostly from L2.
 // ---------------------------------------------------------------------------
 constexpr int kSplitThreads = 256;
@@ -493,25 +494,8 @@ __device__ __forceinline__ uint32_t bf16x2_absmax(uint32_t w) {
     return max(w & 0x7FFFu, (w >> 16) & 0x7FFFu);
 }
 
-// pack the low bytes of 8 ints into 8 bytes
-__device__ __forceinline__ uint2 pack8_i8(const int (&v)[8]) {
-    const uint32_t a = __byte_perm(uint32_t(v[0]), uint32_t(v[1]), 0x0040);   // [v0, v1, 0, 0]
-    const uint32_t b = __byte_perm(uint32_t(v[2]), uint32_t(v[3]), 0x0040);
-    const uint32_t c = __byte_perm(uint32_t(v[4]), uint32_t(v[5]), 0x0040);
-    const uint32_t d = __byte_perm(uint32_t(v[6]), uint32_t(v[7]), 0x0040);
-    return make_uint2(__byte_perm(a, b, 0x5410), __byte_perm(c, d, 0x5410));
-}
-
-// prmt.b32 in its generic mode: a selector nibble with bit 3 set replicates the
-// sign bit of the selected byte (used to turn bf16 sign bits into byte masks)
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
-    return r;
-}
-
 // Philox4x32-10 of the SR stream (purpose word c2 = 1) for counters whose high
-// word c1 is 0 (block index L/4 < 2^32, checked on the host): round 0's
+// word c1 is 0 (block index L/8 < 2^32, checked on the host): round 0's
 // multiply of c2 is the constant M1, and round 1 multiplies c0 = k0[0], a
 // kernel constant the compiler hoists -- 18 IMAD.WIDE per call instead of 20.
 // Same function as philox4x32_10(c0, 0, 1, call_id, K), restated.
@@ -529,131 +513,70 @@ __device__ __forceinline__ Philox4 philox_sr_c1z(uint32_t c0, uint32_t call_id, 
     return {x0, x1, x2, x3};
 }
 
-// The two Philox blocks of an 8-element chunk starting at stream block blk (even).
-template <bool C1Z>
-__device__ __forceinline__ void sr_words(uint64_t blk, uint32_t call_id, const PhiloxKeys& keys, Philox4& p0,
-                                         Philox4& p1) {
-    if (C1Z) {
-        p0 = philox_sr_c1z(uint32_t(blk), call_id, keys);
-        p1 = philox_sr_c1z(uint32_t(blk) + 1u, call_id, keys);
-    } else {                                          // blk even: blk + 1 never carries into the high word
-        p0 = philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSR, call_id, keys);
-        p1 = philox4x32_10(uint32_t(blk) + 1u, uint32_t(blk >> 32), kPurposeSR, call_id, keys);
-    }
-}
-
-// Fast phase 2 for one 8-element chunk (reading Z-10 / Z-11, same arithmetic as
-// the generic loop below, restated for the ALU / fma-heavy pipe budget):
-//   y = fl32(fl32(|g| r8) 2^32) on fp32 pairs (FMUL2): the power-of-two scaling
-//       is exact, so y = a 2^32 bit for bit, including a subnormal fl32(|g| r8)
-//   A = ceil(min(y, 119 2^32)) as u64: high word floor(a), low word T
-//   mag = hi(A) + [u < lo(A)]
-// then sign and split on packed bytes, with no cross-byte carries:
-//   S  = sign bytes (0xFF / 0x00) straight from the bf16 sign bits (PRMT)
-//   t  = (M ^ S ^ 0x80) + (S & 1) + 8 per byte  == q + 136 in [16, 255]
-//        (positive: m + 128 + 8; negative: 127 - m + 1 + 8)
-//   16 hi = (t & 0xF0) ^ 0x80;  lo = ((t & 0x0F) + 0x78) ^ 0x80
-// How T = ceil(frac(a) 2^32) and floor(a) are formed (compile-time; all three are
-// the same integers, tests/test_gpu_parity*.py):
-//   0  A = ceil(a 2^32) as u64 by one F2I.U64.CEIL per element (XU pipe)
-//   1  floor(a) by the magic add fl32_rm(a + 2^23) (FADD2.RM), f = a - floor(a)
-//      (exact), T = F2I.U32.CEIL(f 2^32) (XU, a 32-bit conversion)
-//   2  no conversion instruction: z = f 2^9 in [0, 512), zt = fl32_rm(z + 2^23)
-//      holds floor(z) = floor(y / 2^23) in its low mantissa bits, the rest
-//      yl = (z - floor(z)) 2^23 in [0, 2^23) is rounded up by fl32_rp(yl + 2^23)
-//      (FFMA2.RP, exact below 2^24), and T = floor(z) 2^23 + ceil(yl) is put
-//      together from the two bit patterns by one LEA (y = f 2^32)
-//   3  as 0, with the sign cleared after the multiplies (folded into the
-//      conversion) and mag = high word of (A + ~u) (one 64-bit add, no select)
-#ifndef I4_SR_CVT
-#define I4_SR_CVT 3
-#endif
-template <bool CLAMP>
-__device__ __forceinline__ void split_chunk8(const uint4 raw, const Philox4& p0, const Philox4& p1, const float r8,
-                                             uint2& pq, int& shi, int& slo) {
-    const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+// Fast phase 2 for one 8-element chunk (readings Z-10, Z-11, Z-20):
+//   v = fl32(g r8) on fp32 pairs (FMUL2), y = v 2^32 (exact power-of-two scaling, also
+//       for a subnormal fl32(g r8)); CLAMP: y in [-119 2^32, 119 2^32]
+//   A = ceil(y) as s64 (F2I.S64.CEIL); q = hi32(A + u): the floor form of SR
+//   u = (h1 << 16) | h4, h_p = 16-bit half (L mod 8) of Philox block L / 8 of purpose p.
+//   The high half decides unless the low word of A + (h1 << 16) is above 0xFFFF0000
+//   (probability < 2^-16 per element); only then is the purpose-4 block drawn and
+//   q += [h4 > ~lo32(A + (h1 << 16))] (a divergent branch the warp rarely takes).
+// then, on 4 packed codes: t = (q ^ 0x80) + 8 per byte = q + 136 (no cross-byte carry),
+//   16 hi = (t ^ 0x80) & 0xF0 (signed byte), x = t & 0x0F = lo + 8, x | 0xF0 = lo - 8:
+//   dp4a(16 hi, 16 hi) = 256 sum hi^2 and dp4a(x, x | 0xF0) = sum lo^2 - 64 per element
+//   (the 64 s are added back per chunk).
+constexpr uint32_t kPurposeSRLow = 4;
+template <bool CLAMP, bool C1Z>
+__device__ __forceinline__ void split_chunk8(const uint4 raw, uint64_t blk, uint32_t call_id, const PhiloxKeys& keys,
+                                             const float r8, uint2& pq, int& shi, int& slo) {
+    const Philox4 p = C1Z ? philox_sr_c1z(uint32_t(blk), call_id, keys)
+                          : philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSR, call_id, keys);
+    const uint32_t pw[4] = {p.x, p.y, p.z, p.w};
     const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
     const uint64_t r2 = f2_pack(r8, r8);
-    uint32_t mag[8];
-    if constexpr (I4_SR_CVT == 3) {
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-            // elements i (low bf16) and i + 1 (high bf16) as one signed fp32 pair; |.| is taken
-            // after the multiplies (exact: IEEE products are sign-symmetric) and folds into the
-            // conversion; mag = high word of A + ~u = floor(a) + [u < T] (one 64-bit add)
-            const uint32_t wv = w[i >> 1];
-            const uint64_t g2 = f2_pack(__uint_as_float(__byte_perm(wv, 0u, 0x1044u)), __uint_as_float(wv & 0xFFFF0000u));
-            float y0, y1;
-            f2_unpack(f2_mul(f2_mul(g2, r2), f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
-            y0 = fabsf(y0);
-            y1 = fabsf(y1);
-            if (CLAMP) { y0 = fminf(y0, 511101108224.0f); y1 = fminf(y1, 511101108224.0f); }   // 119 * 2^32
-            const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
-            mag[i] = uint32_t((A0 + uint64_t(~u[i])) >> 32);
-            mag[i + 1] = uint32_t((A1 + uint64_t(~u[i + 1])) >> 32);
-        }
-    } else {
+    int qv[8];
+    uint32_t L[8];
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
-        // |g| of elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
-        const uint64_t ag = uint64_t((w[i >> 1] << 16) & 0x7FFFFFFFu) | (uint64_t(w[i >> 1] & 0x7FFF0000u) << 32);
-        uint64_t a2 = f2_mul(ag, r2);                                   // a = fl32(|g| r8)
-        if (CLAMP) {
-            float a0, a1;
-            f2_unpack(a2, a0, a1);
-            a2 = f2_pack(fminf(a0, 119.0f), fminf(a1, 119.0f));
+        // elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
+        const uint32_t wv = w[i >> 1];
+        const uint64_t g2 = f2_pack(__uint_as_float(__byte_perm(wv, 0u, 0x1044u)), __uint_as_float(wv & 0xFFFF0000u));
+        float y0, y1;
+        f2_unpack(f2_mul(f2_mul(g2, r2), f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
+        if (CLAMP) {                                                   // 119 2^32
+            y0 = fmaxf(fminf(y0, 511101108224.0f), -511101108224.0f);
+            y1 = fmaxf(fminf(y1, 511101108224.0f), -511101108224.0f);
         }
-        if constexpr (I4_SR_CVT == 0) {
-            float y0, y1;
-            f2_unpack(f2_mul(a2, f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);   // exact 2^32 scaling
-            const uint64_t A0 = __float2ull_ru(y0), A1 = __float2ull_ru(y1);
-            mag[i] = uint32_t(A0 >> 32) + (u[i] < uint32_t(A0) ? 1u : 0u);
-            mag[i + 1] = uint32_t(A1 >> 32) + (u[i + 1] < uint32_t(A1) ? 1u : 0u);
-        } else {
-            const uint64_t m23 = f2_pack(8388608.0f, 8388608.0f);
-            const uint64_t t2 = f2_add_rm(a2, m23);                      // 2^23 + floor(a), exact
-            const uint64_t f2 = f2_sub(a2, f2_sub(t2, m23));             // frac(a), exact
-            uint32_t T0, T1;
-            if constexpr (I4_SR_CVT == 1) {
-                float y0, y1;
-                f2_unpack(f2_mul(f2, f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
-                T0 = __float2uint_ru(y0);
-                T1 = __float2uint_ru(y1);
-            } else {
-                const uint64_t z2 = f2_mul(f2, f2_pack(512.0f, 512.0f));  // y / 2^23, exact
-                const uint64_t zt = f2_add_rm(z2, m23);                  // 2^23 + floor(z)
-                const uint64_t zr = f2_sub(z2, f2_sub(zt, m23));         // frac(z), exact
-                const uint64_t cw = f2_fma_rp(zr, m23, m23);             // 2^23 + ceil(frac(z) 2^23)
-                float zt0, zt1, cw0, cw1;
-                f2_unpack(zt, zt0, zt1);
-                f2_unpack(cw, cw0, cw1);
-                // (bits(zt) << 23) drops the exponent bits; bits(cw) - 0x4B000000 = ceil(yl)
-                T0 = (__float_as_uint(zt0) << 23) + __float_as_uint(cw0) - 0x4B000000u;
-                T1 = (__float_as_uint(zt1) << 23) + __float_as_uint(cw1) - 0x4B000000u;
-            }
-            float t0, t1;
-            f2_unpack(t2, t0, t1);
-            // the low byte of bits(t) is floor(a) <= 119 (no carry out of it below)
-            mag[i] = __float_as_uint(t0) + (u[i] < T0 ? 1u : 0u);
-            mag[i + 1] = __float_as_uint(t1) + (u[i + 1] < T1 ? 1u : 0u);
+        const uint64_t s0 = uint64_t(__float2ll_ru(y0)) + uint64_t(pw[i >> 1] << 16);
+        const uint64_t s1 = uint64_t(__float2ll_ru(y1)) + uint64_t(pw[i >> 1] & 0xFFFF0000u);
+        qv[i] = int(uint32_t(s0 >> 32));
+        qv[i + 1] = int(uint32_t(s1 >> 32));
+        L[i] = uint32_t(s0);
+        L[i + 1] = uint32_t(s1);
+    }
+    const uint32_t lmax = max(max(max(L[0], L[1]), max(L[2], L[3])), max(max(L[4], L[5]), max(L[6], L[7])));
+    if (__builtin_expect(lmax > 0xFFFF0000u, 0)) {                     // the low halves decide
+        const Philox4 pl = philox4x32_10(uint32_t(blk), uint32_t(blk >> 32), kPurposeSRLow, call_id, keys);
+        const uint32_t lw[4] = {pl.x, pl.y, pl.z, pl.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t h4 = (i & 1) ? (lw[i >> 1] >> 16) : (lw[i >> 1] & 0xFFFFu);
+            if (L[i] > 0xFFFF0000u && h4 > ~L[i]) qv[i] += 1;
         }
     }
-    }
+    const uint32_t c80 = 0x80808080u;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const uint32_t M = __byte_perm(__byte_perm(mag[4 * h], mag[4 * h + 1], 0x0040),
-                                       __byte_perm(mag[4 * h + 2], mag[4 * h + 3], 0x0040), 0x5410);
-        const uint32_t S = prmt(w[2 * h], w[2 * h + 1], 0xFDB9u);     // sign bytes of the 4 elements
-        const uint32_t t = (M ^ S ^ 0x80808080u) + (S & 0x01010101u) + 0x08080808u;
-        const uint32_t hi16 = (t & 0xF0F0F0F0u) ^ 0x80808080u;
-        const uint32_t lo = ((t & 0x0F0F0F0Fu) + 0x78787878u) ^ 0x80808080u;
+        const uint32_t q = __byte_perm(__byte_perm(uint32_t(qv[4 * h]), uint32_t(qv[4 * h + 1]), 0x0040),
+                                       __byte_perm(uint32_t(qv[4 * h + 2]), uint32_t(qv[4 * h + 3]), 0x0040), 0x5410);
+        const uint32_t t = (q ^ c80) + 0x08080808u;
+        uint32_t hi16;                                                  // (t ^ 0x80) & 0xF0 per byte
+        asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(hi16) : "r"(t), "r"(c80), "r"(0xF0F0F0F0u));
         shi = __dp4a(int(hi16), int(hi16), shi);
-        slo = __dp4a(int(lo), int(lo), slo);
-        // q = 16 hi + lo per byte (fits int8), added without cross-byte carries:
-        // low 7 bits summed, bit 7 = xor of the operands' bit 7 and the low carry
-        const uint32_t q = ((hi16 & 0x7F7F7F7Fu) + (lo & 0x7F7F7F7Fu)) ^ ((hi16 ^ lo) & 0x80808080u);
+        slo = __dp4a(int(t & 0x0F0F0F0Fu), int(t | 0xF0F0F0F0u), slo);
         if (h == 0) pq.x = q; else pq.y = q;
     }
+    slo += 8 * 64;
 }
 
 // Work unit = G chunks of 256 columns of one row (one 16-byte load of 8 bf16 per
@@ -710,10 +633,8 @@ __device__ __forceinline__ void split_unit(const uint4 (&cur)[G], int64_t un, co
 #pragma unroll
     for (int gi = 0; gi < G; ++gi) {
         const int64_t flat = (un * G + gi) * 256 + lane * 8;
-        Philox4 p0, p1;
-        sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
         uint2 pq;
-        split_chunk8<CLAMP>(cur[gi], p0, p1, r8, pq, shi, slo);
+        split_chunk8<CLAMP, C1Z>(cur[gi], (tbase + uint64_t(flat)) >> 3, call_id, keys, r8, pq, shi, slo);
         *reinterpret_cast<uint2*>(q8 + flat) = pq;
     }
 }
@@ -898,40 +819,11 @@ grad_split_kernel(const uint16_t* __restrict__ g, int64_t N, int C, uint32_t* __
             for (int gi = 0; gi < kBsGroup; ++gi) {
                 const int col = (g0 + gi) * 256 + lane * 8;
                 if (g0 + gi >= nch || col >= C) continue;
-                float v[8];
-                unpack_bf16x8(raw[gi], v);
-                // Philox words for the 8 elements: L = tglob * C + col + i, block L / 4 (Z-20)
-                const uint64_t b0 = (tglob * uint64_t(C) + uint64_t(col)) >> 2;
-                const Philox4 p0 = philox4x32_10(uint32_t(b0), uint32_t(b0 >> 32), kPurposeSR, call_id, keys);
-                const Philox4 p1 = philox4x32_10(uint32_t(b0 + 1), uint32_t((b0 + 1) >> 32), kPurposeSR, call_id, keys);
-                const uint32_t u[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-                int qv[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float sv = zero ? 0.0f : __fmul_rn(v[i], r8);
-                    const float a = fminf(fabsf(sv), 119.0f);
-                    const uint64_t A = __float2ull_ru(__fmul_rn(a, 4294967296.0f));   // exact ceil(a 2^32)
-                    const int mag = int(uint32_t(A >> 32)) + int(u[i] < uint32_t(A));
-                    qv[i] = sv < 0.0f ? -mag : mag;
-                }
-                // bit split (for the norms) on 4 packed codes at a time: t = (q + 128) + 8 per
-                // byte (no carries: q + 136 <= 255); hi = floor((q + 8) / 16) = (t >> 4) - 8,
-                // so 16 hi = (t & 0xF0) - 128 = (t & 0xF0) ^ 0x80; the low nibble t & 15 =
-                // lo + 8, i.e. lo in 4-bit two's complement after ^ 8, sign-extended to a
-                // byte by adding 0xF0 when its bit 3 is set
-                const uint2 qp = pack8_i8(qv);
-                uint32_t ph[2], pl[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t t = ((h ? qp.y : qp.x) ^ 0x80808080u) + 0x08080808u;
-                    ph[h] = (t & 0xF0F0F0F0u) ^ 0x80808080u;
-                    const uint32_t x = (t & 0x0F0F0F0Fu) ^ 0x08080808u;
-                    pl[h] = (x & 0x08080808u) * 0x1Eu + x;
-                }
-                // sums of squares: ph holds 16 hi, so its dp4a sum is 256 sum hi^2
-                shi = __dp4a(int(ph[0]), int(ph[0]), __dp4a(int(ph[1]), int(ph[1]), shi));
-                slo = __dp4a(int(pl[0]), int(pl[0]), __dp4a(int(pl[1]), int(pl[1]), slo));
-                *reinterpret_cast<uint2*>(qr + col) = qp;          // the 8-bit code plane Q
+                uint2 qp = make_uint2(0u, 0u);
+                if (!zero)                                             // L = tglob C + col (Z-20)
+                    split_chunk8<true, C1Z>(raw[gi], (tglob * uint64_t(C) + uint64_t(col)) >> 3, call_id, keys, r8,
+                                            qp, shi, slo);
+                *reinterpret_cast<uint2*>(qr + col) = qp;              // the 8-bit code plane Q
             }
         }
 #pragma unroll
@@ -999,8 +891,8 @@ static cudaError_t launch_grad_split_c(const uint16_t* g, int64_t N, int C, uint
                                        const PhiloxKeys& keys, uint32_t call_id, int64_t token_offset, int8_t* q8,
                                        int32_t* a_sq, float* s_down, uint32_t* amax_out, int32_t* status,
                                        cudaStream_t s) {
-    // every SR block index L / 4 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
-    const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 34);
+    // every SR block index L / 8 below 2^32 (L < (token_offset + N) C): Philox counter word c1 = 0
+    const bool c1z = (uint64_t(token_offset) + uint64_t(N)) * uint64_t(C) <= (uint64_t(1) << 35);
     if (c1z)
         return launch_grad_split_g<G, true>(g, N, C, block_max, keys, call_id, token_offset, q8, a_sq, s_down,
                                             amax_out, status, s);
@@ -1116,9 +1008,7 @@ batch_split_kernel(const uint16_t* __restrict__ g, int64_t rows, int C, int64_t 
                 const int64_t flat = row * C + col;
                 uint2 pq = make_uint2(0u, 0u);
                 if (!zero) {
-                    Philox4 p0, p1;
-                    sr_words<C1Z>((tbase + uint64_t(flat)) >> 2, call_id, keys, p0, p1);
-                    split_chunk8<true>(u[q], p0, p1, r8, pq, shi, slo);
+                    split_chunk8<true, C1Z>(u[q], (tbase + uint64_t(flat)) >> 3, call_id, keys, r8, pq, shi, slo);
                 }
                 *reinterpret_cast<uint2*>(q8 + flat) = pq;
             }
@@ -1167,7 +1057,7 @@ cudaError_t launch_grad_split_batched(const uint16_t* g, int64_t rows, int64_t C
     const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(sms) * 8);
     cfg.gridDim = dim3(unsigned(blocks));
     const PhiloxKeys keys = philox_keys(uint32_t(seed), uint32_t(seed >> 32));
-    const bool c1z = (uint64_t(token_offset) + uint64_t(rows)) * uint64_t(C) <= (uint64_t(1) << 34);
+    const bool c1z = (uint64_t(token_offset) + uint64_t(rows)) * uint64_t(C) <= (uint64_t(1) << 35);
     if (c1z)
         return cudaLaunchKernelEx(&cfg, batch_split_kernel<true>, g, rows, int(C), nb, keys, call_id, token_offset,
                                   q8, a_sq, s_down, amax_out, status, static_cast<const uint32_t*>(bamax));

@@ -145,8 +145,8 @@ def test_token_sharded_backward_sum_equals_oracle_shards():
 def test_sr_subnormal_products_bit_exact():
     """Reading Z-10 computes v = fl32(g r8) in fp32; when |g| r8 is subnormal
     (|g| / amax < 2^-126 / 119) v is a subnormal or flushes to 0 and the SR
-    threshold is T = ceil(frac(|v|) 2^32) of that value.  The kernel forms the
-    same fl32(|g| r8) and scales by 2^32 exactly afterwards, so codes are
+    rounds A = ceil(v 2^32) of that value.  The kernel forms the same
+    fl32(g r8) and scales by 2^32 exactly afterwards, so codes are
     bit-identical to the oracle across the subnormal range."""
     N, C = 64, 512
     rng = np.random.default_rng(5)
@@ -164,6 +164,34 @@ def test_sr_subnormal_products_bit_exact():
     mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, 2, 0, o_lss.MODE_BERNOULLI, plan.plan)
     torch.cuda.synchronize()
     assert np.array_equal(plan.q8.cpu().numpy().astype(np.int64)[:N], bs["q"])
+    assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
+
+
+def test_sr_low_half_draws_bit_exact():
+    """Reading Z-20: an element's 32-bit uniform is (purpose-1 half) 2^16 +
+    (purpose-4 half); the kernel draws the purpose-4 block only when the high
+    half leaves the decision open (the low word of A + half1 2^16 above
+    0xFFFF0000).  At 2^-16 per element a 4096 x 2048 gradient has ~100 such
+    elements: count them from the oracle's streams and require bit-exact codes
+    and norms."""
+    N, C = 4096, 2048
+    g = synth.grad_output(N, C, dense=True)
+    bs = o_bs.bit_split(g, synth.PHILOX_SEED, 6, 3)
+    from oracle import philox as o_ph
+    u = o_ph.sr_uniforms(synth.PHILOX_SEED, 6, 3, N, C).astype(np.int64)
+    _, _, r8 = o_bs.scales(g)
+    v = np.clip(g * r8, np.float32(-119), np.float32(119))
+    A = np.ceil(v.astype(np.float64) * 2.0 ** 32).astype(np.int64)
+    hi = (u >> 16) << 16
+    open_ = np.floor_divide(A + hi, 1 << 32) != np.floor_divide(A + hi + 0xFFFF, 1 << 32)
+    assert open_.sum() >= 20, open_.sum()
+    mod = p()
+    plan = mod._PlanBuffers(N, C, "cuda")
+    xsq = torch.ones(N, dtype=torch.int32, device="cuda")
+    mod.bitsplit_lss(to_bf16_cuda(g), xsq, synth.PHILOX_SEED, 6, 3, o_lss.MODE_BERNOULLI, plan.plan)
+    torch.cuda.synchronize()
+    q = plan.q8.cpu().numpy().astype(np.int64)[:N]
+    assert np.array_equal(q, bs["q"])
     assert np.array_equal(plan.a_sq.cpu().numpy().reshape(2, N), bs["a_sq"])
 
 

@@ -30,27 +30,41 @@ def test_p15b_golden():
         assert qq == q
         h, l = bitsplit.split(np.array([qq]))
         assert (int(h[0]), int(l[0])) == (hi, lo)
-    for gv, v_expect, T, q_down, q_up in g["stochastic"]:
+    for gv, v_expect, A, u_thr, q_below, q_at in g["stochastic"]:
         v = np.float32(gv) * r8
         assert v == np.float32(v_expect)
-        # u just below T rounds away from zero, u = T does not
-        assert bitsplit.stochastic_round(np.array([v]), np.array([T - 1]))[0] == q_up
-        assert bitsplit.stochastic_round(np.array([v]), np.array([T]))[0] == q_down
+        assert np.ceil(np.float64(v) * 2.0 ** 32) == A
+        # u just below the threshold keeps floor(v), u = threshold rounds up
+        assert bitsplit.stochastic_round(np.array([v]), np.array([u_thr - 1]))[0] == q_below
+        assert bitsplit.stochastic_round(np.array([v]), np.array([u_thr]))[0] == q_at
     for q, hi, lo in g["split_ties"]:
         h, l = bitsplit.split(np.array([q]))
         assert (int(h[0]), int(l[0])) == (hi, lo)
 
 
 def test_sr_threshold_is_exact_fraction():
-    # Z-10: P(up) = T / 2^32 equals frac(|v|) exactly when frac has <= 32 bits;
-    # the sign-magnitude form avoids the cancellation of floor-based SR for
-    # tiny negative v.
+    # Z-10 floor form: P(q = floor(v) + 1) = ceil(frac(v) 2^32) / 2^32, i.e. the
+    # fraction exactly when it has <= 32 bits; a tiny negative v (frac(v) within
+    # 2^-32 of 1) rounds to 0 for every u, a tiny positive one up only for the
+    # largest u.
     v = np.array([-1e-10, 1e-10, -118.75, 0.0, 119.0, -119.0], dtype=np.float32)
-    # u = 0 always rounds away from zero unless frac == 0
     q0 = bitsplit.stochastic_round(v, np.zeros(6, dtype=np.uint64))
-    assert q0.tolist() == [-1, 1, -119, 0, 119, -119]
+    assert q0.tolist() == [0, 0, -119, 0, 119, -119]
     q1 = bitsplit.stochastic_round(v, np.full(6, 2 ** 32 - 1, dtype=np.uint64))
-    assert q1.tolist() == [0, 0, -118, 0, 119, -119]
+    assert q1.tolist() == [0, 1, -118, 0, 119, -119]
+    # the count of u in [0, 2^32) rounding up is T = ceil(frac(v) 2^32), from the
+    # threshold u >= 2^32 - T: check both sides of it for a spread of fractions
+    rng = np.random.default_rng(3)
+    vs = (rng.integers(-119 * 2 ** 16, 119 * 2 ** 16, 200) / 2.0 ** 16).astype(np.float32)
+    for x in vs:
+        fl = int(np.floor(np.float64(x)))
+        T = int(np.ceil((np.float64(x) - fl) * 2.0 ** 32))
+        if T == 0:
+            assert bitsplit.stochastic_round(np.array([x]), np.array([2 ** 32 - 1]))[0] == fl
+            continue
+        thr = 2 ** 32 - T
+        assert bitsplit.stochastic_round(np.array([x]), np.array([thr - 1]))[0] == fl
+        assert bitsplit.stochastic_round(np.array([x]), np.array([thr]))[0] == fl + 1
 
 
 def test_p8_sr_unbiased_over_seeds():

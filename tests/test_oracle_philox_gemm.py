@@ -36,6 +36,26 @@ def test_philox_stream_layout_is_shard_invariant():
     assert abs(u.mean() - 0.5) < 0.01 and u.min() >= 0 and u.max() < 1
 
 
+def test_sr_uniform_halves_layout():
+    # Z-20: element L's uniform is (16-bit half L % 8 of block L // 8, purpose 1) << 16
+    # plus the same half of purpose 4; halves are independent and uniform.
+    n_rows, n_cols, t0 = 3, 40, 2
+    u = philox.sr_uniforms(9, 5, t0, n_rows, n_cols)
+    key = [9, 0]
+    for (t, c) in [(0, 0), (0, 7), (1, 13), (2, 39)]:
+        L = (t0 + t) * n_cols + c
+        b1 = philox.philox4x32_10([L // 8, 0, philox.PURPOSE_SR, 5], key).tolist()
+        b4 = philox.philox4x32_10([L // 8, 0, philox.PURPOSE_SR_LOW, 5], key).tolist()
+        j = L % 8
+        h1 = (b1[j // 2] >> (16 * (j % 2))) & 0xFFFF
+        h4 = (b4[j // 2] >> (16 * (j % 2))) & 0xFFFF
+        assert int(u[t, c]) == (h1 << 16) | h4
+    big = philox.sr_uniforms(2, 0, 0, 256, 256)
+    lo, hi = (big & 0xFFFF).astype(np.float64), (big >> 16).astype(np.float64)
+    assert abs(lo.mean() / 65536 - 0.5) < 0.01 and abs(hi.mean() / 65536 - 0.5) < 0.01
+    assert abs(np.corrcoef(lo.ravel(), hi.ravel())[0, 1]) < 0.02
+
+
 def test_p6_int_gemm_brute_force():
     assert gemm.int_matmul_abt([[1, 2]], [[3, 4]]).tolist() == [[11]]
     rng = np.random.default_rng(0)

@@ -1,8 +1,7 @@
-"""grad_split phase timing from per-CTA globaltimer stamps (I4_BS_EXP=8 build-in
-experiment): prints, in us from the earliest CTA start, the min / median / max
+"""grad_split phase timing from per-CTA globaltimer stamps (a -DI4_STAMPS=1 build,
+loaded through I4_LIB_OVERRIDE): prints, in us from the earliest CTA start, the min / median / max
 over CTAs of: phase 1 done, barrier passed, amax known, phase 2 done."""
 import ctypes, os, sys
-os.environ["I4_BS_EXP"] = "8"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
