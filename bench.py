@@ -1015,42 +1015,69 @@ def run_e2e(st, args, dev, world, ops, flush):
     """The same step through the public API (Int4Linear.forward / backward over the C
     ABI, eager launches) with host buffers: every step copies every linear's X, W and
     grad_Y from pinned host memory to the device and reads every grad_W bucket back
-    (the step's result: the weight gradients an optimizer consumes)."""
+    (the step's result: the weight gradients an optimizer consumes).  The copies are
+    pipelined with the compute as a training loop would stream them: one copy
+    stream brings X and W in forward order, then grad_Y in backward order, and the
+    compute stream waits for each linear's own inputs only; a second copy stream
+    (the other PCIe direction) reads each layer's grad_W bucket back as soon as its
+    backward (and, for N > 1, its all-reduce) is done.  The timed region runs from
+    the first copy to the last read-back."""
     import torch
     import torch.distributed as dist
     host_in = {nm: [torch.from_numpy(synth.bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16).pin_memory()
                     for a in xwg] for nm, xwg in st.host.items()}
     host_out = [torch.empty(b.numel(), dtype=torch.float32).pin_memory() for b in st.dW_bucket]
+    main = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    n = len(st.lins)
+    ev_xw = [torch.cuda.Event() for _ in range(n)]
+    ev_g = [torch.cuda.Event() for _ in range(n)]
+    ev_layer = [torch.cuda.Event() for _ in range(st.n_layers)]
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bwd_order = [i for layer in reversed(range(st.n_layers)) for i in reversed(st.per_layer[layer])]
     times = []
     for it in range(args.warmup + min(args.steps, 10)):
         flush()
         torch.cuda.synchronize()
-        a0.record()
-        for i, ln in enumerate(st.lins):
-            hx, hw, hg = host_in[ln[0]]
-            st.X[i].copy_(hx, non_blocking=True)
-            st.W[i].copy_(hw, non_blocking=True)
-            st.G[i].copy_(hg, non_blocking=True)
-        st.fwd_body()
-        handles = []
+        a0.record(main)
+        h2d.wait_stream(main)
+        d2h.wait_stream(main)
+        with torch.cuda.stream(h2d):
+            for i, ln in enumerate(st.lins):
+                hx, hw, _ = host_in[ln[0]]
+                st.X[i].copy_(hx, non_blocking=True)
+                st.W[i].copy_(hw, non_blocking=True)
+                ev_xw[i].record(h2d)
+            for i in bwd_order:
+                st.G[i].copy_(host_in[st.lins[i][0]][2], non_blocking=True)
+                ev_g[i].record(h2d)
+        for i in range(n):
+            main.wait_event(ev_xw[i])
+            st.fwd_one(i)
         for layer in reversed(range(st.n_layers)):
-            st.bwd_body(layer)
-            if world > 1:
-                handles.append(dist.all_reduce(st.dW_bucket[layer], op=dist.ReduceOp.SUM, async_op=True))
-        for h in handles:
-            h.wait()
-        for b, hb in zip(st.dW_bucket, host_out):
-            hb.copy_(b, non_blocking=True)
-        a1.record()
+            for i in reversed(st.per_layer[layer]):
+                main.wait_event(ev_g[i])
+                st.bwd_one(i)
+            h = dist.all_reduce(st.dW_bucket[layer], op=dist.ReduceOp.SUM, async_op=True) if world > 1 else None
+            ev_layer[layer].record(main)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_layer[layer])
+                if h is not None:
+                    h.wait()                      # the read-back waits for this bucket's all-reduce
+                host_out[layer].copy_(st.dW_bucket[layer], non_blocking=True)
+        main.wait_stream(d2h)
+        main.wait_stream(h2d)
+        a1.record(main)
         torch.cuda.synchronize()
         if it >= args.warmup:
             times.append(a0.elapsed_time(a1))
     t = max_over_ranks(statistics.mean(times), dev, world)
     return {"value": ops * world / (t * 1e-3) / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(st.bytes_h2d()),
             "d2h_bytes_per_step": int(sum(b.numel() * 4 for b in st.dW_bucket)), "ms_per_step": t,
-            "path": "pinned host X, W, grad_Y of every linear -> device; Int4Linear.forward / backward (C ABI, "
-                    "eager launches); every layer's grad_W bucket -> pinned host"}
+            "path": "pinned host X, W, grad_Y of every linear -> device on a copy stream (forward order, then "
+                    "grad_Y in backward order), each linear's Int4Linear.forward / backward (C ABI, eager "
+                    "launches) waiting for its own inputs only; every layer's grad_W bucket -> pinned host on a "
+                    "second copy stream as soon as the layer's backward is done"}
 
 
 # ---------------------------------------------------------------------------- dry run (CPU)
