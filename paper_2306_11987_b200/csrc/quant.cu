@@ -526,6 +526,12 @@ __device__ __forceinline__ Philox4 philox_sr_c1z(uint32_t c0, uint32_t call_id, 
 //   dp4a(16 hi, 16 hi) = 256 sum hi^2 and dp4a(x, x | 0xF0) = sum lo^2 - 64 per element
 //   (the 64 s are added back per chunk).
 constexpr uint32_t kPurposeSRLow = 4;
+#ifndef I4_GS_UNPACK
+#define I4_GS_UNPACK 1
+#endif
+#ifndef I4_GS_PACK
+#define I4_GS_PACK 1
+#endif
 template <bool CLAMP, bool C1Z>
 __device__ __forceinline__ void split_chunk8(const uint4 raw, uint64_t blk, uint32_t call_id, const PhiloxKeys& keys,
                                              const float r8, uint2& pq, int& shi, int& slo) {
@@ -540,7 +546,13 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, uint64_t blk, uint
     for (int i = 0; i < 8; i += 2) {
         // elements i (low bf16) and i + 1 (high bf16) as one fp32 pair
         const uint32_t wv = w[i >> 1];
-        const uint64_t g2 = f2_pack(__uint_as_float(__byte_perm(wv, 0u, 0x1044u)), __uint_as_float(wv & 0xFFFF0000u));
+#if I4_GS_UNPACK
+        uint32_t lo16;                                                 // low bf16 as fp32 by a shift (fma pipe)
+        asm("mul.lo.u32 %0, %1, 65536;" : "=r"(lo16) : "r"(wv));
+#else
+        const uint32_t lo16 = __byte_perm(wv, 0u, 0x1044u);
+#endif
+        const uint64_t g2 = f2_pack(__uint_as_float(lo16), __uint_as_float(wv & 0xFFFF0000u));
         float y0, y1;
         f2_unpack(f2_mul(f2_mul(g2, r2), f2_pack(4294967296.0f, 4294967296.0f)), y0, y1);
         if (CLAMP) {                                                   // 119 2^32
@@ -567,8 +579,14 @@ __device__ __forceinline__ void split_chunk8(const uint4 raw, uint64_t blk, uint
     const uint32_t c80 = 0x80808080u;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+#if I4_GS_PACK
+        uint32_t q, q23;                                               // saturating packs (exact: |q| <= 119)
+        asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(q23) : "r"(qv[4 * h + 3]), "r"(qv[4 * h + 2]));
+        asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(q) : "r"(qv[4 * h + 1]), "r"(qv[4 * h]), "r"(q23));
+#else
         const uint32_t q = __byte_perm(__byte_perm(uint32_t(qv[4 * h]), uint32_t(qv[4 * h + 1]), 0x0040),
                                        __byte_perm(uint32_t(qv[4 * h + 2]), uint32_t(qv[4 * h + 3]), 0x0040), 0x5410);
+#endif
         const uint32_t t = (q ^ c80) + 0x08080808u;
         uint32_t hi16;                                                  // (t ^ 0x80) & 0xF0 per byte
         asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(hi16) : "r"(t), "r"(c80), "r"(0xF0F0F0F0u));
