@@ -886,7 +886,10 @@ def dominant_roofline(st, kernels, shape_stats, args, flush, int8_peak, peaks):
         achieved = amount / avg_s / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
                 "frac": achieved / int8_peak, "traffic": traffic,
-                "peak_source": f"{peaks['source']}: bf16 {peaks['bf16_tflops']} TF/s x nominal INT8:BF16 = 2 (int8 TOPS)",
+                "peak_source": f"{peaks['source']}: bf16 {peaks['bf16_tflops']} TF/s (burst) x nominal INT8:BF16 = 2 "
+                               f"(int8 TOPS); the burst figure because the step runs at full clocks (see clocks)",
+                "peak_sustained": 2 * peaks["bf16_tflops_sustained"],
+                "frac_vs_sustained": achieved / (2 * peaks["bf16_tflops_sustained"]),
                 "work_per_launch": f"2*M*N*K = {amount:.4g} int ops"}
     else:
         achieved = amount / avg_s / 1e9
