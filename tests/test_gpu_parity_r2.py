@@ -102,6 +102,21 @@ def test_full_size_vit(cfg):
     _full_size(cfg, dense_g=False)
 
 
+@pytest.mark.parametrize("cfg,dense_g", [("cfg3_bert_large_qkv", False), ("cfg3_bert_large_ffn_down", False),
+                                         ("cfg3_bert_large_qkv", True), ("cfg3_bert_large_ffn_down", True),
+                                         ("cfgT_transformer_base_ffn_up", False),
+                                         ("cfgT16k_transformer_base_qkv", True)])
+def test_full_size_remaining_linears(cfg, dense_g):
+    """The rest of the BERT-large layer set and the translation (Transformer-base)
+    linears at full size, in both grad_Y regimes (sparse: the bench default, usually
+    deterministic masks and the dense code-plane operands; dense: binding budgets)."""
+    layer, mw, mx = _full_size(cfg, dense_g=dense_g)
+    flags = tuple(int(v) for v in layer.dense_flags().cpu().numpy())
+    assert all(f in (0, 1, 2) for f in flags)
+    if dense_g:
+        assert mw["count"] < 2 * layer.N and mx["count"] < 2 * layer.N
+
+
 # ----------------------------------------------------------------------------- sharding
 def test_token_sharded_backward_sum_equals_oracle_shards():
     """SURVEY.md §8(e) parity: the CUDA operator run on G token shards (each with
