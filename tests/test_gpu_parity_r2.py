@@ -38,13 +38,16 @@ def test_backward_low_hadamard_orders(k, mode, dense_g, expect):
 
 
 # ----------------------------------------------------------------------------- full size
-def _full_size(cfg, dense_g, n_rows=48, n_ch=24):
+def _full_size(cfg, dense_g, n_rows=48, n_ch=24, dims=None):
     """BASELINE config at full size in the bench's launch configuration (fp32
     outputs for parity): codes on sampled rows, the bit split in full, both
     sampler lists in full, grad_X on sampled tokens and grad_W on sampled
-    channels from the verified intermediates."""
-    c = synth.CONFIGS[cfg]
-    N, D, C, k = c["N"], c["D"], c["C"], c["k"]
+    channels from the verified intermediates.  dims = (N, D, C, k) overrides cfg."""
+    if dims is not None:
+        N, D, C, k = dims
+    else:
+        c = synth.CONFIGS[cfg]
+        N, D, C, k = c["N"], c["D"], c["C"], c["k"]
     x, w, s_x, s_w, layer, g, dX, dW = _bwd_case(N, D, C, k, dense=dense_g)
     xq, wq = layer.xq.cpu().numpy(), layer.wq.cpu().numpy()
     rows = np.sort(np.random.default_rng(1).choice(N, n_rows, replace=False))
@@ -115,6 +118,13 @@ def test_full_size_remaining_linears(cfg, dense_g):
     assert all(f in (0, 1, 2) for f in flags)
     if dense_g:
         assert mw["count"] < 2 * layer.N and mx["count"] < 2 * layer.N
+
+
+@pytest.mark.parametrize("dense_g", [False, True])
+def test_max_tokens_per_call(dense_g):
+    """N = 65536 tokens, the largest backward call (reading Z-21: grad_W's INT32
+    accumulator bound K_W 128 112 < 2^31; 131072 items on 16-CTA sampler clusters)."""
+    _full_size(None, dense_g=dense_g, dims=(65536, 256, 512, 5))
 
 
 # ----------------------------------------------------------------------------- sharding
