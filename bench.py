@@ -85,6 +85,8 @@ def parse(argv=None):
     ap.add_argument("--mode", choices=list(MODES), default="bernoulli")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--layer-graphs", action="store_true",
+                    help="N > 1 step structure (per-layer graphs + async all-reduce) on a one-rank NCCL group")
     ap.add_argument("--no-per-linear", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the pre-timing oracle parity gate")
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no operator compute")
@@ -443,8 +445,15 @@ def run_ours(args):
     rank, world, local = env_world()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    # --layer-graphs: the N > 1 step structure (per-layer backward graphs, an async NCCL
+    # all-reduce per layer) on a one-rank group -- exercises that path on one GPU
+    multi = world > 1 or args.layer_graphs
+    if multi and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        with stdout_to_stderr():          # NCCL may print its version line: stdout carries only the JSON line
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+            dist.barrier()
     lins, n_layers = workload(args.config)
     peaks = load_peaks()
     int8_peak = peaks["bf16_tflops"] * INT8_OVER_BF16
@@ -472,7 +481,7 @@ def run_ours(args):
         for layer in reversed(range(n_layers)):
             st.bwd_body(layer)
 
-    if world == 1:      # no exchange: the whole step is one graph (no gaps between graph launches)
+    if not multi:       # no exchange: the whole step is one graph (no gaps between graph launches)
         g_fwd, g_bwd = capture(whole_step), [None] * n_layers
     else:               # the all-reduces go between the per-layer backward graphs
         g_fwd = capture(st.fwd_body)
@@ -488,7 +497,7 @@ def run_ours(args):
         for layer in reversed(range(n_layers)):
             if gb[layer] is not None:
                 gb[layer].replay()
-            if world > 1 and not fused:   # async on NCCL's stream: overlaps the next (lower) layer's backward
+            if multi and not fused:       # async on NCCL's stream: overlaps the next (lower) layer's backward
                 handles.append(dist.all_reduce(buckets[layer], op=dist.ReduceOp.SUM, async_op=True))
         for h in handles:
             h.wait()        # the compute stream waits for every all-reduce before the step ends
@@ -547,7 +556,7 @@ def run_ours(args):
 
     bf_step()
     torch.cuda.synchronize()
-    if world == 1:
+    if not multi:
         gb_fwd, gb_bwd = capture(bf_step), [None] * n_layers
     else:
         gb_fwd = capture(bf_fwd)
@@ -635,14 +644,29 @@ def run_ours(args):
                                "(multimem.red.add; symmetric-memory barrier at the step's end)") if nvls else
                               ("per layer grad_W bucket (fp32), async on NCCL's stream after the layer's backward "
                                "graph, overlapping the next layer's backward; waited before the step's end event"))
-                if world > 1 else None}
+                if multi else None}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(lins, args.grad, args.mode)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+class stdout_to_stderr:
+    """File-descriptor-level redirect of stdout to stderr (native libraries print with printf)."""
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
 
 
 def max_over_ranks(value, device, world):
