@@ -43,3 +43,25 @@ def test_bench_workload_tables():
     assert bench.work_ops(lins) == 24 * 6.0 * 8192 * (1024 * 3072 + 2 * 1024 * 4096)
     lins, layers = bench.workload("cfg2_bert_base_ffn1")
     assert layers == 1 and lins[0][1:4] == (4096, 768, 3072)
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_layer_graph_path_on_one_gpu():
+    """The N > 1 step structure (forward graph, per-layer backward graphs, an async NCCL
+    all-reduce per layer overlapping the next layer's backward) on a one-rank group:
+    stdout is exactly one JSON line (NCCL's init output kept off it)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--layer-graphs", "--config",
+                        "cfgT_transformer_base_stack", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+                        "--no-e2e", "--no-per-linear"], capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["allreduce"] is not None and d["ms_per_step"] > 0 and d["parity_gate"] is not None
